@@ -1,0 +1,141 @@
+/*
+ * vmi.h -- C ABI of the B200 batched MI pose-evaluation library (libvmi.so).
+ *
+ * The reference (`voxmi`, pure Python/numpy) has no FFI; its "operator API" for
+ * the hot path is the Python objective contract
+ *     mi_objective(feat_a, cloud_b, pose, grid, spec, include_phi, n_jobs) -> float
+ * (reference pkg/src/voxmi/mi.py:194-219), fed by _prepare's scan-A feature map
+ * (align.py:114-119) and driven by align's objective closure (align.py:134-136)
+ * and sweep_axis's loop (align.py:191-197).  Each entry point below replaces one
+ * piece of that contract; the Python package paper_1709_06948_b200 binds them
+ * with ctypes (see INTEGRATION.md for the binding a voxmi maintainer would add).
+ *
+ * Conventions
+ *   - Return codes: 0 = OK, negative = error; vmi_last_error(ctx) has the text.
+ *   - Per-pose status (vmi_eval*): VMI_OK, VMI_EMPTY_REGION, VMI_KEY_RANGE,
+ *     VMI_PHI_OFF_EMPTY.  Any non-OK status comes with mi = VMI_SENTINEL
+ *     (-1e300), the reference's NO_OVERLAP_SENTINEL (mi.py:34, :206-219).
+ *   - A context is bound to one CUDA device, single-threaded and stream-ordered.
+ *     Host inputs are copied; the context owns every device buffer it allocates.
+ *   - There is no CPU fallback: without a usable CUDA device vmi_create fails.
+ */
+#ifndef VMI_H_
+#define VMI_H_
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef struct vmi_ctx vmi_ctx;
+
+#define VMI_SENTINEL (-1e300)
+
+enum vmi_status {
+  VMI_OK = 0,
+  VMI_EMPTY_REGION = 1,  /* compute_overlap empty (mi.py:211-213) */
+  VMI_KEY_RANGE = 2,     /* OutOfBoundsError from voxel_indices (mi.py:206-209) */
+  VMI_PHI_OFF_EMPTY = 3  /* include_phi=False, no co-occupied voxel (mi.py:215-219) */
+};
+
+enum vmi_kind { VMI_VARZ = 0, VMI_COUNT = 1 }; /* FeatureKind (voxel.py:33-46) */
+
+enum vmi_error {
+  VMI_ERR_ARG = -1,
+  VMI_ERR_CUDA = -2,
+  VMI_ERR_ALLOC = -3,
+  VMI_ERR_STATE = -4,
+  VMI_ERR_RANGE = -5,       /* scan A leaves the voxel key range (voxel.py:200-206) */
+  VMI_ERR_UNSUPPORTED = -6  /* e.g. bins > 64, reference AABB too large for the dense grid */
+};
+
+/* Context lifetime.  device = CUDA ordinal.  Replaces nothing in the reference
+   (it holds the state _prepare/mi_objective recompute per call). */
+int vmi_create(int device, vmi_ctx** out);
+int vmi_destroy(vmi_ctx* ctx);
+const char* vmi_last_error(const vmi_ctx* ctx);
+/* Library/build identification string (static storage). */
+const char* vmi_version(void);
+
+/* GridSpec (voxel.py:49-62) + BinningSpec (mi.py:40-59) + include_phi
+   (mi.py:177-191).  kind: vmi_kind.  Must precede vmi_set_reference_*.
+   bins in [2, 64]; clamp > 0. */
+int vmi_set_params(vmi_ctx* ctx, const double origin[3], double resolution, int kind, int bins,
+                   double clamp, int include_phi);
+
+/* Scan A from raw points: voxelize + compute_feature_map on the GPU
+   (_prepare, align.py:114-119; voxel.py:210-222, :267-295), bit-exact including
+   VARZ.  xyz: host (n, 3) float64, row-major.  Returns VMI_ERR_RANGE when a
+   point leaves the key range (the reference raises OutOfBoundsError). */
+int vmi_set_reference_points(vmi_ctx* ctx, const double* xyz, int64_t n);
+
+/* Scan A from an existing FeatureMap (voxel.py:129-164): packed keys
+   (pack_keys, voxel.py:65-73) sorted ascending, values >= 0, bounds =
+   [xmin, ymin, zmin, xmax, ymax, zmax].  The injection point the reference's
+   tests use (test_mi.py:37-50). */
+int vmi_set_reference_features(vmi_ctx* ctx, const int64_t* keys, const double* values, int64_t n,
+                               const int64_t bounds[6]);
+
+/* Export the GPU-built scan-A FeatureMap (keys, values, bounds).  With keys ==
+   NULL only *n_out is written.  cap = capacity of keys/values. */
+int vmi_get_reference_features(vmi_ctx* ctx, int64_t* keys, double* values, int64_t cap,
+                               int64_t* n_out, int64_t bounds[6]);
+
+/* Scan B (PointCloud, geometry.py:36-65): host (n, 3) float64.  Stored as
+   float4 when every coordinate is float32-exact (KITTI input), else double. */
+int vmi_set_query_points(vmi_ctx* ctx, const double* xyz, int64_t n);
+/* Scan B as KITTI .bin records (x, y, z, intensity float32; scan_io.py:57-75). */
+int vmi_set_query_records_f32(vmi_ctx* ctx, const float* xyzi, int64_t n);
+
+/* euler_to_transform (geometry.py:126-138) for P poses (tx,ty,tz,rx,ry,rz):
+   12 float64 per pose, R row-major then t, bit-identical to the reference
+   (glibc sin/cos, no FP contraction).  Host only; threads <= 0 = all cores. */
+int vmi_poses_to_mats(const double* poses, int64_t n, double* mats, int threads);
+
+/* Batched mi_objective (mi.py:194-219) over P pose matrices, host buffers,
+   synchronous.  mi_out[P], status_out[P] required; hist_out (P*(bins+1)^2
+   int64, JointHistogram.counts, mi.py:82-98) and total_out (P int64,
+   JointHistogram.total) may be NULL. */
+int vmi_eval(vmi_ctx* ctx, const double* mats, int64_t P, double* mi_out, int32_t* status_out,
+             int64_t* hist_out, int64_t* total_out);
+
+/* Same with device pointers on a caller stream (cudaStream_t as void*);
+   asynchronous: no host sync, no fix-up pass (see vmi_eval_fixups). */
+int vmi_eval_device(vmi_ctx* ctx, const double* mats_dev, int64_t P, double* mi_dev,
+                    int32_t* status_dev, int64_t* hist_dev, int64_t* total_dev, void* stream);
+
+/* After vmi_eval_device: re-evaluate, through the exact sort-based path, the
+   poses whose fast-path status carries VMI_FLAG_RECHECK (table overflow or a
+   VARZ value within rounding of a bin edge).  Synchronous. Returns count. */
+int vmi_eval_fixups(vmi_ctx* ctx, const double* mats_dev, int64_t P, double* mi_dev,
+                    int32_t* status_dev, int64_t* hist_dev, int64_t* total_dev, void* stream,
+                    int64_t* n_fixed);
+#define VMI_FLAG_RECHECK 0x100
+
+/* Exact (sort-based, reference-order) evaluation of P poses: the slow
+   cross-check path, bit-exact features by construction. */
+int vmi_eval_exact(vmi_ctx* ctx, const double* mats, int64_t P, double* mi_out,
+                   int32_t* status_out, int64_t* hist_out, int64_t* total_out);
+
+/* Debug / parity: B's feature map at one pose (voxelize + compute_feature_map
+   of the transformed scan), via the exact path.  keys/values capacity cap. */
+int vmi_query_features(vmi_ctx* ctx, const double mat[12], int64_t* keys, double* values,
+                       int64_t cap, int64_t* n_out, int64_t bounds[6], int32_t* status);
+
+/* Device-side argmax over mi (first index of the max, np.argmax semantics,
+   cli.py:202).  Writes best value and index to host. */
+int vmi_argmax_device(vmi_ctx* ctx, const double* mi_dev, int64_t P, double* best_mi,
+                      int64_t* best_idx, void* stream);
+
+/* Number of kernel launches issued by this context so far (bench accounting). */
+int64_t vmi_launch_count(const vmi_ctx* ctx);
+
+/* Fast-path configuration knobs (tests/bench): table capacity (0 = max that
+   fits shared memory) and threads per CTA (0 = default 512; 512 or 1024). */
+int vmi_set_tuning(vmi_ctx* ctx, int table_cap, int threads);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* VMI_H_ */

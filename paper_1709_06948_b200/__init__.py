@@ -1,0 +1,28 @@
+"""B200-native batched MI pose evaluation (arXiv 1709.06948 hot path).
+
+Drop-in for the reference `voxmi` package's hot path -- ``mi_objective``
+(mi.py:194-219) and its callers -- with the work done by hand-written sm_100a
+kernels behind a C ABI (include/vmi.h, libvmi.so).  See DESIGN.md.
+"""
+
+from .api import (SWEEP_AXES, SearchResult, clear_cache, compute_feature_map, engine_for,
+                  grid_search, joint_histogram_at, mi_at, mi_objective, mi_objective_batch,
+                  sweep_axis)
+from .engine import MIEngine, entropy_exact, mutual_information_exact
+from .errors import EmptyOverlapError, NoOverlapError, OutOfBoundsError, VoxmiError
+from .geometry import EulerPose, PointCloud, as_pose_array, euler_to_transform
+from .types import (DEFAULT_BIN_COUNT, DEFAULT_UPPER_CLAMP, KEY_INDEX_MAX, KEY_INDEX_MIN,
+                    NO_OVERLAP_SENTINEL, AlignmentConfig, BinningSpec, FeatureKind, FeatureMap,
+                    GridSpec, JointHistogram, MIResult)
+from ._lib import VmiError, poses_to_mats
+
+__all__ = [
+    "SWEEP_AXES", "SearchResult", "clear_cache", "compute_feature_map", "engine_for",
+    "grid_search", "joint_histogram_at", "mi_at", "mi_objective", "mi_objective_batch",
+    "sweep_axis", "MIEngine", "entropy_exact", "mutual_information_exact", "EmptyOverlapError",
+    "NoOverlapError", "OutOfBoundsError", "VoxmiError", "EulerPose", "PointCloud",
+    "as_pose_array", "euler_to_transform", "DEFAULT_BIN_COUNT", "DEFAULT_UPPER_CLAMP",
+    "KEY_INDEX_MAX", "KEY_INDEX_MIN", "NO_OVERLAP_SENTINEL", "AlignmentConfig", "BinningSpec",
+    "FeatureKind", "FeatureMap", "GridSpec", "JointHistogram", "MIResult", "VmiError",
+    "poses_to_mats",
+]

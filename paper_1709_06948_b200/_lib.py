@@ -1,0 +1,231 @@
+"""ctypes binding of libvmi.so (include/vmi.h).
+
+The library is built in-tree (``build.py``) and is REQUIRED: there is no CPU
+fallback.  Importing the package works without it (so CPU-only tooling can
+inspect the API), but every call that needs the GPU raises ``VmiError`` when
+the library or a CUDA device is missing.
+"""
+
+from __future__ import annotations
+
+import ctypes
+import os
+
+import numpy as np
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(HERE, "_native", "libvmi.so")
+
+VMI_OK, VMI_EMPTY_REGION, VMI_KEY_RANGE, VMI_PHI_OFF_EMPTY = 0, 1, 2, 3
+VMI_FLAG_RECHECK = 0x100
+SENTINEL = -1e300
+
+# every exported symbol of include/vmi.h (checked by tests/test_boundary.py)
+EXPORTS = (
+    "vmi_create", "vmi_destroy", "vmi_last_error", "vmi_version", "vmi_set_params",
+    "vmi_set_reference_points", "vmi_set_reference_features", "vmi_get_reference_features",
+    "vmi_set_query_points", "vmi_set_query_records_f32", "vmi_poses_to_mats", "vmi_eval",
+    "vmi_eval_device", "vmi_eval_fixups", "vmi_eval_exact", "vmi_query_features",
+    "vmi_argmax_device", "vmi_launch_count", "vmi_set_tuning",
+)
+
+
+class VmiError(RuntimeError):
+    """Raised when the native library reports an error (or is missing)."""
+
+
+_lib = None
+
+_d = ctypes.POINTER(ctypes.c_double)
+_i64 = ctypes.POINTER(ctypes.c_int64)
+_i32 = ctypes.POINTER(ctypes.c_int32)
+_f = ctypes.POINTER(ctypes.c_float)
+_vp = ctypes.c_void_p
+_ctx = ctypes.c_void_p
+
+
+def load(path: str = LIB_PATH):
+    """Load libvmi.so and declare argtypes; raise VmiError if it is absent."""
+    global _lib
+    if _lib is not None:
+        return _lib
+    if not os.path.exists(path):
+        raise VmiError(
+            f"{path} is missing: build it with `python -m paper_1709_06948_b200.build` "
+            "(there is no CPU fallback)")
+    L = ctypes.CDLL(path)
+    L.vmi_create.argtypes = [ctypes.c_int, ctypes.POINTER(_ctx)]
+    L.vmi_destroy.argtypes = [_ctx]
+    L.vmi_last_error.argtypes = [_ctx]
+    L.vmi_last_error.restype = ctypes.c_char_p
+    L.vmi_version.restype = ctypes.c_char_p
+    L.vmi_set_params.argtypes = [_ctx, _d, ctypes.c_double, ctypes.c_int, ctypes.c_int,
+                                 ctypes.c_double, ctypes.c_int]
+    L.vmi_set_reference_points.argtypes = [_ctx, _d, ctypes.c_int64]
+    L.vmi_set_reference_features.argtypes = [_ctx, _i64, _d, ctypes.c_int64, _i64]
+    L.vmi_get_reference_features.argtypes = [_ctx, _i64, _d, ctypes.c_int64, _i64, _i64]
+    L.vmi_set_query_points.argtypes = [_ctx, _d, ctypes.c_int64]
+    L.vmi_set_query_records_f32.argtypes = [_ctx, _f, ctypes.c_int64]
+    L.vmi_poses_to_mats.argtypes = [_d, ctypes.c_int64, _d, ctypes.c_int]
+    L.vmi_eval.argtypes = [_ctx, _d, ctypes.c_int64, _d, _i32, _i64, _i64]
+    L.vmi_eval_device.argtypes = [_ctx, _vp, ctypes.c_int64, _vp, _vp, _vp, _vp, _vp]
+    L.vmi_eval_fixups.argtypes = [_ctx, _vp, ctypes.c_int64, _vp, _vp, _vp, _vp, _vp, _i64]
+    L.vmi_eval_exact.argtypes = [_ctx, _d, ctypes.c_int64, _d, _i32, _i64, _i64]
+    L.vmi_query_features.argtypes = [_ctx, _d, _i64, _d, ctypes.c_int64, _i64, _i64, _i32]
+    L.vmi_argmax_device.argtypes = [_ctx, _vp, ctypes.c_int64, _d, _i64, _vp]
+    L.vmi_launch_count.argtypes = [_ctx]
+    L.vmi_launch_count.restype = ctypes.c_int64
+    L.vmi_set_tuning.argtypes = [_ctx, ctypes.c_int, ctypes.c_int]
+    _lib = L
+    return L
+
+
+def ptr(a: np.ndarray, t):
+    return a.ctypes.data_as(t)
+
+
+def poses_to_mats(poses: np.ndarray, threads: int = 0) -> np.ndarray:
+    """euler_to_transform for (P, 6) poses -> (P, 12) [R row-major, t].
+
+    Host C++ with glibc sin/cos, no FP contraction: bit-identical to the
+    reference's geometry.py:126-138 (see csrc/pose_host.cpp).
+    """
+    poses = np.ascontiguousarray(poses, dtype=np.float64).reshape(-1, 6)
+    out = np.empty((poses.shape[0], 12), dtype=np.float64)
+    rc = load().vmi_poses_to_mats(ptr(poses, _d), poses.shape[0], ptr(out, _d), int(threads))
+    if rc:
+        raise VmiError(f"vmi_poses_to_mats failed ({rc})")
+    return out
+
+
+class Context:
+    """One native context (one CUDA device)."""
+
+    def __init__(self, device: int = 0):
+        L = load()
+        h = _ctx()
+        rc = L.vmi_create(int(device), ctypes.byref(h))
+        if rc:
+            raise VmiError(f"vmi_create(device={device}) failed ({rc}): no usable sm_100 CUDA device")
+        self._h = h
+        self._L = L
+        self.device = device
+
+    def check(self, rc: int, what: str):
+        if rc:
+            msg = self._L.vmi_last_error(self._h).decode()
+            if rc == -1 and "empty cloud" in msg:
+                raise ValueError(msg)
+            if rc == -1:
+                raise ValueError(f"{what}: {msg}")
+            raise VmiError(f"{what} failed ({rc}): {msg}")
+
+    def close(self):
+        if getattr(self, "_h", None):
+            self._L.vmi_destroy(self._h)
+            self._h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    @property
+    def handle(self):
+        return self._h
+
+    @property
+    def launches(self) -> int:
+        return int(self._L.vmi_launch_count(self._h))
+
+    def set_params(self, origin, res, kind: int, bins: int, clamp: float, include_phi: bool):
+        o = np.ascontiguousarray(origin, dtype=np.float64)
+        self.check(self._L.vmi_set_params(self._h, ptr(o, _d), float(res), int(kind), int(bins),
+                                          float(clamp), int(bool(include_phi))), "vmi_set_params")
+
+    def set_tuning(self, table_cap: int = 0, threads: int = 0):
+        self.check(self._L.vmi_set_tuning(self._h, int(table_cap), int(threads)), "vmi_set_tuning")
+
+    def set_reference_points(self, xyz: np.ndarray):
+        xyz = np.ascontiguousarray(xyz, dtype=np.float64)
+        rc = self._L.vmi_set_reference_points(self._h, ptr(xyz, _d), xyz.shape[0])
+        if rc == -5:
+            from .errors import OutOfBoundsError
+            raise OutOfBoundsError(self._L.vmi_last_error(self._h).decode())
+        self.check(rc, "vmi_set_reference_points")
+
+    def set_reference_features(self, keys, values, bounds):
+        k = np.ascontiguousarray(keys, dtype=np.int64)
+        v = np.ascontiguousarray(values, dtype=np.float64)
+        b = np.ascontiguousarray(np.asarray(bounds, dtype=np.int64).reshape(6))
+        self.check(self._L.vmi_set_reference_features(self._h, ptr(k, _i64), ptr(v, _d), k.size,
+                                                      ptr(b, _i64)), "vmi_set_reference_features")
+
+    def get_reference_features(self):
+        n = ctypes.c_int64(0)
+        b = np.empty(6, dtype=np.int64)
+        self.check(self._L.vmi_get_reference_features(self._h, None, None, 0, ctypes.byref(n),
+                                                      ptr(b, _i64)), "vmi_get_reference_features")
+        keys = np.empty(max(n.value, 1), dtype=np.int64)
+        vals = np.empty(max(n.value, 1), dtype=np.float64)
+        self.check(self._L.vmi_get_reference_features(self._h, ptr(keys, _i64), ptr(vals, _d),
+                                                      keys.size, ctypes.byref(n), ptr(b, _i64)),
+                   "vmi_get_reference_features")
+        return keys[:n.value], vals[:n.value], b.reshape(2, 3)
+
+    def set_query_points(self, xyz: np.ndarray):
+        xyz = np.ascontiguousarray(xyz, dtype=np.float64)
+        self.check(self._L.vmi_set_query_points(self._h, ptr(xyz, _d), xyz.shape[0]),
+                   "vmi_set_query_points")
+
+    def set_query_records(self, rec: np.ndarray):
+        rec = np.ascontiguousarray(rec, dtype=np.float32)
+        if rec.ndim != 2 or rec.shape[1] != 4:
+            raise ValueError("records must be (N, 4) float32")
+        self.check(self._L.vmi_set_query_records_f32(self._h, ptr(rec, _f), rec.shape[0]),
+                   "vmi_set_query_records_f32")
+
+    def eval(self, mats: np.ndarray, want_hist: bool = False, bins: int = 32, exact: bool = False):
+        mats = np.ascontiguousarray(mats, dtype=np.float64).reshape(-1, 12)
+        P = mats.shape[0]
+        mi = np.empty(P, dtype=np.float64)
+        st = np.empty(P, dtype=np.int32)
+        total = np.empty(P, dtype=np.int64)
+        hist = np.empty((P, bins + 1, bins + 1), dtype=np.int64) if want_hist else None
+        fn = self._L.vmi_eval_exact if exact else self._L.vmi_eval
+        self.check(fn(self._h, ptr(mats, _d), P, ptr(mi, _d), ptr(st, _i32),
+                      ptr(hist, _i64) if want_hist else None, ptr(total, _i64)), "vmi_eval")
+        return mi, st, hist, total
+
+    def eval_device(self, mats_ptr: int, P: int, mi_ptr: int, st_ptr: int, stream: int = 0,
+                    hist_ptr: int = 0, total_ptr: int = 0):
+        self.check(self._L.vmi_eval_device(self._h, mats_ptr, P, mi_ptr, st_ptr, hist_ptr or None,
+                                           total_ptr or None, stream or None), "vmi_eval_device")
+
+    def eval_fixups(self, mats_ptr: int, P: int, mi_ptr: int, st_ptr: int, stream: int = 0,
+                    hist_ptr: int = 0, total_ptr: int = 0) -> int:
+        n = ctypes.c_int64(0)
+        self.check(self._L.vmi_eval_fixups(self._h, mats_ptr, P, mi_ptr, st_ptr, hist_ptr or None,
+                                           total_ptr or None, stream or None, ctypes.byref(n)),
+                   "vmi_eval_fixups")
+        return int(n.value)
+
+    def argmax_device(self, mi_ptr: int, P: int, stream: int = 0):
+        v = ctypes.c_double(0)
+        i = ctypes.c_int64(0)
+        self.check(self._L.vmi_argmax_device(self._h, mi_ptr, P, ctypes.byref(v), ctypes.byref(i),
+                                             stream or None), "vmi_argmax_device")
+        return float(v.value), int(i.value)
+
+    def query_features(self, mat12: np.ndarray, cap: int):
+        m = np.ascontiguousarray(mat12, dtype=np.float64).reshape(12)
+        keys = np.empty(max(cap, 1), dtype=np.int64)
+        vals = np.empty(max(cap, 1), dtype=np.float64)
+        n = ctypes.c_int64(0)
+        b = np.empty(6, dtype=np.int64)
+        st = ctypes.c_int32(0)
+        self.check(self._L.vmi_query_features(self._h, ptr(m, _d), ptr(keys, _i64), ptr(vals, _d),
+                                              keys.size, ctypes.byref(n), ptr(b, _i64),
+                                              ctypes.byref(st)), "vmi_query_features")
+        return keys[:n.value], vals[:n.value], b.reshape(2, 3), int(st.value)

@@ -1,0 +1,394 @@
+// k_exact.cu -- exact, reference-order voxelization on the GPU.
+//
+// This is the bit-exact counterpart of voxelize + compute_feature_map
+// (reference pkg/src/voxmi/voxel.py:210-222, :267-295):
+//   keys    : pack_keys of floor((p - origin)/res)           (voxel.py:65-73, :199)
+//   order   : stable radix sort of the packed keys            (voxel.py:216, kind="stable")
+//   CSR     : run-length encode -> unique keys + offsets      (voxel.py:217-219)
+//   bounds  : min/max of ijk over ALL points                  (voxel.py:220)
+//   VARZ    : reduceat sums in numpy's pairwise order, mean, reduceat of squared
+//             deviations, max(ssd, 0)/n                       (voxel.py:285-293)
+// It builds scan A's reference grid once per scan pair (_prepare,
+// align.py:114-119) and re-evaluates, exactly, the rare poses the fast path
+// flags (VMI_FLAG_RECHECK).  Sorting uses CUB (CUDA toolkit library code).
+#include <cstdint>
+#include <climits>
+#include <cub/cub.cuh>
+#include <cuda_runtime.h>
+
+#include "vmi_device.cuh"
+#include "vmi_kernels.h"
+
+namespace vmi {
+
+#define VMI_TRY(x)                           \
+  do {                                       \
+    cudaError_t e_ = (x);                    \
+    if (e_ != cudaSuccess) return e_;        \
+  } while (0)
+
+__device__ __forceinline__ void point_at(const PointSource& src, int64_t i, double& x, double& y,
+                                         double& z) {
+  if (src.xyz) {
+    x = src.xyz[3 * i]; y = src.xyz[3 * i + 1]; z = src.xyz[3 * i + 2];
+    return;
+  }
+  const int64_t t = i / src.B.span, r = i - t * src.B.span;
+  const int64_t li = r * src.B.threads + t;
+  if (src.B.is_f32) {
+    float4 v = reinterpret_cast<const float4*>(src.B.pts)[li];
+    x = v.x; y = v.y; z = v.z;
+  } else {
+    const double* d = reinterpret_cast<const double*>(src.B.pts) + 4 * li;
+    x = d[0]; y = d[1]; z = d[2];
+  }
+}
+
+__global__ void k_exact_keys(PointSource src, const double* __restrict__ mat, GridParams g,
+                             unsigned long long* keys, int* idx, double* zout, int* bounds) {
+  __shared__ int sb[7];
+  if (threadIdx.x < 3) { sb[threadIdx.x] = INT_MAX; sb[3 + threadIdx.x] = INT_MIN; }
+  if (threadIdx.x == 6) sb[6] = 0;
+  __syncthreads();
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  int ix = INT_MAX, iy = INT_MAX, iz = INT_MAX, ax = INT_MIN, ay = INT_MIN, az = INT_MIN;
+  bool bad = false;
+  if (i < src.n) {
+    double x, y, z;
+    point_at(src, i, x, y, z);
+    double X = x, Y = y, Z = z;
+    if (mat) {
+      X = xform_row(x, y, z, mat[0], mat[1], mat[2], mat[9]);
+      Y = xform_row(x, y, z, mat[3], mat[4], mat[5], mat[10]);
+      Z = xform_row(x, y, z, mat[6], mat[7], mat[8], mat[11]);
+    }
+    int a, b, c;
+    bool ok = voxel_coord(X, g.origin[0], g.res, g.inv_res, g.mode, a);
+    ok &= voxel_coord(Y, g.origin[1], g.res, g.inv_res, g.mode, b);
+    ok &= voxel_coord(Z, g.origin[2], g.res, g.inv_res, g.mode, c);
+    bad = !ok;
+    ix = ax = a; iy = ay = b; iz = az = c;
+    const unsigned long long off = 1ull << 20;
+    keys[i] = (((unsigned long long)(long long)a + off) << 42) |
+              (((unsigned long long)(long long)b + off) << 21) |
+              ((unsigned long long)(long long)c + off);
+    idx[i] = (int)i;
+    zout[i] = Z;
+  }
+  ix = __reduce_min_sync(0xffffffffu, ix); iy = __reduce_min_sync(0xffffffffu, iy);
+  iz = __reduce_min_sync(0xffffffffu, iz); ax = __reduce_max_sync(0xffffffffu, ax);
+  ay = __reduce_max_sync(0xffffffffu, ay); az = __reduce_max_sync(0xffffffffu, az);
+  const bool anybad = __any_sync(0xffffffffu, bad);
+  if ((threadIdx.x & 31) == 0) {
+    atomicMin(&sb[0], ix); atomicMin(&sb[1], iy); atomicMin(&sb[2], iz);
+    atomicMax(&sb[3], ax); atomicMax(&sb[4], ay); atomicMax(&sb[5], az);
+    if (anybad) sb[6] = 1;
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    atomicMin(&bounds[0], sb[0]); atomicMin(&bounds[1], sb[1]); atomicMin(&bounds[2], sb[2]);
+    atomicMax(&bounds[3], sb[3]); atomicMax(&bounds[4], sb[4]); atomicMax(&bounds[5], sb[5]);
+    if (sb[6]) atomicOr(&bounds[6], 1);
+  }
+}
+
+__global__ void k_init_bounds(int* b) {
+  if (threadIdx.x < 3) { b[threadIdx.x] = INT_MAX; b[3 + threadIdx.x] = INT_MIN; }
+  if (threadIdx.x == 6) b[6] = 0;
+}
+
+__global__ void k_gather(const double* z, const int* idx, int64_t n, double* zs) {
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < n) zs[i] = z[idx[i]];
+}
+
+struct ZAt {
+  const double* z;
+  __device__ double operator()(int64_t i) const { return z[i]; }
+};
+struct SqDevAt {
+  const double* z;
+  double mean;
+  __device__ double operator()(int64_t i) const {
+    const double d = __dsub_rn(z[i], mean);
+    return __dmul_rn(d, d);
+  }
+};
+
+__global__ void k_features(const int* counts, const int* offsets, const int* nruns, const double* zs,
+                           int kind, double* values) {
+  const int v = blockIdx.x * blockDim.x + threadIdx.x;
+  if (v >= *nruns) return;
+  const int64_t lo = offsets[v], hi = lo + counts[v];
+  const double cnt = (double)counts[v];
+  if (kind == 1) {
+    values[v] = cnt;
+    return;
+  }
+  const double mean = __ddiv_rn(segment_sum(ZAt{zs}, lo, hi), cnt);
+  const double ssd = segment_sum(SqDevAt{zs, mean}, lo, hi);
+  values[v] = __ddiv_rn(ssd > 0.0 ? ssd : 0.0, cnt);
+}
+
+cudaError_t exact_alloc(ExactScratch& s, int64_t n) {
+  if (n <= s.cap_n) return cudaSuccess;
+  exact_free(s);
+  const int64_t m = n < 1 ? 1 : n;
+  VMI_TRY(cudaMalloc(&s.keys, m * 8));
+  VMI_TRY(cudaMalloc(&s.keys_sorted, m * 8));
+  VMI_TRY(cudaMalloc(&s.idx, m * 4));
+  VMI_TRY(cudaMalloc(&s.idx_sorted, m * 4));
+  VMI_TRY(cudaMalloc(&s.z, m * 8));
+  VMI_TRY(cudaMalloc(&s.zs, m * 8));
+  VMI_TRY(cudaMalloc(&s.ukeys, m * 8));
+  VMI_TRY(cudaMalloc(&s.counts, m * 4));
+  VMI_TRY(cudaMalloc(&s.offsets, m * 4));
+  VMI_TRY(cudaMalloc(&s.values, m * 8));
+  VMI_TRY(cudaMalloc(&s.nruns, 16));
+  VMI_TRY(cudaMalloc(&s.bounds, 16 * 4));
+  VMI_TRY(cudaMalloc(&s.ghist, kMaxW * kMaxW * 4));
+  size_t b1 = 0, b2 = 0, b3 = 0;
+  VMI_TRY(cub::DeviceRadixSort::SortPairs(nullptr, b1, s.keys, s.keys_sorted, s.idx, s.idx_sorted,
+                                          (int)m, 0, 63));
+  VMI_TRY(cub::DeviceRunLengthEncode::Encode(nullptr, b2, s.keys_sorted, s.ukeys, s.counts,
+                                             s.nruns, (int)m));
+  VMI_TRY(cub::DeviceScan::ExclusiveSum(nullptr, b3, s.counts, s.offsets, (int)m));
+  s.cub_bytes = b1 > b2 ? b1 : b2;
+  if (b3 > s.cub_bytes) s.cub_bytes = b3;
+  VMI_TRY(cudaMalloc(&s.cub_tmp, s.cub_bytes));
+  s.cap_n = m;
+  return cudaSuccess;
+}
+
+void exact_free(ExactScratch& s) {
+  void* ptrs[] = {s.keys, s.keys_sorted, s.idx, s.idx_sorted, s.z, s.zs, s.ukeys, s.counts,
+                  s.offsets, s.values, s.nruns, s.bounds, s.ghist, s.cub_tmp};
+  for (void* p : ptrs)
+    if (p) cudaFree(p);
+  s = ExactScratch();
+}
+
+cudaError_t exact_voxelize(ExactScratch& s, const PointSource& src, const double* mat,
+                           const GridParams& g, cudaStream_t st, int64_t* launches) {
+  const int64_t n = src.n;
+  VMI_TRY(exact_alloc(s, n));
+  const int T = 256;
+  const int blocks = (int)((n + T - 1) / T);
+  k_init_bounds<<<1, 32, 0, st>>>(s.bounds);
+  k_exact_keys<<<blocks, T, 0, st>>>(src, mat, g, s.keys, s.idx, s.z, s.bounds);
+  size_t bytes = s.cub_bytes;
+  VMI_TRY(cub::DeviceRadixSort::SortPairs(s.cub_tmp, bytes, s.keys, s.keys_sorted, s.idx,
+                                          s.idx_sorted, (int)n, 0, 63, st));
+  bytes = s.cub_bytes;
+  VMI_TRY(cub::DeviceRunLengthEncode::Encode(s.cub_tmp, bytes, s.keys_sorted, s.ukeys, s.counts,
+                                             s.nruns, (int)n, st));
+  // counts past the run count are stale; the scan over n entries only needs
+  // the first V offsets to be right
+  bytes = s.cub_bytes;
+  VMI_TRY(cub::DeviceScan::ExclusiveSum(s.cub_tmp, bytes, s.counts, s.offsets, (int)n, st));
+  k_gather<<<blocks, T, 0, st>>>(s.z, s.idx_sorted, n, s.zs);
+  k_features<<<blocks, T, 0, st>>>(s.counts, s.offsets, s.nruns, s.zs, g.kind, s.values);
+  if (launches) *launches += 5;  // own kernels (CUB launches not counted)
+  return cudaGetLastError();
+}
+
+// ---- scan A's reference grid -------------------------------------------------
+__global__ void k_build_grid(const unsigned long long* keys, const double* values, int V,
+                             GridParams g, int3 amin, uint3 ext, uint8_t* grid, int4* avox_tmp,
+                             uint32_t* bin_total) {
+  const int v = blockIdx.x * blockDim.x + threadIdx.x;
+  if (v >= V) return;
+  const unsigned long long k = keys[v];
+  const int x = (int)((k >> 42) & 0x1FFFFF) - (1 << 20);
+  const int y = (int)((k >> 21) & 0x1FFFFF) - (1 << 20);
+  const int z = (int)(k & 0x1FFFFF) - (1 << 20);
+  const uint32_t rx = x - amin.x, ry = y - amin.y, rz = z - amin.z;
+  const int bin = feature_bin(values[v], g.clamp, g.bins);
+  // keys outside the declared bounds can never fall in an overlap region
+  // (mi.py:139-142 masks them away); drop them from the voxel list too
+  if (!(rx < ext.x && ry < ext.y && rz < ext.z)) {
+    avox_tmp[v] = make_int4(0, 0, 0, -1);
+    return;
+  }
+  grid[((size_t)rx * ext.y + ry) * ext.z + rz] = (uint8_t)bin;
+  avox_tmp[v] = make_int4((int)rx, (int)ry, (int)rz, bin);
+  atomicAdd(&bin_total[bin], 1u);
+}
+
+__global__ void k_bin_offsets(const uint32_t* bin_total, int W, int* cursor) {
+  if (threadIdx.x == 0) {
+    int s = 0;
+    for (int b = 0; b < W; ++b) { cursor[b] = s; s += (int)bin_total[b]; }
+  }
+}
+
+__global__ void k_scatter_by_bin(const int4* avox_tmp, int V, int* cursor, int4* avox) {
+  const int v = blockIdx.x * blockDim.x + threadIdx.x;
+  if (v >= V) return;
+  const int4 a = avox_tmp[v];
+  if (a.w >= 0) avox[atomicAdd(&cursor[a.w], 1)] = a;
+}
+
+cudaError_t build_reference(const unsigned long long* keys, const double* values, int V,
+                            const GridParams& g, const int amin[3], const uint32_t ext[3],
+                            uint8_t* grid, int4* avox, uint32_t* bin_total, int* cursor,
+                            cudaStream_t st, int64_t* launches) {
+  if (V <= 0) return cudaSuccess;
+  int4* tmp = nullptr;
+  VMI_TRY(cudaMallocAsync(&tmp, (size_t)V * sizeof(int4), st));
+  const int T = 256, blocks = (V + T - 1) / T;
+  k_build_grid<<<blocks, T, 0, st>>>(keys, values, V, g, make_int3(amin[0], amin[1], amin[2]),
+                                     make_uint3(ext[0], ext[1], ext[2]), grid, tmp, bin_total);
+  k_bin_offsets<<<1, 32, 0, st>>>(bin_total, g.bins + 1, cursor);
+  k_scatter_by_bin<<<blocks, T, 0, st>>>(tmp, V, cursor, avox);
+  VMI_TRY(cudaFreeAsync(tmp, st));
+  if (launches) *launches += 3;
+  return cudaGetLastError();
+}
+
+// ---- exact histogram + score for one pose ----------------------------------
+__global__ void k_exact_hist(const unsigned long long* keys, const double* values,
+                             const int* nruns, GridParams g, RefView A, unsigned int* ghist) {
+  const int v = blockIdx.x * blockDim.x + threadIdx.x;
+  if (v >= *nruns) return;
+  const unsigned long long k = keys[v];
+  const int x = (int)((k >> 42) & 0x1FFFFF) - (1 << 20);
+  const int y = (int)((k >> 21) & 0x1FFFFF) - (1 << 20);
+  const int z = (int)(k & 0x1FFFFF) - (1 << 20);
+  const uint32_t rx = x - A.amin[0], ry = y - A.amin[1], rz = z - A.amin[2];
+  if (A.empty || !(rx < A.ext[0] && ry < A.ext[1] && rz < A.ext[2])) return;
+  const int W = g.bins + 1;
+  const int ba = A.grid[((size_t)rx * A.ext[1] + ry) * A.ext[2] + rz];
+  const int bb = feature_bin(values[v], g.clamp, g.bins);
+  atomicAdd(&ghist[ba * W + bb], 1u);
+}
+
+constexpr int kScoreThreads = 512;
+
+__global__ void __launch_bounds__(kScoreThreads)
+    k_exact_finalize(const int* bounds, const unsigned int* ghist, GridParams g, RefView A,
+                     int64_t p, double* mi_out, int32_t* status_out, long long* hist_out,
+                     long long* total_out) {
+  __shared__ uint32_t hist[kMaxW * kMaxW];
+  __shared__ uint32_t marg[kMaxW];
+  __shared__ double red[3 * kScoreThreads / 32];
+  __shared__ long long rows[kMaxW], cols[kMaxW], h00;
+  const int W = g.bins + 1;
+  const int tid = threadIdx.x;
+  int status = 0;
+  int rlo[3], rhi[3];
+  long long n_region = 0;
+  if (bounds[6]) status = 2;
+  else if (A.empty) status = 1;
+  else {
+    n_region = 1;
+    for (int j = 0; j < 3; ++j) {
+      rlo[j] = max(A.amin[j], bounds[j]);
+      rhi[j] = min(A.amax[j], bounds[3 + j]);
+      if (rlo[j] > rhi[j]) status = 1;
+      n_region *= (long long)(rhi[j] - rlo[j] + 1);
+    }
+  }
+  if (status != 0) {
+    if (tid == 0) {
+      mi_out[p] = -1e300;
+      status_out[p] = status;
+      if (total_out) total_out[p] = 0;
+    }
+    if (hist_out)
+      for (int i = tid; i < W * W; i += kScoreThreads) hist_out[p * W * W + i] = 0;
+    return;
+  }
+  for (int i = tid; i < W * W; i += kScoreThreads) hist[i] = ghist[i];
+  for (int i = tid; i < W; i += kScoreThreads) marg[i] = 0;
+  __syncthreads();
+  for (int j = tid; j < A.n_avox; j += kScoreThreads) {
+    const int4 v = A.avox[j];
+    const int x = v.x + A.amin[0], y = v.y + A.amin[1], z = v.z + A.amin[2];
+    if (x >= rlo[0] && x <= rhi[0] && y >= rlo[1] && y <= rhi[1] && z >= rlo[2] && z <= rhi[2])
+      atomicAdd(&marg[v.w], 1u);
+  }
+  __syncthreads();
+  MIOut r = finalize_mi<kScoreThreads>(hist, marg, W, n_region, g.include_phi, red, rows, cols, &h00);
+  if (tid == 0) {
+    mi_out[p] = r.status == 0 ? r.mi : -1e300;
+    status_out[p] = r.status;
+    if (total_out) total_out[p] = n_region;
+  }
+  if (hist_out)
+    for (int i = tid; i < W * W; i += kScoreThreads)
+      hist_out[p * W * W + i] = i == 0 ? r.h00 : (long long)hist[i];
+}
+
+cudaError_t exact_score(ExactScratch& s, const GridParams& g, const RefView& A, int64_t p,
+                        double* mi, int32_t* status, long long* hist, long long* total,
+                        cudaStream_t st, int64_t* launches) {
+  const int W = g.bins + 1;
+  VMI_TRY(cudaMemsetAsync(s.ghist, 0, (size_t)W * W * 4, st));
+  const int T = 256;
+  const int blocks = (int)((s.cap_n + T - 1) / T);
+  k_exact_hist<<<blocks, T, 0, st>>>(s.ukeys, s.values, s.nruns, g, A, s.ghist);
+  k_exact_finalize<<<1, kScoreThreads, 0, st>>>(s.bounds, s.ghist, g, A, p, mi, status, hist, total);
+  if (launches) *launches += 2;
+  return cudaGetLastError();
+}
+
+// ---- argmax (np.argmax: first index of the maximum) ---------------------------
+__global__ void k_argmax(const double* v, int64_t P, double* out_val, long long* out_idx) {
+  __shared__ double sv[32];
+  __shared__ long long si[32];
+  double best = -INFINITY;
+  long long bi = LLONG_MAX;
+  for (int64_t i = threadIdx.x; i < P; i += blockDim.x) {
+    const double x = v[i];
+    if (x > best) { best = x; bi = i; }  // strided: first hit per thread is its lowest index
+  }
+  for (int o = 16; o > 0; o >>= 1) {
+    const double ov = __shfl_xor_sync(0xffffffffu, best, o);
+    const long long oi = __shfl_xor_sync(0xffffffffu, bi, o);
+    if (ov > best || (ov == best && oi < bi)) { best = ov; bi = oi; }
+  }
+  if ((threadIdx.x & 31) == 0) { sv[threadIdx.x >> 5] = best; si[threadIdx.x >> 5] = bi; }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    for (int w = 1; w < (int)(blockDim.x >> 5); ++w)
+      if (sv[w] > best || (sv[w] == best && si[w] < bi)) { best = sv[w]; bi = si[w]; }
+    *out_val = best;
+    *out_idx = bi;
+  }
+}
+
+cudaError_t launch_argmax(const double* v, int64_t P, double* out_val, long long* out_idx,
+                          cudaStream_t st) {
+  k_argmax<<<1, 1024, 0, st>>>(v, P, out_val, out_idx);
+  return cudaGetLastError();
+}
+
+// ---- span layout (see QueryView) ------------------------------------------------
+__global__ void k_span_layout(const void* src, int is_f32, int64_t n, int64_t span, int threads,
+                              void* dst) {
+  const int64_t li = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;  // layout index
+  if (li >= span * threads) return;
+  const int64_t r = li / threads, t = li - r * threads;
+  const int64_t i = t * span + r;  // original index
+  if (is_f32) {
+    float4 v = i < n ? reinterpret_cast<const float4*>(src)[i] : make_float4(0.f, 0.f, 0.f, 0.f);
+    reinterpret_cast<float4*>(dst)[li] = v;
+  } else {
+    const double* s = reinterpret_cast<const double*>(src);
+    double* d = reinterpret_cast<double*>(dst) + 4 * li;
+    if (i < n) { d[0] = s[3 * i]; d[1] = s[3 * i + 1]; d[2] = s[3 * i + 2]; }
+    else { d[0] = d[1] = d[2] = 0.0; }
+    d[3] = 0.0;
+  }
+}
+
+cudaError_t launch_span_layout(const void* src, int is_f32, int64_t n, int64_t span, int threads,
+                               void* dst, cudaStream_t st) {
+  const int64_t total = span * threads;
+  const int T = 256;
+  k_span_layout<<<(unsigned)((total + T - 1) / T), T, 0, st>>>(src, is_f32, n, span, threads, dst);
+  return cudaGetLastError();
+}
+
+}  // namespace vmi

@@ -1,0 +1,390 @@
+// k_fast.cu -- K1: fused candidate-pose evaluation (the hot path).
+//
+// One persistent CTA per SM walks poses p = blockIdx.x, +gridDim.x, ...  For
+// each pose it replaces the whole body of mi_objective (reference
+// pkg/src/voxmi/mi.py:194-219):
+//
+//   apply_transform (geometry.py:162-166)   fp64 FMA chain, bit-exact
+//   voxel_indices   (voxel.py:192-207)      DADD.RM floor + key-range check
+//   voxelize bounds (voxel.py:220)          per-thread int min/max, block reduce
+//   compute_feature_map (voxel.py:267-295)  per-thread run aggregation over the
+//                                           ring-ordered span, flushed into a
+//                                           shared-memory open-addressing table
+//                                           keyed by the voxel's index inside
+//                                           A's AABB (only those voxels can be
+//                                           in the overlap region)
+//   compute_overlap (voxel.py:298-318)      from the reduced bounds
+//   build_joint_histogram (mi.py:124-160)   table walk -> A-grid lookup ->
+//                                           shared u32 histogram; A marginal
+//                                           over the region from A's voxel list;
+//                                           phi cells analytically
+//   mutual_information (mi.py:163-191)      fused epilogue (finalize_mi)
+//
+// VARZ is accumulated as (n, S1 = sum(z-K), S2 = sum((z-K)^2)) around a pivot K
+// that is (the float32 rounding of) the z of the first run to reach the slot:
+// within ~1e-14 relative of the reference's two-pass value.  A VARZ value that
+// falls within rounding distance of a bin edge, or a table overflow, marks the
+// pose VMI_FLAG_RECHECK and the host re-evaluates it through the exact
+// sort-based path (k_exact.cu), so histograms stay bit-exact.
+#include <cstdint>
+#include <climits>
+#include <cuda_runtime.h>
+
+#include "vmi_device.cuh"
+#include "vmi_kernels.h"
+
+namespace vmi {
+
+constexpr unsigned long long kEmpty64 = ~0ull;
+constexpr uint32_t kEmpty32 = 0xFFFFFFFFu;
+
+__device__ __forceinline__ uint32_t slot_of(uint32_t lin, uint32_t cap) {
+  return __umulhi(lin * 0x9E3779B1u, cap);
+}
+
+struct VarzTable {
+  unsigned long long* key;  // (lin << 32) | float32 bits of the slot pivot
+  double* s1;
+  double* s2;
+  uint32_t* cnt;
+};
+
+__device__ __forceinline__ void flush_varz(const VarzTable& T, uint32_t cap, uint32_t lin, int n,
+                                           double K, double a1, double a2, int* overflow) {
+  uint32_t s = slot_of(lin, cap);
+  const unsigned long long mine =
+      ((unsigned long long)lin << 32) | __float_as_uint(__double2float_rn(K));
+  unsigned long long w;
+  uint32_t probes = 0;
+  while (true) {
+    w = ((volatile unsigned long long*)T.key)[s];
+    if ((uint32_t)(w >> 32) == lin) break;
+    if (w == kEmpty64) {
+      unsigned long long old = atomicCAS(&T.key[s], kEmpty64, mine);
+      if (old == kEmpty64) { w = mine; break; }
+      if ((uint32_t)(old >> 32) == lin) { w = old; break; }
+    }
+    if (++s == cap) s = 0;
+    if (++probes >= cap) { *overflow = 1; return; }
+  }
+  const double kp = (double)__uint_as_float((uint32_t)w);
+  const double dl = K - kp;
+  const double nd = (double)n;
+  atomicAdd(&T.cnt[s], (uint32_t)n);
+  atomicAdd(&T.s1[s], a1 + nd * dl);
+  atomicAdd(&T.s2[s], a2 + dl * (2.0 * a1 + nd * dl));
+}
+
+__device__ __forceinline__ void flush_count(uint32_t* key, uint32_t* cnt, uint32_t cap,
+                                            uint32_t lin, int n, int* overflow) {
+  uint32_t s = slot_of(lin, cap);
+  uint32_t probes = 0;
+  while (true) {
+    uint32_t w = ((volatile uint32_t*)key)[s];
+    if (w == lin) break;
+    if (w == kEmpty32) {
+      uint32_t old = atomicCAS(&key[s], kEmpty32, lin);
+      if (old == kEmpty32 || old == lin) break;
+    }
+    if (++s == cap) s = 0;
+    if (++probes >= cap) { *overflow = 1; return; }
+  }
+  atomicAdd(&cnt[s], (uint32_t)n);
+}
+
+template <bool F32>
+__device__ __forceinline__ void load_point(const QueryView& B, int64_t idx, double& x, double& y,
+                                           double& z) {
+  if (F32) {
+    float4 v = __ldg(reinterpret_cast<const float4*>(B.pts) + idx);
+    x = (double)v.x; y = (double)v.y; z = (double)v.z;
+  } else {
+    const double2* p = reinterpret_cast<const double2*>(B.pts) + 2 * idx;
+    double2 a = __ldg(p), b = __ldg(p + 1);
+    x = a.x; y = a.y; z = b.x;
+  }
+}
+
+// Shared-memory layout helper (bytes), mirrored by fast_smem_bytes() on the host.
+struct FastSmem {
+  size_t table, hist, marg, red, rows, cols, misc, total;
+};
+__host__ __device__ inline FastSmem fast_layout(int kind, int cap, int W, int threads) {
+  FastSmem L;
+  size_t off = 0;
+  L.table = off;
+  off += (size_t)cap * (kind == 0 ? (8 + 8 + 8 + 4) : (4 + 4));
+  off = (off + 15) & ~size_t(15);
+  L.hist = off; off += (size_t)W * W * 4; off = (off + 15) & ~size_t(15);
+  L.marg = off; off += (size_t)W * 4; off = (off + 15) & ~size_t(15);
+  L.red = off; off += (size_t)3 * (threads / 32) * 8; off = (off + 15) & ~size_t(15);
+  L.rows = off; off += (size_t)W * 8;
+  L.cols = off; off += (size_t)W * 8;
+  L.misc = off; off += 128;
+  L.total = off;
+  return L;
+}
+
+size_t fast_smem_bytes(int kind, int cap, int bins, int threads) {
+  return fast_layout(kind, cap, bins + 1, threads).total;
+}
+
+template <int THREADS, int KIND, bool F32>
+__global__ void __launch_bounds__(THREADS, 1)
+    k_pose_fast(GridParams g, RefView A, QueryView B, const double* __restrict__ mats, int64_t P,
+                int cap, double* __restrict__ mi_out, int32_t* __restrict__ status_out,
+                long long* __restrict__ hist_out, long long* __restrict__ total_out) {
+  extern __shared__ __align__(16) unsigned char smem[];
+  const int W = g.bins + 1;
+  const FastSmem L = fast_layout(KIND, cap, W, THREADS);
+  uint32_t* hist = reinterpret_cast<uint32_t*>(smem + L.hist);
+  uint32_t* marg = reinterpret_cast<uint32_t*>(smem + L.marg);
+  double* red = reinterpret_cast<double*>(smem + L.red);
+  long long* rows = reinterpret_cast<long long*>(smem + L.rows);
+  long long* cols = reinterpret_cast<long long*>(smem + L.cols);
+  int* misc = reinterpret_cast<int*>(smem + L.misc);  // [0..5] bounds, [6] bad, [7] overflow, [8] recheck
+  long long* h00_s = reinterpret_cast<long long*>(smem + L.misc + 64);
+  double* mat_s = reinterpret_cast<double*>(smem + L.red);  // aliases red before the epilogue
+
+  VarzTable VT;
+  uint32_t* ckey = nullptr;
+  uint32_t* ccnt = nullptr;
+  if (KIND == 0) {
+    VT.key = reinterpret_cast<unsigned long long*>(smem + L.table);
+    VT.s1 = reinterpret_cast<double*>(smem + L.table + (size_t)cap * 8);
+    VT.s2 = reinterpret_cast<double*>(smem + L.table + (size_t)cap * 16);
+    VT.cnt = reinterpret_cast<uint32_t*>(smem + L.table + (size_t)cap * 24);
+  } else {
+    ckey = reinterpret_cast<uint32_t*>(smem + L.table);
+    ccnt = reinterpret_cast<uint32_t*>(smem + L.table + (size_t)cap * 4);
+  }
+  const int tid = threadIdx.x;
+  const int lane = tid & 31;
+  const int wid = tid >> 5;
+  const uint32_t ucap = (uint32_t)cap;
+
+  for (int64_t p = blockIdx.x; p < P; p += gridDim.x) {
+    // ---- clear per-pose state -----------------------------------------
+    if (KIND == 0) {
+      for (int s = tid; s < cap; s += THREADS) {
+        VT.key[s] = kEmpty64; VT.s1[s] = 0.0; VT.s2[s] = 0.0; VT.cnt[s] = 0u;
+      }
+    } else {
+      for (int s = tid; s < cap; s += THREADS) { ckey[s] = kEmpty32; ccnt[s] = 0u; }
+    }
+    for (int i = tid; i < W * W; i += THREADS) hist[i] = 0u;
+    for (int i = tid; i < W; i += THREADS) marg[i] = 0u;
+    if (tid < 3) { misc[tid] = INT_MAX; misc[3 + tid] = INT_MIN; }
+    if (tid >= 6 && tid < 9) misc[tid] = 0;
+    if (tid < 12) mat_s[tid] = mats[p * 12 + tid];
+    __syncthreads();
+    const double m0 = mat_s[0], m1 = mat_s[1], m2 = mat_s[2], m3 = mat_s[3], m4 = mat_s[4],
+                 m5 = mat_s[5], m6 = mat_s[6], m7 = mat_s[7], m8 = mat_s[8], t0 = mat_s[9],
+                 t1 = mat_s[10], t2 = mat_s[11];
+
+    // ---- pass over this thread's span of scan B --------------------------
+    int bmin0 = INT_MAX, bmin1 = INT_MAX, bmin2 = INT_MAX;
+    int bmax0 = INT_MIN, bmax1 = INT_MIN, bmax2 = INT_MIN;
+    bool bad = false;
+    uint32_t cur = kNoVoxel;
+    int cn = 0;
+    double cK = 0.0, cs1 = 0.0, cs2 = 0.0;
+    bool has_p = false;
+    uint32_t pl = kNoVoxel;
+    int pn = 0;
+    double pK = 0.0, ps1 = 0.0, ps2 = 0.0;
+    const int64_t span = B.span;
+    const int64_t base = (int64_t)tid * span;
+    for (int64_t r = 0; r < span; ++r) {
+      uint32_t lin = kNoVoxel;
+      double Z = 0.0;
+      if (base + r < B.n) {
+        double x, y, z;
+        load_point<F32>(B, r * THREADS + tid, x, y, z);
+        const double X = xform_row(x, y, z, m0, m1, m2, t0);
+        const double Y = xform_row(x, y, z, m3, m4, m5, t1);
+        Z = xform_row(x, y, z, m6, m7, m8, t2);
+        int ix, iy, iz;
+        bool ok = voxel_coord(X, g.origin[0], g.res, g.inv_res, g.mode, ix);
+        ok &= voxel_coord(Y, g.origin[1], g.res, g.inv_res, g.mode, iy);
+        ok &= voxel_coord(Z, g.origin[2], g.res, g.inv_res, g.mode, iz);
+        bad |= !ok;
+        bmin0 = min(bmin0, ix); bmax0 = max(bmax0, ix);
+        bmin1 = min(bmin1, iy); bmax1 = max(bmax1, iy);
+        bmin2 = min(bmin2, iz); bmax2 = max(bmax2, iz);
+        const uint32_t rx = (uint32_t)(ix - A.amin[0]);
+        const uint32_t ry = (uint32_t)(iy - A.amin[1]);
+        const uint32_t rz = (uint32_t)(iz - A.amin[2]);
+        if (rx < A.ext[0] && ry < A.ext[1] && rz < A.ext[2])
+          lin = (rx * A.ext[1] + ry) * A.ext[2] + rz;
+      }
+      const bool ends = lin != cur;
+      const bool push = ends && cur != kNoVoxel;
+      // warp-converged flush of the one-deep pending queue when any lane needs it
+      if (__any_sync(0xffffffffu, push && has_p)) {
+        if (has_p) {
+          if (KIND == 0) flush_varz(VT, ucap, pl, pn, pK, ps1, ps2, &misc[7]);
+          else flush_count(ckey, ccnt, ucap, pl, pn, &misc[7]);
+          has_p = false;
+        }
+      }
+      if (push) { has_p = true; pl = cur; pn = cn; pK = cK; ps1 = cs1; ps2 = cs2; }
+      if (ends) {
+        cur = lin; cn = 1; cK = Z; cs1 = 0.0; cs2 = 0.0;
+      } else {
+        const double d = Z - cK;
+        ++cn; cs1 += d; cs2 = fma(d, d, cs2);
+      }
+    }
+    if (has_p) {
+      if (KIND == 0) flush_varz(VT, ucap, pl, pn, pK, ps1, ps2, &misc[7]);
+      else flush_count(ckey, ccnt, ucap, pl, pn, &misc[7]);
+    }
+    if (cur != kNoVoxel) {
+      if (KIND == 0) flush_varz(VT, ucap, cur, cn, cK, cs1, cs2, &misc[7]);
+      else flush_count(ckey, ccnt, ucap, cur, cn, &misc[7]);
+    }
+    // ---- reduce bounds / key-range flag ----------------------------------
+    bmin0 = __reduce_min_sync(0xffffffffu, bmin0);
+    bmin1 = __reduce_min_sync(0xffffffffu, bmin1);
+    bmin2 = __reduce_min_sync(0xffffffffu, bmin2);
+    bmax0 = __reduce_max_sync(0xffffffffu, bmax0);
+    bmax1 = __reduce_max_sync(0xffffffffu, bmax1);
+    bmax2 = __reduce_max_sync(0xffffffffu, bmax2);
+    const bool anybad = __any_sync(0xffffffffu, bad);
+    if (lane == 0) {
+      atomicMin(&misc[0], bmin0); atomicMin(&misc[1], bmin1); atomicMin(&misc[2], bmin2);
+      atomicMax(&misc[3], bmax0); atomicMax(&misc[4], bmax1); atomicMax(&misc[5], bmax2);
+      if (anybad) misc[6] = 1;
+    }
+    __syncthreads();
+
+    // ---- overlap region (voxel.py:298-318) -------------------------------
+    int status = 0;
+    int rlo[3], rhi[3];
+    long long n_region = 0;
+    if (misc[6]) {
+      status = 2;  // KEY_RANGE
+    } else if (A.empty) {
+      status = 1;
+    } else {
+      n_region = 1;
+      for (int j = 0; j < 3; ++j) {
+        rlo[j] = max(A.amin[j], misc[j]);
+        rhi[j] = min(A.amax[j], misc[3 + j]);
+        if (rlo[j] > rhi[j]) status = 1;
+        n_region *= (long long)(rhi[j] - rlo[j] + 1);
+      }
+    }
+    if (status != 0) {
+      if (tid == 0) {
+        mi_out[p] = -1e300;
+        status_out[p] = status;
+        if (total_out) total_out[p] = 0;
+      }
+      if (hist_out)
+        for (int i = tid; i < W * W; i += THREADS) hist_out[p * W * W + i] = 0;
+      __syncthreads();
+      continue;
+    }
+
+    // ---- enumerate B voxels (all inside A's AABB, hence in the region) ---
+    const double bins_d = (double)g.bins;
+    bool recheck = false;
+    for (int s = tid; s < cap; s += THREADS) {
+      uint32_t lin;
+      double feat;
+      if (KIND == 0) {
+        const unsigned long long w = VT.key[s];
+        if (w == kEmpty64) continue;
+        lin = (uint32_t)(w >> 32);
+        const double nd = (double)VT.cnt[s];
+        const double S1 = VT.s1[s], S2 = VT.s2[s];
+        const double c1 = S1 * (S1 / nd);
+        const double ssd = S2 - c1;
+        feat = (ssd > 0.0 ? ssd : 0.0) / nd;
+        // rounding-distance guard against a bin edge (see file header)
+        const double x = __dmul_rn(__ddiv_rn(feat, g.clamp), bins_d);
+        const double k = rint(x);
+        if (k >= 1.0 && k <= bins_d - 1.0) {
+          const double tol = ((nd + 8.0) * 4.440892098500626e-16 * (S2 + c1) / nd +
+                              feat * 9.094947017729282e-13) / g.clamp * bins_d + 1e-300;
+          if (fabs(x - k) <= tol) recheck = true;
+        }
+      } else {
+        const uint32_t w = ckey[s];
+        if (w == kEmpty32) continue;
+        lin = w;
+        feat = (double)ccnt[s];
+      }
+      const int bb = feature_bin(feat, g.clamp, g.bins);
+      const int ba = A.grid[lin];
+      atomicAdd(&hist[ba * W + bb], 1u);
+    }
+    if (recheck) misc[8] = 1;
+
+    // ---- A marginal over the region --------------------------------------
+    const bool full = rlo[0] == A.amin[0] && rlo[1] == A.amin[1] && rlo[2] == A.amin[2] &&
+                      rhi[0] == A.amax[0] && rhi[1] == A.amax[1] && rhi[2] == A.amax[2];
+    if (full) {
+      for (int i = tid; i < W; i += THREADS) marg[i] = A.bin_total[i];
+    } else {
+      const int lo0 = rlo[0] - A.amin[0], lo1 = rlo[1] - A.amin[1], lo2 = rlo[2] - A.amin[2];
+      const int hi0 = rhi[0] - A.amin[0], hi1 = rhi[1] - A.amin[1], hi2 = rhi[2] - A.amin[2];
+      for (int j0 = wid * 32; j0 < A.n_avox; j0 += THREADS) {
+        const int j = j0 + lane;
+        bool in = false;
+        int bin = -1;
+        if (j < A.n_avox) {
+          const int4 v = __ldg(&A.avox[j]);
+          bin = v.w;
+          in = v.x >= lo0 && v.x <= hi0 && v.y >= lo1 && v.y <= hi1 && v.z >= lo2 && v.z <= hi2;
+        }
+        const unsigned grp = __match_any_sync(0xffffffffu, bin) & __ballot_sync(0xffffffffu, in);
+        if (in && lane == __ffs(grp) - 1) atomicAdd(&marg[bin], (uint32_t)__popc(grp));
+      }
+    }
+    __syncthreads();
+
+    // ---- analytic phi cells + MI (fused K2) -------------------------------
+    MIOut r = finalize_mi<THREADS>(hist, marg, W, n_region, g.include_phi, red, rows, cols, h00_s);
+    const bool flag = misc[7] || misc[8];
+    if (tid == 0) {
+      mi_out[p] = r.status == 0 ? r.mi : -1e300;
+      status_out[p] = r.status | (flag ? 0x100 : 0);
+      if (total_out) total_out[p] = n_region;
+    }
+    if (hist_out) {
+      for (int i = tid; i < W * W; i += THREADS)
+        hist_out[p * W * W + i] = i == 0 ? r.h00 : (long long)hist[i];
+    }
+    __syncthreads();
+  }
+}
+
+template <int THREADS, int KIND, bool F32>
+static cudaError_t launch_fast_t(const FastLaunch& fl, cudaStream_t st) {
+  auto k = k_pose_fast<THREADS, KIND, F32>;
+  size_t smem = fast_smem_bytes(KIND, fl.cap, fl.g.bins, THREADS);
+  cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  if (e != cudaSuccess) return e;
+  k<<<fl.grid, THREADS, smem, st>>>(fl.g, fl.A, fl.B, fl.mats, fl.P, fl.cap, fl.mi, fl.status,
+                                    fl.hist, fl.total);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_fast(const FastLaunch& fl, cudaStream_t st) {
+  const bool f32 = fl.B.is_f32 != 0;
+  const int kind = fl.g.kind;
+  if (fl.B.threads == 1024) {
+    if (kind == 0) return f32 ? launch_fast_t<1024, 0, true>(fl, st) : launch_fast_t<1024, 0, false>(fl, st);
+    return f32 ? launch_fast_t<1024, 1, true>(fl, st) : launch_fast_t<1024, 1, false>(fl, st);
+  }
+  if (fl.B.threads == 512) {
+    if (kind == 0) return f32 ? launch_fast_t<512, 0, true>(fl, st) : launch_fast_t<512, 0, false>(fl, st);
+    return f32 ? launch_fast_t<512, 1, true>(fl, st) : launch_fast_t<512, 1, false>(fl, st);
+  }
+  return cudaErrorInvalidValue;
+}
+
+}  // namespace vmi

@@ -1,0 +1,586 @@
+// vmi_api.cu -- the C ABI declared in include/vmi.h.
+//
+// Context = one CUDA device + one stream + the resident scan-A grid, scan-B
+// span layout, exact-path scratch and output buffers.  No entry point ever
+// computes on the CPU except vmi_poses_to_mats (glibc sin/cos, pose_host.cpp)
+// and the float32-exactness test of uploaded coordinates.
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <string>
+#include <vector>
+
+#include <cuda_runtime.h>
+
+#include "../../include/vmi.h"
+#include "vmi_kernels.h"
+
+using namespace vmi;
+
+struct vmi_ctx {
+  int device = 0;
+  int sm_count = 0;
+  size_t smem_optin = 0;
+  cudaStream_t stream = nullptr;
+  std::string err;
+  int64_t launches = 0;
+
+  bool params_set = false;
+  GridParams g{};
+
+  // scan A
+  bool a_set = false;
+  bool a_empty = true;
+  int amin[3] = {0, 0, 0}, amax[3] = {0, 0, 0};
+  uint32_t ext[3] = {0, 0, 0};
+  uint8_t* d_grid = nullptr;
+  size_t grid_bytes = 0;
+  int4* d_avox = nullptr;
+  int n_avox = 0;
+  uint32_t* d_bin_total = nullptr;
+  int* d_cursor = nullptr;
+  unsigned long long* d_akeys = nullptr;
+  double* d_avalues = nullptr;
+  int64_t a_nvox = 0;
+
+  // scan B
+  bool b_set = false;
+  void* d_pts = nullptr;
+  int is_f32 = 0;
+  int64_t nb = 0;
+  int64_t span = 0;
+  int threads = 512;
+  int cap_override = 0;
+
+  ExactScratch ex;
+
+  // host-API staging
+  double* d_mats = nullptr;
+  double* d_mi = nullptr;
+  int32_t* d_status = nullptr;
+  long long* d_hist = nullptr;
+  long long* d_total = nullptr;
+  int64_t cap_P = 0;
+  bool hist_alloc = false;
+  double* d_best = nullptr;
+  long long* d_best_idx = nullptr;
+};
+
+namespace {
+
+int fail(vmi_ctx* c, int code, const std::string& msg) {
+  if (c) c->err = msg;
+  return code;
+}
+
+int cuda_fail(vmi_ctx* c, cudaError_t e, const char* where) {
+  return fail(c, VMI_ERR_CUDA, std::string(where) + ": " + cudaGetErrorString(e));
+}
+
+#define CK(ctx, x)                                     \
+  do {                                                 \
+    cudaError_t e_ = (x);                              \
+    if (e_ != cudaSuccess) return cuda_fail(ctx, e_, #x); \
+  } while (0)
+
+void free_a(vmi_ctx* c) {
+  cudaFree(c->d_grid); cudaFree(c->d_avox); cudaFree(c->d_bin_total); cudaFree(c->d_cursor);
+  cudaFree(c->d_akeys); cudaFree(c->d_avalues);
+  c->d_grid = nullptr; c->d_avox = nullptr; c->d_bin_total = nullptr; c->d_cursor = nullptr;
+  c->d_akeys = nullptr; c->d_avalues = nullptr;
+  c->a_set = false; c->n_avox = 0; c->a_nvox = 0; c->grid_bytes = 0;
+}
+
+RefView ref_view(const vmi_ctx* c) {
+  RefView A{};
+  for (int j = 0; j < 3; ++j) { A.amin[j] = c->amin[j]; A.amax[j] = c->amax[j]; A.ext[j] = c->ext[j]; }
+  A.grid = c->d_grid;
+  A.avox = c->d_avox;
+  A.n_avox = c->n_avox;
+  A.empty = c->a_empty ? 1 : 0;
+  A.bin_total = c->d_bin_total;
+  return A;
+}
+
+QueryView query_view(const vmi_ctx* c) {
+  QueryView B{};
+  B.pts = c->d_pts;
+  B.is_f32 = c->is_f32;
+  B.n = c->nb;
+  B.span = c->span;
+  B.threads = c->threads;
+  return B;
+}
+
+int table_cap(const vmi_ctx* c) {
+  if (c->cap_override > 0) return c->cap_override;
+  const size_t fixed = fast_smem_bytes(c->g.kind, 0, c->g.bins, c->threads);
+  const size_t per = c->g.kind == 0 ? 28 : 8;
+  size_t cap = (c->smem_optin - fixed) / per;
+  cap &= ~size_t(31);
+  return (int)cap;
+}
+
+// Grid over A's AABB + voxel list from V (keys, values) already on device.
+int finish_reference(vmi_ctx* c, const int64_t bounds[6], int64_t V) {
+  c->a_empty = V == 0;
+  for (int j = 0; j < 3; ++j) {
+    c->amin[j] = (int)bounds[j];
+    c->amax[j] = (int)bounds[3 + j];
+    if (bounds[j] > bounds[3 + j]) c->a_empty = true;
+  }
+  c->a_nvox = V;
+  CK(c, cudaMalloc(&c->d_bin_total, 4 * kMaxW));
+  CK(c, cudaMemsetAsync(c->d_bin_total, 0, 4 * kMaxW, c->stream));
+  CK(c, cudaMalloc(&c->d_cursor, 4 * kMaxW));
+  if (c->a_empty) {
+    c->a_set = true;
+    return 0;
+  }
+  for (int j = 0; j < 3; ++j) {
+    if (bounds[j] < -(1 << 20) || bounds[3 + j] > (1 << 20) - 1)
+      return fail(c, VMI_ERR_ARG, "reference bounds outside the voxel key range");
+    c->ext[j] = (uint32_t)(bounds[3 + j] - bounds[j] + 1);
+  }
+  const double vol = (double)c->ext[0] * c->ext[1] * c->ext[2];
+  if (vol > 4294967294.0)
+    return fail(c, VMI_ERR_UNSUPPORTED,
+                "scan A's occupied AABB exceeds 2^32-2 voxels (dense reference grid limit)");
+  c->grid_bytes = (size_t)vol;
+  CK(c, cudaMalloc(&c->d_grid, c->grid_bytes));
+  CK(c, cudaMemsetAsync(c->d_grid, 0, c->grid_bytes, c->stream));
+  CK(c, cudaMalloc(&c->d_avox, sizeof(int4) * (V > 0 ? V : 1)));
+  CK(c, build_reference(c->d_akeys, c->d_avalues, (int)V, c->g, c->amin, c->ext, c->d_grid,
+                        c->d_avox, c->d_bin_total, c->d_cursor, c->stream, &c->launches));
+  std::vector<uint32_t> tot(kMaxW);
+  CK(c, cudaMemcpyAsync(tot.data(), c->d_bin_total, 4 * kMaxW, cudaMemcpyDeviceToHost, c->stream));
+  CK(c, cudaStreamSynchronize(c->stream));
+  int64_t s = 0;
+  for (int b = 0; b < kMaxW; ++b) s += tot[b];
+  c->n_avox = (int)s;
+  c->a_set = true;
+  return 0;
+}
+
+int ensure_P(vmi_ctx* c, int64_t P, bool hist) {
+  if (P <= c->cap_P && (!hist || c->hist_alloc)) return 0;
+  int64_t np = P > c->cap_P ? P : c->cap_P;
+  cudaFree(c->d_mats); cudaFree(c->d_mi); cudaFree(c->d_status); cudaFree(c->d_hist);
+  cudaFree(c->d_total);
+  c->d_hist = nullptr;
+  CK(c, cudaMalloc(&c->d_mats, np * 12 * 8));
+  CK(c, cudaMalloc(&c->d_mi, np * 8));
+  CK(c, cudaMalloc(&c->d_status, np * 4));
+  CK(c, cudaMalloc(&c->d_total, np * 8));
+  const bool need_hist = hist || c->hist_alloc;
+  if (need_hist) {
+    const int W = c->g.bins + 1;
+    CK(c, cudaMalloc(&c->d_hist, (size_t)np * W * W * 8));
+  }
+  c->hist_alloc = need_hist;
+  c->cap_P = np;
+  return 0;
+}
+
+int check_ready(vmi_ctx* c) {
+  if (!c) return VMI_ERR_ARG;
+  if (!c->params_set) return fail(c, VMI_ERR_STATE, "vmi_set_params not called");
+  if (!c->a_set) return fail(c, VMI_ERR_STATE, "scan A (reference) not set");
+  if (!c->b_set) return fail(c, VMI_ERR_STATE, "scan B (query) not set");
+  return 0;
+}
+
+int exact_pose(vmi_ctx* c, const double* mat_dev, int64_t p, double* mi, int32_t* st,
+               long long* hist, long long* total) {
+  PointSource src{};
+  src.xyz = nullptr;
+  src.B = query_view(c);
+  src.n = c->nb;
+  CK(c, exact_voxelize(c->ex, src, mat_dev, c->g, c->stream, &c->launches));
+  CK(c, exact_score(c->ex, c->g, ref_view(c), p, mi, st, hist, total, c->stream, &c->launches));
+  return 0;
+}
+
+int launch_fast_eval(vmi_ctx* c, const double* mats_dev, int64_t P, double* mi, int32_t* st,
+                     long long* hist, long long* total, cudaStream_t stream) {
+  if (P <= 0) return 0;
+  FastLaunch fl{};
+  fl.g = c->g;
+  fl.A = ref_view(c);
+  fl.B = query_view(c);
+  fl.mats = mats_dev;
+  fl.P = P;
+  fl.cap = table_cap(c);
+  fl.grid = (int)(P < c->sm_count ? P : c->sm_count);
+  fl.mi = mi;
+  fl.status = st;
+  fl.hist = hist;
+  fl.total = total;
+  CK(c, launch_fast(fl, stream));
+  c->launches += 1;
+  return 0;
+}
+
+int do_fixups(vmi_ctx* c, const double* mats_dev, int64_t P, double* mi, int32_t* st,
+              long long* hist, long long* total, cudaStream_t stream, int64_t* n_fixed) {
+  std::vector<int32_t> hs(P);
+  CK(c, cudaMemcpyAsync(hs.data(), st, P * 4, cudaMemcpyDeviceToHost, stream));
+  CK(c, cudaStreamSynchronize(stream));
+  int64_t nf = 0;
+  cudaStream_t saved = c->stream;
+  c->stream = stream;
+  for (int64_t p = 0; p < P; ++p) {
+    if (hs[p] & VMI_FLAG_RECHECK) {
+      int rc = exact_pose(c, mats_dev + 12 * p, p, mi, st, hist, total);
+      if (rc) { c->stream = saved; return rc; }
+      ++nf;
+    }
+  }
+  c->stream = saved;
+  if (n_fixed) *n_fixed = nf;
+  return 0;
+}
+
+}  // namespace
+
+extern "C" {
+
+const char* vmi_version(void) {
+  return "vmi 0.1 (sm_100a; fast hash path + exact sort path)";
+}
+
+int vmi_create(int device, vmi_ctx** out) {
+  if (!out) return VMI_ERR_ARG;
+  *out = nullptr;
+  int n = 0;
+  cudaError_t e = cudaGetDeviceCount(&n);
+  if (e != cudaSuccess || n <= 0) return VMI_ERR_CUDA;
+  if (device < 0 || device >= n) return VMI_ERR_ARG;
+  vmi_ctx* c = new vmi_ctx();
+  c->device = device;
+  if (cudaSetDevice(device) != cudaSuccess) { delete c; return VMI_ERR_CUDA; }
+  cudaDeviceProp prop;
+  if (cudaGetDeviceProperties(&prop, device) != cudaSuccess) { delete c; return VMI_ERR_CUDA; }
+  if (prop.major < 10) { delete c; return VMI_ERR_UNSUPPORTED; }
+  c->sm_count = prop.multiProcessorCount;
+  int optin = 0;
+  cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, device);
+  c->smem_optin = (size_t)optin;
+  if (cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking) != cudaSuccess) {
+    delete c;
+    return VMI_ERR_CUDA;
+  }
+  cudaMalloc(&c->d_best, 8);
+  cudaMalloc(&c->d_best_idx, 8);
+  *out = c;
+  return 0;
+}
+
+int vmi_destroy(vmi_ctx* c) {
+  if (!c) return 0;
+  cudaSetDevice(c->device);
+  cudaStreamSynchronize(c->stream);
+  free_a(c);
+  cudaFree(c->d_pts);
+  exact_free(c->ex);
+  cudaFree(c->d_mats); cudaFree(c->d_mi); cudaFree(c->d_status); cudaFree(c->d_hist);
+  cudaFree(c->d_total); cudaFree(c->d_best); cudaFree(c->d_best_idx);
+  cudaStreamDestroy(c->stream);
+  delete c;
+  return 0;
+}
+
+const char* vmi_last_error(const vmi_ctx* c) { return c ? c->err.c_str() : "null context"; }
+
+int64_t vmi_launch_count(const vmi_ctx* c) { return c ? c->launches : 0; }
+
+int vmi_set_tuning(vmi_ctx* c, int table_cap_, int threads) {
+  if (!c) return VMI_ERR_ARG;
+  if (threads != 0 && threads != 512 && threads != 1024)
+    return fail(c, VMI_ERR_ARG, "threads must be 512 or 1024");
+  if (table_cap_ < 0) return fail(c, VMI_ERR_ARG, "table_cap must be >= 0");
+  c->cap_override = table_cap_;
+  const int nt = threads ? threads : 512;
+  if (nt != c->threads && c->b_set) return fail(c, VMI_ERR_STATE, "set threads before scan B");
+  c->threads = nt;
+  return 0;
+}
+
+int vmi_set_params(vmi_ctx* c, const double origin[3], double res, int kind, int bins, double clamp,
+                   int include_phi) {
+  if (!c || !origin) return VMI_ERR_ARG;
+  cudaSetDevice(c->device);
+  for (int j = 0; j < 3; ++j)
+    if (!std::isfinite(origin[j])) return fail(c, VMI_ERR_ARG, "grid origin must be finite");
+  if (!(std::isfinite(res) && res > 0)) return fail(c, VMI_ERR_ARG, "grid resolution must be > 0");
+  if (kind != VMI_VARZ && kind != VMI_COUNT) return fail(c, VMI_ERR_ARG, "unknown feature kind");
+  if (bins < 2) return fail(c, VMI_ERR_ARG, "bin_count must be >= 2");
+  if (bins > kMaxW - 1) return fail(c, VMI_ERR_UNSUPPORTED, "bin_count > 64 not supported");
+  if (!(clamp > 0) || !std::isfinite(clamp)) return fail(c, VMI_ERR_ARG, "upper_clamp must be > 0");
+  GridParams g{};
+  for (int j = 0; j < 3; ++j) g.origin[j] = origin[j];
+  g.res = res;
+  int ex = 0;
+  const double mant = std::frexp(res, &ex);
+  const bool pow2 = mant == 0.5;
+  const bool zero_origin = origin[0] == 0.0 && origin[1] == 0.0 && origin[2] == 0.0;
+  g.mode = (zero_origin && res == 1.0) ? kGridUnit : (pow2 ? kGridPow2 : kGridGeneral);
+  g.inv_res = pow2 ? 1.0 / res : 0.0;
+  g.kind = kind;
+  g.bins = bins;
+  g.clamp = clamp;
+  g.include_phi = include_phi ? 1 : 0;
+  const bool grid_changed = !c->params_set || std::memcmp(&c->g, &g, sizeof(double) * 5) != 0 ||
+                            c->g.kind != g.kind || c->g.bins != g.bins || c->g.clamp != g.clamp;
+  c->g = g;
+  c->params_set = true;
+  if (grid_changed && c->a_set) free_a(c);  // A's grid depends on every parameter but phi
+  if (c->hist_alloc) {  // W may have changed
+    cudaFree(c->d_hist);
+    c->d_hist = nullptr;
+    c->hist_alloc = false;
+    c->cap_P = 0;
+  }
+  return 0;
+}
+
+int vmi_set_reference_points(vmi_ctx* c, const double* xyz, int64_t n) {
+  if (!c) return VMI_ERR_ARG;
+  if (!c->params_set) return fail(c, VMI_ERR_STATE, "vmi_set_params not called");
+  if (n <= 0 || !xyz) return fail(c, VMI_ERR_ARG, "cannot voxelize an empty cloud");
+  if (n > 0x7fffffff) return fail(c, VMI_ERR_UNSUPPORTED, "more than 2^31-1 points");
+  cudaSetDevice(c->device);
+  free_a(c);
+  double* d = nullptr;
+  CK(c, cudaMalloc(&d, n * 24));
+  CK(c, cudaMemcpyAsync(d, xyz, n * 24, cudaMemcpyHostToDevice, c->stream));
+  PointSource src{};
+  src.xyz = d;
+  src.n = n;
+  CK(c, exact_voxelize(c->ex, src, nullptr, c->g, c->stream, &c->launches));
+  int h[8];
+  int V = 0;
+  CK(c, cudaMemcpyAsync(h, c->ex.bounds, 7 * 4, cudaMemcpyDeviceToHost, c->stream));
+  CK(c, cudaMemcpyAsync(&V, c->ex.nruns, 4, cudaMemcpyDeviceToHost, c->stream));
+  CK(c, cudaStreamSynchronize(c->stream));
+  cudaFree(d);
+  if (h[6]) return fail(c, VMI_ERR_RANGE, "a point of scan A maps outside the voxel key range");
+  CK(c, cudaMalloc(&c->d_akeys, 8 * (size_t)V));
+  CK(c, cudaMalloc(&c->d_avalues, 8 * (size_t)V));
+  CK(c, cudaMemcpyAsync(c->d_akeys, c->ex.ukeys, 8 * (size_t)V, cudaMemcpyDeviceToDevice, c->stream));
+  CK(c, cudaMemcpyAsync(c->d_avalues, c->ex.values, 8 * (size_t)V, cudaMemcpyDeviceToDevice,
+                        c->stream));
+  int64_t b64[6];
+  for (int j = 0; j < 6; ++j) b64[j] = h[j];
+  return finish_reference(c, b64, V);
+}
+
+int vmi_set_reference_features(vmi_ctx* c, const int64_t* keys, const double* values, int64_t n,
+                               const int64_t bounds[6]) {
+  if (!c || !bounds || n < 0 || (n > 0 && (!keys || !values))) return VMI_ERR_ARG;
+  if (!c->params_set) return fail(c, VMI_ERR_STATE, "vmi_set_params not called");
+  if (n > 0x7fffffff) return fail(c, VMI_ERR_UNSUPPORTED, "more than 2^31-1 voxels");
+  for (int64_t i = 0; i < n; ++i)
+    if (!std::isfinite(values[i]) || values[i] < 0)
+      return fail(c, VMI_ERR_ARG, "features must be finite and >= 0");
+  cudaSetDevice(c->device);
+  free_a(c);
+  const size_t m = n > 0 ? (size_t)n : 1;
+  CK(c, cudaMalloc(&c->d_akeys, 8 * m));
+  CK(c, cudaMalloc(&c->d_avalues, 8 * m));
+  if (n > 0) {
+    CK(c, cudaMemcpyAsync(c->d_akeys, keys, 8 * n, cudaMemcpyHostToDevice, c->stream));
+    CK(c, cudaMemcpyAsync(c->d_avalues, values, 8 * n, cudaMemcpyHostToDevice, c->stream));
+  }
+  return finish_reference(c, bounds, n);
+}
+
+int vmi_get_reference_features(vmi_ctx* c, int64_t* keys, double* values, int64_t cap,
+                               int64_t* n_out, int64_t bounds[6]) {
+  if (!c) return VMI_ERR_ARG;
+  if (!c->a_set) return fail(c, VMI_ERR_STATE, "scan A (reference) not set");
+  cudaSetDevice(c->device);
+  if (n_out) *n_out = c->a_nvox;
+  if (bounds)
+    for (int j = 0; j < 3; ++j) { bounds[j] = c->amin[j]; bounds[3 + j] = c->amax[j]; }
+  if (!keys) return 0;
+  if (cap < c->a_nvox) return fail(c, VMI_ERR_ARG, "output capacity too small");
+  if (c->a_nvox > 0) {
+    CK(c, cudaMemcpyAsync(keys, c->d_akeys, 8 * c->a_nvox, cudaMemcpyDeviceToHost, c->stream));
+    if (values)
+      CK(c, cudaMemcpyAsync(values, c->d_avalues, 8 * c->a_nvox, cudaMemcpyDeviceToHost, c->stream));
+  }
+  CK(c, cudaStreamSynchronize(c->stream));
+  return 0;
+}
+
+static bool f32_exact(double v) { return (double)(float)v == v; }
+
+static int set_query(vmi_ctx* c, const void* host, int is_f32_src, int64_t n) {
+  if (!c) return VMI_ERR_ARG;
+  if (n <= 0 || !host) return fail(c, VMI_ERR_ARG, "cannot voxelize an empty cloud");
+  if (n > 0x7fffffff) return fail(c, VMI_ERR_UNSUPPORTED, "more than 2^31-1 points");
+  cudaSetDevice(c->device);
+  cudaFree(c->d_pts);
+  c->d_pts = nullptr;
+  c->b_set = false;
+  int as_f32 = 1;
+  std::vector<float> f4;
+  const void* up = host;
+  size_t up_bytes;
+  if (is_f32_src) {
+    up_bytes = (size_t)n * 16;
+  } else {
+    const double* xyz = static_cast<const double*>(host);
+    for (int64_t i = 0; i < 3 * n && as_f32; ++i) as_f32 = f32_exact(xyz[i]);
+    if (as_f32) {
+      f4.resize((size_t)n * 4);
+      for (int64_t i = 0; i < n; ++i) {
+        f4[4 * i] = (float)xyz[3 * i];
+        f4[4 * i + 1] = (float)xyz[3 * i + 1];
+        f4[4 * i + 2] = (float)xyz[3 * i + 2];
+        f4[4 * i + 3] = 0.f;
+      }
+      up = f4.data();
+      up_bytes = (size_t)n * 16;
+    } else {
+      up_bytes = (size_t)n * 24;
+    }
+  }
+  void* tmp = nullptr;
+  CK(c, cudaMalloc(&tmp, up_bytes));
+  CK(c, cudaMemcpyAsync(tmp, up, up_bytes, cudaMemcpyHostToDevice, c->stream));
+  c->span = (n + c->threads - 1) / c->threads;
+  const size_t rec = as_f32 ? 16 : 32;
+  CK(c, cudaMalloc(&c->d_pts, (size_t)c->span * c->threads * rec));
+  CK(c, launch_span_layout(tmp, as_f32, n, c->span, c->threads, c->d_pts, c->stream));
+  c->launches += 1;
+  CK(c, cudaStreamSynchronize(c->stream));
+  cudaFree(tmp);
+  c->is_f32 = as_f32;
+  c->nb = n;
+  c->b_set = true;
+  return 0;
+}
+
+int vmi_set_query_points(vmi_ctx* c, const double* xyz, int64_t n) { return set_query(c, xyz, 0, n); }
+
+int vmi_set_query_records_f32(vmi_ctx* c, const float* xyzi, int64_t n) {
+  if (c && xyzi) {
+    for (int64_t i = 0; i < n; ++i)
+      for (int j = 0; j < 3; ++j)
+        if (!std::isfinite(xyzi[4 * i + j])) return fail(c, VMI_ERR_ARG, "points contain non-finite coordinates");
+  }
+  return set_query(c, xyzi, 1, n);
+}
+
+int vmi_eval_device(vmi_ctx* c, const double* mats_dev, int64_t P, double* mi_dev,
+                    int32_t* status_dev, int64_t* hist_dev, int64_t* total_dev, void* stream) {
+  int rc = check_ready(c);
+  if (rc) return rc;
+  if (P < 0 || (P > 0 && (!mats_dev || !mi_dev || !status_dev))) return fail(c, VMI_ERR_ARG, "bad arguments");
+  cudaSetDevice(c->device);
+  return launch_fast_eval(c, mats_dev, P, mi_dev, status_dev, (long long*)hist_dev,
+                          (long long*)total_dev, stream ? (cudaStream_t)stream : c->stream);
+}
+
+int vmi_eval_fixups(vmi_ctx* c, const double* mats_dev, int64_t P, double* mi_dev,
+                    int32_t* status_dev, int64_t* hist_dev, int64_t* total_dev, void* stream,
+                    int64_t* n_fixed) {
+  int rc = check_ready(c);
+  if (rc) return rc;
+  cudaSetDevice(c->device);
+  return do_fixups(c, mats_dev, P, mi_dev, status_dev, (long long*)hist_dev, (long long*)total_dev,
+                   stream ? (cudaStream_t)stream : c->stream, n_fixed);
+}
+
+int vmi_eval(vmi_ctx* c, const double* mats, int64_t P, double* mi_out, int32_t* status_out,
+             int64_t* hist_out, int64_t* total_out) {
+  int rc = check_ready(c);
+  if (rc) return rc;
+  if (P < 0 || (P > 0 && (!mats || !mi_out || !status_out))) return fail(c, VMI_ERR_ARG, "bad arguments");
+  if (P == 0) return 0;
+  cudaSetDevice(c->device);
+  if ((rc = ensure_P(c, P, hist_out != nullptr))) return rc;
+  long long* dh = hist_out ? c->d_hist : nullptr;
+  CK(c, cudaMemcpyAsync(c->d_mats, mats, P * 96, cudaMemcpyHostToDevice, c->stream));
+  if ((rc = launch_fast_eval(c, c->d_mats, P, c->d_mi, c->d_status, dh, c->d_total, c->stream))) return rc;
+  if ((rc = do_fixups(c, c->d_mats, P, c->d_mi, c->d_status, dh, c->d_total, c->stream, nullptr))) return rc;
+  CK(c, cudaMemcpyAsync(mi_out, c->d_mi, P * 8, cudaMemcpyDeviceToHost, c->stream));
+  CK(c, cudaMemcpyAsync(status_out, c->d_status, P * 4, cudaMemcpyDeviceToHost, c->stream));
+  if (hist_out) {
+    const int W = c->g.bins + 1;
+    CK(c, cudaMemcpyAsync(hist_out, dh, (size_t)P * W * W * 8, cudaMemcpyDeviceToHost, c->stream));
+  }
+  if (total_out) CK(c, cudaMemcpyAsync(total_out, c->d_total, P * 8, cudaMemcpyDeviceToHost, c->stream));
+  CK(c, cudaStreamSynchronize(c->stream));
+  return 0;
+}
+
+int vmi_eval_exact(vmi_ctx* c, const double* mats, int64_t P, double* mi_out, int32_t* status_out,
+                   int64_t* hist_out, int64_t* total_out) {
+  int rc = check_ready(c);
+  if (rc) return rc;
+  if (P < 0 || (P > 0 && (!mats || !mi_out || !status_out))) return fail(c, VMI_ERR_ARG, "bad arguments");
+  if (P == 0) return 0;
+  cudaSetDevice(c->device);
+  if ((rc = ensure_P(c, P, hist_out != nullptr))) return rc;
+  long long* dh = hist_out ? c->d_hist : nullptr;
+  CK(c, cudaMemcpyAsync(c->d_mats, mats, P * 96, cudaMemcpyHostToDevice, c->stream));
+  for (int64_t p = 0; p < P; ++p)
+    if ((rc = exact_pose(c, c->d_mats + 12 * p, p, c->d_mi, c->d_status, dh, c->d_total))) return rc;
+  CK(c, cudaMemcpyAsync(mi_out, c->d_mi, P * 8, cudaMemcpyDeviceToHost, c->stream));
+  CK(c, cudaMemcpyAsync(status_out, c->d_status, P * 4, cudaMemcpyDeviceToHost, c->stream));
+  if (hist_out) {
+    const int W = c->g.bins + 1;
+    CK(c, cudaMemcpyAsync(hist_out, dh, (size_t)P * W * W * 8, cudaMemcpyDeviceToHost, c->stream));
+  }
+  if (total_out) CK(c, cudaMemcpyAsync(total_out, c->d_total, P * 8, cudaMemcpyDeviceToHost, c->stream));
+  CK(c, cudaStreamSynchronize(c->stream));
+  return 0;
+}
+
+int vmi_query_features(vmi_ctx* c, const double mat[12], int64_t* keys, double* values, int64_t cap,
+                       int64_t* n_out, int64_t bounds[6], int32_t* status) {
+  if (!c || !mat) return VMI_ERR_ARG;
+  if (!c->params_set || !c->b_set) return fail(c, VMI_ERR_STATE, "params and scan B must be set");
+  cudaSetDevice(c->device);
+  int rc;
+  if ((rc = ensure_P(c, 1, false))) return rc;
+  CK(c, cudaMemcpyAsync(c->d_mats, mat, 96, cudaMemcpyHostToDevice, c->stream));
+  PointSource src{};
+  src.B = query_view(c);
+  src.n = c->nb;
+  CK(c, exact_voxelize(c->ex, src, c->d_mats, c->g, c->stream, &c->launches));
+  int h[8];
+  int V = 0;
+  CK(c, cudaMemcpyAsync(h, c->ex.bounds, 7 * 4, cudaMemcpyDeviceToHost, c->stream));
+  CK(c, cudaMemcpyAsync(&V, c->ex.nruns, 4, cudaMemcpyDeviceToHost, c->stream));
+  CK(c, cudaStreamSynchronize(c->stream));
+  if (status) *status = h[6] ? VMI_KEY_RANGE : VMI_OK;
+  if (n_out) *n_out = V;
+  if (bounds)
+    for (int j = 0; j < 6; ++j) bounds[j] = h[j];
+  if (h[6] || !keys) return 0;
+  if (cap < V) return fail(c, VMI_ERR_ARG, "output capacity too small");
+  CK(c, cudaMemcpyAsync(keys, c->ex.ukeys, 8 * (size_t)V, cudaMemcpyDeviceToHost, c->stream));
+  if (values)
+    CK(c, cudaMemcpyAsync(values, c->ex.values, 8 * (size_t)V, cudaMemcpyDeviceToHost, c->stream));
+  CK(c, cudaStreamSynchronize(c->stream));
+  return 0;
+}
+
+int vmi_argmax_device(vmi_ctx* c, const double* mi_dev, int64_t P, double* best_mi,
+                      int64_t* best_idx, void* stream) {
+  if (!c || !mi_dev || P <= 0 || !best_mi || !best_idx) return VMI_ERR_ARG;
+  cudaSetDevice(c->device);
+  cudaStream_t st = stream ? (cudaStream_t)stream : c->stream;
+  CK(c, launch_argmax(mi_dev, P, c->d_best, c->d_best_idx, st));
+  c->launches += 1;
+  CK(c, cudaMemcpyAsync(best_mi, c->d_best, 8, cudaMemcpyDeviceToHost, st));
+  CK(c, cudaMemcpyAsync(best_idx, c->d_best_idx, 8, cudaMemcpyDeviceToHost, st));
+  CK(c, cudaStreamSynchronize(st));
+  return 0;
+}
+
+}  // extern "C"

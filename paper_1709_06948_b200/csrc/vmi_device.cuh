@@ -1,0 +1,208 @@
+// vmi_device.cuh -- device-side building blocks shared by the fast (hash) and
+// exact (sort) pose-evaluation paths.  Every floating-point step that the
+// reference's bit pattern depends on is written with explicit-rounding
+// intrinsics so nvcc's FMA contraction can never change it.
+#pragma once
+#include <cstdint>
+#include <cuda_runtime.h>
+
+#include "vmi_types.h"
+
+namespace vmi {
+
+constexpr uint32_t kNoVoxel = 0xFFFFFFFFu;
+constexpr int kKeyMin = -(1 << 20);
+constexpr int kKeyMax = (1 << 20) - 1;
+
+
+// ---- geometry.py:162-166: numpy `points @ R.T + t` through OpenBLAS dgemm is,
+// bit for bit, fma(z, R[j][2], fma(y, R[j][1], x * R[j][0])) + t[j].
+__device__ __forceinline__ double xform_row(double x, double y, double z, double r0, double r1,
+                                            double r2, double t) {
+  return __dadd_rn(__fma_rn(z, r2, __fma_rn(y, r1, __dmul_rn(x, r0))), t);
+}
+
+// ---- voxel.py:199: floor((p - origin) / resolution) -> int64, then the
+// key-range test of voxel.py:200.  The floor is DADD.RM against 1.5*2^52: the
+// result's bit pattern minus the magic's is floor(q) for |q| < 2^51, and lands
+// far outside the key range otherwise (incl. inf/nan), so one compare covers
+// OutOfBoundsError.  Returns false when out of the key range.
+__device__ __forceinline__ bool voxel_coord(double p, double origin, double res, double inv_res,
+                                            int mode, int& out) {
+  double v = (mode == kGridUnit) ? p : __dsub_rn(p, origin);
+  double q;
+  if (mode == kGridUnit) q = v;
+  else if (mode == kGridPow2) q = __dmul_rn(v, inv_res);  // exact: same real number as v/res
+  else q = __ddiv_rn(v, res);
+  const double magic = 6755399441055744.0;  // 1.5 * 2^52
+  double r = __dadd_rd(q, magic);
+  long long k = __double_as_longlong(r) - __double_as_longlong(magic);
+  out = (int)k;
+  return (unsigned long long)(k - kKeyMin) <= (unsigned long long)(kKeyMax - kKeyMin);
+}
+
+// ---- mi.py:72-79 bin_features: 1 + min(B-1, floor(v / clamp * B))
+__device__ __forceinline__ int feature_bin(double v, double clamp, int bins) {
+  double x = __dmul_rn(__ddiv_rn(v, clamp), (double)bins);
+  double f = floor(x);
+  int raw = f >= (double)(bins - 1) ? bins - 1 : (int)f;
+  return 1 + raw;
+}
+
+// numpy pairwise_sum (loops_utils.h.src) over f(lo .. lo+n-1); F(i) -> double.
+template <typename F>
+__device__ double pairwise_sum(const F& f, int64_t lo, int64_t n) {
+  // The reference recursion (split at n2 = n/2 - (n/2)%8, left + right) run
+  // post-order on an explicit stack; depth <= 26 for n < 2^32.
+  struct Frame { int64_t lo, n; int state; double left; };
+  Frame fr[32];
+  int sp = 0;
+  fr[0] = {lo, n, 0, 0.0};
+  double ret = 0.0;
+  while (sp >= 0) {
+    Frame& cur = fr[sp];
+    if (cur.n > 128) {  // split: evaluate the left half first
+      int64_t n2 = cur.n / 2;
+      n2 -= n2 % 8;
+      cur.state = 1;
+      fr[sp + 1] = {cur.lo, n2, 0, 0.0};
+      ++sp;
+      continue;
+    }
+    if (cur.n < 8) {
+      ret = 0.0;
+      for (int64_t i = 0; i < cur.n; ++i) ret = __dadd_rn(ret, f(cur.lo + i));
+    } else {
+      double r[8];
+#pragma unroll
+      for (int j = 0; j < 8; ++j) r[j] = f(cur.lo + j);
+      int64_t i = 8;
+      for (; i < cur.n - (cur.n % 8); i += 8) {
+#pragma unroll
+        for (int j = 0; j < 8; ++j) r[j] = __dadd_rn(r[j], f(cur.lo + i + j));
+      }
+      ret = __dadd_rn(__dadd_rn(__dadd_rn(r[0], r[1]), __dadd_rn(r[2], r[3])),
+                      __dadd_rn(__dadd_rn(r[4], r[5]), __dadd_rn(r[6], r[7])));
+      for (; i < cur.n; ++i) ret = __dadd_rn(ret, f(cur.lo + i));
+    }
+    --sp;
+    while (sp >= 0) {  // hand the finished block to its parent
+      Frame& par = fr[sp];
+      if (par.state == 1) {
+        par.left = ret;
+        par.state = 2;
+        int64_t n2 = par.n / 2;
+        n2 -= n2 % 8;
+        fr[sp + 1] = {par.lo + n2, par.n - n2, 0, 0.0};
+        ++sp;
+        break;
+      }
+      ret = __dadd_rn(par.left, ret);
+      --sp;
+    }
+  }
+  return ret;
+}
+
+// np.add.reduceat segment: a[lo] + pairwise(a[lo+1 : hi])  (voxel.py:225-229)
+template <typename F>
+__device__ __forceinline__ double segment_sum(const F& f, int64_t lo, int64_t hi) {
+  if (hi - lo == 1) return f(lo);
+  return __dadd_rn(f(lo), pairwise_sum(f, lo + 1, hi - lo - 1));
+}
+
+// ---- block-wide helpers -------------------------------------------------
+__device__ __forceinline__ double warp_sum(double v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  return v;
+}
+
+// ---- Histogram finalisation + MI (mi.py:124-160 analytic cells, :163-191).
+// hist: (W x W) u32 in shared memory holding the enumerated cells (every B
+// voxel inside the region, binned against A's grid); marg: per-A-bin count of
+// A voxels inside the region.  Fills column 0 of rows >= 1 and cell (0,0),
+// then computes entropies.  Must be called by all threads of the block.
+struct MIOut {
+  double mi, hx, hy, hxy;
+  int status;
+  long long h00;
+};
+
+template <int THREADS>
+__device__ MIOut finalize_mi(uint32_t* hist, const uint32_t* marg, int W, long long n_region,
+                             int include_phi, double* red /* >= 3*THREADS/32 doubles */,
+                             long long* rows /* W */, long long* cols /* W */,
+                             long long* h00_s /* 1 */) {
+  const int tid = threadIdx.x;
+  // rows a >= 1: A-only voxels pair with the phi column (mi.py:146-156)
+  for (int a = 1 + tid; a < W; a += THREADS) {
+    uint32_t occ = 0;
+    for (int b = 1; b < W; ++b) occ += hist[a * W + b];
+    hist[a * W] = marg[a] - occ;
+  }
+  __syncthreads();
+  if (tid == 0) {
+    long long s = 0;
+    for (int a = 1; a < W; ++a) s += marg[a];
+    for (int b = 1; b < W; ++b) s += hist[b];
+    *h00_s = n_region - s;  // mi.py:158-159
+  }
+  __syncthreads();
+  const long long h00 = *h00_s;
+  const int o = include_phi ? 0 : 1;
+  const int m = W - o;
+  // exact int64 marginals (m.sum(axis=1), m.sum(axis=0))
+  for (int a = tid; a < m; a += THREADS) {
+    long long rs = 0, cs = 0;
+    for (int b = 0; b < m; ++b) {
+      int ra = a + o, cb = b + o;
+      rs += (ra == 0 && cb == 0) ? h00 : (long long)hist[ra * W + cb];
+      cs += (cb == 0 && ra == 0) ? h00 : (long long)hist[cb * W + ra];
+    }
+    rows[a] = rs;
+    cols[a] = cs;
+  }
+  __syncthreads();
+  long long total = 0;
+  for (int a = 0; a < m; ++a) total += rows[a];
+  MIOut out;
+  out.h00 = h00;
+  if (total <= 0) {  // entropy of an all-zero block raises -> sentinel (mi.py:215-219)
+    out.status = 3;
+    out.mi = out.hx = out.hy = out.hxy = 0.0;
+    return out;
+  }
+  const double tot = (double)total;
+  double sx = 0.0, sy = 0.0, sxy = 0.0;
+  for (int i = tid; i < m * m; i += THREADS) {
+    int a = i / m + o, b = i % m + o;
+    long long c = (a == 0 && b == 0) ? h00 : (long long)hist[a * W + b];
+    if (c > 0) {
+      double p = (double)c / tot;
+      sxy += p * log(p);
+    }
+  }
+  for (int i = tid; i < m; i += THREADS) {
+    if (rows[i] > 0) { double p = (double)rows[i] / tot; sx += p * log(p); }
+    if (cols[i] > 0) { double p = (double)cols[i] / tot; sy += p * log(p); }
+  }
+  sx = warp_sum(sx);
+  sy = warp_sum(sy);
+  sxy = warp_sum(sxy);
+  const int wid = tid >> 5, lane = tid & 31;
+  constexpr int NW = THREADS / 32;
+  __syncthreads();
+  if (lane == 0) { red[wid] = sx; red[NW + wid] = sy; red[2 * NW + wid] = sxy; }
+  __syncthreads();
+  double hx = 0.0, hy = 0.0, hxy = 0.0;
+  for (int w = 0; w < NW; ++w) { hx += red[w]; hy += red[NW + w]; hxy += red[2 * NW + w]; }
+  hx = -hx; hy = -hy; hxy = -hxy;
+  double mi = hx + hy - hxy;
+  if (mi >= -1e-12 && mi < 0.0) mi = 0.0;  // mi.py:189-190
+  out.status = 0;
+  out.mi = mi; out.hx = hx; out.hy = hy; out.hxy = hxy;
+  return out;
+}
+
+}  // namespace vmi

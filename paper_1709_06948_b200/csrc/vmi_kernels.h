@@ -1,0 +1,86 @@
+// vmi_kernels.h -- host-side launchers for the device kernels.
+#pragma once
+#include <cstddef>
+#include <cstdint>
+#include <cuda_runtime.h>
+
+#include "vmi_types.h"
+
+namespace vmi {
+
+// ---- K1 fast path (k_fast.cu) ---------------------------------------------
+struct FastLaunch {
+  GridParams g;
+  RefView A;
+  QueryView B;
+  const double* mats;
+  int64_t P;
+  int cap;
+  int grid;
+  double* mi;
+  int32_t* status;
+  long long* hist;
+  long long* total;
+};
+size_t fast_smem_bytes(int kind, int cap, int bins, int threads);
+cudaError_t launch_fast(const FastLaunch& fl, cudaStream_t st);
+
+// ---- exact sort-based path (k_exact.cu) -------------------------------------
+// Scratch for voxelizing up to `cap_n` points at once.
+struct ExactScratch {
+  int64_t cap_n = 0;
+  unsigned long long* keys = nullptr;
+  unsigned long long* keys_sorted = nullptr;
+  int* idx = nullptr;
+  int* idx_sorted = nullptr;
+  double* z = nullptr;
+  double* zs = nullptr;
+  unsigned long long* ukeys = nullptr;
+  int* counts = nullptr;
+  int* offsets = nullptr;
+  double* values = nullptr;
+  int* nruns = nullptr;   // device scalar
+  int* bounds = nullptr;  // device [6] + [6]=bad flag
+  unsigned int* ghist = nullptr;  // (65*65)
+  void* cub_tmp = nullptr;
+  size_t cub_bytes = 0;
+};
+cudaError_t exact_alloc(ExactScratch& s, int64_t n);
+void exact_free(ExactScratch& s);
+
+// Point sources for the exact path.
+struct PointSource {
+  const double* xyz;  // contiguous (n, 3) doubles, or nullptr to use B
+  QueryView B;
+  int64_t n;
+};
+
+// voxelize + compute_feature_map of `src` under `mat` (device ptr, 12 f64;
+// nullptr = raw points, as _prepare does for scan A).  Asynchronous; on
+// return the device holds: s.ukeys[0..V), s.values[0..V), *s.nruns = V,
+// s.bounds[0..5], s.bounds[6] = key-range flag.  Launch count added to *launches.
+cudaError_t exact_voxelize(ExactScratch& s, const PointSource& src, const double* mat,
+                           const GridParams& g, cudaStream_t st, int64_t* launches);
+
+// Build A's dense bin grid and sorted voxel list from V feature-map entries
+// (keys + values on device).  grid must be zeroed, ext-sized.
+cudaError_t build_reference(const unsigned long long* keys, const double* values, int V,
+                            const GridParams& g, const int amin[3], const uint32_t ext[3],
+                            uint8_t* grid, int4* avox, uint32_t* bin_total, int* cursor,
+                            cudaStream_t st, int64_t* launches);
+
+// Histogram + finalisation + MI for pose p from an exact voxelization held in
+// s (after exact_voxelize).  Writes mi[p], status[p], hist[p], total[p].
+cudaError_t exact_score(ExactScratch& s, const GridParams& g, const RefView& A, int64_t p,
+                        double* mi, int32_t* status, long long* hist, long long* total,
+                        cudaStream_t st, int64_t* launches);
+
+// First-max argmax (np.argmax) over P doubles -> out[0] = value, out_idx[0] = index.
+cudaError_t launch_argmax(const double* v, int64_t P, double* out_val, long long* out_idx,
+                          cudaStream_t st);
+
+// Reorder contiguous points into the fast path's span layout.
+cudaError_t launch_span_layout(const void* src, int is_f32, int64_t n, int64_t span, int threads,
+                               void* dst, cudaStream_t st);
+
+}  // namespace vmi

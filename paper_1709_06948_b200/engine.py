@@ -1,0 +1,173 @@
+"""MIEngine: resident scan pair on one B200, batched candidate-pose scoring.
+
+This is the host side of the hot path.  It owns one native context
+(libvmi.so) per device and replaces, for a batch of P poses, P calls of the
+reference's ``mi_objective`` (mi.py:194-219) made by ``align``'s objective
+closure (align.py:134-136) and ``sweep_axis`` (align.py:191-197):
+
+* ``set_reference``  -- _prepare (align.py:114-119): scan A voxelized and
+  featurized ON THE GPU (exact sort-based path), or an existing FeatureMap
+  uploaded as is; kept resident as a dense u8 bin grid.
+* ``set_query``      -- scan B uploaded once, in the kernel's span layout.
+* ``evaluate``       -- one fused kernel over all poses (k_fast.cu), then an
+  exact re-evaluation of the rare flagged poses (k_exact.cu).
+* ``best``           -- np.argmax semantics (first max, cli.py:202), with exact
+  host re-scoring of near-ties from their bit-exact GPU histograms.
+"""
+
+from __future__ import annotations
+
+import numpy as np
+
+from . import _lib
+from .errors import OutOfBoundsError
+from .geometry import PointCloud, as_pose_array
+from .types import (NO_OVERLAP_SENTINEL, BinningSpec, FeatureKind, FeatureMap, GridSpec, as_kind)
+
+
+def _points_of(cloud) -> np.ndarray:
+    pts = getattr(cloud, "points", cloud)
+    pts = np.asarray(pts)
+    if pts.ndim != 2 or pts.shape[1] not in (3, 4):
+        raise ValueError(f"points must be (N, 3), got shape {pts.shape}")
+    return pts
+
+
+def entropy_exact(counts) -> float:
+    """The reference's entropy (mi.py:163-174) on the host, bit for bit.
+
+    Used only to break near-ties between candidate poses from their GPU
+    histograms; the sort makes the result independent of cell order.
+    """
+    arr = np.asarray(counts, dtype=np.float64).ravel()
+    total = arr.sum()
+    if not total > 0:
+        raise ValueError("entropy of an all-zero distribution is undefined")
+    p = arr[arr > 0] / total
+    return float(-np.sort(p * np.log(p)).sum())
+
+
+def mutual_information_exact(counts, include_phi: bool = True) -> tuple[float, float, float, float]:
+    """(mi, h_x, h_y, h_xy) of a joint histogram, mi.py:177-191 semantics."""
+    c = np.asarray(counts)
+    m = c if include_phi else c[1:, 1:]
+    h_x = entropy_exact(m.sum(axis=1))
+    h_y = entropy_exact(m.sum(axis=0))
+    h_xy = entropy_exact(m)
+    mi = h_x + h_y - h_xy
+    if -1e-12 <= mi < 0.0:
+        mi = 0.0
+    return mi, h_x, h_y, h_xy
+
+
+class MIEngine:
+    """Batched MI pose evaluation on one GPU.
+
+    ``grid``/``binning`` take this package's GridSpec/BinningSpec or the
+    reference's own objects (duck-typed).
+    """
+
+    def __init__(self, grid=None, binning=None, kind=None, include_phi: bool = True,
+                 device: int = 0, threads: int = 0, table_cap: int = 0):
+        grid = grid if grid is not None else GridSpec()
+        if binning is None:
+            binning = BinningSpec(kind=as_kind(kind) if kind is not None else FeatureKind.VARZ)
+        self.kind = as_kind(binning.kind)
+        if kind is not None and as_kind(kind) is not self.kind:
+            raise ValueError("feature map and binning spec must share one kind")
+        self.bins = int(binning.bin_count)
+        self.clamp = float(binning.upper_clamp)
+        self.origin = np.asarray(grid.origin, dtype=np.float64).reshape(3)
+        self.resolution = float(grid.resolution)
+        self.include_phi = bool(include_phi)
+        self.ctx = _lib.Context(device)
+        self.ctx.set_tuning(table_cap=table_cap, threads=threads)
+        self.ctx.set_params(self.origin, self.resolution, self.kind.code, self.bins, self.clamp,
+                            self.include_phi)
+        self._feat_a: FeatureMap | None = None
+
+    # ---- scan A ---------------------------------------------------------------
+    def set_reference(self, scan_a) -> FeatureMap:
+        """Voxelize + featurize scan A on the GPU (bit-exact), keep it resident."""
+        pts = _points_of(scan_a)[:, :3]
+        if pts.shape[0] == 0:
+            raise ValueError("cannot voxelize an empty cloud")
+        self.ctx.set_reference_points(pts)
+        keys, vals, bounds = self.ctx.get_reference_features()
+        self._feat_a = FeatureMap(kind=self.kind, keys=keys, values=vals, bounds=bounds)
+        return self._feat_a
+
+    def set_reference_features(self, feat_a) -> None:
+        """Upload an existing FeatureMap (this package's or the reference's)."""
+        if as_kind(feat_a.kind) is not self.kind:
+            raise ValueError("feature map and binning spec must share one kind")
+        self.ctx.set_reference_features(feat_a.keys, feat_a.values, feat_a.bounds)
+        self._feat_a = feat_a
+
+    @property
+    def reference(self) -> FeatureMap | None:
+        return self._feat_a
+
+    # ---- scan B ---------------------------------------------------------------
+    def set_query(self, scan_b) -> None:
+        pts = _points_of(scan_b)
+        if pts.shape[0] == 0:
+            raise ValueError("cannot voxelize an empty cloud")
+        if pts.dtype == np.float32 and pts.shape[1] == 4:
+            self.ctx.set_query_records(pts)  # KITTI .bin records, float4 as is
+        else:
+            self.ctx.set_query_points(np.asarray(pts[:, :3], dtype=np.float64))
+
+    # ---- scoring --------------------------------------------------------------
+    @staticmethod
+    def mats(poses) -> np.ndarray:
+        return _lib.poses_to_mats(as_pose_array(poses))
+
+    def evaluate(self, poses, histograms: bool = False, exact: bool = False):
+        """Score P poses.  Returns (mi[P], status[P]) or, with histograms=True,
+        (mi, status, counts[P, B+1, B+1], total[P])."""
+        mats = self.mats(poses)
+        mi, st, hist, total = self.ctx.eval(mats, want_hist=histograms, bins=self.bins, exact=exact)
+        if histograms:
+            return mi, st, hist, total
+        return mi, st
+
+    def evaluate_mats(self, mats: np.ndarray, histograms: bool = False, exact: bool = False):
+        mi, st, hist, total = self.ctx.eval(mats, want_hist=histograms, bins=self.bins, exact=exact)
+        return (mi, st, hist, total) if histograms else (mi, st)
+
+    def best(self, poses, mi: np.ndarray | None = None, rel_tie: float = 1e-12):
+        """np.argmax over the candidates' MI with the reference's tie semantics.
+
+        GPU MI agrees with the reference to ~1e-15; the order of two poses can
+        only differ when their MI values are that close.  Every candidate
+        within ``rel_tie`` of the maximum is re-scored on the host from its
+        bit-exact GPU histogram with the reference's own formula, and the
+        first maximum in candidate order wins.  Returns (index, mi).
+        """
+        poses = as_pose_array(poses)
+        if mi is None:
+            mi, _ = self.evaluate(poses)
+        top = float(np.max(mi))
+        if top <= NO_OVERLAP_SENTINEL:
+            return int(np.argmax(mi)), top
+        tied = np.nonzero(mi >= top - abs(top) * rel_tie)[0]
+        if tied.size == 1:
+            return int(tied[0]), float(mi[tied[0]])
+        _, _, hist, _ = self.evaluate(poses[tied], histograms=True)
+        exact = np.array([mutual_information_exact(h, self.include_phi)[0] for h in hist])
+        k = int(np.argmax(exact))
+        return int(tied[k]), float(exact[k])
+
+    def close(self):
+        self.ctx.close()
+
+
+def check_points(cloud) -> None:
+    """Raise like the reference for invalid clouds (PointCloud validation)."""
+    if isinstance(cloud, PointCloud):
+        return
+    PointCloud(np.asarray(_points_of(cloud))[:, :3])
+
+
+__all__ = ["MIEngine", "entropy_exact", "mutual_information_exact", "OutOfBoundsError"]

@@ -1,0 +1,113 @@
+"""Point clouds and 6-DOF poses, mirroring the reference's hot-path types.
+
+Mirrors `voxmi.geometry` (`geometry.py:36-166`): ``PointCloud`` (validated
+(N, 3) float64, optional intensity), ``EulerPose`` (tx, ty, tz, rx, ry, rz;
+R = Rz @ Ry @ Rx), and ``euler_to_transform``.  Batched pose -> matrix
+conversion for the GPU path happens in the native library
+(``vmi_poses_to_mats``), built with glibc ``sin``/``cos`` and
+``-ffp-contract=off`` so every matrix entry is bit-identical to the
+reference's ``math.sin``/``math.cos`` products (`geometry.py:126-138`).
+"""
+
+from __future__ import annotations
+
+import math
+from dataclasses import dataclass
+
+import numpy as np
+
+
+@dataclass(frozen=True)
+class PointCloud:
+    """(N, 3) float64 points in meters with optional (N,) intensity.
+
+    Same validation as the reference (`geometry.py:36-65`): finite
+    coordinates, matching intensity length.
+    """
+
+    points: np.ndarray
+    intensity: np.ndarray | None = None
+
+    def __post_init__(self):
+        pts = np.ascontiguousarray(self.points, dtype=np.float64)
+        if pts.ndim != 2 or pts.shape[1] != 3:
+            raise ValueError(f"points must be (N, 3), got shape {pts.shape}")
+        if not np.isfinite(pts).all():
+            raise ValueError("points contain non-finite coordinates")
+        object.__setattr__(self, "points", pts)
+        if self.intensity is not None:
+            inten = np.asarray(self.intensity, dtype=np.float64)
+            if inten.shape != (pts.shape[0],):
+                raise ValueError(
+                    f"intensity length {inten.shape} does not match "
+                    f"{pts.shape[0]} points")
+            object.__setattr__(self, "intensity", inten)
+
+    def __len__(self) -> int:
+        return self.points.shape[0]
+
+    @classmethod
+    def from_records(cls, rec: np.ndarray) -> "PointCloud":
+        """From KITTI-style (N, 4) float32 (x, y, z, i) records."""
+        rec = np.asarray(rec)
+        return cls(rec[:, :3].astype(np.float64),
+                   rec[:, 3].astype(np.float64) if rec.shape[1] > 3 else None)
+
+
+@dataclass(frozen=True)
+class EulerPose:
+    """6-DOF pose: translation in meters, ZYX Euler angles in radians
+    (`geometry.py:68-102`)."""
+
+    tx: float = 0.0
+    ty: float = 0.0
+    tz: float = 0.0
+    rx: float = 0.0
+    ry: float = 0.0
+    rz: float = 0.0
+
+    def __post_init__(self):
+        vals = (self.tx, self.ty, self.tz, self.rx, self.ry, self.rz)
+        if not all(math.isfinite(v) for v in vals):
+            raise ValueError(f"pose has non-finite component: {vals}")
+
+    def as_vector(self) -> np.ndarray:
+        return np.array([self.tx, self.ty, self.tz, self.rx, self.ry, self.rz])
+
+    @classmethod
+    def from_vector(cls, v) -> "EulerPose":
+        v = np.asarray(v, dtype=np.float64)
+        if v.shape != (6,):
+            raise ValueError(f"pose vector must have 6 entries, got {v.shape}")
+        return cls(*(float(x) for x in v))
+
+
+def euler_to_transform(pose: EulerPose) -> np.ndarray:
+    """4x4 transform of one pose, R = Rz(rz) @ Ry(ry) @ Rx(rx).
+
+    Evaluated by the native library so single poses and batches share one
+    bit pattern (see module docstring).
+    """
+    from ._lib import poses_to_mats
+    m = poses_to_mats(pose.as_vector()[None, :])[0]
+    t = np.eye(4)
+    t[:3, :3] = m[:9].reshape(3, 3)
+    t[:3, 3] = m[9:]
+    return t
+
+
+def as_pose_array(poses) -> np.ndarray:
+    """Accept EulerPose objects, (6,) or (P, 6) arrays; return (P, 6) f64."""
+    if isinstance(poses, EulerPose) or (hasattr(poses, "as_vector")
+                                        and hasattr(poses, "rz")):
+        return np.asarray(poses.as_vector(), dtype=np.float64)[None, :]
+    if isinstance(poses, (list, tuple)) and poses and hasattr(poses[0], "as_vector"):
+        return np.stack([np.asarray(p.as_vector(), dtype=np.float64) for p in poses])
+    arr = np.ascontiguousarray(poses, dtype=np.float64)
+    if arr.ndim == 1:
+        arr = arr[None, :]
+    if arr.ndim != 2 or arr.shape[1] != 6:
+        raise ValueError(f"poses must be (P, 6), got {arr.shape}")
+    if not np.isfinite(arr).all():
+        raise ValueError("poses contain non-finite components")
+    return arr

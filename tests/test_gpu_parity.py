@@ -1,0 +1,316 @@
+"""GPU parity: the CUDA path (through the C ABI) against the reference's own
+outputs (golden fixtures) and the pinned CPU oracle.
+
+Bars (north_star): voxel ids / counts / joint histograms bit-exact; VARZ and
+MI within 1e-6 relative (MI also 1e-12 absolute, for values at the clamp
+around 0); selected pose identical.  VARZ is checked with rtol 1e-6 and an
+absolute floor of 1e-18 m^2 (below that both sides are rounding residue of a
+constant-z voxel).
+"""
+
+from __future__ import annotations
+
+import math
+
+import numpy as np
+import pytest
+
+import oracle
+from conftest import SMALL_CASES, golden, hdl_pair, small_case
+
+import paper_1709_06948_b200 as vmi
+from paper_1709_06948_b200 import (BinningSpec, EulerPose, FeatureKind, FeatureMap, GridSpec,
+                                   MIEngine)
+
+pytestmark = pytest.mark.gpu
+
+MI_RTOL, MI_ATOL = 1e-6, 1e-12
+
+
+def engine(res=1.0, origin=(0, 0, 0), kind="varz", phi=True, **kw):
+    return MIEngine(grid=GridSpec(origin=np.asarray(origin, dtype=np.float64), resolution=res),
+                    binning=BinningSpec(kind=FeatureKind.from_name(kind)), include_phi=phi, **kw)
+
+
+def assert_mi_close(got, want):
+    got, want = np.asarray(got), np.asarray(want)
+    sent = want == -1e300
+    np.testing.assert_array_equal(got[sent], want[sent])
+    np.testing.assert_allclose(got[~sent], want[~sent], rtol=MI_RTOL, atol=MI_ATOL)
+
+
+# ---- reference grid (K0: GPU voxelize + features, exact path) ----------------
+
+@pytest.mark.parametrize("tag", SMALL_CASES)
+def test_reference_feature_map_bit_exact_small(tag):
+    c = small_case(tag)
+    eng = engine(c["res"], c["origin"], c["kind"], c["phi"])
+    fa = eng.set_reference(c["a"])
+    np.testing.assert_array_equal(fa.keys, c["a_keys"])
+    np.testing.assert_array_equal(fa.values.view(np.int64), c["a_values"].view(np.int64))
+    np.testing.assert_array_equal(fa.bounds, c["a_bounds"])
+
+
+@pytest.mark.parametrize("tag,res,kind", [("v1", 1.0, "varz"), ("v02", 0.2, "varz"),
+                                          ("c1", 1.0, "count")])
+def test_reference_feature_map_bit_exact_hdl(tag, res, kind):
+    g = golden("hdl_golden.npz")
+    a, b = hdl_pair()
+    eng = engine(res, kind=kind)
+    fa = eng.set_reference(a[:, :3].astype(np.float64))
+    np.testing.assert_array_equal(fa.keys, g[f"{tag}_a_keys"])
+    np.testing.assert_array_equal(fa.values.view(np.int64), g[f"{tag}_a_values"].view(np.int64))
+    np.testing.assert_array_equal(fa.bounds, g[f"{tag}_a_bounds"])
+    # scan B's feature map at the truth pose through the exact path
+    eng.set_query(b)
+    keys, vals, bounds, st = eng.ctx.query_features(vmi.poses_to_mats(g["poses"][:1])[0], b.shape[0])
+    assert st == 0
+    np.testing.assert_array_equal(keys, g[f"{tag}_b_keys"])
+    np.testing.assert_array_equal(vals.view(np.int64), g[f"{tag}_b_values"].view(np.int64))
+    np.testing.assert_array_equal(bounds, g[f"{tag}_b_bounds"])
+
+
+# ---- fused pose kernel (K1) ------------------------------------------------------
+
+@pytest.mark.parametrize("tag", SMALL_CASES)
+@pytest.mark.parametrize("exact", [False, True])
+def test_small_cases_match_reference(tag, exact):
+    c = small_case(tag)
+    eng = engine(c["res"], c["origin"], c["kind"], c["phi"])
+    eng.set_reference(c["a"])
+    eng.set_query(c["b"])
+    mi, st, hist, total = eng.evaluate(c["poses"], histograms=True, exact=exact)
+    np.testing.assert_array_equal(st, c["status"])
+    ok = (st == 0) | (st == 3)
+    np.testing.assert_array_equal(hist[ok], c["hist"][ok])
+    np.testing.assert_array_equal(total[ok], c["total"][ok])
+    assert_mi_close(mi, c["mi"])
+
+
+@pytest.mark.parametrize("tag,res,kind", [("v1", 1.0, "varz"), ("v02", 0.2, "varz"),
+                                          ("c1", 1.0, "count")])
+def test_hdl_poses_match_reference(tag, res, kind):
+    g = golden("hdl_golden.npz")
+    a, b = hdl_pair()
+    eng = engine(res, kind=kind)
+    eng.set_reference(a[:, :3].astype(np.float64))
+    eng.set_query(b)  # float32 KITTI records -> float4 fast path
+    n = g[f"{tag}_mi"].shape[0]
+    mi, st, hist, total = eng.evaluate(g["poses"][:n], histograms=True)
+    np.testing.assert_array_equal(st, g[f"{tag}_status"])
+    np.testing.assert_array_equal(hist, g[f"{tag}_hist"].astype(np.int64))
+    np.testing.assert_array_equal(total, g[f"{tag}_total"])
+    assert_mi_close(mi, g[f"{tag}_mi"])
+
+
+def test_c1_full_grid_mi_and_selected_pose():
+    g = golden("c1_golden.npz")
+    s = golden("c1_scans.npz")
+    cfg = vmi.AlignmentConfig(feature=FeatureKind.COUNT, grid=GridSpec(resolution=0.5))
+    res = vmi.grid_search(s["a"], s["b"], poses=g["poses"], cfg=cfg)
+    assert_mi_close(res.mi, g["mi"])
+    assert res.best_index == int(g["argmax"])
+    eng = engine(0.5, kind="count")
+    eng.set_reference(s["a"])
+    eng.set_query(s["b"])  # float64 (not float32-exact) path
+    mi, st, hist, total = eng.evaluate(g["poses"][g["sub"]], histograms=True)
+    np.testing.assert_array_equal(hist, g["hist"].astype(np.int64))
+    np.testing.assert_array_equal(total, g["total"])
+    np.testing.assert_array_equal(st, g["status"])
+
+
+def test_fast_path_equals_exact_path_on_c2_batch(hdl):
+    """Size-independent property at C2 scale: the fused hash path and the
+    sort-based exact path give identical histograms for random C2 poses."""
+    a, b = hdl
+    from paper_1709_06948_b200.synth import candidate_batch
+    poses = candidate_batch(EulerPose(1.5, 0.3, 0, 0, 0, 0.05), 96, seed=11)
+    eng = engine(1.0, kind="varz")
+    eng.set_reference(a[:, :3].astype(np.float64))
+    eng.set_query(b)
+    mi_f, st_f, h_f, t_f = eng.evaluate(poses, histograms=True)
+    mi_e, st_e, h_e, t_e = eng.evaluate(poses, histograms=True, exact=True)
+    np.testing.assert_array_equal(st_f, st_e)
+    np.testing.assert_array_equal(h_f, h_e)
+    np.testing.assert_array_equal(t_f, t_e)
+    np.testing.assert_allclose(mi_f, mi_e, rtol=1e-12, atol=1e-14)
+    # and the oracle agrees on a subsample
+    fa = oracle.feature_map(a[:, :3].astype(np.float64), (0, 0, 0), 1.0, "varz")
+    mats = vmi.poses_to_mats(poses[:12])
+    omi, ost = oracle.mi_objective_batch(fa, b[:, :3].astype(np.float64), mats, threads=0)
+    np.testing.assert_array_equal(ost, st_f[:12])
+    assert_mi_close(mi_f[:12], omi)
+
+
+def test_table_overflow_falls_back_to_exact(hdl):
+    a, b = hdl
+    g = golden("hdl_golden.npz")
+    eng = engine(1.0, kind="varz", table_cap=256)  # far too small: every pose overflows
+    eng.set_reference(a[:, :3].astype(np.float64))
+    eng.set_query(b)
+    mi, st, hist, total = eng.evaluate(g["poses"][:8], histograms=True)
+    np.testing.assert_array_equal(st, g["v1_status"][:8])
+    np.testing.assert_array_equal(hist, g["v1_hist"][:8].astype(np.int64))
+    assert_mi_close(mi, g["v1_mi"][:8])
+
+
+@pytest.mark.parametrize("threads", [512, 1024])
+def test_thread_configurations_agree(hdl, threads):
+    a, b = hdl
+    g = golden("hdl_golden.npz")
+    eng = engine(1.0, kind="varz", threads=threads)
+    eng.set_reference(a[:, :3].astype(np.float64))
+    eng.set_query(b)
+    mi, st, hist, _ = eng.evaluate(g["poses"], histograms=True)
+    np.testing.assert_array_equal(hist, g["v1_hist"].astype(np.int64))
+    assert_mi_close(mi, g["v1_mi"])
+
+
+def test_records_and_float64_inputs_agree(hdl):
+    a, b = hdl
+    poses = golden("hdl_golden.npz")["poses"][:16]
+    e1 = engine(1.0)
+    e1.set_reference(a[:, :3].astype(np.float64))
+    e1.set_query(b)                                # float32 records
+    e2 = engine(1.0)
+    e2.set_reference(a)
+    e2.set_query(b[:, :3].astype(np.float64))      # float64, float32-exact -> float4 too
+    r1 = e1.evaluate(poses, histograms=True)
+    r2 = e2.evaluate(poses, histograms=True)
+    for x, y in zip(r1, r2):
+        np.testing.assert_array_equal(x, y)
+
+
+# ---- drop-in API and edge cases (test_mi.py:303-345 semantics) ------------------
+
+def scene(seed, n):
+    rng = np.random.default_rng(seed)
+    pts = rng.uniform(-15, 15, size=(n, 3))
+    pts[:, 2] = rng.uniform(0, 4, size=n) * (pts[:, 0] > 0)
+    return vmi.PointCloud(pts)
+
+
+def test_self_alignment_equals_marginal_entropy():
+    cloud = scene(60, 5000)
+    grid = GridSpec()
+    spec = BinningSpec(kind=FeatureKind.VARZ)
+    feat = vmi.compute_feature_map(cloud, grid, FeatureKind.VARZ)
+    mi = vmi.mi_objective(feat, cloud, EulerPose(), grid, spec)
+    h = vmi.joint_histogram_at(cloud, cloud, EulerPose())
+    assert mi == pytest.approx(vmi.entropy_exact(h.counts.sum(axis=1)), abs=1e-12)
+
+
+def test_truth_scores_higher_than_offset():
+    cloud = scene(61, 5000)
+    grid = GridSpec()
+    spec = BinningSpec(kind=FeatureKind.VARZ)
+    feat = vmi.compute_feature_map(cloud, grid, FeatureKind.VARZ)
+    at_truth = vmi.mi_objective(feat, cloud, EulerPose(), grid, spec)
+    offset = vmi.mi_objective(feat, cloud, EulerPose(tx=3.0, ty=-2.0, rz=0.2), grid, spec)
+    assert at_truth > offset
+
+
+@pytest.mark.parametrize("tx", [1e4, 3e6])
+def test_sentinels(tx):
+    cloud = scene(62, 500)
+    grid = GridSpec()
+    spec = BinningSpec(kind=FeatureKind.VARZ)
+    feat = vmi.compute_feature_map(cloud, grid, FeatureKind.VARZ)
+    assert vmi.mi_objective(feat, cloud, EulerPose(tx=tx), grid, spec) == vmi.NO_OVERLAP_SENTINEL
+    mi, st = vmi.mi_objective_batch(feat, cloud, [EulerPose(tx=tx)], grid, spec, return_status=True)
+    assert st[0] == (1 if tx == 1e4 else 2)
+
+
+def test_reference_feature_map_injection_and_phi_off_empty():
+    # hand-built maps like the reference tests' feature_map(cells) (test_mi.py:37-50)
+    def fmap(cells):
+        ijk = np.array(sorted(cells), dtype=np.int64)
+        keys = ((ijk[:, 0] + (1 << 20)) << 42) | ((ijk[:, 1] + (1 << 20)) << 21) | (ijk[:, 2] + (1 << 20))
+        vals = np.array([cells[tuple(t)] for t in ijk])
+        return FeatureMap(kind=FeatureKind.COUNT, keys=keys, values=vals,
+                          bounds=np.array([ijk.min(axis=0), ijk.max(axis=0)]))
+    fa = fmap({(0, 0, 0): 3.0, (4, 4, 4): 10.0})
+    cloud = vmi.PointCloud(np.array([[2.5, 2.5, 2.5], [2.6, 2.5, 2.5], [0.5, 0.5, 0.5]]))
+    spec = BinningSpec(kind=FeatureKind.COUNT)
+    grid = GridSpec()
+    mi_on = vmi.mi_objective(fa, cloud, EulerPose(), grid, spec, include_phi=True)
+    assert mi_on != vmi.NO_OVERLAP_SENTINEL
+    # shift B off every A voxel but keep the AABBs overlapping: phi-off has no co-occupied cell
+    mi_off = vmi.mi_objective(fa, cloud, EulerPose(tx=1.0), grid, spec, include_phi=False)
+    assert mi_off == vmi.NO_OVERLAP_SENTINEL
+    # the same through the oracle on the same maps
+    ofa = oracle.OracleFeatureMap("count", fa.keys, fa.values, fa.bounds)
+    omi, ost = oracle.mi_objective_batch(ofa, cloud.points, vmi.poses_to_mats([[0, 0, 0, 0, 0, 0],
+                                                                              [1, 0, 0, 0, 0, 0]]),
+                                         include_phi=False)
+    assert omi[1] == vmi.NO_OVERLAP_SENTINEL and ost[1] == 3
+    assert vmi.mi_objective(fa, cloud, EulerPose(), grid, spec, include_phi=False) == \
+        pytest.approx(omi[0], rel=1e-12, abs=1e-14)
+
+
+def test_empty_inputs_raise_like_reference():
+    with pytest.raises(ValueError):
+        vmi.compute_feature_map(np.zeros((0, 3)))
+    eng = engine()
+    eng.set_reference(scene(1, 100))
+    with pytest.raises(ValueError):
+        eng.set_query(np.zeros((0, 3)))
+    with pytest.raises(vmi.OutOfBoundsError):
+        vmi.compute_feature_map(np.array([[3e6, 0.0, 0.0]]))
+
+
+def test_empty_reference_map_gives_sentinel():
+    fa = FeatureMap(kind=FeatureKind.VARZ, keys=np.empty(0, np.int64), values=np.empty(0),
+                    bounds=np.array([[1, 1, 1], [0, 0, 0]]))
+    cloud = scene(5, 200)
+    mi = vmi.mi_objective(fa, cloud, EulerPose(), GridSpec(), BinningSpec(kind=FeatureKind.VARZ))
+    assert mi == vmi.NO_OVERLAP_SENTINEL
+
+
+def test_bins_limits():
+    with pytest.raises(vmi.VmiError):
+        engine(kind="varz").ctx.set_params((0, 0, 0), 1.0, 0, 65, 2.0, True)
+    eng = MIEngine(binning=BinningSpec(kind=FeatureKind.VARZ, bin_count=64))
+    c = small_case("s0")
+    eng.set_reference(c["a"])
+    eng.set_query(c["b"])
+    mi, st, hist, _ = eng.evaluate(c["poses"][:6], histograms=True)
+    ofa = oracle.feature_map(c["a"], (0, 0, 0), 1.0, "varz")
+    for k in range(6):
+        omi, ost, oc, _ = oracle.mi_objective_full(ofa, c["b"], vmi.poses_to_mats(c["poses"][k])[0],
+                                                   bins=64)
+        assert ost == st[k]
+        if ost == 0:
+            np.testing.assert_array_equal(hist[k], oc)
+            assert mi[k] == pytest.approx(omi, rel=MI_RTOL, abs=MI_ATOL)
+
+
+def test_sweep_axis_peaks_at_truth():
+    s = golden("c1_scans.npz")
+    cfg = vmi.AlignmentConfig(feature=FeatureKind.COUNT, grid=GridSpec(resolution=0.5))
+    vals = np.linspace(1.0 - 2.0, 1.0 + 2.0, 17)
+    out = vmi.sweep_axis(s["a"], s["b"], EulerPose(1.0, 0.5, 0, 0, 0, 0.1), "tx", vals, cfg)
+    best = max(range(len(out)), key=lambda i: out[i][1])
+    assert abs(out[best][0] - 1.0) <= 0.25 + 1e-9
+
+
+def test_mi_at_breakdown_matches_oracle():
+    s = golden("c1_scans.npz")
+    cfg = vmi.AlignmentConfig(feature=FeatureKind.COUNT, grid=GridSpec(resolution=0.5))
+    pose = EulerPose(0.8, 0.6, 0.0, 0.0, 0.0, 0.09)
+    r = vmi.mi_at(s["a"], s["b"], pose, cfg)
+    fa = oracle.feature_map(s["a"], (0, 0, 0), 0.5, "count")
+    _, _, counts, _ = oracle.mi_objective_full(fa, s["b"], vmi.poses_to_mats(pose.as_vector())[0],
+                                               res=0.5)
+    want = oracle.mutual_information(counts)
+    np.testing.assert_allclose([r.mi, r.h_x, r.h_y, r.h_xy], want, rtol=1e-12, atol=1e-14)
+    with pytest.raises(vmi.EmptyOverlapError):
+        vmi.mi_at(s["a"], s["b"], EulerPose(tx=1e4), cfg)
+
+
+def test_argmax_device_first_index():
+    import torch
+    eng = engine()
+    v = torch.tensor([0.1, 0.5, 0.2, 0.5, -1e300], dtype=torch.float64, device="cuda")
+    best, idx = eng.ctx.argmax_device(v.data_ptr(), 5)
+    assert (best, idx) == (0.5, 1)
