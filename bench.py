@@ -226,8 +226,10 @@ def run_ours(args, world, rank, local):
         import torch.distributed as dist
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     a, b, poses_all = workload(world, args.poses)
-    P = args.poses
-    poses = poses_all[rank * P:(rank + 1) * P]
+    from paper_1709_06948_b200.shard import pick_global, shard_bounds
+    lo, hi = shard_bounds(poses_all.shape[0], world, rank)
+    poses = poses_all[lo:hi]
+    P = poses.shape[0]
     eng = vmi.MIEngine(grid=vmi.GridSpec(resolution=1.0),
                        binning=vmi.BinningSpec(kind=vmi.FeatureKind.VARZ), device=local,
                        threads=args.threads)
@@ -264,12 +266,11 @@ def run_ours(args, world, rank, local):
         if world > 1:
             with torch.cuda.stream(stream):
                 winner[0] = best
-                winner[1] = float(rank * P + idx)
+                winner[1] = float(lo + idx)
                 dist.all_gather_into_tensor(gathered, winner)
-                g = gathered.view(world, 2).cpu().numpy()
-            k = int(np.lexsort((g[:, 1], -g[:, 0]))[0])
-            return g[k, 0], int(g[k, 1])
-        return best, rank * P + idx
+                g = gathered.cpu().numpy()
+            return pick_global(g)
+        return best, lo + idx
 
     for _ in range(args.warmup):
         step()

@@ -33,8 +33,7 @@ __device__ __forceinline__ void point_at(const PointSource& src, int64_t i, doub
     x = src.xyz[3 * i]; y = src.xyz[3 * i + 1]; z = src.xyz[3 * i + 2];
     return;
   }
-  const int64_t t = i / src.B.span, r = i - t * src.B.span;
-  const int64_t li = r * src.B.threads + t;
+  const int64_t li = span_slot(i, src.B.span, src.B.rem, src.B.threads);
   if (src.B.is_f32) {
     float4 v = reinterpret_cast<const float4*>(src.B.pts)[li];
     x = v.x; y = v.y; z = v.z;
@@ -365,29 +364,32 @@ cudaError_t launch_argmax(const double* v, int64_t P, double* out_val, long long
 }
 
 // ---- span layout (see QueryView) ------------------------------------------------
-__global__ void k_span_layout(const void* src, int is_f32, int64_t n, int64_t span, int threads,
-                              void* dst) {
-  const int64_t li = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;  // layout index
-  if (li >= span * threads) return;
-  const int64_t r = li / threads, t = li - r * threads;
-  const int64_t i = t * span + r;  // original index
+__global__ void k_span_layout(const void* src, int is_f32, int64_t n, int span, int rem,
+                              int threads, void* dst) {
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;  // original index
+  const int64_t total = (int64_t)span * threads;
+  if (i >= total) return;
+  if (i >= n) {  // padding slots: the (threads - rem) unused last-iteration entries
+    const int64_t li = (int64_t)(span - 1) * threads + thread_of_span(rem + (int)(i - n), threads);
+    if (is_f32) reinterpret_cast<float4*>(dst)[li] = make_float4(0.f, 0.f, 0.f, 0.f);
+    else reinterpret_cast<double4*>(dst)[li] = make_double4(0.0, 0.0, 0.0, 0.0);
+    return;
+  }
+  const int64_t li = span_slot(i, span, rem, threads);
   if (is_f32) {
-    float4 v = i < n ? reinterpret_cast<const float4*>(src)[i] : make_float4(0.f, 0.f, 0.f, 0.f);
-    reinterpret_cast<float4*>(dst)[li] = v;
+    reinterpret_cast<float4*>(dst)[li] = reinterpret_cast<const float4*>(src)[i];
   } else {
     const double* s = reinterpret_cast<const double*>(src);
-    double* d = reinterpret_cast<double*>(dst) + 4 * li;
-    if (i < n) { d[0] = s[3 * i]; d[1] = s[3 * i + 1]; d[2] = s[3 * i + 2]; }
-    else { d[0] = d[1] = d[2] = 0.0; }
-    d[3] = 0.0;
+    reinterpret_cast<double4*>(dst)[li] = make_double4(s[3 * i], s[3 * i + 1], s[3 * i + 2], 0.0);
   }
 }
 
-cudaError_t launch_span_layout(const void* src, int is_f32, int64_t n, int64_t span, int threads,
-                               void* dst, cudaStream_t st) {
-  const int64_t total = span * threads;
+cudaError_t launch_span_layout(const void* src, int is_f32, int64_t n, int span, int rem,
+                               int threads, void* dst, cudaStream_t st) {
+  const int64_t total = (int64_t)span * threads;
   const int T = 256;
-  k_span_layout<<<(unsigned)((total + T - 1) / T), T, 0, st>>>(src, is_f32, n, span, threads, dst);
+  k_span_layout<<<(unsigned)((total + T - 1) / T), T, 0, st>>>(src, is_f32, n, span, rem, threads,
+                                                               dst);
   return cudaGetLastError();
 }
 

@@ -28,6 +28,7 @@
 // sort-based path (k_exact.cu), so histograms stay bit-exact.
 #include <cstdint>
 #include <climits>
+#include <type_traits>
 #include <cuda_runtime.h>
 
 #include "vmi_device.cuh"
@@ -92,22 +93,15 @@ __device__ __forceinline__ void flush_count(uint32_t* key, uint32_t* cnt, uint32
   atomicAdd(&cnt[s], (uint32_t)n);
 }
 
-template <bool F32>
-__device__ __forceinline__ void load_point(const QueryView& B, int64_t idx, double& x, double& y,
-                                           double& z) {
-  if (F32) {
-    float4 v = __ldg(reinterpret_cast<const float4*>(B.pts) + idx);
-    x = (double)v.x; y = (double)v.y; z = (double)v.z;
-  } else {
-    const double2* p = reinterpret_cast<const double2*>(B.pts) + 2 * idx;
-    double2 a = __ldg(p), b = __ldg(p + 1);
-    x = a.x; y = a.y; z = b.x;
-  }
-}
+// Warp-private flush queue: run records pushed by any lane, drained 32 at a
+// time by the whole warp so the hash/atomic path always runs converged.
+constexpr int kQueue = 64;  // entries per warp (a round pushes <= 32)
 
 // Shared-memory layout helper (bytes), mirrored by fast_smem_bytes() on the host.
+constexpr int kCountLut = 1024;  // COUNT bins precomputed for n < kCountLut
+
 struct FastSmem {
-  size_t table, hist, marg, red, rows, cols, misc, total;
+  size_t table, queue, hist, marg, red, rows, cols, misc, lut, total;
 };
 __host__ __device__ inline FastSmem fast_layout(int kind, int cap, int W, int threads) {
   FastSmem L;
@@ -115,12 +109,17 @@ __host__ __device__ inline FastSmem fast_layout(int kind, int cap, int W, int th
   L.table = off;
   off += (size_t)cap * (kind == 0 ? (8 + 8 + 8 + 4) : (4 + 4));
   off = (off + 15) & ~size_t(15);
+  L.queue = off;
+  off += (size_t)(threads / 32) * kQueue * (kind == 0 ? (4 + 4 + 8 + 8 + 8) : (4 + 4));
+  off = (off + 15) & ~size_t(15);
   L.hist = off; off += (size_t)W * W * 4; off = (off + 15) & ~size_t(15);
   L.marg = off; off += (size_t)W * 4; off = (off + 15) & ~size_t(15);
   L.red = off; off += (size_t)3 * (threads / 32) * 8; off = (off + 15) & ~size_t(15);
   L.rows = off; off += (size_t)W * 8;
   L.cols = off; off += (size_t)W * 8;
   L.misc = off; off += 128;
+  L.lut = off; off += kind == 1 ? kCountLut : 0;
+  off = (off + 15) & ~size_t(15);
   L.total = off;
   return L;
 }
@@ -129,12 +128,21 @@ size_t fast_smem_bytes(int kind, int cap, int bins, int threads) {
   return fast_layout(kind, cap, bins + 1, threads).total;
 }
 
-template <int THREADS, int KIND, bool F32>
+struct WarpQueue {
+  uint32_t* lin;
+  uint32_t* n;
+  double* K;
+  double* s1;
+  double* s2;
+};
+
+template <int THREADS, int KIND, bool F32, int MODE>
 __global__ void __launch_bounds__(THREADS, 1)
     k_pose_fast(GridParams g, RefView A, QueryView B, const double* __restrict__ mats, int64_t P,
                 int cap, double* __restrict__ mi_out, int32_t* __restrict__ status_out,
                 long long* __restrict__ hist_out, long long* __restrict__ total_out) {
   extern __shared__ __align__(16) unsigned char smem[];
+  constexpr int NW = THREADS / 32;
   const int W = g.bins + 1;
   const FastSmem L = fast_layout(KIND, cap, W, THREADS);
   uint32_t* hist = reinterpret_cast<uint32_t*>(smem + L.hist);
@@ -146,32 +154,55 @@ __global__ void __launch_bounds__(THREADS, 1)
   long long* h00_s = reinterpret_cast<long long*>(smem + L.misc + 64);
   double* mat_s = reinterpret_cast<double*>(smem + L.red);  // aliases red before the epilogue
 
-  VarzTable VT;
-  uint32_t* ckey = nullptr;
-  uint32_t* ccnt = nullptr;
-  if (KIND == 0) {
-    VT.key = reinterpret_cast<unsigned long long*>(smem + L.table);
-    VT.s1 = reinterpret_cast<double*>(smem + L.table + (size_t)cap * 8);
-    VT.s2 = reinterpret_cast<double*>(smem + L.table + (size_t)cap * 16);
-    VT.cnt = reinterpret_cast<uint32_t*>(smem + L.table + (size_t)cap * 24);
-  } else {
-    ckey = reinterpret_cast<uint32_t*>(smem + L.table);
-    ccnt = reinterpret_cast<uint32_t*>(smem + L.table + (size_t)cap * 4);
-  }
   const int tid = threadIdx.x;
   const int lane = tid & 31;
   const int wid = tid >> 5;
+  const unsigned lt_mask = (1u << lane) - 1u;
   const uint32_t ucap = (uint32_t)cap;
 
-  for (int64_t p = blockIdx.x; p < P; p += gridDim.x) {
-    // ---- clear per-pose state -----------------------------------------
+  VarzTable VT;
+  uint32_t* ckey = nullptr;
+  uint32_t* ccnt = nullptr;
+  WarpQueue Q;
+  {
+    unsigned char* qb = smem + L.queue;
     if (KIND == 0) {
-      for (int s = tid; s < cap; s += THREADS) {
-        VT.key[s] = kEmpty64; VT.s1[s] = 0.0; VT.s2[s] = 0.0; VT.cnt[s] = 0u;
-      }
+      VT.key = reinterpret_cast<unsigned long long*>(smem + L.table);
+      VT.s1 = reinterpret_cast<double*>(smem + L.table + (size_t)cap * 8);
+      VT.s2 = reinterpret_cast<double*>(smem + L.table + (size_t)cap * 16);
+      VT.cnt = reinterpret_cast<uint32_t*>(smem + L.table + (size_t)cap * 24);
+      Q.K = reinterpret_cast<double*>(qb) + wid * kQueue;
+      Q.s1 = reinterpret_cast<double*>(qb + (size_t)NW * kQueue * 8) + wid * kQueue;
+      Q.s2 = reinterpret_cast<double*>(qb + (size_t)NW * kQueue * 16) + wid * kQueue;
+      Q.lin = reinterpret_cast<uint32_t*>(qb + (size_t)NW * kQueue * 24) + wid * kQueue;
+      Q.n = reinterpret_cast<uint32_t*>(qb + (size_t)NW * kQueue * 28) + wid * kQueue;
     } else {
-      for (int s = tid; s < cap; s += THREADS) { ckey[s] = kEmpty32; ccnt[s] = 0u; }
+      ckey = reinterpret_cast<uint32_t*>(smem + L.table);
+      ccnt = reinterpret_cast<uint32_t*>(smem + L.table + (size_t)cap * 4);
+      Q.lin = reinterpret_cast<uint32_t*>(qb) + wid * kQueue;
+      Q.n = reinterpret_cast<uint32_t*>(qb + (size_t)NW * kQueue * 4) + wid * kQueue;
+      Q.K = Q.s1 = Q.s2 = nullptr;
     }
+  }
+
+  // The table is cleared once here; afterwards the per-pose table walk resets
+  // every slot it reads, so each pose starts from an empty table.
+  auto clear_table = [&]() {
+    uint4* t4 = reinterpret_cast<uint4*>(smem + L.table);
+    const int key_words = KIND == 0 ? cap / 2 : cap / 4;  // uint4s holding keys
+    const int all_words = (int)((L.queue - L.table) / 16);
+    const uint4 ones = make_uint4(~0u, ~0u, ~0u, ~0u), zero = make_uint4(0u, 0u, 0u, 0u);
+    for (int i = tid; i < all_words; i += THREADS) t4[i] = i < key_words ? ones : zero;
+  };
+  clear_table();
+  // COUNT features are small integers: their bins (mi.py:72-79) come from a LUT
+  uint8_t* count_lut = reinterpret_cast<uint8_t*>(smem + L.lut);
+  if (KIND == 1)
+    for (int n = tid; n < kCountLut; n += THREADS)
+      count_lut[n] = (uint8_t)feature_bin((double)n, g.clamp, g.bins);
+  const double bin_scale = (double)g.bins / g.clamp;
+
+  for (int64_t p = blockIdx.x; p < P; p += gridDim.x) {
     for (int i = tid; i < W * W; i += THREADS) hist[i] = 0u;
     for (int i = tid; i < W; i += THREADS) marg[i] = 0u;
     if (tid < 3) { misc[tid] = INT_MAX; misc[3 + tid] = INT_MIN; }
@@ -185,30 +216,42 @@ __global__ void __launch_bounds__(THREADS, 1)
     // ---- pass over this thread's span of scan B --------------------------
     int bmin0 = INT_MAX, bmin1 = INT_MAX, bmin2 = INT_MAX;
     int bmax0 = INT_MIN, bmax1 = INT_MIN, bmax2 = INT_MIN;
-    bool bad = false;
+    unsigned badacc = 0u;
     uint32_t cur = kNoVoxel;
     int cn = 0;
     double cK = 0.0, cs1 = 0.0, cs2 = 0.0;
-    bool has_p = false;
-    uint32_t pl = kNoVoxel;
-    int pn = 0;
-    double pK = 0.0, ps1 = 0.0, ps2 = 0.0;
-    const int64_t span = B.span;
-    const int64_t base = (int64_t)tid * span;
-    for (int64_t r = 0; r < span; ++r) {
+    uint32_t qh = 0, qt = 0;  // warp-uniform queue head / tail
+
+    auto drain32 = [&]() {  // whole warp: flush records [qh, qh+32)
+      __syncwarp();
+      const int i = (qh + lane) & (kQueue - 1);
+      if (KIND == 0) flush_varz(VT, ucap, Q.lin[i], (int)Q.n[i], Q.K[i], Q.s1[i], Q.s2[i], &misc[7]);
+      else flush_count(ckey, ccnt, ucap, Q.lin[i], (int)Q.n[i], &misc[7]);
+      qh += 32;
+      __syncwarp();
+    };
+    auto push = [&](bool do_push) {  // whole warp: enqueue the finished runs of some lanes
+      const unsigned m = __ballot_sync(0xffffffffu, do_push);
+      if (m == 0u) return;
+      if (do_push) {
+        const int i = (qt + __popc(m & lt_mask)) & (kQueue - 1);
+        Q.lin[i] = cur;
+        Q.n[i] = (uint32_t)cn;
+        if (KIND == 0) { Q.K[i] = cK; Q.s1[i] = cs1; Q.s2[i] = cs2; }
+      }
+      qt += __popc(m);
+      if (qt - qh >= 32) drain32();
+    };
+    // one point: transform, voxel, bounds, run aggregation (valid = real point)
+    auto point = [&](double x, double y, double z, bool valid) {
+      const double X = xform_row(x, y, z, m0, m1, m2, t0);
+      const double Y = xform_row(x, y, z, m3, m4, m5, t1);
+      const double Z = xform_row(x, y, z, m6, m7, m8, t2);
+      const int ix = floor_i32(grid_q<MODE>(X, g.origin[0], g.res, g.inv_res), badacc);
+      const int iy = floor_i32(grid_q<MODE>(Y, g.origin[1], g.res, g.inv_res), badacc);
+      const int iz = floor_i32(grid_q<MODE>(Z, g.origin[2], g.res, g.inv_res), badacc);
       uint32_t lin = kNoVoxel;
-      double Z = 0.0;
-      if (base + r < B.n) {
-        double x, y, z;
-        load_point<F32>(B, r * THREADS + tid, x, y, z);
-        const double X = xform_row(x, y, z, m0, m1, m2, t0);
-        const double Y = xform_row(x, y, z, m3, m4, m5, t1);
-        Z = xform_row(x, y, z, m6, m7, m8, t2);
-        int ix, iy, iz;
-        bool ok = voxel_coord(X, g.origin[0], g.res, g.inv_res, g.mode, ix);
-        ok &= voxel_coord(Y, g.origin[1], g.res, g.inv_res, g.mode, iy);
-        ok &= voxel_coord(Z, g.origin[2], g.res, g.inv_res, g.mode, iz);
-        bad |= !ok;
+      if (valid) {
         bmin0 = min(bmin0, ix); bmax0 = max(bmax0, ix);
         bmin1 = min(bmin1, iy); bmax1 = max(bmax1, iy);
         bmin2 = min(bmin2, iz); bmax2 = max(bmax2, iz);
@@ -219,30 +262,50 @@ __global__ void __launch_bounds__(THREADS, 1)
           lin = (rx * A.ext[1] + ry) * A.ext[2] + rz;
       }
       const bool ends = lin != cur;
-      const bool push = ends && cur != kNoVoxel;
-      // warp-converged flush of the one-deep pending queue when any lane needs it
-      if (__any_sync(0xffffffffu, push && has_p)) {
-        if (has_p) {
-          if (KIND == 0) flush_varz(VT, ucap, pl, pn, pK, ps1, ps2, &misc[7]);
-          else flush_count(ckey, ccnt, ucap, pl, pn, &misc[7]);
-          has_p = false;
-        }
-      }
-      if (push) { has_p = true; pl = cur; pn = cn; pK = cK; ps1 = cs1; ps2 = cs2; }
+      push(ends && cur != kNoVoxel);
       if (ends) {
         cur = lin; cn = 1; cK = Z; cs1 = 0.0; cs2 = 0.0;
       } else {
         const double d = Z - cK;
         ++cn; cs1 += d; cs2 = fma(d, d, cs2);
       }
+    };
+
+    using Rec = typename std::conditional<F32, float4, double4>::type;
+    const Rec* pts = reinterpret_cast<const Rec*>(B.pts) + tid;
+    const int full = B.span - 1;          // iterations every thread owns
+    const bool has_last = span_of_thread(tid, THREADS) < B.rem;  // spans with one more point
+    constexpr int PF = 4;                 // prefetch depth (points per thread)
+    Rec cb[PF];
+#pragma unroll
+    for (int u = 0; u < PF; ++u) cb[u] = u < full ? pts[u * THREADS] : Rec{};
+    int r0 = 0;
+    for (; r0 + PF <= full; r0 += PF) {
+#pragma unroll
+      for (int u = 0; u < PF; ++u) {
+        const Rec pv = cb[u];
+        if (r0 + PF + u < full) cb[u] = pts[(r0 + PF + u) * THREADS];
+        point((double)pv.x, (double)pv.y, (double)pv.z, true);
+      }
     }
-    if (has_p) {
-      if (KIND == 0) flush_varz(VT, ucap, pl, pn, pK, ps1, ps2, &misc[7]);
-      else flush_count(ckey, ccnt, ucap, pl, pn, &misc[7]);
+#pragma unroll
+    for (int u = 0; u < PF; ++u)  // remainder (< PF) of the full iterations
+      if (r0 + u < full) point((double)cb[u].x, (double)cb[u].y, (double)cb[u].z, true);
+    {  // the ragged last iteration
+      const Rec v = pts[full * THREADS];
+      point((double)v.x, (double)v.y, (double)v.z, has_last);
     }
-    if (cur != kNoVoxel) {
-      if (KIND == 0) flush_varz(VT, ucap, cur, cn, cK, cs1, cs2, &misc[7]);
-      else flush_count(ckey, ccnt, ucap, cur, cn, &misc[7]);
+    push(cur != kNoVoxel);
+    while (qh != qt) {  // drain the tail (partial round)
+      __syncwarp();
+      const uint32_t i = qh + lane;
+      if (i - qh < qt - qh) {
+        const int j = i & (kQueue - 1);
+        if (KIND == 0) flush_varz(VT, ucap, Q.lin[j], (int)Q.n[j], Q.K[j], Q.s1[j], Q.s2[j], &misc[7]);
+        else flush_count(ckey, ccnt, ucap, Q.lin[j], (int)Q.n[j], &misc[7]);
+      }
+      qh = (qt - qh > 32u) ? qh + 32 : qt;
+      __syncwarp();
     }
     // ---- reduce bounds / key-range flag ----------------------------------
     bmin0 = __reduce_min_sync(0xffffffffu, bmin0);
@@ -251,12 +314,17 @@ __global__ void __launch_bounds__(THREADS, 1)
     bmax0 = __reduce_max_sync(0xffffffffu, bmax0);
     bmax1 = __reduce_max_sync(0xffffffffu, bmax1);
     bmax2 = __reduce_max_sync(0xffffffffu, bmax2);
-    const bool anybad = __any_sync(0xffffffffu, bad);
+    const bool anybad = __any_sync(0xffffffffu, badacc != 0u);
     if (lane == 0) {
       atomicMin(&misc[0], bmin0); atomicMin(&misc[1], bmin1); atomicMin(&misc[2], bmin2);
       atomicMax(&misc[3], bmax0); atomicMax(&misc[4], bmax1); atomicMax(&misc[5], bmax2);
       if (anybad) misc[6] = 1;
     }
+    __syncthreads();
+    // voxel.py:200-206: any index outside [-2^20, 2^20-1] -> OutOfBoundsError
+    if (tid == 0 && (misc[0] < kKeyMin || misc[1] < kKeyMin || misc[2] < kKeyMin ||
+                     misc[3] > kKeyMax || misc[4] > kKeyMax || misc[5] > kKeyMax))
+      misc[6] = 1;
     __syncthreads();
 
     // ---- overlap region (voxel.py:298-318) -------------------------------
@@ -284,64 +352,94 @@ __global__ void __launch_bounds__(THREADS, 1)
       }
       if (hist_out)
         for (int i = tid; i < W * W; i += THREADS) hist_out[p * W * W + i] = 0;
+      clear_table();  // the walk below (which resets slots) is skipped
       __syncthreads();
       continue;
     }
 
     // ---- enumerate B voxels (all inside A's AABB, hence in the region) ---
+    // Four slots per thread per step so four A-grid loads are in flight; every
+    // slot read is reset for the next pose.  VARZ bins use var * (B / clamp):
+    // our VARZ is itself within ~1e-14 of the reference's, and any value within
+    // rounding distance of a bin edge marks the pose for the exact path.
     const double bins_d = (double)g.bins;
     bool recheck = false;
-    for (int s = tid; s < cap; s += THREADS) {
-      uint32_t lin;
-      double feat;
-      if (KIND == 0) {
-        const unsigned long long w = VT.key[s];
-        if (w == kEmpty64) continue;
-        lin = (uint32_t)(w >> 32);
-        const double nd = (double)VT.cnt[s];
-        const double S1 = VT.s1[s], S2 = VT.s2[s];
-        const double c1 = S1 * (S1 / nd);
-        const double ssd = S2 - c1;
-        feat = (ssd > 0.0 ? ssd : 0.0) / nd;
-        // rounding-distance guard against a bin edge (see file header)
-        const double x = __dmul_rn(__ddiv_rn(feat, g.clamp), bins_d);
-        const double k = rint(x);
-        if (k >= 1.0 && k <= bins_d - 1.0) {
-          const double tol = ((nd + 8.0) * 4.440892098500626e-16 * (S2 + c1) / nd +
-                              feat * 9.094947017729282e-13) / g.clamp * bins_d + 1e-300;
-          if (fabs(x - k) <= tol) recheck = true;
+    for (int s0 = tid; s0 < cap; s0 += 4 * THREADS) {
+      uint32_t lin4[4];
+      int ba4[4];
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        const int s = s0 + u * THREADS;
+        lin4[u] = kNoVoxel;
+        if (s < cap) {
+          if (KIND == 0) {
+            const unsigned long long w = VT.key[s];
+            if (w != kEmpty64) lin4[u] = (uint32_t)(w >> 32);
+          } else {
+            const uint32_t w = ckey[s];
+            if (w != kEmpty32) lin4[u] = w;
+          }
         }
-      } else {
-        const uint32_t w = ckey[s];
-        if (w == kEmpty32) continue;
-        lin = w;
-        feat = (double)ccnt[s];
+        ba4[u] = lin4[u] != kNoVoxel ? (int)__ldg(&A.grid[lin4[u]]) : 0;
       }
-      const int bb = feature_bin(feat, g.clamp, g.bins);
-      const int ba = A.grid[lin];
-      atomicAdd(&hist[ba * W + bb], 1u);
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        if (lin4[u] == kNoVoxel) continue;
+        const int s = s0 + u * THREADS;
+        int bb;
+        if (KIND == 0) {
+          const double nd = (double)VT.cnt[s];
+          const double S1 = VT.s1[s], S2 = VT.s2[s];
+          VT.key[s] = kEmpty64; VT.cnt[s] = 0u; VT.s1[s] = 0.0; VT.s2[s] = 0.0;
+          const double rn = __drcp_rn(nd);
+          const double c1 = S1 * S1 * rn;
+          const double ssd = S2 - c1;
+          const double feat = (ssd > 0.0 ? ssd : 0.0) * rn;
+          const double x = feat * bin_scale;
+          const double k = rint(x);
+          if (k >= 1.0 && k <= bins_d - 1.0) {
+            const double tol = ((nd + 8.0) * 4.440892098500626e-16 * (S2 + c1) * rn +
+                                feat * 9.094947017729282e-13) * bin_scale + 1e-300;
+            if (fabs(x - k) <= tol) recheck = true;
+          }
+          const double f = floor(x);
+          bb = 1 + (f >= bins_d - 1.0 ? g.bins - 1 : (int)f);
+        } else {
+          const uint32_t n = ccnt[s];
+          ckey[s] = kEmpty32; ccnt[s] = 0u;
+          bb = n < (uint32_t)kCountLut ? (int)count_lut[n] : feature_bin((double)n, g.clamp, g.bins);
+        }
+        atomicAdd(&hist[ba4[u] * W + bb], 1u);
+      }
     }
     if (recheck) misc[8] = 1;
 
     // ---- A marginal over the region --------------------------------------
-    const bool full = rlo[0] == A.amin[0] && rlo[1] == A.amin[1] && rlo[2] == A.amin[2] &&
+    const bool cover_all = rlo[0] == A.amin[0] && rlo[1] == A.amin[1] && rlo[2] == A.amin[2] &&
                       rhi[0] == A.amax[0] && rhi[1] == A.amax[1] && rhi[2] == A.amax[2];
-    if (full) {
+    if (cover_all) {
       for (int i = tid; i < W; i += THREADS) marg[i] = A.bin_total[i];
     } else {
       const int lo0 = rlo[0] - A.amin[0], lo1 = rlo[1] - A.amin[1], lo2 = rlo[2] - A.amin[2];
       const int hi0 = rhi[0] - A.amin[0], hi1 = rhi[1] - A.amin[1], hi2 = rhi[2] - A.amin[2];
-      for (int j0 = wid * 32; j0 < A.n_avox; j0 += THREADS) {
-        const int j = j0 + lane;
-        bool in = false;
-        int bin = -1;
-        if (j < A.n_avox) {
-          const int4 v = __ldg(&A.avox[j]);
-          bin = v.w;
-          in = v.x >= lo0 && v.x <= hi0 && v.y >= lo1 && v.y <= hi1 && v.z >= lo2 && v.z <= hi2;
+      for (int j0 = wid * 32; j0 < A.n_avox; j0 += 2 * THREADS) {
+        int4 v[2];
+        bool in[2];
+        int bin[2];
+#pragma unroll
+        for (int u = 0; u < 2; ++u) {
+          const int j = j0 + u * THREADS + lane;
+          v[u] = j < A.n_avox ? __ldg(&A.avox[j]) : make_int4(-1, -1, -1, -1);
         }
-        const unsigned grp = __match_any_sync(0xffffffffu, bin) & __ballot_sync(0xffffffffu, in);
-        if (in && lane == __ffs(grp) - 1) atomicAdd(&marg[bin], (uint32_t)__popc(grp));
+#pragma unroll
+        for (int u = 0; u < 2; ++u) {
+          bin[u] = v[u].w;
+          in[u] = bin[u] >= 0 && v[u].x >= lo0 && v[u].x <= hi0 && v[u].y >= lo1 &&
+                  v[u].y <= hi1 && v[u].z >= lo2 && v[u].z <= hi2;
+          const unsigned grp =
+              __match_any_sync(0xffffffffu, bin[u]) & __ballot_sync(0xffffffffu, in[u]);
+          if (in[u] && lane == __ffs(grp) - 1) atomicAdd(&marg[bin[u]], (uint32_t)__popc(grp));
+        }
       }
     }
     __syncthreads();
@@ -362,9 +460,9 @@ __global__ void __launch_bounds__(THREADS, 1)
   }
 }
 
-template <int THREADS, int KIND, bool F32>
+template <int THREADS, int KIND, bool F32, int MODE>
 static cudaError_t launch_fast_t(const FastLaunch& fl, cudaStream_t st) {
-  auto k = k_pose_fast<THREADS, KIND, F32>;
+  auto k = k_pose_fast<THREADS, KIND, F32, MODE>;
   size_t smem = fast_smem_bytes(KIND, fl.cap, fl.g.bins, THREADS);
   cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e != cudaSuccess) return e;
@@ -373,17 +471,25 @@ static cudaError_t launch_fast_t(const FastLaunch& fl, cudaStream_t st) {
   return cudaGetLastError();
 }
 
-cudaError_t launch_fast(const FastLaunch& fl, cudaStream_t st) {
+template <int T, int KIND, bool F32>
+static cudaError_t launch_mode(const FastLaunch& fl, cudaStream_t st) {
+  switch (fl.g.mode) {
+    case kGridUnit: return launch_fast_t<T, KIND, F32, kGridUnit>(fl, st);
+    case kGridPow2: return launch_fast_t<T, KIND, F32, kGridPow2>(fl, st);
+    default: return launch_fast_t<T, KIND, F32, kGridGeneral>(fl, st);
+  }
+}
+
+template <int T>
+static cudaError_t launch_threads(const FastLaunch& fl, cudaStream_t st) {
   const bool f32 = fl.B.is_f32 != 0;
-  const int kind = fl.g.kind;
-  if (fl.B.threads == 1024) {
-    if (kind == 0) return f32 ? launch_fast_t<1024, 0, true>(fl, st) : launch_fast_t<1024, 0, false>(fl, st);
-    return f32 ? launch_fast_t<1024, 1, true>(fl, st) : launch_fast_t<1024, 1, false>(fl, st);
-  }
-  if (fl.B.threads == 512) {
-    if (kind == 0) return f32 ? launch_fast_t<512, 0, true>(fl, st) : launch_fast_t<512, 0, false>(fl, st);
-    return f32 ? launch_fast_t<512, 1, true>(fl, st) : launch_fast_t<512, 1, false>(fl, st);
-  }
+  if (fl.g.kind == 0) return f32 ? launch_mode<T, 0, true>(fl, st) : launch_mode<T, 0, false>(fl, st);
+  return f32 ? launch_mode<T, 1, true>(fl, st) : launch_mode<T, 1, false>(fl, st);
+}
+
+cudaError_t launch_fast(const FastLaunch& fl, cudaStream_t st) {
+  if (fl.B.threads == kFastThreads) return launch_threads<kFastThreads>(fl, st);
+  if (fl.B.threads == kFastThreadsAlt) return launch_threads<kFastThreadsAlt>(fl, st);
   return cudaErrorInvalidValue;
 }
 

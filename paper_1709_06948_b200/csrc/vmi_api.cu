@@ -48,8 +48,9 @@ struct vmi_ctx {
   void* d_pts = nullptr;
   int is_f32 = 0;
   int64_t nb = 0;
-  int64_t span = 0;
-  int threads = 512;
+  int span = 0;
+  int rem = 0;
+  int threads = kFastThreads;
   int cap_override = 0;
 
   ExactScratch ex;
@@ -108,6 +109,7 @@ QueryView query_view(const vmi_ctx* c) {
   B.is_f32 = c->is_f32;
   B.n = c->nb;
   B.span = c->span;
+  B.rem = c->rem;
   B.threads = c->threads;
   return B;
 }
@@ -296,11 +298,11 @@ int64_t vmi_launch_count(const vmi_ctx* c) { return c ? c->launches : 0; }
 
 int vmi_set_tuning(vmi_ctx* c, int table_cap_, int threads) {
   if (!c) return VMI_ERR_ARG;
-  if (threads != 0 && threads != 512 && threads != 1024)
-    return fail(c, VMI_ERR_ARG, "threads must be 512 or 1024");
+  if (threads != 0 && threads != kFastThreads && threads != kFastThreadsAlt)
+    return fail(c, VMI_ERR_ARG, "threads must be 0 (default), 512 or 768");
   if (table_cap_ < 0) return fail(c, VMI_ERR_ARG, "table_cap must be >= 0");
-  c->cap_override = table_cap_;
-  const int nt = threads ? threads : 512;
+  c->cap_override = (table_cap_ + 31) & ~31;  // the clear loop writes 16-byte words
+  const int nt = threads ? threads : kFastThreads;
   if (nt != c->threads && c->b_set) return fail(c, VMI_ERR_STATE, "set threads before scan B");
   c->threads = nt;
   return 0;
@@ -450,10 +452,11 @@ static int set_query(vmi_ctx* c, const void* host, int is_f32_src, int64_t n) {
   void* tmp = nullptr;
   CK(c, cudaMalloc(&tmp, up_bytes));
   CK(c, cudaMemcpyAsync(tmp, up, up_bytes, cudaMemcpyHostToDevice, c->stream));
-  c->span = (n + c->threads - 1) / c->threads;
+  c->span = (int)((n + c->threads - 1) / c->threads);
+  c->rem = (int)(n - (int64_t)(c->span - 1) * c->threads);
   const size_t rec = as_f32 ? 16 : 32;
   CK(c, cudaMalloc(&c->d_pts, (size_t)c->span * c->threads * rec));
-  CK(c, launch_span_layout(tmp, as_f32, n, c->span, c->threads, c->d_pts, c->stream));
+  CK(c, launch_span_layout(tmp, as_f32, n, c->span, c->rem, c->threads, c->d_pts, c->stream));
   c->launches += 1;
   CK(c, cudaStreamSynchronize(c->stream));
   cudaFree(tmp);

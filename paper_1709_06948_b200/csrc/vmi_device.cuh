@@ -41,6 +41,27 @@ __device__ __forceinline__ bool voxel_coord(double p, double origin, double res,
   return (unsigned long long)(k - kKeyMin) <= (unsigned long long)(kKeyMax - kKeyMin);
 }
 
+// Compile-time-specialised q = (p - origin) / resolution (voxel.py:199).
+template <int MODE>
+__device__ __forceinline__ double grid_q(double p, double origin, double res, double inv_res) {
+  if (MODE == kGridUnit) return p;
+  const double v = __dsub_rn(p, origin);
+  if (MODE == kGridPow2) return __dmul_rn(v, inv_res);  // exact: same real number as v/res
+  return __ddiv_rn(v, res);
+}
+
+// floor(q) as int32 via DADD.RM against 1.5*2^52 (bits(r) = bits(magic) + floor(q)).
+// `bad` collects any |floor(q)| >= 2^31 (and inf/nan): the high word must then
+// equal 0x43380000, or 0x4337FFFF for a negative result.  The +-2^20 key range
+// itself is checked once per pose on the reduced bounds.
+__device__ __forceinline__ int floor_i32(double q, unsigned& bad) {
+  const double r = __dadd_rd(q, 6755399441055744.0);
+  const int lo = __double2loint(r);
+  const unsigned hi = (unsigned)__double2hiint(r);
+  bad |= hi + ((unsigned)lo >> 31) - 0x43380000u;
+  return lo;
+}
+
 // ---- mi.py:72-79 bin_features: 1 + min(B-1, floor(v / clamp * B))
 __device__ __forceinline__ int feature_bin(double v, double clamp, int bins) {
   double x = __dmul_rn(__ddiv_rn(v, clamp), (double)bins);

@@ -80,7 +80,7 @@ cudaError_t launch_argmax(const double* v, int64_t P, double* out_val, long long
                           cudaStream_t st);
 
 // Reorder contiguous points into the fast path's span layout.
-cudaError_t launch_span_layout(const void* src, int is_f32, int64_t n, int64_t span, int threads,
-                               void* dst, cudaStream_t st);
+cudaError_t launch_span_layout(const void* src, int is_f32, int64_t n, int span, int rem,
+                               int threads, void* dst, cudaStream_t st);
 
 }  // namespace vmi

@@ -38,15 +38,47 @@ struct RefView {
   const uint32_t* bin_total;  // per-bin count of all A voxels (full-cover shortcut)
 };
 
-// Scan B in the fast path's "span layout": thread t of a CTA with T threads
-// owns original points [t*span, (t+1)*span); element r of that span is stored
-// at r*T + t so every warp load is 32 consecutive records.
+// Scan B in the fast path's "span layout".  The ring-ordered scan is cut into
+// T contiguous spans: the first `rem` spans hold `span` points, the others
+// `span - 1` (n = T*(span-1) + rem, 0 < rem <= T).  Span s is walked by thread
+// t = (s % NW)*32 + s / NW (NW = T/32 warps), so each warp's 32 lanes sample
+// the whole scan and every warp gets a similar share of voxel-run records
+// (far rings produce many more than near ones).  Element r of thread t's
+// span is stored at r*T + t: every warp load is 32 consecutive records.
+constexpr int kFastThreads = 512;     // default CTA size of the fast kernel
+constexpr int kFastThreadsAlt = 768;  // alternative (fewer registers per thread)
+
 struct QueryView {
   const void* pts;  // float4 (x, y, z, i) or double4 (x, y, z, pad)
   int is_f32;
   int64_t n;
-  int64_t span;
+  int span;
+  int rem;
   int threads;
 };
+
+__host__ __device__ inline int span_of_thread(int t, int threads) {
+  return (t & 31) * (threads >> 5) + (t >> 5);
+}
+
+__host__ __device__ inline int thread_of_span(int s, int threads) {
+  const int nw = threads >> 5;
+  return (s % nw) * 32 + s / nw;
+}
+
+// Layout slot of original point i (inverse of the ownership rule above).
+__host__ __device__ inline int64_t span_slot(int64_t i, int span, int rem, int threads) {
+  int64_t s, r;
+  const int64_t head = (int64_t)rem * span;
+  if (i < head) {
+    s = i / span;
+    r = i - s * span;
+  } else {
+    const int64_t j = i - head;
+    s = rem + j / (span - 1);
+    r = j - (s - rem) * (span - 1);
+  }
+  return r * threads + thread_of_span((int)s, threads);
+}
 
 }  // namespace vmi

@@ -1,0 +1,45 @@
+"""Multi-GPU pose sharding.
+
+Candidate poses are independent, so a batch is split into contiguous index
+ranges, one per rank, with scan A's grid and scan B replicated on every GPU
+(built locally; no broadcast).  The only exchange is the per-rank winner
+(max MI, global index): one all-gather of 16 bytes per rank over NCCL, after
+which every rank applies np.argmax's first-max rule.
+"""
+
+from __future__ import annotations
+
+import numpy as np
+
+
+def shard_bounds(P: int, world: int, rank: int) -> tuple[int, int]:
+    """Contiguous [lo, hi) range of rank ``rank`` (sizes differ by at most ceil)."""
+    per = -(-P // world) if world > 0 else P
+    lo = min(P, rank * per)
+    return lo, min(P, lo + per)
+
+
+def local_winner(mi: np.ndarray, offset: int) -> tuple[float, int]:
+    """np.argmax of one shard, as (value, global index); empty -> (-inf, big)."""
+    if mi.size == 0:
+        return float("-inf"), np.iinfo(np.int64).max
+    k = int(np.argmax(mi))
+    return float(mi[k]), offset + k
+
+
+def pick_global(winners: np.ndarray) -> tuple[float, int]:
+    """(W, 2) [mi, index] rows -> the np.argmax winner over the whole batch:
+    largest MI, lowest global index among equal maxima."""
+    w = np.asarray(winners, dtype=np.float64).reshape(-1, 2)
+    k = int(np.lexsort((w[:, 1], -w[:, 0]))[0])
+    return float(w[k, 0]), int(w[k, 1])
+
+
+def all_gather_winner(value: float, index: int, dist, device) -> tuple[float, int]:
+    """Exchange per-rank winners with torch.distributed (NCCL or gloo)."""
+    import torch
+    world = dist.get_world_size()
+    mine = torch.tensor([value, float(index)], dtype=torch.float64, device=device)
+    out = torch.empty(2 * world, dtype=torch.float64, device=device)
+    dist.all_gather_into_tensor(out, mine)
+    return pick_global(out.cpu().numpy())
