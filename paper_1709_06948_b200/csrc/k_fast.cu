@@ -128,13 +128,32 @@ size_t fast_smem_bytes(int kind, int cap, int bins, int threads) {
   return fast_layout(kind, cap, bins + 1, threads).total;
 }
 
-struct WarpQueue {
-  uint32_t* lin;
-  uint32_t* n;
-  double* K;
-  double* s1;
-  double* s2;
-};
+__device__ __forceinline__ void st_shared_v4(uint32_t a, uint32_t x, uint32_t y, uint32_t z,
+                                             uint32_t w) {
+  asm volatile("st.shared.v4.u32 [%0], {%1, %2, %3, %4};" ::"r"(a), "r"(x), "r"(y), "r"(z), "r"(w)
+               : "memory");
+}
+__device__ __forceinline__ void st_shared_v2(uint32_t a, uint32_t x, uint32_t y) {
+  asm volatile("st.shared.v2.u32 [%0], {%1, %2};" ::"r"(a), "r"(x), "r"(y) : "memory");
+}
+__device__ __forceinline__ uint4 ld_shared_v4(uint32_t a) {
+  uint4 v;
+  asm volatile("ld.shared.v4.u32 {%0, %1, %2, %3}, [%4];"
+               : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w)
+               : "r"(a)
+               : "memory");
+  return v;
+}
+__device__ __forceinline__ uint2 ld_shared_v2(uint32_t a) {
+  uint2 v;
+  asm volatile("ld.shared.v2.u32 {%0, %1}, [%2];" : "=r"(v.x), "=r"(v.y) : "r"(a) : "memory");
+  return v;
+}
+__device__ __forceinline__ uint32_t dlo(double d) { return (uint32_t)__double2loint(d); }
+__device__ __forceinline__ uint32_t dhi(double d) { return (uint32_t)__double2hiint(d); }
+__device__ __forceinline__ double mkd(uint32_t lo, uint32_t hi) {
+  return __hiloint2double((int)hi, (int)lo);
+}
 
 template <int THREADS, int KIND, bool F32, int MODE>
 __global__ void __launch_bounds__(THREADS, 1)
@@ -142,7 +161,6 @@ __global__ void __launch_bounds__(THREADS, 1)
                 int cap, double* __restrict__ mi_out, int32_t* __restrict__ status_out,
                 long long* __restrict__ hist_out, long long* __restrict__ total_out) {
   extern __shared__ __align__(16) unsigned char smem[];
-  constexpr int NW = THREADS / 32;
   const int W = g.bins + 1;
   const FastSmem L = fast_layout(KIND, cap, W, THREADS);
   uint32_t* hist = reinterpret_cast<uint32_t*>(smem + L.hist);
@@ -163,26 +181,17 @@ __global__ void __launch_bounds__(THREADS, 1)
   VarzTable VT;
   uint32_t* ckey = nullptr;
   uint32_t* ccnt = nullptr;
-  WarpQueue Q;
-  {
-    unsigned char* qb = smem + L.queue;
-    if (KIND == 0) {
-      VT.key = reinterpret_cast<unsigned long long*>(smem + L.table);
-      VT.s1 = reinterpret_cast<double*>(smem + L.table + (size_t)cap * 8);
-      VT.s2 = reinterpret_cast<double*>(smem + L.table + (size_t)cap * 16);
-      VT.cnt = reinterpret_cast<uint32_t*>(smem + L.table + (size_t)cap * 24);
-      Q.K = reinterpret_cast<double*>(qb) + wid * kQueue;
-      Q.s1 = reinterpret_cast<double*>(qb + (size_t)NW * kQueue * 8) + wid * kQueue;
-      Q.s2 = reinterpret_cast<double*>(qb + (size_t)NW * kQueue * 16) + wid * kQueue;
-      Q.lin = reinterpret_cast<uint32_t*>(qb + (size_t)NW * kQueue * 24) + wid * kQueue;
-      Q.n = reinterpret_cast<uint32_t*>(qb + (size_t)NW * kQueue * 28) + wid * kQueue;
-    } else {
-      ckey = reinterpret_cast<uint32_t*>(smem + L.table);
-      ccnt = reinterpret_cast<uint32_t*>(smem + L.table + (size_t)cap * 4);
-      Q.lin = reinterpret_cast<uint32_t*>(qb) + wid * kQueue;
-      Q.n = reinterpret_cast<uint32_t*>(qb + (size_t)NW * kQueue * 4) + wid * kQueue;
-      Q.K = Q.s1 = Q.s2 = nullptr;
-    }
+  // warp queue: AoS records, VARZ 32 B {lin, n, K, S1, S2}, COUNT 8 B {lin, n}
+  constexpr uint32_t kRec = KIND == 0 ? 32u : 8u;
+  const uint32_t qbase = (uint32_t)__cvta_generic_to_shared(smem + L.queue) + wid * kQueue * kRec;
+  if (KIND == 0) {
+    VT.key = reinterpret_cast<unsigned long long*>(smem + L.table);
+    VT.s1 = reinterpret_cast<double*>(smem + L.table + (size_t)cap * 8);
+    VT.s2 = reinterpret_cast<double*>(smem + L.table + (size_t)cap * 16);
+    VT.cnt = reinterpret_cast<uint32_t*>(smem + L.table + (size_t)cap * 24);
+  } else {
+    ckey = reinterpret_cast<uint32_t*>(smem + L.table);
+    ccnt = reinterpret_cast<uint32_t*>(smem + L.table + (size_t)cap * 4);
   }
 
   // The table is cleared once here; afterwards the per-pose table walk resets
@@ -212,44 +221,75 @@ __global__ void __launch_bounds__(THREADS, 1)
     const double m0 = mat_s[0], m1 = mat_s[1], m2 = mat_s[2], m3 = mat_s[3], m4 = mat_s[4],
                  m5 = mat_s[5], m6 = mat_s[6], m7 = mat_s[7], m8 = mat_s[8], t0 = mat_s[9],
                  t1 = mat_s[10], t2 = mat_s[11];
+    // Every |q| < 2^30 here (rotation rows bound |R p| by sum|R_jk| * max|p|), so
+    // floor(q) fits int32 without a per-point check; the +-2^20 key range is
+    // checked exactly on the reduced bounds.  Poses beyond that (translations
+    // of ~1e9 voxels) go to the exact path, which reports KEY_RANGE.
+    {
+      const double lim = 1073741824.0 * g.res;
+      const double mx = B.max_abs;
+      const bool unsafe =
+          fabs(t0 - g.origin[0]) + (fabs(m0) + fabs(m1) + fabs(m2)) * mx >= lim ||
+          fabs(t1 - g.origin[1]) + (fabs(m3) + fabs(m4) + fabs(m5)) * mx >= lim ||
+          fabs(t2 - g.origin[2]) + (fabs(m6) + fabs(m7) + fabs(m8)) * mx >= lim;
+      if (unsafe) {
+        if (tid == 0) {
+          mi_out[p] = -1e300;
+          status_out[p] = 0x100;
+          if (total_out) total_out[p] = 0;
+        }
+        __syncthreads();
+        continue;
+      }
+    }
 
     // ---- pass over this thread's span of scan B --------------------------
     int bmin0 = INT_MAX, bmin1 = INT_MAX, bmin2 = INT_MAX;
     int bmax0 = INT_MIN, bmax1 = INT_MIN, bmax2 = INT_MIN;
-    unsigned badacc = 0u;
     uint32_t cur = kNoVoxel;
     int cn = 0;
     double cK = 0.0, cs1 = 0.0, cs2 = 0.0;
     uint32_t qh = 0, qt = 0;  // warp-uniform queue head / tail
 
-    auto drain32 = [&]() {  // whole warp: flush records [qh, qh+32)
-      __syncwarp();
-      const int i = (qh + lane) & (kQueue - 1);
-      if (KIND == 0) flush_varz(VT, ucap, Q.lin[i], (int)Q.n[i], Q.K[i], Q.s1[i], Q.s2[i], &misc[7]);
-      else flush_count(ckey, ccnt, ucap, Q.lin[i], (int)Q.n[i], &misc[7]);
-      qh += 32;
-      __syncwarp();
+    auto flush_rec = [&](uint32_t idx) {  // one queued record -> table
+      const uint32_t a = qbase + (idx & (kQueue - 1)) * kRec;
+      if (KIND == 0) {
+        const uint4 r0 = ld_shared_v4(a), r1 = ld_shared_v4(a + 16);
+        flush_varz(VT, ucap, r0.x, (int)r0.y, mkd(r0.z, r0.w), mkd(r1.x, r1.y), mkd(r1.z, r1.w),
+                   &misc[7]);
+      } else {
+        const uint2 r0 = ld_shared_v2(a);
+        flush_count(ckey, ccnt, ucap, r0.x, (int)r0.y, &misc[7]);
+      }
     };
     auto push = [&](bool do_push) {  // whole warp: enqueue the finished runs of some lanes
       const unsigned m = __ballot_sync(0xffffffffu, do_push);
       if (m == 0u) return;
       if (do_push) {
-        const int i = (qt + __popc(m & lt_mask)) & (kQueue - 1);
-        Q.lin[i] = cur;
-        Q.n[i] = (uint32_t)cn;
-        if (KIND == 0) { Q.K[i] = cK; Q.s1[i] = cs1; Q.s2[i] = cs2; }
+        const uint32_t a = qbase + ((qt + __popc(m & lt_mask)) & (kQueue - 1)) * kRec;
+        if (KIND == 0) {
+          st_shared_v4(a, cur, (uint32_t)cn, dlo(cK), dhi(cK));
+          st_shared_v4(a + 16, dlo(cs1), dhi(cs1), dlo(cs2), dhi(cs2));
+        } else {
+          st_shared_v2(a, cur, (uint32_t)cn);
+        }
       }
       qt += __popc(m);
-      if (qt - qh >= 32) drain32();
+      if (qt - qh >= 32) {  // drain 32 records, whole warp converged
+        __syncwarp();
+        flush_rec(qh + lane);
+        qh += 32;
+        __syncwarp();
+      }
     };
     // one point: transform, voxel, bounds, run aggregation (valid = real point)
     auto point = [&](double x, double y, double z, bool valid) {
       const double X = xform_row(x, y, z, m0, m1, m2, t0);
       const double Y = xform_row(x, y, z, m3, m4, m5, t1);
       const double Z = xform_row(x, y, z, m6, m7, m8, t2);
-      const int ix = floor_i32(grid_q<MODE>(X, g.origin[0], g.res, g.inv_res), badacc);
-      const int iy = floor_i32(grid_q<MODE>(Y, g.origin[1], g.res, g.inv_res), badacc);
-      const int iz = floor_i32(grid_q<MODE>(Z, g.origin[2], g.res, g.inv_res), badacc);
+      const int ix = floor_i32(grid_q<MODE>(X, g.origin[0], g.res, g.inv_res));
+      const int iy = floor_i32(grid_q<MODE>(Y, g.origin[1], g.res, g.inv_res));
+      const int iz = floor_i32(grid_q<MODE>(Z, g.origin[2], g.res, g.inv_res));
       uint32_t lin = kNoVoxel;
       if (valid) {
         bmin0 = min(bmin0, ix); bmax0 = max(bmax0, ix);
@@ -275,7 +315,7 @@ __global__ void __launch_bounds__(THREADS, 1)
     const Rec* pts = reinterpret_cast<const Rec*>(B.pts) + tid;
     const int full = B.span - 1;          // iterations every thread owns
     const bool has_last = span_of_thread(tid, THREADS) < B.rem;  // spans with one more point
-    constexpr int PF = 4;                 // prefetch depth (points per thread)
+    constexpr int PF = THREADS >= 768 ? 2 : 4;  // prefetch depth (points per thread)
     Rec cb[PF];
 #pragma unroll
     for (int u = 0; u < PF; ++u) cb[u] = u < full ? pts[u * THREADS] : Rec{};
@@ -298,12 +338,7 @@ __global__ void __launch_bounds__(THREADS, 1)
     push(cur != kNoVoxel);
     while (qh != qt) {  // drain the tail (partial round)
       __syncwarp();
-      const uint32_t i = qh + lane;
-      if (i - qh < qt - qh) {
-        const int j = i & (kQueue - 1);
-        if (KIND == 0) flush_varz(VT, ucap, Q.lin[j], (int)Q.n[j], Q.K[j], Q.s1[j], Q.s2[j], &misc[7]);
-        else flush_count(ckey, ccnt, ucap, Q.lin[j], (int)Q.n[j], &misc[7]);
-      }
+      if ((uint32_t)lane < qt - qh) flush_rec(qh + lane);
       qh = (qt - qh > 32u) ? qh + 32 : qt;
       __syncwarp();
     }
@@ -314,11 +349,9 @@ __global__ void __launch_bounds__(THREADS, 1)
     bmax0 = __reduce_max_sync(0xffffffffu, bmax0);
     bmax1 = __reduce_max_sync(0xffffffffu, bmax1);
     bmax2 = __reduce_max_sync(0xffffffffu, bmax2);
-    const bool anybad = __any_sync(0xffffffffu, badacc != 0u);
     if (lane == 0) {
       atomicMin(&misc[0], bmin0); atomicMin(&misc[1], bmin1); atomicMin(&misc[2], bmin2);
       atomicMax(&misc[3], bmax0); atomicMax(&misc[4], bmax1); atomicMax(&misc[5], bmax2);
-      if (anybad) misc[6] = 1;
     }
     __syncthreads();
     // voxel.py:200-206: any index outside [-2^20, 2^20-1] -> OutOfBoundsError

@@ -50,6 +50,7 @@ struct vmi_ctx {
   int64_t nb = 0;
   int span = 0;
   int rem = 0;
+  double max_abs = 0.0;
   int threads = kFastThreads;
   int cap_override = 0;
 
@@ -111,6 +112,7 @@ QueryView query_view(const vmi_ctx* c) {
   B.span = c->span;
   B.rem = c->rem;
   B.threads = c->threads;
+  B.max_abs = c->max_abs;
   return B;
 }
 
@@ -449,6 +451,14 @@ static int set_query(vmi_ctx* c, const void* host, int is_f32_src, int64_t n) {
       up_bytes = (size_t)n * 24;
     }
   }
+  double mx = 0.0;
+  for (int64_t i = 0; i < n; ++i)
+    for (int j = 0; j < 3; ++j) {
+      const double v = is_f32_src ? (double)static_cast<const float*>(host)[4 * i + j]
+                                  : static_cast<const double*>(host)[3 * i + j];
+      mx = std::fmax(mx, std::fabs(v));
+    }
+  c->max_abs = mx;
   void* tmp = nullptr;
   CK(c, cudaMalloc(&tmp, up_bytes));
   CK(c, cudaMemcpyAsync(tmp, up, up_bytes, cudaMemcpyHostToDevice, c->stream));

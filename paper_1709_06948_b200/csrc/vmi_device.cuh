@@ -50,16 +50,10 @@ __device__ __forceinline__ double grid_q(double p, double origin, double res, do
   return __ddiv_rn(v, res);
 }
 
-// floor(q) as int32 via DADD.RM against 1.5*2^52 (bits(r) = bits(magic) + floor(q)).
-// `bad` collects any |floor(q)| >= 2^31 (and inf/nan): the high word must then
-// equal 0x43380000, or 0x4337FFFF for a negative result.  The +-2^20 key range
-// itself is checked once per pose on the reduced bounds.
-__device__ __forceinline__ int floor_i32(double q, unsigned& bad) {
-  const double r = __dadd_rd(q, 6755399441055744.0);
-  const int lo = __double2loint(r);
-  const unsigned hi = (unsigned)__double2hiint(r);
-  bad |= hi + ((unsigned)lo >> 31) - 0x43380000u;
-  return lo;
+// floor(q) as int32 via DADD.RM against 1.5*2^52: bits(r) = bits(magic) + floor(q),
+// so the low word is floor(q) whenever |q| < 2^31 (callers guarantee |q| < 2^30).
+__device__ __forceinline__ int floor_i32(double q) {
+  return __double2loint(__dadd_rd(q, 6755399441055744.0));
 }
 
 // ---- mi.py:72-79 bin_features: 1 + min(B-1, floor(v / clamp * B))

@@ -55,6 +55,7 @@ struct QueryView {
   int span;
   int rem;
   int threads;
+  double max_abs;  // max |coordinate| of scan B (pose safety bound)
 };
 
 __host__ __device__ inline int span_of_thread(int t, int threads) {
