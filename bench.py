@@ -220,11 +220,19 @@ def run_ours(args, world, rank, local):
     import paper_1709_06948_b200 as vmi
     from paper_1709_06948_b200 import _lib
 
+    # one rank per GPU; VMI_DIST_BACKEND=gloo exercises the N>1 code path on a
+    # box with fewer GPUs (functional check only: ranks then share devices)
+    backend = os.environ.get("VMI_DIST_BACKEND", "nccl")
+    local = local % max(1, torch.cuda.device_count())
     torch.cuda.set_device(local)
     dist = None
     if world > 1:
         import torch.distributed as dist
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        if backend == "nccl":
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        else:
+            dist.init_process_group(backend)
+    cdev = f"cuda:{local}" if backend == "nccl" else "cpu"  # collective tensors
     a, b, poses_all = workload(world, args.poses)
     from paper_1709_06948_b200.shard import pick_global, shard_bounds
     lo, hi = shard_bounds(poses_all.shape[0], world, rank)
@@ -248,8 +256,8 @@ def run_ours(args, world, rank, local):
     mi = torch.empty(P, dtype=torch.float64, device=f"cuda:{local}")
     st = torch.empty(P, dtype=torch.int32, device=f"cuda:{local}")
     flush = torch.empty(256 * 1024 * 1024 // 4, dtype=torch.float32, device=f"cuda:{local}")
-    winner = torch.empty(2, dtype=torch.float64, device=f"cuda:{local}")
-    gathered = torch.empty(2 * world, dtype=torch.float64, device=f"cuda:{local}")
+    winner = torch.empty(2, dtype=torch.float64, device=cdev)
+    gathered = [torch.empty(2, dtype=torch.float64, device=cdev) for _ in range(world)]
 
     fixups_total = 0
 
@@ -267,8 +275,8 @@ def run_ours(args, world, rank, local):
             with torch.cuda.stream(stream):
                 winner[0] = best
                 winner[1] = float(lo + idx)
-                dist.all_gather_into_tensor(gathered, winner)
-                g = gathered.cpu().numpy()
+                dist.all_gather(gathered, winner)
+                g = torch.stack(gathered).cpu().numpy()
             return pick_global(g)
         return best, lo + idx
 
@@ -296,7 +304,7 @@ def run_ours(args, world, rank, local):
     launches = ctx.launches - launches0
     total_ms = float(sum(step_ms))
     if dist:
-        t = torch.tensor([total_ms], dtype=torch.float64, device=f"cuda:{local}")
+        t = torch.tensor([total_ms], dtype=torch.float64, device=cdev)
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         total_ms = float(t.item())
         dist.barrier()
@@ -315,7 +323,7 @@ def run_ours(args, world, rank, local):
         e2e_times.append(time.perf_counter() - t0)
     e2e_s = float(np.mean(e2e_times))
     if dist:
-        t = torch.tensor([e2e_s], dtype=torch.float64, device=f"cuda:{local}")
+        t = torch.tensor([e2e_s], dtype=torch.float64, device=cdev)
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         e2e_s = float(t.item())
     e2e_value = P * world / e2e_s

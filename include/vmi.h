@@ -123,6 +123,12 @@ int vmi_eval_exact(vmi_ctx* ctx, const double* mats, int64_t P, double* mi_out,
 int vmi_query_features(vmi_ctx* ctx, const double mat[12], int64_t* keys, double* values,
                        int64_t cap, int64_t* n_out, int64_t bounds[6], int32_t* status);
 
+/* Debug / parity: B's per-voxel features at one pose as the FAST path computed
+   them (voxels inside scan A's AABB only; VARZ from the pivot-shifted sums),
+   unsorted.  *n_out = number of voxels (may exceed cap: then nothing copied). */
+int vmi_fast_features(vmi_ctx* ctx, const double mat[12], int64_t* keys, double* values,
+                      int64_t cap, int64_t* n_out, int32_t* status);
+
 /* Device-side argmax over mi (first index of the max, np.argmax semantics,
    cli.py:202).  Writes best value and index to host. */
 int vmi_argmax_device(vmi_ctx* ctx, const double* mi_dev, int64_t P, double* best_mi,

@@ -26,6 +26,7 @@ EXPORTS = (
     "vmi_set_reference_points", "vmi_set_reference_features", "vmi_get_reference_features",
     "vmi_set_query_points", "vmi_set_query_records_f32", "vmi_poses_to_mats", "vmi_eval",
     "vmi_eval_device", "vmi_eval_fixups", "vmi_eval_exact", "vmi_query_features",
+    "vmi_fast_features",
     "vmi_argmax_device", "vmi_launch_count", "vmi_set_tuning",
 )
 
@@ -72,6 +73,7 @@ def load(path: str = LIB_PATH):
     L.vmi_eval_fixups.argtypes = [_ctx, _vp, ctypes.c_int64, _vp, _vp, _vp, _vp, _vp, _i64]
     L.vmi_eval_exact.argtypes = [_ctx, _d, ctypes.c_int64, _d, _i32, _i64, _i64]
     L.vmi_query_features.argtypes = [_ctx, _d, _i64, _d, ctypes.c_int64, _i64, _i64, _i32]
+    L.vmi_fast_features.argtypes = [_ctx, _d, _i64, _d, ctypes.c_int64, _i64, _i32]
     L.vmi_argmax_device.argtypes = [_ctx, _vp, ctypes.c_int64, _d, _i64, _vp]
     L.vmi_launch_count.argtypes = [_ctx]
     L.vmi_launch_count.restype = ctypes.c_int64
@@ -217,6 +219,21 @@ class Context:
         self.check(self._L.vmi_argmax_device(self._h, mi_ptr, P, ctypes.byref(v), ctypes.byref(i),
                                              stream or None), "vmi_argmax_device")
         return float(v.value), int(i.value)
+
+    def fast_features(self, mat12: np.ndarray, cap: int):
+        """B's features at one pose from the fast path (inside A's AABB), sorted by key."""
+        m = np.ascontiguousarray(mat12, dtype=np.float64).reshape(12)
+        keys = np.empty(max(cap, 1), dtype=np.int64)
+        vals = np.empty(max(cap, 1), dtype=np.float64)
+        n = ctypes.c_int64(0)
+        st = ctypes.c_int32(0)
+        self.check(self._L.vmi_fast_features(self._h, ptr(m, _d), ptr(keys, _i64), ptr(vals, _d),
+                                             keys.size, ctypes.byref(n), ctypes.byref(st)),
+                   "vmi_fast_features")
+        if n.value > cap:
+            raise VmiError(f"fast_features: {n.value} voxels > capacity {cap}")
+        order = np.argsort(keys[:n.value], kind="stable")
+        return keys[:n.value][order], vals[:n.value][order], int(st.value)
 
     def query_features(self, mat12: np.ndarray, cap: int):
         m = np.ascontiguousarray(mat12, dtype=np.float64).reshape(12)

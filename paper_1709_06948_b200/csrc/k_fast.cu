@@ -159,7 +159,8 @@ template <int THREADS, int KIND, bool F32, int MODE>
 __global__ void __launch_bounds__(THREADS, 1)
     k_pose_fast(GridParams g, RefView A, QueryView B, const double* __restrict__ mats, int64_t P,
                 int cap, double* __restrict__ mi_out, int32_t* __restrict__ status_out,
-                long long* __restrict__ hist_out, long long* __restrict__ total_out) {
+                long long* __restrict__ hist_out, long long* __restrict__ total_out,
+                FeatureDump dump) {
   extern __shared__ __align__(16) unsigned char smem[];
   const int W = g.bins + 1;
   const FastSmem L = fast_layout(KIND, cap, W, THREADS);
@@ -420,6 +421,7 @@ __global__ void __launch_bounds__(THREADS, 1)
         if (lin4[u] == kNoVoxel) continue;
         const int s = s0 + u * THREADS;
         int bb;
+        double dump_feat = 0.0;
         if (KIND == 0) {
           const double nd = (double)VT.cnt[s];
           const double S1 = VT.s1[s], S2 = VT.s2[s];
@@ -437,12 +439,27 @@ __global__ void __launch_bounds__(THREADS, 1)
           }
           const double f = floor(x);
           bb = 1 + (f >= bins_d - 1.0 ? g.bins - 1 : (int)f);
+          dump_feat = feat;
         } else {
           const uint32_t n = ccnt[s];
           ckey[s] = kEmpty32; ccnt[s] = 0u;
           bb = n < (uint32_t)kCountLut ? (int)count_lut[n] : feature_bin((double)n, g.clamp, g.bins);
+          dump_feat = (double)n;
         }
         atomicAdd(&hist[ba4[u] * W + bb], 1u);
+        if (dump.keys) {  // debug export (vmi_fast_features): lin -> packed key, feature
+          const int j = atomicAdd(dump.n, 1);
+          if (j < dump.cap) {
+            const uint32_t l = lin4[u];
+            const uint32_t rz = l % A.ext[2], rxy = l / A.ext[2];
+            const uint32_t ry = rxy % A.ext[1], rx = rxy / A.ext[1];
+            const unsigned long long off = 1ull << 20;
+            dump.keys[j] = ((unsigned long long)(long long)((int)rx + A.amin[0]) + off) << 42 |
+                           ((unsigned long long)(long long)((int)ry + A.amin[1]) + off) << 21 |
+                           ((unsigned long long)(long long)((int)rz + A.amin[2]) + off);
+            dump.values[j] = dump_feat;
+          }
+        }
       }
     }
     if (recheck) misc[8] = 1;
@@ -500,7 +517,7 @@ static cudaError_t launch_fast_t(const FastLaunch& fl, cudaStream_t st) {
   cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e != cudaSuccess) return e;
   k<<<fl.grid, THREADS, smem, st>>>(fl.g, fl.A, fl.B, fl.mats, fl.P, fl.cap, fl.mi, fl.status,
-                                    fl.hist, fl.total);
+                                    fl.hist, fl.total, fl.dump);
   return cudaGetLastError();
 }
 

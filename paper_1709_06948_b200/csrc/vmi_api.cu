@@ -583,6 +583,53 @@ int vmi_query_features(vmi_ctx* c, const double mat[12], int64_t* keys, double* 
   return 0;
 }
 
+int vmi_fast_features(vmi_ctx* c, const double mat[12], int64_t* keys, double* values, int64_t cap,
+                      int64_t* n_out, int32_t* status) {
+  int rc = check_ready(c);
+  if (rc) return rc;
+  if (!mat || !n_out || cap < 0) return fail(c, VMI_ERR_ARG, "bad arguments");
+  cudaSetDevice(c->device);
+  if ((rc = ensure_P(c, 1, false))) return rc;
+  const int64_t m = cap > 0 ? cap : 1;
+  unsigned long long* dk = nullptr;
+  double* dv = nullptr;
+  int* dn = nullptr;
+  CK(c, cudaMalloc(&dk, 8 * m));
+  CK(c, cudaMalloc(&dv, 8 * m));
+  CK(c, cudaMalloc(&dn, 4));
+  CK(c, cudaMemsetAsync(dn, 0, 4, c->stream));
+  CK(c, cudaMemcpyAsync(c->d_mats, mat, 96, cudaMemcpyHostToDevice, c->stream));
+  FastLaunch fl{};
+  fl.g = c->g;
+  fl.A = ref_view(c);
+  fl.B = query_view(c);
+  fl.mats = c->d_mats;
+  fl.P = 1;
+  fl.cap = table_cap(c);
+  fl.grid = 1;
+  fl.mi = c->d_mi;
+  fl.status = c->d_status;
+  fl.total = c->d_total;
+  fl.dump.keys = dk;
+  fl.dump.values = dv;
+  fl.dump.n = dn;
+  fl.dump.cap = (int)m;
+  CK(c, launch_fast(fl, c->stream));
+  c->launches += 1;
+  int n = 0;
+  CK(c, cudaMemcpyAsync(&n, dn, 4, cudaMemcpyDeviceToHost, c->stream));
+  CK(c, cudaMemcpyAsync(status, c->d_status, 4, cudaMemcpyDeviceToHost, c->stream));
+  CK(c, cudaStreamSynchronize(c->stream));
+  *n_out = n;
+  if (n <= cap && n > 0 && keys) {
+    CK(c, cudaMemcpyAsync(keys, dk, 8 * (size_t)n, cudaMemcpyDeviceToHost, c->stream));
+    if (values) CK(c, cudaMemcpyAsync(values, dv, 8 * (size_t)n, cudaMemcpyDeviceToHost, c->stream));
+    CK(c, cudaStreamSynchronize(c->stream));
+  }
+  cudaFree(dk); cudaFree(dv); cudaFree(dn);
+  return 0;
+}
+
 int vmi_argmax_device(vmi_ctx* c, const double* mi_dev, int64_t P, double* best_mi,
                       int64_t* best_idx, void* stream) {
   if (!c || !mi_dev || P <= 0 || !best_mi || !best_idx) return VMI_ERR_ARG;

@@ -9,6 +9,12 @@
 namespace vmi {
 
 // ---- K1 fast path (k_fast.cu) ---------------------------------------------
+struct FeatureDump {
+  unsigned long long* keys = nullptr;  // packed reference keys (pack_keys)
+  double* values = nullptr;            // VARZ / COUNT as the fast path computed it
+  int* n = nullptr;                    // device counter
+  int cap = 0;
+};
 struct FastLaunch {
   GridParams g;
   RefView A;
@@ -21,6 +27,7 @@ struct FastLaunch {
   int32_t* status;
   long long* hist;
   long long* total;
+  FeatureDump dump;  // debug: B's per-voxel features from the fast path (P == 1)
 };
 size_t fast_smem_bytes(int kind, int cap, int bins, int threads);
 cudaError_t launch_fast(const FastLaunch& fl, cudaStream_t st);

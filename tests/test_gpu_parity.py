@@ -314,3 +314,34 @@ def test_argmax_device_first_index():
     v = torch.tensor([0.1, 0.5, 0.2, 0.5, -1e300], dtype=torch.float64, device="cuda")
     best, idx = eng.ctx.argmax_device(v.data_ptr(), 5)
     assert (best, idx) == (0.5, 1)
+
+
+def unpack(keys):
+    k = np.asarray(keys, dtype=np.int64)
+    m = (1 << 21) - 1
+    return np.stack([(k >> 42) & m, (k >> 21) & m, k & m], axis=1) - (1 << 20)
+
+
+@pytest.mark.parametrize("tag,res,kind", [("v1", 1.0, "varz"), ("c1", 1.0, "count")])
+def test_fast_path_features_match_reference(tag, res, kind):
+    """The fused kernel's own per-voxel features (pivot-shifted VARZ sums) for
+    scan B at the truth pose: voxel ids and COUNT exact, VARZ within 1e-6."""
+    g = golden("hdl_golden.npz")
+    a, b = hdl_pair()
+    eng = engine(res, kind=kind)
+    eng.set_reference(a[:, :3].astype(np.float64))
+    eng.set_query(b)
+    keys, vals, st = eng.ctx.fast_features(vmi.poses_to_mats(g["poses"][:1])[0], 50000)
+    assert st == 0
+    bk, bv = g[f"{tag}_b_keys"], g[f"{tag}_b_values"]
+    lo, hi = g[f"{tag}_a_bounds"]
+    ijk = unpack(bk)
+    inside = ((ijk >= lo) & (ijk <= hi)).all(axis=1)
+    np.testing.assert_array_equal(keys, bk[inside])
+    if kind == "count":
+        np.testing.assert_array_equal(vals, bv[inside])
+    else:
+        want = bv[inside]
+        np.testing.assert_allclose(vals, want, rtol=1e-6, atol=1e-18)
+        rel = np.abs(vals - want) / np.maximum(np.abs(want), 1e-300)
+        assert np.max(rel[want > 1e-12]) < 1e-11  # measured headroom, not the bar
