@@ -299,8 +299,8 @@ __global__ void __launch_bounds__(THREADS, 1)
         const uint32_t rx = (uint32_t)(ix - A.amin[0]);
         const uint32_t ry = (uint32_t)(iy - A.amin[1]);
         const uint32_t rz = (uint32_t)(iz - A.amin[2]);
-        if (rx < A.ext[0] && ry < A.ext[1] && rz < A.ext[2])
-          lin = (rx * A.ext[1] + ry) * A.ext[2] + rz;
+        const bool inside = (rx < A.ext[0]) & (ry < A.ext[1]) & (rz < A.ext[2]);
+        lin = inside ? (rx * A.ext[1] + ry) * A.ext[2] + rz : kNoVoxel;
       }
       const bool ends = lin != cur;
       push(ends && cur != kNoVoxel);

@@ -149,34 +149,40 @@ __device__ MIOut finalize_mi(uint32_t* hist, const uint32_t* marg, int W, long l
                              int include_phi, double* red /* >= 3*THREADS/32 doubles */,
                              long long* rows /* W */, long long* cols /* W */,
                              long long* h00_s /* 1 */) {
-  const int tid = threadIdx.x;
-  // rows a >= 1: A-only voxels pair with the phi column (mi.py:146-156)
-  for (int a = 1 + tid; a < W; a += THREADS) {
-    uint32_t occ = 0;
-    for (int b = 1; b < W; ++b) occ += hist[a * W + b];
-    hist[a * W] = marg[a] - occ;
+  const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
+  constexpr int NW = THREADS / 32;
+  // (1) rows a >= 1: A-only voxels pair with the phi column (mi.py:146-156);
+  //     one warp per row, two cells per lane (W <= 65)
+  for (int a = 1 + wid; a < W; a += NW) {
+    uint32_t v = 0;
+    if (lane + 1 < W) v += hist[a * W + lane + 1];
+    if (lane + 33 < W) v += hist[a * W + lane + 33];
+    v = __reduce_add_sync(0xffffffffu, v);
+    if (lane == 0) hist[a * W] = marg[a] - v;
   }
-  __syncthreads();
-  if (tid == 0) {
-    long long s = 0;
-    for (int a = 1; a < W; ++a) s += marg[a];
-    for (int b = 1; b < W; ++b) s += hist[b];
-    *h00_s = n_region - s;  // mi.py:158-159
+  // (2) (phi, phi) = region - |A in region| - |B-only in region|  (mi.py:158-159)
+  if (wid == NW - 1) {
+    uint32_t v = 0;
+    for (int i = 1 + lane; i < W; i += 32) v += marg[i] + hist[i];
+    v = __reduce_add_sync(0xffffffffu, v);
+    if (lane == 0) *h00_s = n_region - (long long)v;
   }
   __syncthreads();
   const long long h00 = *h00_s;
   const int o = include_phi ? 0 : 1;
   const int m = W - o;
-  // exact int64 marginals (m.sum(axis=1), m.sum(axis=0))
-  for (int a = tid; a < m; a += THREADS) {
-    long long rs = 0, cs = 0;
-    for (int b = 0; b < m; ++b) {
-      int ra = a + o, cb = b + o;
-      rs += (ra == 0 && cb == 0) ? h00 : (long long)hist[ra * W + cb];
-      cs += (cb == 0 && ra == 0) ? h00 : (long long)hist[cb * W + ra];
-    }
-    rows[a] = rs;
-    cols[a] = cs;
+  auto cell = [&](int a, int b) -> long long {
+    return (a == 0 && b == 0) ? h00 : (long long)hist[a * W + b];
+  };
+  // (3) exact int64 marginals m.sum(axis=1) / m.sum(axis=0): one warp per line
+  for (int j = wid; j < 2 * m; j += NW) {
+    const bool is_row = j < m;
+    const int x = (is_row ? j : j - m) + o;
+    long long v = 0;
+    for (int y = o + lane; y < W; y += 32) v += is_row ? cell(x, y) : cell(y, x);
+#pragma unroll
+    for (int off = 16; off > 0; off >>= 1) v += __shfl_xor_sync(0xffffffffu, v, off);
+    if (lane == 0) (is_row ? rows : cols)[x - o] = v;
   }
   __syncthreads();
   long long total = 0;
@@ -188,26 +194,23 @@ __device__ MIOut finalize_mi(uint32_t* hist, const uint32_t* marg, int W, long l
     out.mi = out.hx = out.hy = out.hxy = 0.0;
     return out;
   }
-  const double tot = (double)total;
+  // (4) -sum p log p, fixed-order block reduction (deterministic)
+  const double inv_tot = 1.0 / (double)total;
   double sx = 0.0, sy = 0.0, sxy = 0.0;
   for (int i = tid; i < m * m; i += THREADS) {
-    int a = i / m + o, b = i % m + o;
-    long long c = (a == 0 && b == 0) ? h00 : (long long)hist[a * W + b];
+    const long long c = cell(i / m + o, i % m + o);
     if (c > 0) {
-      double p = (double)c / tot;
+      const double p = (double)c * inv_tot;
       sxy += p * log(p);
     }
   }
   for (int i = tid; i < m; i += THREADS) {
-    if (rows[i] > 0) { double p = (double)rows[i] / tot; sx += p * log(p); }
-    if (cols[i] > 0) { double p = (double)cols[i] / tot; sy += p * log(p); }
+    if (rows[i] > 0) { const double p = (double)rows[i] * inv_tot; sx += p * log(p); }
+    if (cols[i] > 0) { const double p = (double)cols[i] * inv_tot; sy += p * log(p); }
   }
   sx = warp_sum(sx);
   sy = warp_sum(sy);
   sxy = warp_sum(sxy);
-  const int wid = tid >> 5, lane = tid & 31;
-  constexpr int NW = THREADS / 32;
-  __syncthreads();
   if (lane == 0) { red[wid] = sx; red[NW + wid] = sy; red[2 * NW + wid] = sxy; }
   __syncthreads();
   double hx = 0.0, hy = 0.0, hxy = 0.0;
