@@ -313,6 +313,7 @@ def run_ours(args, world, rank, local):
     # end to end through the public API: host poses in (pose->matrix on host,
     # H2D), host MI out (D2H), host argmax; wall clock, synchronised.
     e2e_times = []
+    eng.evaluate(poses)  # untimed: first call allocates the host-API staging buffers
     for _ in range(args.e2e_steps):
         torch.cuda.synchronize()
         if dist:

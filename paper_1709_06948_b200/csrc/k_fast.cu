@@ -43,6 +43,40 @@ __device__ __forceinline__ uint32_t slot_of(uint32_t lin, uint32_t cap) {
   return __umulhi(lin * 0x9E3779B1u, cap);
 }
 
+// ---- cp.async staging of scan-B records (LDGSTS, L1 bypass) ---------------
+template <bool F32>
+__host__ __device__ constexpr int kStages() { return F32 ? 4 : 2; }
+template <typename Rec>
+__device__ __forceinline__ void cp_async_rec(uint32_t dst, const Rec* src) {
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(dst), "l"(src) : "memory");
+  if (sizeof(Rec) == 32)
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(dst + 16),
+                 "l"(reinterpret_cast<const char*>(src) + 16)
+                 : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+template <int N>
+__device__ __forceinline__ void cp_async_wait() {
+  asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory");
+}
+template <typename Rec>
+__device__ __forceinline__ Rec lds_rec(uint32_t a);
+template <>
+__device__ __forceinline__ float4 lds_rec<float4>(uint32_t a) {
+  float4 v;
+  asm volatile("ld.shared.v4.f32 {%0, %1, %2, %3}, [%4];"
+               : "=f"(v.x), "=f"(v.y), "=f"(v.z), "=f"(v.w)
+               : "r"(a)
+               : "memory");
+  return v;
+}
+template <>
+__device__ __forceinline__ double4 lds_rec<double4>(uint32_t a) {
+  double4 v;
+  asm volatile("ld.shared.v2.f64 {%0, %1}, [%2];" : "=d"(v.x), "=d"(v.y) : "r"(a) : "memory");
+  asm volatile("ld.shared.v2.f64 {%0, %1}, [%2];" : "=d"(v.z), "=d"(v.w) : "r"(a + 16) : "memory");
+  return v;
+}
 struct VarzTable {
   unsigned long long* key;  // (lin << 32) | float32 bits of the slot pivot
   double* s1;
@@ -95,22 +129,25 @@ __device__ __forceinline__ void flush_count(uint32_t* key, uint32_t* cnt, uint32
 
 // Warp-private flush queue: run records pushed by any lane, drained 32 at a
 // time by the whole warp so the hash/atomic path always runs converged.
-constexpr int kQueue = 64;  // entries per warp (a round pushes <= 32)
+constexpr int kQueueMax = 128;  // entries per warp: a step pushes <= 32*NS, drained at 32
 
 // Shared-memory layout helper (bytes), mirrored by fast_smem_bytes() on the host.
 constexpr int kCountLut = 1024;  // COUNT bins precomputed for n < kCountLut
 
 struct FastSmem {
-  size_t table, queue, hist, marg, red, rows, cols, misc, lut, total;
+  size_t stage, table, queue, hist, marg, red, rows, cols, misc, lut, total;
 };
-__host__ __device__ inline FastSmem fast_layout(int kind, int cap, int W, int threads) {
+__host__ __device__ inline FastSmem fast_layout(int kind, int cap, int W, int threads, int f32,
+                                                int ns) {
   FastSmem L;
   size_t off = 0;
+  L.stage = off;
+  off += (size_t)threads * ns * (f32 ? 16 * kStages<true>() : 32 * kStages<false>());
   L.table = off;
   off += (size_t)cap * (kind == 0 ? (8 + 8 + 8 + 4) : (4 + 4));
   off = (off + 15) & ~size_t(15);
   L.queue = off;
-  off += (size_t)(threads / 32) * kQueue * (kind == 0 ? (4 + 4 + 8 + 8 + 8) : (4 + 4));
+  off += (size_t)(threads / 32) * (ns == 1 ? 64 : kQueueMax) * (kind == 0 ? (4 + 4 + 8 + 8 + 8) : (4 + 4));
   off = (off + 15) & ~size_t(15);
   L.hist = off; off += (size_t)W * W * 4; off = (off + 15) & ~size_t(15);
   L.marg = off; off += (size_t)W * 4; off = (off + 15) & ~size_t(15);
@@ -124,8 +161,8 @@ __host__ __device__ inline FastSmem fast_layout(int kind, int cap, int W, int th
   return L;
 }
 
-size_t fast_smem_bytes(int kind, int cap, int bins, int threads) {
-  return fast_layout(kind, cap, bins + 1, threads).total;
+size_t fast_smem_bytes(int kind, int cap, int bins, int threads, int f32, int ns) {
+  return fast_layout(kind, cap, bins + 1, threads, f32, ns).total;
 }
 
 __device__ __forceinline__ void st_shared_v4(uint32_t a, uint32_t x, uint32_t y, uint32_t z,
@@ -155,7 +192,7 @@ __device__ __forceinline__ double mkd(uint32_t lo, uint32_t hi) {
   return __hiloint2double((int)hi, (int)lo);
 }
 
-template <int THREADS, int KIND, bool F32, int MODE>
+template <int THREADS, int NS, int KIND, bool F32, int MODE>
 __global__ void __launch_bounds__(THREADS, 1)
     k_pose_fast(GridParams g, RefView A, QueryView B, const double* __restrict__ mats, int64_t P,
                 int cap, double* __restrict__ mi_out, int32_t* __restrict__ status_out,
@@ -163,7 +200,8 @@ __global__ void __launch_bounds__(THREADS, 1)
                 FeatureDump dump) {
   extern __shared__ __align__(16) unsigned char smem[];
   const int W = g.bins + 1;
-  const FastSmem L = fast_layout(KIND, cap, W, THREADS);
+  const FastSmem L = fast_layout(KIND, cap, W, THREADS, F32 ? 1 : 0, NS);
+  const uint32_t stage_base = (uint32_t)__cvta_generic_to_shared(smem + L.stage);
   uint32_t* hist = reinterpret_cast<uint32_t*>(smem + L.hist);
   uint32_t* marg = reinterpret_cast<uint32_t*>(smem + L.marg);
   double* red = reinterpret_cast<double*>(smem + L.red);
@@ -184,6 +222,7 @@ __global__ void __launch_bounds__(THREADS, 1)
   uint32_t* ccnt = nullptr;
   // warp queue: AoS records, VARZ 32 B {lin, n, K, S1, S2}, COUNT 8 B {lin, n}
   constexpr uint32_t kRec = KIND == 0 ? 32u : 8u;
+  constexpr int kQueue = NS == 1 ? 64 : 128;
   const uint32_t qbase = (uint32_t)__cvta_generic_to_shared(smem + L.queue) + wid * kQueue * kRec;
   if (KIND == 0) {
     VT.key = reinterpret_cast<unsigned long long*>(smem + L.table);
@@ -244,12 +283,17 @@ __global__ void __launch_bounds__(THREADS, 1)
       }
     }
 
-    // ---- pass over this thread's span of scan B --------------------------
+    // ---- pass over this thread's span(s) of scan B ------------------------
+    // Each thread walks NS spans ("virtual threads" tid + k*THREADS of the
+    // span layout) in lock step: NS independent dependency chains per thread.
+    constexpr int VTH = THREADS * NS;  // virtual threads = spans per CTA
     int bmin0 = INT_MAX, bmin1 = INT_MAX, bmin2 = INT_MAX;
     int bmax0 = INT_MIN, bmax1 = INT_MIN, bmax2 = INT_MIN;
-    uint32_t cur = kNoVoxel;
-    int cn = 0;
-    double cK = 0.0, cs1 = 0.0, cs2 = 0.0;
+    uint32_t cur[NS];
+    int cn[NS];
+    double cK[NS], cs1[NS], cs2[NS];
+#pragma unroll
+    for (int k = 0; k < NS; ++k) { cur[k] = kNoVoxel; cn[k] = 0; cK[k] = cs1[k] = cs2[k] = 0.0; }
     uint32_t qh = 0, qt = 0;  // warp-uniform queue head / tail
 
     auto flush_rec = [&](uint32_t idx) {  // one queued record -> table
@@ -263,35 +307,45 @@ __global__ void __launch_bounds__(THREADS, 1)
         flush_count(ckey, ccnt, ucap, r0.x, (int)r0.y, &misc[7]);
       }
     };
-    auto push = [&](bool do_push) {  // whole warp: enqueue the finished runs of some lanes
-      const unsigned m = __ballot_sync(0xffffffffu, do_push);
-      if (m == 0u) return;
-      if (do_push) {
-        const uint32_t a = qbase + ((qt + __popc(m & lt_mask)) & (kQueue - 1)) * kRec;
-        if (KIND == 0) {
-          st_shared_v4(a, cur, (uint32_t)cn, dlo(cK), dhi(cK));
-          st_shared_v4(a + 16, dlo(cs1), dhi(cs1), dlo(cs2), dhi(cs2));
-        } else {
-          st_shared_v2(a, cur, (uint32_t)cn);
-        }
+    auto store_rec = [&](uint32_t pos, int k) {
+      const uint32_t a = qbase + (pos & (kQueue - 1)) * kRec;
+      if (KIND == 0) {
+        st_shared_v4(a, cur[k], (uint32_t)cn[k], dlo(cK[k]), dhi(cK[k]));
+        st_shared_v4(a + 16, dlo(cs1[k]), dhi(cs1[k]), dlo(cs2[k]), dhi(cs2[k]));
+      } else {
+        st_shared_v2(a, cur[k], (uint32_t)cn[k]);
       }
-      qt += __popc(m);
-      if (qt - qh >= 32) {  // drain 32 records, whole warp converged
+    };
+    // whole warp: enqueue the finished runs, drain 32 at a time (converged)
+    auto push = [&](const bool* do_push) {
+      unsigned m[NS];
+      unsigned any = 0u;
+#pragma unroll
+      for (int k = 0; k < NS; ++k) { m[k] = __ballot_sync(0xffffffffu, do_push[k]); any |= m[k]; }
+      if (any == 0u) return;
+      uint32_t base = qt;
+#pragma unroll
+      for (int k = 0; k < NS; ++k) {
+        if (do_push[k]) store_rec(base + __popc(m[k] & lt_mask), k);
+        base += __popc(m[k]);
+      }
+      qt = base;
+      while (qt - qh >= 32) {
         __syncwarp();
         flush_rec(qh + lane);
         qh += 32;
         __syncwarp();
       }
     };
-    // one point: transform, voxel, bounds, run aggregation (valid = real point)
-    auto point = [&](double x, double y, double z, bool valid) {
+    // transform, voxel index, bounds, voxel inside A's AABB (pure per point)
+    auto locate = [&](double x, double y, double z, bool valid, uint32_t& lin, double& Z) {
       const double X = xform_row(x, y, z, m0, m1, m2, t0);
       const double Y = xform_row(x, y, z, m3, m4, m5, t1);
-      const double Z = xform_row(x, y, z, m6, m7, m8, t2);
+      Z = xform_row(x, y, z, m6, m7, m8, t2);
       const int ix = floor_i32(grid_q<MODE>(X, g.origin[0], g.res, g.inv_res));
       const int iy = floor_i32(grid_q<MODE>(Y, g.origin[1], g.res, g.inv_res));
       const int iz = floor_i32(grid_q<MODE>(Z, g.origin[2], g.res, g.inv_res));
-      uint32_t lin = kNoVoxel;
+      lin = kNoVoxel;
       if (valid) {
         bmin0 = min(bmin0, ix); bmax0 = max(bmax0, ix);
         bmin1 = min(bmin1, iy); bmax1 = max(bmax1, iy);
@@ -302,41 +356,82 @@ __global__ void __launch_bounds__(THREADS, 1)
         const bool inside = (rx < A.ext[0]) & (ry < A.ext[1]) & (rz < A.ext[2]);
         lin = inside ? (rx * A.ext[1] + ry) * A.ext[2] + rz : kNoVoxel;
       }
-      const bool ends = lin != cur;
-      push(ends && cur != kNoVoxel);
-      if (ends) {
-        cur = lin; cn = 1; cK = Z; cs1 = 0.0; cs2 = 0.0;
-      } else {
-        const double d = Z - cK;
-        ++cn; cs1 += d; cs2 = fma(d, d, cs2);
+    };
+    // run aggregation for one point of every stream
+    auto advance = [&](const uint32_t* lin, const double* Z) {
+      bool ends[NS], pushes[NS];
+#pragma unroll
+      for (int k = 0; k < NS; ++k) {
+        ends[k] = lin[k] != cur[k];
+        pushes[k] = ends[k] && cur[k] != kNoVoxel;
+      }
+      push(pushes);
+#pragma unroll
+      for (int k = 0; k < NS; ++k) {
+        if (ends[k]) {
+          cur[k] = lin[k]; cn[k] = 1; cK[k] = Z[k]; cs1[k] = 0.0; cs2[k] = 0.0;
+        } else {
+          const double d = Z[k] - cK[k];
+          ++cn[k]; cs1[k] += d; cs2[k] = fma(d, d, cs2[k]);
+        }
       }
     };
 
     using Rec = typename std::conditional<F32, float4, double4>::type;
     const Rec* pts = reinterpret_cast<const Rec*>(B.pts) + tid;
-    const int full = B.span - 1;          // iterations every thread owns
-    const bool has_last = span_of_thread(tid, THREADS) < B.rem;  // spans with one more point
-    constexpr int PF = THREADS >= 768 ? 2 : 4;  // prefetch depth (points per thread)
-    Rec cb[PF];
+    const int full = B.span - 1;  // iterations every span owns
+    // Scan-B records are staged through shared memory with cp.async: each
+    // virtual thread streams its own span kStages-1 records ahead into a
+    // private ring slot (no cross-thread dependency, so no barrier), then reads
+    // the record back with one LDS when it is its turn.  Keeping the prefetch
+    // out of the register file stops the compiler from hoisting conversions of
+    // in-flight data (which turned a register prefetch into stalls).
+    constexpr int S = kStages<F32>();
+    const uint32_t my_stage = stage_base + (uint32_t)tid * (uint32_t)sizeof(Rec);
+    constexpr uint32_t kStageStride = (uint32_t)(VTH * sizeof(Rec));
+    constexpr uint32_t kStreamOff = (uint32_t)(THREADS * sizeof(Rec));
+    auto issue = [&](int r) {
+      if (r < full) {
 #pragma unroll
-    for (int u = 0; u < PF; ++u) cb[u] = u < full ? pts[u * THREADS] : Rec{};
-    int r0 = 0;
-    for (; r0 + PF <= full; r0 += PF) {
-#pragma unroll
-      for (int u = 0; u < PF; ++u) {
-        const Rec pv = cb[u];
-        if (r0 + PF + u < full) cb[u] = pts[(r0 + PF + u) * THREADS];
-        point((double)pv.x, (double)pv.y, (double)pv.z, true);
+        for (int k = 0; k < NS; ++k)
+          cp_async_rec<Rec>(my_stage + (uint32_t)(r % S) * kStageStride + k * kStreamOff,
+                            pts + r * VTH + k * THREADS);
       }
-    }
+      cp_async_commit();
+    };
 #pragma unroll
-    for (int u = 0; u < PF; ++u)  // remainder (< PF) of the full iterations
-      if (r0 + u < full) point((double)cb[u].x, (double)cb[u].y, (double)cb[u].z, true);
-    {  // the ragged last iteration
-      const Rec v = pts[full * THREADS];
-      point((double)v.x, (double)v.y, (double)v.z, has_last);
+    for (int r = 0; r < S - 1; ++r) issue(r);
+#pragma unroll 2
+    for (int r = 0; r < full; ++r) {
+      issue(r + S - 1);
+      cp_async_wait<S - 1>();
+      uint32_t lin[NS];
+      double Z[NS];
+#pragma unroll
+      for (int k = 0; k < NS; ++k) {
+        const Rec v = lds_rec<Rec>(my_stage + (uint32_t)(r % S) * kStageStride + k * kStreamOff);
+        locate((double)v.x, (double)v.y, (double)v.z, true, lin[k], Z[k]);
+      }
+      advance(lin, Z);
     }
-    push(cur != kNoVoxel);
+    cp_async_wait<0>();
+    {  // the ragged last iteration
+      uint32_t lin[NS];
+      double Z[NS];
+#pragma unroll
+      for (int k = 0; k < NS; ++k) {
+        const Rec v = pts[full * VTH + k * THREADS];
+        const bool has_last = span_of_thread(tid + k * THREADS, VTH) < B.rem;
+        locate((double)v.x, (double)v.y, (double)v.z, has_last, lin[k], Z[k]);
+      }
+      advance(lin, Z);
+    }
+    {
+      bool fin[NS];
+#pragma unroll
+      for (int k = 0; k < NS; ++k) fin[k] = cur[k] != kNoVoxel;
+      push(fin);
+    }
     while (qh != qt) {  // drain the tail (partial round)
       __syncwarp();
       if ((uint32_t)lane < qt - qh) flush_rec(qh + lane);
@@ -510,10 +605,10 @@ __global__ void __launch_bounds__(THREADS, 1)
   }
 }
 
-template <int THREADS, int KIND, bool F32, int MODE>
+template <int THREADS, int NS, int KIND, bool F32, int MODE>
 static cudaError_t launch_fast_t(const FastLaunch& fl, cudaStream_t st) {
-  auto k = k_pose_fast<THREADS, KIND, F32, MODE>;
-  size_t smem = fast_smem_bytes(KIND, fl.cap, fl.g.bins, THREADS);
+  auto k = k_pose_fast<THREADS, NS, KIND, F32, MODE>;
+  size_t smem = fast_smem_bytes(KIND, fl.cap, fl.g.bins, THREADS, F32 ? 1 : 0, NS);
   cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e != cudaSuccess) return e;
   k<<<fl.grid, THREADS, smem, st>>>(fl.g, fl.A, fl.B, fl.mats, fl.P, fl.cap, fl.mi, fl.status,
@@ -521,26 +616,27 @@ static cudaError_t launch_fast_t(const FastLaunch& fl, cudaStream_t st) {
   return cudaGetLastError();
 }
 
-template <int T, int KIND, bool F32>
+template <int T, int NS, int KIND, bool F32>
 static cudaError_t launch_mode(const FastLaunch& fl, cudaStream_t st) {
   switch (fl.g.mode) {
-    case kGridUnit: return launch_fast_t<T, KIND, F32, kGridUnit>(fl, st);
-    case kGridPow2: return launch_fast_t<T, KIND, F32, kGridPow2>(fl, st);
-    default: return launch_fast_t<T, KIND, F32, kGridGeneral>(fl, st);
+    case kGridUnit: return launch_fast_t<T, NS, KIND, F32, kGridUnit>(fl, st);
+    case kGridPow2: return launch_fast_t<T, NS, KIND, F32, kGridPow2>(fl, st);
+    default: return launch_fast_t<T, NS, KIND, F32, kGridGeneral>(fl, st);
   }
 }
 
-template <int T>
+template <int T, int NS>
 static cudaError_t launch_threads(const FastLaunch& fl, cudaStream_t st) {
   const bool f32 = fl.B.is_f32 != 0;
-  if (fl.g.kind == 0) return f32 ? launch_mode<T, 0, true>(fl, st) : launch_mode<T, 0, false>(fl, st);
-  return f32 ? launch_mode<T, 1, true>(fl, st) : launch_mode<T, 1, false>(fl, st);
+  if (fl.g.kind == 0)
+    return f32 ? launch_mode<T, NS, 0, true>(fl, st) : launch_mode<T, NS, 0, false>(fl, st);
+  return f32 ? launch_mode<T, NS, 1, true>(fl, st) : launch_mode<T, NS, 1, false>(fl, st);
 }
 
 cudaError_t launch_fast(const FastLaunch& fl, cudaStream_t st) {
-  if (fl.B.threads == kFastThreads) return launch_threads<kFastThreads>(fl, st);
-  if (fl.B.threads == kFastThreadsAlt) return launch_threads<kFastThreadsAlt>(fl, st);
-  return cudaErrorInvalidValue;
+  if (fl.B.threads != kFastThreads) return cudaErrorInvalidValue;
+  if (fl.streams == 2) return launch_threads<kFastThreads / 2, 2>(fl, st);
+  return launch_threads<kFastThreads, 1>(fl, st);
 }
 
 }  // namespace vmi

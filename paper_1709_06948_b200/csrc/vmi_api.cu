@@ -51,7 +51,8 @@ struct vmi_ctx {
   int span = 0;
   int rem = 0;
   double max_abs = 0.0;
-  int threads = kFastThreads;
+  int threads = kFastThreads;  // span-layout threads
+  int streams = 2;             // spans per CUDA thread in the fast kernel
   int cap_override = 0;
 
   ExactScratch ex;
@@ -118,7 +119,8 @@ QueryView query_view(const vmi_ctx* c) {
 
 int table_cap(const vmi_ctx* c) {
   if (c->cap_override > 0) return c->cap_override;
-  const size_t fixed = fast_smem_bytes(c->g.kind, 0, c->g.bins, c->threads);
+  const size_t fixed = fast_smem_bytes(c->g.kind, 0, c->g.bins, c->threads / c->streams,
+                                       c->is_f32, c->streams);
   const size_t per = c->g.kind == 0 ? 28 : 8;
   size_t cap = (c->smem_optin - fixed) / per;
   cap &= ~size_t(31);
@@ -216,6 +218,7 @@ int launch_fast_eval(vmi_ctx* c, const double* mats_dev, int64_t P, double* mi, 
   fl.P = P;
   fl.cap = table_cap(c);
   fl.grid = (int)(P < c->sm_count ? P : c->sm_count);
+  fl.streams = c->streams;
   fl.mi = mi;
   fl.status = st;
   fl.hist = hist;
@@ -300,13 +303,12 @@ int64_t vmi_launch_count(const vmi_ctx* c) { return c ? c->launches : 0; }
 
 int vmi_set_tuning(vmi_ctx* c, int table_cap_, int threads) {
   if (!c) return VMI_ERR_ARG;
-  if (threads != 0 && threads != kFastThreads && threads != kFastThreadsAlt)
-    return fail(c, VMI_ERR_ARG, "threads must be 0 (default), 512 or 768");
+  // threads = CUDA threads per CTA: 512 (one span each) or 256 (two spans each)
+  if (threads != 0 && threads != kFastThreads && threads != kFastThreads / 2)
+    return fail(c, VMI_ERR_ARG, "threads must be 0 (default), 512 or 256");
   if (table_cap_ < 0) return fail(c, VMI_ERR_ARG, "table_cap must be >= 0");
   c->cap_override = (table_cap_ + 31) & ~31;  // the clear loop writes 16-byte words
-  const int nt = threads ? threads : kFastThreads;
-  if (nt != c->threads && c->b_set) return fail(c, VMI_ERR_STATE, "set threads before scan B");
-  c->threads = nt;
+  if (threads) c->streams = threads == kFastThreads ? 1 : 2;
   return 0;
 }
 
@@ -607,6 +609,7 @@ int vmi_fast_features(vmi_ctx* c, const double mat[12], int64_t* keys, double* v
   fl.P = 1;
   fl.cap = table_cap(c);
   fl.grid = 1;
+  fl.streams = c->streams;
   fl.mi = c->d_mi;
   fl.status = c->d_status;
   fl.total = c->d_total;

@@ -45,8 +45,7 @@ struct RefView {
 // the whole scan and every warp gets a similar share of voxel-run records
 // (far rings produce many more than near ones).  Element r of thread t's
 // span is stored at r*T + t: every warp load is 32 consecutive records.
-constexpr int kFastThreads = 512;     // default CTA size of the fast kernel
-constexpr int kFastThreadsAlt = 768;  // alternative (fewer registers per thread)
+constexpr int kFastThreads = 512;  // spans per CTA (span layout "threads") of the fast kernel
 
 struct QueryView {
   const void* pts;  // float4 (x, y, z, i) or double4 (x, y, z, pad)
