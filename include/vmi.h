@@ -138,8 +138,8 @@ int vmi_argmax_device(vmi_ctx* ctx, const double* mi_dev, int64_t P, double* bes
 int64_t vmi_launch_count(const vmi_ctx* ctx);
 
 /* Fast-path configuration knobs (tests/bench): table capacity (0 = max that
-   fits shared memory) and CUDA threads per CTA (0 = default; 512 = one scan-B span per thread,
-   256 = two spans per thread). */
+   fits shared memory) and CUDA threads per CTA (0 = default = 512, one scan-B span per
+   thread). */
 int vmi_set_tuning(vmi_ctx* ctx, int table_cap, int threads);
 
 #ifdef __cplusplus

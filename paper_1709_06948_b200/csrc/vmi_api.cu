@@ -52,7 +52,7 @@ struct vmi_ctx {
   int rem = 0;
   double max_abs = 0.0;
   int threads = kFastThreads;  // span-layout threads
-  int streams = 2;             // spans per CUDA thread in the fast kernel
+  int streams = 1;             // spans per CUDA thread in the fast kernel
   int cap_override = 0;
 
   ExactScratch ex;
@@ -303,12 +303,11 @@ int64_t vmi_launch_count(const vmi_ctx* c) { return c ? c->launches : 0; }
 
 int vmi_set_tuning(vmi_ctx* c, int table_cap_, int threads) {
   if (!c) return VMI_ERR_ARG;
-  // threads = CUDA threads per CTA: 512 (one span each) or 256 (two spans each)
-  if (threads != 0 && threads != kFastThreads && threads != kFastThreads / 2)
-    return fail(c, VMI_ERR_ARG, "threads must be 0 (default), 512 or 256");
+  // threads = CUDA threads per CTA (one scan-B span each)
+  if (threads != 0 && threads != kFastThreads)
+    return fail(c, VMI_ERR_ARG, "threads must be 0 (default) or 512");
   if (table_cap_ < 0) return fail(c, VMI_ERR_ARG, "table_cap must be >= 0");
   c->cap_override = (table_cap_ + 31) & ~31;  // the clear loop writes 16-byte words
-  if (threads) c->streams = threads == kFastThreads ? 1 : 2;
   return 0;
 }
 

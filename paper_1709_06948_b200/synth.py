@@ -75,24 +75,54 @@ def _ray_dirs(spec: LidarSceneSpec) -> np.ndarray:
     return d.reshape(-1, 3)
 
 
+def _slab(origin, d, inv, b):
+    """Slab-method entry distance of rays ``d`` into boxes ``b`` (inf = miss)."""
+    t0 = (b[None, :, :3] - origin) * inv[:, None, :]
+    t1 = (b[None, :, 3:] - origin) * inv[:, None, :]
+    tn = np.nanmax(np.minimum(t0, t1), axis=2)
+    tf = np.nanmin(np.maximum(t0, t1), axis=2)
+    hit = (tn <= tf) & (tf > 0) & (tn > 0)
+    return np.where(hit, tn, np.inf).min(axis=1)
+
+
 def _cast(origin: np.ndarray, dirs: np.ndarray, boxes: np.ndarray,
-          max_range: float) -> np.ndarray:
-    """Nearest hit distance per ray (inf = no return) against plane + boxes."""
+          max_range: float, azimuths: int | None = None, yaw: float = 0.0) -> np.ndarray:
+    """Nearest hit distance per ray (inf = no return) against plane + boxes.
+
+    With ``azimuths`` given (ring-major rays, azimuth step 2*pi/azimuths in the
+    sensor frame, sensor yaw ``yaw``), each box is only tested against the rays
+    inside its conservative azimuth window; the per (ray, box) arithmetic is
+    unchanged, so the result is identical to testing every box.
+    """
     t = np.full(dirs.shape[0], np.inf)
     dz = dirs[:, 2]
     down = dz < 0
     t[down] = -origin[2] / dz[down]
     with np.errstate(divide="ignore", invalid="ignore"):
         inv = 1.0 / dirs
-        for chunk in range(0, boxes.shape[0], 32):
-            b = boxes[chunk:chunk + 32]
-            t0 = (b[None, :, :3] - origin) * inv[:, None, :]
-            t1 = (b[None, :, 3:] - origin) * inv[:, None, :]
-            tn = np.nanmax(np.minimum(t0, t1), axis=2)
-            tf = np.nanmin(np.maximum(t0, t1), axis=2)
-            hit = (tn <= tf) & (tf > 0) & (tn > 0)
-            tb = np.where(hit, tn, np.inf).min(axis=1)
-            t = np.minimum(t, tb)
+        if azimuths is None:
+            for chunk in range(0, boxes.shape[0], 32):
+                t = np.minimum(t, _slab(origin, dirs, inv, boxes[chunk:chunk + 32]))
+        else:
+            n_beams = dirs.shape[0] // azimuths
+            step = 2 * np.pi / azimuths
+            for b in boxes:
+                cx = np.array([b[0], b[3], b[3], b[0]]) - origin[0]
+                cy = np.array([b[1], b[1], b[4], b[4]]) - origin[1]
+                if b[0] <= origin[0] <= b[3] and b[1] <= origin[1] <= b[4]:
+                    cols = np.arange(azimuths)
+                else:
+                    ang = np.arctan2(cy, cx)
+                    mid = np.arctan2(cy.mean(), cx.mean())
+                    rel = np.angle(np.exp(1j * (ang - mid)))
+                    lo = mid + rel.min() - yaw
+                    hi = mid + rel.max() - yaw
+                    k0 = int(np.floor(lo / step)) - 2
+                    k1 = int(np.ceil(hi / step)) + 2
+                    cols = np.arange(k0, k1 + 1) % azimuths
+                idx = (np.arange(n_beams)[:, None] * azimuths + cols[None, :]).ravel()
+                th = _slab(origin, dirs[idx], inv[idx], b[None, :])
+                t[idx] = np.minimum(t[idx], th)
     t[t > max_range] = np.inf
     return t
 
@@ -109,7 +139,7 @@ def scan_from(spec: LidarSceneSpec, boxes: np.ndarray, sensor: EulerPose,
     rot = np.array([[c, -s, 0.0], [s, c, 0.0], [0.0, 0.0, 1.0]])
     dirs_w = dirs_s @ rot.T
     origin = np.array([sensor.tx, sensor.ty, SENSOR_HEIGHT + sensor.tz])
-    t = _cast(origin, dirs_w, boxes, spec.max_range)
+    t = _cast(origin, dirs_w, boxes, spec.max_range, azimuths=spec.azimuths, yaw=sensor.rz)
     keep = np.isfinite(t)
     t = t + rng.normal(0.0, spec.range_noise, size=t.shape)
     pts = dirs_s[keep] * t[keep, None]

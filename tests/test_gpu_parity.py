@@ -154,7 +154,7 @@ def test_table_overflow_falls_back_to_exact(hdl):
     assert_mi_close(mi, g["v1_mi"][:8])
 
 
-@pytest.mark.parametrize("threads", [256, 512])
+@pytest.mark.parametrize("threads", [0, 512])
 def test_thread_configurations_agree(hdl, threads):
     a, b = hdl
     g = golden("hdl_golden.npz")
