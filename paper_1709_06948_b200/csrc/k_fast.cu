@@ -45,7 +45,9 @@ __device__ __forceinline__ uint32_t slot_of(uint32_t lin, uint32_t cap) {
 
 // ---- cp.async staging of scan-B records (LDGSTS, L1 bypass) ---------------
 template <bool F32>
-__host__ __device__ constexpr int kStages() { return F32 ? 4 : 2; }
+__host__ __device__ constexpr int kGroup() { return F32 ? 4 : 2; }
+template <bool F32>
+__host__ __device__ constexpr int kStages() { return 2 * kGroup<F32>(); }
 template <typename Rec>
 __device__ __forceinline__ void cp_async_rec(uint32_t dst, const Rec* src) {
   asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(dst), "l"(src) : "memory");
@@ -77,11 +79,14 @@ __device__ __forceinline__ double4 lds_rec<double4>(uint32_t a) {
   asm volatile("ld.shared.v2.f64 {%0, %1}, [%2];" : "=d"(v.z), "=d"(v.w) : "r"(a + 16) : "memory");
   return v;
 }
+// VARZ table: keys and counts in shared memory; the per-slot pivot-shifted
+// sums (S1, S2) in a per-CTA, L2-resident global array updated with native
+// fire-and-forget f64 reductions (RED.ADD.F64) -- a shared-memory f64
+// atomicAdd is a CAS loop on sm_100 and was ~30% of the kernel's stalls.
 struct VarzTable {
   unsigned long long* key;  // (lin << 32) | float32 bits of the slot pivot
-  double* s1;
-  double* s2;
   uint32_t* cnt;
+  double2* sums;            // global: this CTA's [cap] (S1, S2)
 };
 
 __device__ __forceinline__ void flush_varz(const VarzTable& T, uint32_t cap, uint32_t lin, int n,
@@ -106,8 +111,8 @@ __device__ __forceinline__ void flush_varz(const VarzTable& T, uint32_t cap, uin
   const double dl = K - kp;
   const double nd = (double)n;
   atomicAdd(&T.cnt[s], (uint32_t)n);
-  atomicAdd(&T.s1[s], a1 + nd * dl);
-  atomicAdd(&T.s2[s], a2 + dl * (2.0 * a1 + nd * dl));
+  atomicAdd(&T.sums[s].x, a1 + nd * dl);
+  atomicAdd(&T.sums[s].y, a2 + dl * (2.0 * a1 + nd * dl));
 }
 
 __device__ __forceinline__ void flush_count(uint32_t* key, uint32_t* cnt, uint32_t cap,
@@ -144,7 +149,7 @@ __host__ __device__ inline FastSmem fast_layout(int kind, int cap, int W, int th
   L.stage = off;
   off += (size_t)threads * ns * (f32 ? 16 * kStages<true>() : 32 * kStages<false>());
   L.table = off;
-  off += (size_t)cap * (kind == 0 ? (8 + 8 + 8 + 4) : (4 + 4));
+  off += (size_t)cap * (kind == 0 ? (8 + 4) : (4 + 4));
   off = (off + 15) & ~size_t(15);
   L.queue = off;
   off += (size_t)(threads / 32) * (ns == 1 ? 64 : kQueueMax) * (kind == 0 ? (4 + 4 + 8 + 8 + 8) : (4 + 4));
@@ -197,7 +202,7 @@ __global__ void __launch_bounds__(THREADS, 1)
     k_pose_fast(GridParams g, RefView A, QueryView B, const double* __restrict__ mats, int64_t P,
                 int cap, double* __restrict__ mi_out, int32_t* __restrict__ status_out,
                 long long* __restrict__ hist_out, long long* __restrict__ total_out,
-                FeatureDump dump) {
+                FeatureDump dump, double2* __restrict__ gsums) {
   extern __shared__ __align__(16) unsigned char smem[];
   const int W = g.bins + 1;
   const FastSmem L = fast_layout(KIND, cap, W, THREADS, F32 ? 1 : 0, NS);
@@ -226,9 +231,8 @@ __global__ void __launch_bounds__(THREADS, 1)
   const uint32_t qbase = (uint32_t)__cvta_generic_to_shared(smem + L.queue) + wid * kQueue * kRec;
   if (KIND == 0) {
     VT.key = reinterpret_cast<unsigned long long*>(smem + L.table);
-    VT.s1 = reinterpret_cast<double*>(smem + L.table + (size_t)cap * 8);
-    VT.s2 = reinterpret_cast<double*>(smem + L.table + (size_t)cap * 16);
-    VT.cnt = reinterpret_cast<uint32_t*>(smem + L.table + (size_t)cap * 24);
+    VT.cnt = reinterpret_cast<uint32_t*>(smem + L.table + (size_t)cap * 8);
+    VT.sums = gsums + (size_t)blockIdx.x * cap;
   } else {
     ckey = reinterpret_cast<uint32_t*>(smem + L.table);
     ccnt = reinterpret_cast<uint32_t*>(smem + L.table + (size_t)cap * 4);
@@ -242,6 +246,8 @@ __global__ void __launch_bounds__(THREADS, 1)
     const int all_words = (int)((L.queue - L.table) / 16);
     const uint4 ones = make_uint4(~0u, ~0u, ~0u, ~0u), zero = make_uint4(0u, 0u, 0u, 0u);
     for (int i = tid; i < all_words; i += THREADS) t4[i] = i < key_words ? ones : zero;
+    if (KIND == 0)
+      for (int i = tid; i < cap; i += THREADS) VT.sums[i] = make_double2(0.0, 0.0);
   };
   clear_table();
   // COUNT features are small integers: their bins (mi.py:72-79) come from a LUT
@@ -386,33 +392,46 @@ __global__ void __launch_bounds__(THREADS, 1)
     // the record back with one LDS when it is its turn.  Keeping the prefetch
     // out of the register file stops the compiler from hoisting conversions of
     // in-flight data (which turned a register prefetch into stalls).
-    constexpr int S = kStages<F32>();
+    // Records move in groups of G per thread: group g+1 is in flight (cp.async)
+    // while group g is processed.  Within a group the G points are first
+    // located (transform / voxel / bounds: G independent fp64 chains in one
+    // basic block), then their run-state updates and queue pushes follow.
+    constexpr int G = kGroup<F32>();
+    constexpr int S = 2 * G;  // ring slots per thread
     const uint32_t my_stage = stage_base + (uint32_t)tid * (uint32_t)sizeof(Rec);
     constexpr uint32_t kStageStride = (uint32_t)(VTH * sizeof(Rec));
     constexpr uint32_t kStreamOff = (uint32_t)(THREADS * sizeof(Rec));
-    auto issue = [&](int r) {
-      if (r < full) {
+    auto issue_group = [&](int r0) {  // records r0 .. r0+G-1 (those < full)
 #pragma unroll
-        for (int k = 0; k < NS; ++k)
-          cp_async_rec<Rec>(my_stage + (uint32_t)(r % S) * kStageStride + k * kStreamOff,
-                            pts + r * VTH + k * THREADS);
+      for (int u = 0; u < G; ++u) {
+        const int r = r0 + u;
+        if (r < full) {
+#pragma unroll
+          for (int k = 0; k < NS; ++k)
+            cp_async_rec<Rec>(my_stage + (uint32_t)(r % S) * kStageStride + k * kStreamOff,
+                              pts + r * VTH + k * THREADS);
+        }
       }
       cp_async_commit();
     };
+    issue_group(0);
+    for (int r0 = 0; r0 < full; r0 += G) {
+      issue_group(r0 + G);
+      cp_async_wait<1>();
+      uint32_t lin[G][NS];
+      double Z[G][NS];
 #pragma unroll
-    for (int r = 0; r < S - 1; ++r) issue(r);
-#pragma unroll 4
-    for (int r = 0; r < full; ++r) {
-      issue(r + S - 1);
-      cp_async_wait<S - 1>();
-      uint32_t lin[NS];
-      double Z[NS];
+      for (int u = 0; u < G; ++u) {
 #pragma unroll
-      for (int k = 0; k < NS; ++k) {
-        const Rec v = lds_rec<Rec>(my_stage + (uint32_t)(r % S) * kStageStride + k * kStreamOff);
-        locate((double)v.x, (double)v.y, (double)v.z, true, lin[k], Z[k]);
+        for (int k = 0; k < NS; ++k) {
+          const Rec v = lds_rec<Rec>(my_stage + (uint32_t)((r0 + u) % S) * kStageStride + k * kStreamOff);
+          locate((double)v.x, (double)v.y, (double)v.z, r0 + u < full, lin[u][k], Z[u][k]);
+        }
       }
-      advance(lin, Z);
+#pragma unroll
+      for (int u = 0; u < G; ++u) {
+        if (r0 + u < full) advance(lin[u], Z[u]);  // warp-uniform condition
+      }
     }
     cp_async_wait<0>();
     {  // the ragged last iteration
@@ -496,6 +515,7 @@ __global__ void __launch_bounds__(THREADS, 1)
     for (int s0 = tid; s0 < cap; s0 += 4 * THREADS) {
       uint32_t lin4[4];
       int ba4[4];
+      double2 sum4[4];
 #pragma unroll
       for (int u = 0; u < 4; ++u) {
         const int s = s0 + u * THREADS;
@@ -510,6 +530,8 @@ __global__ void __launch_bounds__(THREADS, 1)
           }
         }
         ba4[u] = lin4[u] != kNoVoxel ? (int)__ldg(&A.grid[lin4[u]]) : 0;
+        // L2 copy (the reductions happen in L2; never trust a stale L1 line)
+        if (KIND == 0) sum4[u] = lin4[u] != kNoVoxel ? __ldcg(&VT.sums[s]) : make_double2(0.0, 0.0);
       }
 #pragma unroll
       for (int u = 0; u < 4; ++u) {
@@ -519,8 +541,9 @@ __global__ void __launch_bounds__(THREADS, 1)
         double dump_feat = 0.0;
         if (KIND == 0) {
           const double nd = (double)VT.cnt[s];
-          const double S1 = VT.s1[s], S2 = VT.s2[s];
-          VT.key[s] = kEmpty64; VT.cnt[s] = 0u; VT.s1[s] = 0.0; VT.s2[s] = 0.0;
+          const double S1 = sum4[u].x, S2 = sum4[u].y;
+          VT.key[s] = kEmpty64; VT.cnt[s] = 0u;
+          VT.sums[s] = make_double2(0.0, 0.0);
           const double rn = __drcp_rn(nd);
           const double c1 = S1 * S1 * rn;
           const double ssd = S2 - c1;
@@ -612,7 +635,7 @@ static cudaError_t launch_fast_t(const FastLaunch& fl, cudaStream_t st) {
   cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e != cudaSuccess) return e;
   k<<<fl.grid, THREADS, smem, st>>>(fl.g, fl.A, fl.B, fl.mats, fl.P, fl.cap, fl.mi, fl.status,
-                                    fl.hist, fl.total, fl.dump);
+                                    fl.hist, fl.total, fl.dump, fl.sums);
   return cudaGetLastError();
 }
 

@@ -51,6 +51,7 @@ struct vmi_ctx {
   int span = 0;
   int rem = 0;
   double max_abs = 0.0;
+  int64_t b_voxels = 0;  // scan B's occupied voxels at the identity pose (table sizing)
   int threads = kFastThreads;  // span-layout threads
   int streams = 1;             // spans per CUDA thread in the fast kernel
   int cap_override = 0;
@@ -67,6 +68,8 @@ struct vmi_ctx {
   bool hist_alloc = false;
   double* d_best = nullptr;
   long long* d_best_idx = nullptr;
+  double2* d_sums = nullptr;  // fast-path VARZ sums scratch (grid * cap)
+  size_t sums_n = 0;
 };
 
 namespace {
@@ -121,10 +124,25 @@ int table_cap(const vmi_ctx* c) {
   if (c->cap_override > 0) return c->cap_override;
   const size_t fixed = fast_smem_bytes(c->g.kind, 0, c->g.bins, c->threads / c->streams,
                                        c->is_f32, c->streams);
-  const size_t per = c->g.kind == 0 ? 28 : 8;
+  const size_t per = c->g.kind == 0 ? 12 : 8;
   size_t cap = (c->smem_optin - fixed) / per;
+  // every slot is walked once per pose: size for a ~40% load at the expected
+  // occupancy (scan B's voxel count) rather than filling shared memory
+  const size_t want = ((size_t)(2.5 * (double)(c->b_voxels > 0 ? c->b_voxels : 4096)) + 31) & ~size_t(31);
+  if (want < cap) cap = want < 2048 ? 2048 : want;
   cap &= ~size_t(31);
   return (int)cap;
+}
+
+int ensure_sums(vmi_ctx* c, int grid, int cap) {
+  if (c->g.kind != 0) return 0;
+  const size_t need = (size_t)grid * cap;
+  if (need <= c->sums_n) return 0;
+  cudaFree(c->d_sums);
+  c->d_sums = nullptr;
+  CK(c, cudaMalloc(&c->d_sums, need * sizeof(double2)));
+  c->sums_n = need;
+  return 0;
 }
 
 // Grid over A's AABB + voxel list from V (keys, values) already on device.
@@ -219,6 +237,9 @@ int launch_fast_eval(vmi_ctx* c, const double* mats_dev, int64_t P, double* mi, 
   fl.cap = table_cap(c);
   fl.grid = (int)(P < c->sm_count ? P : c->sm_count);
   fl.streams = c->streams;
+  int rc = ensure_sums(c, fl.grid, fl.cap);
+  if (rc) return rc;
+  fl.sums = c->d_sums;
   fl.mi = mi;
   fl.status = st;
   fl.hist = hist;
@@ -291,7 +312,7 @@ int vmi_destroy(vmi_ctx* c) {
   cudaFree(c->d_pts);
   exact_free(c->ex);
   cudaFree(c->d_mats); cudaFree(c->d_mi); cudaFree(c->d_status); cudaFree(c->d_hist);
-  cudaFree(c->d_total); cudaFree(c->d_best); cudaFree(c->d_best_idx);
+  cudaFree(c->d_total); cudaFree(c->d_best); cudaFree(c->d_best_idx); cudaFree(c->d_sums);
   cudaStreamDestroy(c->stream);
   delete c;
   return 0;
@@ -474,6 +495,18 @@ static int set_query(vmi_ctx* c, const void* host, int is_f32_src, int64_t n) {
   c->is_f32 = as_f32;
   c->nb = n;
   c->b_set = true;
+  // table sizing hint: scan B's occupied voxel count in its own frame
+  c->b_voxels = 0;
+  if (c->params_set) {
+    PointSource src{};
+    src.B = query_view(c);
+    src.n = n;
+    int V = 0;
+    CK(c, exact_voxelize(c->ex, src, nullptr, c->g, c->stream, &c->launches));
+    CK(c, cudaMemcpyAsync(&V, c->ex.nruns, 4, cudaMemcpyDeviceToHost, c->stream));
+    CK(c, cudaStreamSynchronize(c->stream));
+    c->b_voxels = V;
+  }
   return 0;
 }
 
@@ -609,6 +642,8 @@ int vmi_fast_features(vmi_ctx* c, const double mat[12], int64_t* keys, double* v
   fl.cap = table_cap(c);
   fl.grid = 1;
   fl.streams = c->streams;
+  if ((rc = ensure_sums(c, 1, fl.cap))) return rc;
+  fl.sums = c->d_sums;
   fl.mi = c->d_mi;
   fl.status = c->d_status;
   fl.total = c->d_total;
