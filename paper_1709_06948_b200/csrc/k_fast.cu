@@ -45,9 +45,7 @@ __device__ __forceinline__ uint32_t slot_of(uint32_t lin, uint32_t cap) {
 
 // ---- cp.async staging of scan-B records (LDGSTS, L1 bypass) ---------------
 template <bool F32>
-__host__ __device__ constexpr int kGroup() { return F32 ? 4 : 2; }
-template <bool F32>
-__host__ __device__ constexpr int kStages() { return 2 * kGroup<F32>(); }
+__host__ __device__ constexpr int kStages() { return F32 ? 4 : 2; }
 template <typename Rec>
 __device__ __forceinline__ void cp_async_rec(uint32_t dst, const Rec* src) {
   asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(dst), "l"(src) : "memory");
@@ -392,46 +390,33 @@ __global__ void __launch_bounds__(THREADS, 1)
     // the record back with one LDS when it is its turn.  Keeping the prefetch
     // out of the register file stops the compiler from hoisting conversions of
     // in-flight data (which turned a register prefetch into stalls).
-    // Records move in groups of G per thread: group g+1 is in flight (cp.async)
-    // while group g is processed.  Within a group the G points are first
-    // located (transform / voxel / bounds: G independent fp64 chains in one
-    // basic block), then their run-state updates and queue pushes follow.
-    constexpr int G = kGroup<F32>();
-    constexpr int S = 2 * G;  // ring slots per thread
+    constexpr int S = kStages<F32>();
     const uint32_t my_stage = stage_base + (uint32_t)tid * (uint32_t)sizeof(Rec);
     constexpr uint32_t kStageStride = (uint32_t)(VTH * sizeof(Rec));
     constexpr uint32_t kStreamOff = (uint32_t)(THREADS * sizeof(Rec));
-    auto issue_group = [&](int r0) {  // records r0 .. r0+G-1 (those < full)
+    auto issue = [&](int r) {
+      if (r < full) {
 #pragma unroll
-      for (int u = 0; u < G; ++u) {
-        const int r = r0 + u;
-        if (r < full) {
-#pragma unroll
-          for (int k = 0; k < NS; ++k)
-            cp_async_rec<Rec>(my_stage + (uint32_t)(r % S) * kStageStride + k * kStreamOff,
-                              pts + r * VTH + k * THREADS);
-        }
+        for (int k = 0; k < NS; ++k)
+          cp_async_rec<Rec>(my_stage + (uint32_t)(r % S) * kStageStride + k * kStreamOff,
+                            pts + r * VTH + k * THREADS);
       }
       cp_async_commit();
     };
-    issue_group(0);
-    for (int r0 = 0; r0 < full; r0 += G) {
-      issue_group(r0 + G);
-      cp_async_wait<1>();
-      uint32_t lin[G][NS];
-      double Z[G][NS];
 #pragma unroll
-      for (int u = 0; u < G; ++u) {
+    for (int r = 0; r < S - 1; ++r) issue(r);
+#pragma unroll 4
+    for (int r = 0; r < full; ++r) {
+      issue(r + S - 1);
+      cp_async_wait<S - 1>();
+      uint32_t lin[NS];
+      double Z[NS];
 #pragma unroll
-        for (int k = 0; k < NS; ++k) {
-          const Rec v = lds_rec<Rec>(my_stage + (uint32_t)((r0 + u) % S) * kStageStride + k * kStreamOff);
-          locate((double)v.x, (double)v.y, (double)v.z, r0 + u < full, lin[u][k], Z[u][k]);
-        }
+      for (int k = 0; k < NS; ++k) {
+        const Rec v = lds_rec<Rec>(my_stage + (uint32_t)(r % S) * kStageStride + k * kStreamOff);
+        locate((double)v.x, (double)v.y, (double)v.z, true, lin[k], Z[k]);
       }
-#pragma unroll
-      for (int u = 0; u < G; ++u) {
-        if (r0 + u < full) advance(lin[u], Z[u]);  // warp-uniform condition
-      }
+      advance(lin, Z);
     }
     cp_async_wait<0>();
     {  // the ragged last iteration
