@@ -22,6 +22,7 @@ import argparse
 import json
 import math
 import os
+from dataclasses import dataclass
 import subprocess
 import sys
 import threading
@@ -49,6 +50,8 @@ def parse():
     ap.add_argument("--threads", type=int, default=0, help="CTA size (0 = library default)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--e2e-steps", type=int, default=3)
+    ap.add_argument("--config", default="c2", choices=["c1", "c2", "c3", "c4"],
+                    help="SURVEY.md 8(d) workload (c2 = the headline)")
     return ap.parse_args()
 
 
@@ -59,25 +62,67 @@ def dist_env():
     return world, rank, local
 
 
-def workload(world: int, per_gpu: int):
+@dataclass
+class Workload:
+    name: str
+    a: np.ndarray          # scan A points (N, 3|4)
+    b: np.ndarray          # scan B points / KITTI records
+    poses: np.ndarray      # global candidate list (P, 6)
+    res: float
+    kind: str              # "varz" | "count"
+    scaling: str           # "weak": poses per GPU fixed; "strong": global list fixed
+    desc: str
+
+
+def workload(cfg: str, world: int, per_gpu: int) -> Workload:
+    """SURVEY.md §8(d) configurations (C2 is the headline)."""
     from paper_1709_06948_b200.geometry import EulerPose
-    from paper_1709_06948_b200.synth import LidarSceneSpec, candidate_batch, hdl64_pair
+    from paper_1709_06948_b200.synth import (LidarSceneSpec, candidate_batch, grid_poses,
+                                             hdl64_pair)
+    if cfg == "c1":
+        s = np.load(os.path.join(ROOT, "tests", "golden", "c1_scans.npz"))
+        t = np.array([1.0, 0.5, 0.0, 0.0, 0.0, 0.1])
+        poses = grid_poses(t, {"tx": t[0] + np.arange(-8, 9) * 0.25,
+                               "ty": t[1] + np.arange(-8, 9) * 0.25,
+                               "rz": t[5] + np.radians(np.arange(-10, 11) * 0.5)})
+        return Workload("c1", s["a"], s["b"], poses, 0.5, "count", "strong",
+                        "C1: reference synth_scene_pair(seed=0, 20k points), 0.5 m COUNT, "
+                        "17x17x21 = 6069-pose (tx, ty, yaw) grid around the truth")
+    if cfg == "c4":
+        spec = LidarSceneSpec(extent=100.0, n_boxes=120, box_height=(1.0, 10.0))
+        a, b = hdl64_pair(spec, EulerPose(*TRUTH))
+        poses = candidate_batch(EulerPose(*TRUTH), per_gpu * world, seed=2024)
+        return Workload("c4", a, b, poses, 0.2, "varz", "weak",
+                        "C4: HDL-64-shaped 120k-point scans in a 100 m scene, 0.2 m VARZ "
+                        "(large grid, table overflow -> exact path)")
     a, b = hdl64_pair(LidarSceneSpec(), EulerPose(*TRUTH))
+    if cfg == "c3":
+        t = np.asarray(TRUTH)
+        poses = grid_poses(t, {
+            "tx": t[0] + np.arange(-16, 17) * 0.625, "ty": t[1] + np.arange(-16, 17) * 0.625,
+            "tz": t[2] + np.array([-0.5, 0.0, 0.5]),
+            "rx": t[3] + np.radians([-1.0, 0.0, 1.0]), "ry": t[4] + np.radians([-1.0, 0.0, 1.0]),
+            "rz": t[5] + np.radians(np.arange(-16, 17) * 1.25)})
+        return Workload("c3", a, b, poses, 1.0, "varz", "strong",
+                        "C3: C2 scans, wide 6-DOF grid 33x33x3x3x3x33 = 970,299 poses, "
+                        "sharded across GPUs")
     poses = candidate_batch(EulerPose(*TRUTH), per_gpu * world, seed=2024)
-    return a, b, poses
-
-
-def config(args, world):
-    return {
-        "workload": "C2: HDL-64-shaped synthetic scan pair (120000 float32 points each), "
+    return Workload("c2", a, b, poses, 1.0, "varz", "weak",
+                    "C2: HDL-64-shaped synthetic scan pair (120000 float32 points each), "
                     "1 m voxels, VARZ, 32 bins, phi included; candidate poses uniform in "
-                    "truth +/- (3 m, 3 m, 0.3 m, 1.5 deg, 1.5 deg, 10 deg)",
-        "points": 120000,
-        "voxel_m": 1.0,
-        "feature": "varz",
+                    "truth +/- (3 m, 3 m, 0.3 m, 1.5 deg, 1.5 deg, 10 deg)")
+
+
+def config(args, world, wl: Workload, P: int):
+    return {
+        "workload": wl.desc,
+        "config_id": wl.name,
+        "points": int(wl.b.shape[0]),
+        "voxel_m": wl.res,
+        "feature": wl.kind,
         "bins": 32,
-        "poses_per_gpu": args.poses,
-        "global_batch": args.poses * world,
+        "poses_per_gpu": int(P),
+        "global_batch": int(wl.poses.shape[0]),
         "parallelism": f"dp{world} (contiguous pose shards, NCCL all-gather of per-rank argmax)",
         "l2": "flushed between timed steps (256 MiB write); scan B (1.9 MB) is re-read from "
               "L2 by every pose within a step by design",
@@ -150,24 +195,25 @@ def profiled_traffic():
         return None
 
 
-def cpu_port_baseline(a, b, poses, threads: int, budget_s: float = 15.0):
+def cpu_port_baseline(wl: Workload, poses, threads: int, budget_s: float = 15.0):
     """The reference algorithm's CPU port (oracle/, test infrastructure) on a
     bounded sample of the same batch; returns (poses/s, n_poses, cores)."""
     import oracle
     from paper_1709_06948_b200 import _lib
-    fa = oracle.feature_map(a[:, :3].astype(np.float64), (0, 0, 0), 1.0, "varz")
-    pts = b[:, :3].astype(np.float64)
+    fa = oracle.feature_map(wl.a[:, :3].astype(np.float64), (0, 0, 0), wl.res, wl.kind)
+    pts = wl.b[:, :3].astype(np.float64)
     cores = threads if threads > 0 else oracle.max_threads()
     # calibrate on a few poses, then size the sample to ~budget_s
     stride = max(1, poses.shape[0] // 4096)
     sample = poses[::stride]
     t0 = time.perf_counter()
-    oracle.mi_objective_batch(fa, pts, _lib.poses_to_mats(sample[:cores]), threads=cores)
+    oracle.mi_objective_batch(fa, pts, _lib.poses_to_mats(sample[:cores]), res=wl.res,
+                              threads=cores)
     per = (time.perf_counter() - t0) / cores
     n = int(min(sample.shape[0], max(cores, budget_s / max(per, 1e-6) * cores)))
     mats = _lib.poses_to_mats(sample[:n])
     t0 = time.perf_counter()
-    oracle.mi_objective_batch(fa, pts, mats, threads=cores)
+    oracle.mi_objective_batch(fa, pts, mats, res=wl.res, threads=cores)
     dt = time.perf_counter() - t0
     return n / dt, n, cores
 
@@ -175,15 +221,17 @@ def cpu_port_baseline(a, b, poses, threads: int, budget_s: float = 15.0):
 def run_reference(args, world, rank):
     if rank != 0:
         return
-    a, b, poses = workload(1, args.poses)
+    wl = workload(args.config, 1, args.poses)
+    poses = wl.poses
     import oracle
     cores = oracle.max_threads()
     from paper_1709_06948_b200 import _lib
-    fa = oracle.feature_map(a[:, :3].astype(np.float64), (0, 0, 0), 1.0, "varz")
-    pts = b[:, :3].astype(np.float64)
+    fa = oracle.feature_map(wl.a[:, :3].astype(np.float64), (0, 0, 0), wl.res, wl.kind)
+    pts = wl.b[:, :3].astype(np.float64)
     # each step: a bounded, strided sample of the batch (~1-2 s of all-core CPU work)
     t0 = time.perf_counter()
-    oracle.mi_objective_batch(fa, pts, _lib.poses_to_mats(poses[:cores]), threads=cores)
+    oracle.mi_objective_batch(fa, pts, _lib.poses_to_mats(poses[:cores]), res=wl.res,
+                              threads=cores)
     per_pose = (time.perf_counter() - t0) / cores
     n = max(cores, int(1.5 / max(per_pose, 1e-6)) // cores * cores)
     stride = max(1, poses.shape[0] // n)
@@ -192,7 +240,7 @@ def run_reference(args, world, rank):
         sel = poses[(s % stride)::stride][:n]
         mats = _lib.poses_to_mats(sel)
         t0 = time.perf_counter()
-        mi, st = oracle.mi_objective_batch(fa, pts, mats, threads=cores)
+        mi, st = oracle.mi_objective_batch(fa, pts, mats, res=wl.res, threads=cores)
         int(np.argmax(mi))
         dt = time.perf_counter() - t0
         if s >= args.warmup:
@@ -201,11 +249,11 @@ def run_reference(args, world, rank):
     line = {
         "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * sum(times) / len(times),
-        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
-        "data": "synthetic", "config": config(args, 1),
+        "higher_is_better": True, "scaling": wl.scaling, "vs_baseline": None, "dtype": "f64",
+        "data": "synthetic", "config": config(args, 1, wl, args.poses),
         "cpu_baseline": {"value": value, "unit": UNIT, "cores": cores, "kind": "port",
-                         "sample": f"{n} strided poses of the C2 batch per step, OpenMP over "
-                                   f"{cores} host threads (oracle/voxmi_oracle.c)"},
+                         "sample": f"{n} strided poses of the {wl.name.upper()} batch per step, "
+                                   f"OpenMP over {cores} host threads (oracle/voxmi_oracle.c)"},
         "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line), flush=True)
@@ -233,14 +281,15 @@ def run_ours(args, world, rank, local):
         else:
             dist.init_process_group(backend)
     cdev = f"cuda:{local}" if backend == "nccl" else "cpu"  # collective tensors
-    a, b, poses_all = workload(world, args.poses)
+    wl = workload(args.config, world, args.poses)
+    a, b, poses_all = wl.a, wl.b, wl.poses
     from paper_1709_06948_b200.shard import pick_global, shard_bounds
     lo, hi = shard_bounds(poses_all.shape[0], world, rank)
     poses = poses_all[lo:hi]
     P = poses.shape[0]
-    eng = vmi.MIEngine(grid=vmi.GridSpec(resolution=1.0),
-                       binning=vmi.BinningSpec(kind=vmi.FeatureKind.VARZ), device=local,
-                       threads=args.threads)
+    eng = vmi.MIEngine(grid=vmi.GridSpec(resolution=wl.res),
+                       binning=vmi.BinningSpec(kind=vmi.FeatureKind.from_name(wl.kind)),
+                       device=local, threads=args.threads)
     eng.set_reference(a[:, :3].astype(np.float64))
     eng.set_query(b)
     ctx = eng.ctx
@@ -249,7 +298,10 @@ def run_ours(args, world, rank, local):
     # |V_B in AABB_A| measured from histograms of a strided sample
     _, _, hist, _ = eng.evaluate(poses[:: max(1, P // 256)], histograms=True)
     vb = float(np.mean(hist[:, :, 1:].sum(axis=(1, 2))))
-    bytes_per_pose = 16.0 * b.shape[0] + vb + 8.0
+    pts3 = np.asarray(b[:, :3])
+    f32_exact = bool(np.all(pts3.astype(np.float32).astype(np.float64) == pts3))
+    rec_bytes = 16.0 if f32_exact else 24.0  # float4 KITTI record, else 3 x f64
+    bytes_per_pose = rec_bytes * b.shape[0] + vb + 8.0
 
     stream = torch.cuda.Stream(device=local)
     mats = torch.from_numpy(_lib.poses_to_mats(poses)).to(f"cuda:{local}")
@@ -308,7 +360,8 @@ def run_ours(args, world, rank, local):
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         total_ms = float(t.item())
         dist.barrier()
-    value = P * world * args.steps / (total_ms / 1e3)
+    n_total = poses_all.shape[0]  # all ranks' poses (shards cover the global list)
+    value = n_total * args.steps / (total_ms / 1e3)
 
     # end to end through the public API: host poses in (pose->matrix on host,
     # H2D), host MI out (D2H), host argmax; wall clock, synchronised.
@@ -327,7 +380,7 @@ def run_ours(args, world, rank, local):
         t = torch.tensor([e2e_s], dtype=torch.float64, device=cdev)
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         e2e_s = float(t.item())
-    e2e_value = P * world / e2e_s
+    e2e_value = n_total / e2e_s
 
     kern_s = float(np.mean(kern_ms)) / 1e3
     achieved = bytes_per_pose * P / kern_s / 1e9
@@ -336,8 +389,8 @@ def run_ours(args, world, rank, local):
     line = {
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": total_ms / args.steps, "higher_is_better": True,
-        "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-        "config": config(args, world),
+        "scaling": wl.scaling, "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "config": config(args, world, wl, P),
         "roofline": {
             "bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
             "frac": achieved / peak, "peak_source": peak_src,
@@ -346,7 +399,7 @@ def run_ours(args, world, rank, local):
             "kernel_ms": kern_s * 1e3,
             "algorithmic_bytes_per_pose": bytes_per_pose,
             "mean_vb_in_aabb_a": vb,
-            "bytes_formula": "16*N_B + |V_B in AABB_A| + 8",
+            "bytes_formula": f"{int(rec_bytes)}*N_B + |V_B in AABB_A| + 8",
         },
         "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": int(P * 96),
                 "d2h_bytes_per_step": int(P * 12),
@@ -356,10 +409,10 @@ def run_ours(args, world, rank, local):
         "clocks": clocks.summary(),
     }
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
-        v, n, cores = cpu_port_baseline(a, b, poses, threads=1)
+        v, n, cores = cpu_port_baseline(wl, poses, threads=1)
         line["cpu_baseline"] = {"value": v, "unit": UNIT, "cores": cores, "kind": "port",
-                                "sample": f"{n} strided poses of the C2 batch, single thread "
-                                          "(oracle/voxmi_oracle.c)"}
+                                "sample": f"{n} strided poses of the {wl.name.upper()} batch, "
+                                          "single thread (oracle/voxmi_oracle.c)"}
     if rank == 0:
         print(json.dumps(line), flush=True)
     eng.close()
