@@ -142,6 +142,11 @@ int64_t vmi_launch_count(const vmi_ctx* ctx);
    thread). */
 int vmi_set_tuning(vmi_ctx* ctx, int table_cap, int threads);
 
+/* Voxel-space hash partitions per pose (0 = automatic: enough passes that each
+   pass's share of scan B's voxels fills about half the shared-memory table;
+   large grids such as 0.2 m voxels over 100 m need several). */
+int vmi_set_passes(vmi_ctx* ctx, int npass);
+
 #ifdef __cplusplus
 }
 #endif

@@ -27,7 +27,7 @@ EXPORTS = (
     "vmi_set_query_points", "vmi_set_query_records_f32", "vmi_poses_to_mats", "vmi_eval",
     "vmi_eval_device", "vmi_eval_fixups", "vmi_eval_exact", "vmi_query_features",
     "vmi_fast_features",
-    "vmi_argmax_device", "vmi_launch_count", "vmi_set_tuning",
+    "vmi_argmax_device", "vmi_launch_count", "vmi_set_tuning", "vmi_set_passes",
 )
 
 
@@ -78,6 +78,7 @@ def load(path: str = LIB_PATH):
     L.vmi_launch_count.argtypes = [_ctx]
     L.vmi_launch_count.restype = ctypes.c_int64
     L.vmi_set_tuning.argtypes = [_ctx, ctypes.c_int, ctypes.c_int]
+    L.vmi_set_passes.argtypes = [_ctx, ctypes.c_int]
     _lib = L
     return L
 
@@ -148,6 +149,9 @@ class Context:
 
     def set_tuning(self, table_cap: int = 0, threads: int = 0):
         self.check(self._L.vmi_set_tuning(self._h, int(table_cap), int(threads)), "vmi_set_tuning")
+
+    def set_passes(self, npass: int = 0):
+        self.check(self._L.vmi_set_passes(self._h, int(npass)), "vmi_set_passes")
 
     def set_reference_points(self, xyz: np.ndarray):
         xyz = np.ascontiguousarray(xyz, dtype=np.float64)

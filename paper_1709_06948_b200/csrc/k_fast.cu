@@ -176,6 +176,9 @@ __device__ __forceinline__ void st_shared_v4(uint32_t a, uint32_t x, uint32_t y,
 __device__ __forceinline__ void st_shared_v2(uint32_t a, uint32_t x, uint32_t y) {
   asm volatile("st.shared.v2.u32 [%0], {%1, %2};" ::"r"(a), "r"(x), "r"(y) : "memory");
 }
+__device__ __forceinline__ void st_shared_f64(uint32_t a, double x) {
+  asm volatile("st.shared.f64 [%0], %1;" ::"r"(a), "d"(x) : "memory");
+}
 __device__ __forceinline__ uint4 ld_shared_v4(uint32_t a) {
   uint4 v;
   asm volatile("ld.shared.v4.u32 {%0, %1, %2, %3}, [%4];"
@@ -200,7 +203,7 @@ __global__ void __launch_bounds__(THREADS, 1)
     k_pose_fast(GridParams g, RefView A, QueryView B, const double* __restrict__ mats, int64_t P,
                 int cap, double* __restrict__ mi_out, int32_t* __restrict__ status_out,
                 long long* __restrict__ hist_out, long long* __restrict__ total_out,
-                FeatureDump dump, double2* __restrict__ gsums) {
+                FeatureDump dump, double2* __restrict__ gsums, int npass) {
   extern __shared__ __align__(16) unsigned char smem[];
   const int W = g.bins + 1;
   const FastSmem L = fast_layout(KIND, cap, W, THREADS, F32 ? 1 : 0, NS);
@@ -287,195 +290,291 @@ __global__ void __launch_bounds__(THREADS, 1)
       }
     }
 
-    // ---- pass over this thread's span(s) of scan B ------------------------
-    // Each thread walks NS spans ("virtual threads" tid + k*THREADS of the
-    // span layout) in lock step: NS independent dependency chains per thread.
-    constexpr int VTH = THREADS * NS;  // virtual threads = spans per CTA
-    int bmin0 = INT_MAX, bmin1 = INT_MAX, bmin2 = INT_MAX;
-    int bmax0 = INT_MIN, bmax1 = INT_MIN, bmax2 = INT_MIN;
-    uint32_t cur[NS];
-    int cn[NS];
-    double cK[NS], cs1[NS], cs2[NS];
-#pragma unroll
-    for (int k = 0; k < NS; ++k) { cur[k] = kNoVoxel; cn[k] = 0; cK[k] = cs1[k] = cs2[k] = 0.0; }
-    uint32_t qh = 0, qt = 0;  // warp-uniform queue head / tail
-
-    auto flush_rec = [&](uint32_t idx) {  // one queued record -> table
-      const uint32_t a = qbase + (idx & (kQueue - 1)) * kRec;
-      if (KIND == 0) {
-        const uint4 r0 = ld_shared_v4(a), r1 = ld_shared_v4(a + 16);
-        flush_varz(VT, ucap, r0.x, (int)r0.y, mkd(r0.z, r0.w), mkd(r1.x, r1.y), mkd(r1.z, r1.w),
-                   &misc[7]);
-      } else {
-        const uint2 r0 = ld_shared_v2(a);
-        flush_count(ckey, ccnt, ucap, r0.x, (int)r0.y, &misc[7]);
-      }
-    };
-    auto store_rec = [&](uint32_t pos, int k) {
-      const uint32_t a = qbase + (pos & (kQueue - 1)) * kRec;
-      if (KIND == 0) {
-        st_shared_v4(a, cur[k], (uint32_t)cn[k], dlo(cK[k]), dhi(cK[k]));
-        st_shared_v4(a + 16, dlo(cs1[k]), dhi(cs1[k]), dlo(cs2[k]), dhi(cs2[k]));
-      } else {
-        st_shared_v2(a, cur[k], (uint32_t)cn[k]);
-      }
-    };
-    // whole warp: enqueue the finished runs, drain 32 at a time (converged)
-    auto push = [&](const bool* do_push) {
-      unsigned m[NS];
-      unsigned any = 0u;
-#pragma unroll
-      for (int k = 0; k < NS; ++k) { m[k] = __ballot_sync(0xffffffffu, do_push[k]); any |= m[k]; }
-      if (any == 0u) return;
-      uint32_t base = qt;
-#pragma unroll
-      for (int k = 0; k < NS; ++k) {
-        if (do_push[k]) store_rec(base + __popc(m[k] & lt_mask), k);
-        base += __popc(m[k]);
-      }
-      qt = base;
-      while (qt - qh >= 32) {
-        __syncwarp();
-        flush_rec(qh + lane);
-        qh += 32;
-        __syncwarp();
-      }
-    };
-    // transform, voxel index, bounds, voxel inside A's AABB (pure per point)
-    auto locate = [&](double x, double y, double z, bool valid, uint32_t& lin, double& Z) {
-      const double X = xform_row(x, y, z, m0, m1, m2, t0);
-      const double Y = xform_row(x, y, z, m3, m4, m5, t1);
-      Z = xform_row(x, y, z, m6, m7, m8, t2);
-      const int ix = floor_i32(grid_q<MODE>(X, g.origin[0], g.res, g.inv_res));
-      const int iy = floor_i32(grid_q<MODE>(Y, g.origin[1], g.res, g.inv_res));
-      const int iz = floor_i32(grid_q<MODE>(Z, g.origin[2], g.res, g.inv_res));
-      lin = kNoVoxel;
-      if (valid) {
-        bmin0 = min(bmin0, ix); bmax0 = max(bmax0, ix);
-        bmin1 = min(bmin1, iy); bmax1 = max(bmax1, iy);
-        bmin2 = min(bmin2, iz); bmax2 = max(bmax2, iz);
-        const uint32_t rx = (uint32_t)(ix - A.amin[0]);
-        const uint32_t ry = (uint32_t)(iy - A.amin[1]);
-        const uint32_t rz = (uint32_t)(iz - A.amin[2]);
-        const bool inside = (rx < A.ext[0]) & (ry < A.ext[1]) & (rz < A.ext[2]);
-        lin = inside ? (rx * A.ext[1] + ry) * A.ext[2] + rz : kNoVoxel;
-      }
-    };
-    // run aggregation for one point of every stream
-    auto advance = [&](const uint32_t* lin, const double* Z) {
-      bool ends[NS], pushes[NS];
-#pragma unroll
-      for (int k = 0; k < NS; ++k) {
-        ends[k] = lin[k] != cur[k];
-        pushes[k] = ends[k] && cur[k] != kNoVoxel;
-      }
-      push(pushes);
-#pragma unroll
-      for (int k = 0; k < NS; ++k) {
-        if (ends[k]) {
-          cur[k] = lin[k]; cn[k] = 1; cK[k] = Z[k]; cs1[k] = 0.0; cs2[k] = 0.0;
-        } else {
-          const double d = Z[k] - cK[k];
-          ++cn[k]; cs1[k] += d; cs2[k] = fma(d, d, cs2[k]);
-        }
-      }
-    };
-
-    using Rec = typename std::conditional<F32, float4, double4>::type;
-    const Rec* pts = reinterpret_cast<const Rec*>(B.pts) + tid;
-    const int full = B.span - 1;  // iterations every span owns
-    // Scan-B records are staged through shared memory with cp.async: each
-    // virtual thread streams its own span kStages-1 records ahead into a
-    // private ring slot (no cross-thread dependency, so no barrier), then reads
-    // the record back with one LDS when it is its turn.  Keeping the prefetch
-    // out of the register file stops the compiler from hoisting conversions of
-    // in-flight data (which turned a register prefetch into stalls).
-    constexpr int S = kStages<F32>();
-    const uint32_t my_stage = stage_base + (uint32_t)tid * (uint32_t)sizeof(Rec);
-    constexpr uint32_t kStageStride = (uint32_t)(VTH * sizeof(Rec));
-    constexpr uint32_t kStreamOff = (uint32_t)(THREADS * sizeof(Rec));
-    auto issue = [&](int r) {
-      if (r < full) {
-#pragma unroll
-        for (int k = 0; k < NS; ++k)
-          cp_async_rec<Rec>(my_stage + (uint32_t)(r % S) * kStageStride + k * kStreamOff,
-                            pts + r * VTH + k * THREADS);
-      }
-      cp_async_commit();
-    };
-#pragma unroll
-    for (int r = 0; r < S - 1; ++r) issue(r);
-#pragma unroll 4
-    for (int r = 0; r < full; ++r) {
-      issue(r + S - 1);
-      cp_async_wait<S - 1>();
-      uint32_t lin[NS];
-      double Z[NS];
-#pragma unroll
-      for (int k = 0; k < NS; ++k) {
-        const Rec v = lds_rec<Rec>(my_stage + (uint32_t)(r % S) * kStageStride + k * kStreamOff);
-        locate((double)v.x, (double)v.y, (double)v.z, true, lin[k], Z[k]);
-      }
-      advance(lin, Z);
-    }
-    cp_async_wait<0>();
-    {  // the ragged last iteration
-      uint32_t lin[NS];
-      double Z[NS];
-#pragma unroll
-      for (int k = 0; k < NS; ++k) {
-        const Rec v = pts[full * VTH + k * THREADS];
-        const bool has_last = span_of_thread(tid + k * THREADS, VTH) < B.rem;
-        locate((double)v.x, (double)v.y, (double)v.z, has_last, lin[k], Z[k]);
-      }
-      advance(lin, Z);
-    }
-    {
-      bool fin[NS];
-#pragma unroll
-      for (int k = 0; k < NS; ++k) fin[k] = cur[k] != kNoVoxel;
-      push(fin);
-    }
-    while (qh != qt) {  // drain the tail (partial round)
-      __syncwarp();
-      if ((uint32_t)lane < qt - qh) flush_rec(qh + lane);
-      qh = (qt - qh > 32u) ? qh + 32 : qt;
-      __syncwarp();
-    }
-    // ---- reduce bounds / key-range flag ----------------------------------
-    bmin0 = __reduce_min_sync(0xffffffffu, bmin0);
-    bmin1 = __reduce_min_sync(0xffffffffu, bmin1);
-    bmin2 = __reduce_min_sync(0xffffffffu, bmin2);
-    bmax0 = __reduce_max_sync(0xffffffffu, bmax0);
-    bmax1 = __reduce_max_sync(0xffffffffu, bmax1);
-    bmax2 = __reduce_max_sync(0xffffffffu, bmax2);
-    if (lane == 0) {
-      atomicMin(&misc[0], bmin0); atomicMin(&misc[1], bmin1); atomicMin(&misc[2], bmin2);
-      atomicMax(&misc[3], bmax0); atomicMax(&misc[4], bmax1); atomicMax(&misc[5], bmax2);
-    }
-    __syncthreads();
-    // voxel.py:200-206: any index outside [-2^20, 2^20-1] -> OutOfBoundsError
-    if (tid == 0 && (misc[0] < kKeyMin || misc[1] < kKeyMin || misc[2] < kKeyMin ||
-                     misc[3] > kKeyMax || misc[4] > kKeyMax || misc[5] > kKeyMax))
-      misc[6] = 1;
-    __syncthreads();
-
     // ---- overlap region (voxel.py:298-318) -------------------------------
     int status = 0;
     int rlo[3], rhi[3];
     long long n_region = 0;
-    if (misc[6]) {
-      status = 2;  // KEY_RANGE
-    } else if (A.empty) {
-      status = 1;
-    } else {
-      n_region = 1;
-      for (int j = 0; j < 3; ++j) {
-        rlo[j] = max(A.amin[j], misc[j]);
-        rhi[j] = min(A.amax[j], misc[3 + j]);
-        if (rlo[j] > rhi[j]) status = 1;
-        n_region *= (long long)(rhi[j] - rlo[j] + 1);
+    const double bins_d = (double)g.bins;
+    bool recheck = false;
+    // npass > 1 only when scan B's voxels outgrow the table: pass k aggregates
+    // the voxels of hash partition k, so every voxel is complete in one pass.
+    for (int pass = 0; pass < npass; ++pass) {
+      // ---- pass over this thread's span(s) of scan B ------------------------
+      // Each thread walks NS spans ("virtual threads" tid + k*THREADS of the
+      // span layout) in lock step: NS independent dependency chains per thread.
+      constexpr int VTH = THREADS * NS;  // virtual threads = spans per CTA
+      int bmin0 = INT_MAX, bmin1 = INT_MAX, bmin2 = INT_MAX;
+      int bmax0 = INT_MIN, bmax1 = INT_MIN, bmax2 = INT_MIN;
+      uint32_t cur[NS];
+      int cn[NS];
+      double cK[NS], cs1[NS], cs2[NS];
+  #pragma unroll
+      for (int k = 0; k < NS; ++k) { cur[k] = kNoVoxel; cn[k] = 0; cK[k] = cs1[k] = cs2[k] = 0.0; }
+      uint32_t qh = 0, qt = 0;  // warp-uniform queue head / tail
+
+      auto flush_rec = [&](uint32_t idx) {  // one queued record -> table
+        const uint32_t a = qbase + (idx & (kQueue - 1)) * kRec;
+        if (KIND == 0) {
+          const uint4 r0 = ld_shared_v4(a), r1 = ld_shared_v4(a + 16);
+          flush_varz(VT, ucap, r0.x, (int)r0.y, mkd(r0.z, r0.w), mkd(r1.x, r1.y), mkd(r1.z, r1.w),
+                     &misc[7]);
+        } else {
+          const uint2 r0 = ld_shared_v2(a);
+          flush_count(ckey, ccnt, ucap, r0.x, (int)r0.y, &misc[7]);
+        }
+      };
+      auto store_rec = [&](uint32_t pos, int k) {
+        const uint32_t a = qbase + (pos & (kQueue - 1)) * kRec;
+        if (KIND == 0) {  // scalar stores: no register shuffling into vector quads
+          st_shared_v2(a, cur[k], (uint32_t)cn[k]);
+          st_shared_f64(a + 8, cK[k]);
+          st_shared_f64(a + 16, cs1[k]);
+          st_shared_f64(a + 24, cs2[k]);
+        } else {
+          st_shared_v2(a, cur[k], (uint32_t)cn[k]);
+        }
+      };
+      // whole warp: enqueue the finished runs, drain 32 at a time (converged)
+      auto push = [&](const bool* do_push) {
+        unsigned m[NS];
+        unsigned any = 0u;
+  #pragma unroll
+        for (int k = 0; k < NS; ++k) { m[k] = __ballot_sync(0xffffffffu, do_push[k]); any |= m[k]; }
+        if (any == 0u) return;
+        uint32_t base = qt;
+  #pragma unroll
+        for (int k = 0; k < NS; ++k) {
+          if (do_push[k]) store_rec(base + __popc(m[k] & lt_mask), k);
+          base += __popc(m[k]);
+        }
+        qt = base;
+        while (qt - qh >= 32) {
+          __syncwarp();
+          flush_rec(qh + lane);
+          qh += 32;
+          __syncwarp();
+        }
+      };
+      // transform, voxel index, bounds, voxel inside A's AABB (pure per point)
+      auto locate = [&](double x, double y, double z, bool valid, uint32_t& lin, double& Z) {
+        const double X = xform_row(x, y, z, m0, m1, m2, t0);
+        const double Y = xform_row(x, y, z, m3, m4, m5, t1);
+        Z = xform_row(x, y, z, m6, m7, m8, t2);
+        const int ix = floor_i32(grid_q<MODE>(X, g.origin[0], g.res, g.inv_res));
+        const int iy = floor_i32(grid_q<MODE>(Y, g.origin[1], g.res, g.inv_res));
+        const int iz = floor_i32(grid_q<MODE>(Z, g.origin[2], g.res, g.inv_res));
+        lin = kNoVoxel;
+        if (valid) {
+          bmin0 = min(bmin0, ix); bmax0 = max(bmax0, ix);
+          bmin1 = min(bmin1, iy); bmax1 = max(bmax1, iy);
+          bmin2 = min(bmin2, iz); bmax2 = max(bmax2, iz);
+          const uint32_t rx = (uint32_t)(ix - A.amin[0]);
+          const uint32_t ry = (uint32_t)(iy - A.amin[1]);
+          const uint32_t rz = (uint32_t)(iz - A.amin[2]);
+          const bool inside = (rx < A.ext[0]) & (ry < A.ext[1]) & (rz < A.ext[2]);
+          lin = inside ? (rx * A.ext[1] + ry) * A.ext[2] + rz : kNoVoxel;
+        if (npass > 1 && lin != kNoVoxel && __umulhi(lin * 0x85EBCA6Bu, (uint32_t)npass) != (uint32_t)pass)
+          lin = kNoVoxel;  // another pass's partition
+        }
+      };
+      // run aggregation for one point of every stream
+      auto advance = [&](const uint32_t* lin, const double* Z) {
+        bool ends[NS], pushes[NS];
+  #pragma unroll
+        for (int k = 0; k < NS; ++k) {
+          ends[k] = lin[k] != cur[k];
+          pushes[k] = ends[k] && cur[k] != kNoVoxel;
+        }
+        push(pushes);
+  #pragma unroll
+        for (int k = 0; k < NS; ++k) {
+          if (ends[k]) {
+            cur[k] = lin[k]; cn[k] = 1; cK[k] = Z[k]; cs1[k] = 0.0; cs2[k] = 0.0;
+          } else {
+            const double d = Z[k] - cK[k];
+            ++cn[k]; cs1[k] += d; cs2[k] = fma(d, d, cs2[k]);
+          }
+        }
+      };
+
+      using Rec = typename std::conditional<F32, float4, double4>::type;
+      const Rec* pts = reinterpret_cast<const Rec*>(B.pts) + tid;
+      const int full = B.span - 1;  // iterations every span owns
+      // Scan-B records are staged through shared memory with cp.async: each
+      // virtual thread streams its own span kStages-1 records ahead into a
+      // private ring slot (no cross-thread dependency, so no barrier), then reads
+      // the record back with one LDS when it is its turn.  Keeping the prefetch
+      // out of the register file stops the compiler from hoisting conversions of
+      // in-flight data (which turned a register prefetch into stalls).
+      constexpr int S = kStages<F32>();
+      const uint32_t my_stage = stage_base + (uint32_t)tid * (uint32_t)sizeof(Rec);
+      constexpr uint32_t kStageStride = (uint32_t)(VTH * sizeof(Rec));
+      constexpr uint32_t kStreamOff = (uint32_t)(THREADS * sizeof(Rec));
+      auto issue = [&](int r) {
+        if (r < full) {
+  #pragma unroll
+          for (int k = 0; k < NS; ++k)
+            cp_async_rec<Rec>(my_stage + (uint32_t)(r % S) * kStageStride + k * kStreamOff,
+                              pts + r * VTH + k * THREADS);
+        }
+        cp_async_commit();
+      };
+  #pragma unroll
+      for (int r = 0; r < S - 1; ++r) issue(r);
+      // body for record r held in ring slot `slot` (a compile-time constant in
+      // the unrolled main loop, so every shared address is base + immediate)
+      auto body = [&](int r, int slot) {
+        issue(r + S - 1);
+        cp_async_wait<S - 1>();
+        uint32_t lin[NS];
+        double Z[NS];
+  #pragma unroll
+        for (int k = 0; k < NS; ++k) {
+          const Rec v = lds_rec<Rec>(my_stage + (uint32_t)slot * kStageStride + k * kStreamOff);
+          locate((double)v.x, (double)v.y, (double)v.z, true, lin[k], Z[k]);
+        }
+        advance(lin, Z);
+      };
+      int r0 = 0;
+      for (; r0 + S <= full; r0 += S) {
+  #pragma unroll
+        for (int u = 0; u < S; ++u) body(r0 + u, u);
       }
+      for (int r = r0; r < full; ++r) body(r, r % S);
+      cp_async_wait<0>();
+      {  // the ragged last iteration
+        uint32_t lin[NS];
+        double Z[NS];
+  #pragma unroll
+        for (int k = 0; k < NS; ++k) {
+          const Rec v = pts[full * VTH + k * THREADS];
+          const bool has_last = span_of_thread(tid + k * THREADS, VTH) < B.rem;
+          locate((double)v.x, (double)v.y, (double)v.z, has_last, lin[k], Z[k]);
+        }
+        advance(lin, Z);
+      }
+      {
+        bool fin[NS];
+  #pragma unroll
+        for (int k = 0; k < NS; ++k) fin[k] = cur[k] != kNoVoxel;
+        push(fin);
+      }
+      while (qh != qt) {  // drain the tail (partial round)
+        __syncwarp();
+        if ((uint32_t)lane < qt - qh) flush_rec(qh + lane);
+        qh = (qt - qh > 32u) ? qh + 32 : qt;
+        __syncwarp();
+      }
+      if (pass == 0) {
+        // ---- reduce bounds / key-range flag ----------------------------------
+        bmin0 = __reduce_min_sync(0xffffffffu, bmin0);
+        bmin1 = __reduce_min_sync(0xffffffffu, bmin1);
+        bmin2 = __reduce_min_sync(0xffffffffu, bmin2);
+        bmax0 = __reduce_max_sync(0xffffffffu, bmax0);
+        bmax1 = __reduce_max_sync(0xffffffffu, bmax1);
+        bmax2 = __reduce_max_sync(0xffffffffu, bmax2);
+        if (lane == 0) {
+          atomicMin(&misc[0], bmin0); atomicMin(&misc[1], bmin1); atomicMin(&misc[2], bmin2);
+          atomicMax(&misc[3], bmax0); atomicMax(&misc[4], bmax1); atomicMax(&misc[5], bmax2);
+        }
+        __syncthreads();
+        // voxel.py:200-206: any index outside [-2^20, 2^20-1] -> OutOfBoundsError
+        if (tid == 0 && (misc[0] < kKeyMin || misc[1] < kKeyMin || misc[2] < kKeyMin ||
+                         misc[3] > kKeyMax || misc[4] > kKeyMax || misc[5] > kKeyMax))
+          misc[6] = 1;
+        __syncthreads();
+
+        if (misc[6]) {
+          status = 2;  // KEY_RANGE
+        } else if (A.empty) {
+          status = 1;
+        } else {
+          n_region = 1;
+          for (int j = 0; j < 3; ++j) {
+            rlo[j] = max(A.amin[j], misc[j]);
+            rhi[j] = min(A.amax[j], misc[3 + j]);
+            if (rlo[j] > rhi[j]) status = 1;
+            n_region *= (long long)(rhi[j] - rlo[j] + 1);
+          }
+        }
+        if (status != 0) break;  // block-uniform
+      } else {
+        __syncthreads();  // every flush of this pass has landed
+      }
+      // ---- enumerate B voxels (all inside A's AABB, hence in the region) ---
+      // Four slots per thread per step so four A-grid loads are in flight; every
+      // slot read is reset for the next pose.  VARZ bins use var * (B / clamp):
+      // our VARZ is itself within ~1e-14 of the reference's, and any value within
+      // rounding distance of a bin edge marks the pose for the exact path.
+      for (int s0 = tid; s0 < cap; s0 += 4 * THREADS) {
+        uint32_t lin4[4];
+        int ba4[4];
+        double2 sum4[4];
+  #pragma unroll
+        for (int u = 0; u < 4; ++u) {
+          const int s = s0 + u * THREADS;
+          lin4[u] = kNoVoxel;
+          if (s < cap) {
+            if (KIND == 0) {
+              const unsigned long long w = VT.key[s];
+              if (w != kEmpty64) lin4[u] = (uint32_t)(w >> 32);
+            } else {
+              const uint32_t w = ckey[s];
+              if (w != kEmpty32) lin4[u] = w;
+            }
+          }
+          ba4[u] = lin4[u] != kNoVoxel ? (int)__ldg(&A.grid[lin4[u]]) : 0;
+          // L2 copy (the reductions happen in L2; never trust a stale L1 line)
+          if (KIND == 0) sum4[u] = lin4[u] != kNoVoxel ? __ldcg(&VT.sums[s]) : make_double2(0.0, 0.0);
+        }
+  #pragma unroll
+        for (int u = 0; u < 4; ++u) {
+          if (lin4[u] == kNoVoxel) continue;
+          const int s = s0 + u * THREADS;
+          int bb;
+          double dump_feat = 0.0;
+          if (KIND == 0) {
+            const double nd = (double)VT.cnt[s];
+            const double S1 = sum4[u].x, S2 = sum4[u].y;
+            VT.key[s] = kEmpty64; VT.cnt[s] = 0u;
+            VT.sums[s] = make_double2(0.0, 0.0);
+            const double rn = __drcp_rn(nd);
+            const double c1 = S1 * S1 * rn;
+            const double ssd = S2 - c1;
+            const double feat = (ssd > 0.0 ? ssd : 0.0) * rn;
+            const double x = feat * bin_scale;
+            const double k = rint(x);
+            if (k >= 1.0 && k <= bins_d - 1.0) {
+              const double tol = ((nd + 8.0) * 4.440892098500626e-16 * (S2 + c1) * rn +
+                                  feat * 9.094947017729282e-13) * bin_scale + 1e-300;
+              if (fabs(x - k) <= tol) recheck = true;
+            }
+            const double f = floor(x);
+            bb = 1 + (f >= bins_d - 1.0 ? g.bins - 1 : (int)f);
+            dump_feat = feat;
+          } else {
+            const uint32_t n = ccnt[s];
+            ckey[s] = kEmpty32; ccnt[s] = 0u;
+            bb = n < (uint32_t)kCountLut ? (int)count_lut[n] : feature_bin((double)n, g.clamp, g.bins);
+            dump_feat = (double)n;
+          }
+          atomicAdd(&hist[ba4[u] * W + bb], 1u);
+          if (dump.keys) {  // debug export (vmi_fast_features): lin -> packed key, feature
+            const int j = atomicAdd(dump.n, 1);
+            if (j < dump.cap) {
+              const uint32_t l = lin4[u];
+              const uint32_t rz = l % A.ext[2], rxy = l / A.ext[2];
+              const uint32_t ry = rxy % A.ext[1], rx = rxy / A.ext[1];
+              const unsigned long long off = 1ull << 20;
+              dump.keys[j] = ((unsigned long long)(long long)((int)rx + A.amin[0]) + off) << 42 |
+                             ((unsigned long long)(long long)((int)ry + A.amin[1]) + off) << 21 |
+                             ((unsigned long long)(long long)((int)rz + A.amin[2]) + off);
+              dump.values[j] = dump_feat;
+            }
+          }
+        }
+      }
+      __syncthreads();  // walk done (slots reset) before the next pass refills
     }
     if (status != 0) {
       if (tid == 0) {
@@ -488,82 +587,6 @@ __global__ void __launch_bounds__(THREADS, 1)
       clear_table();  // the walk below (which resets slots) is skipped
       __syncthreads();
       continue;
-    }
-
-    // ---- enumerate B voxels (all inside A's AABB, hence in the region) ---
-    // Four slots per thread per step so four A-grid loads are in flight; every
-    // slot read is reset for the next pose.  VARZ bins use var * (B / clamp):
-    // our VARZ is itself within ~1e-14 of the reference's, and any value within
-    // rounding distance of a bin edge marks the pose for the exact path.
-    const double bins_d = (double)g.bins;
-    bool recheck = false;
-    for (int s0 = tid; s0 < cap; s0 += 4 * THREADS) {
-      uint32_t lin4[4];
-      int ba4[4];
-      double2 sum4[4];
-#pragma unroll
-      for (int u = 0; u < 4; ++u) {
-        const int s = s0 + u * THREADS;
-        lin4[u] = kNoVoxel;
-        if (s < cap) {
-          if (KIND == 0) {
-            const unsigned long long w = VT.key[s];
-            if (w != kEmpty64) lin4[u] = (uint32_t)(w >> 32);
-          } else {
-            const uint32_t w = ckey[s];
-            if (w != kEmpty32) lin4[u] = w;
-          }
-        }
-        ba4[u] = lin4[u] != kNoVoxel ? (int)__ldg(&A.grid[lin4[u]]) : 0;
-        // L2 copy (the reductions happen in L2; never trust a stale L1 line)
-        if (KIND == 0) sum4[u] = lin4[u] != kNoVoxel ? __ldcg(&VT.sums[s]) : make_double2(0.0, 0.0);
-      }
-#pragma unroll
-      for (int u = 0; u < 4; ++u) {
-        if (lin4[u] == kNoVoxel) continue;
-        const int s = s0 + u * THREADS;
-        int bb;
-        double dump_feat = 0.0;
-        if (KIND == 0) {
-          const double nd = (double)VT.cnt[s];
-          const double S1 = sum4[u].x, S2 = sum4[u].y;
-          VT.key[s] = kEmpty64; VT.cnt[s] = 0u;
-          VT.sums[s] = make_double2(0.0, 0.0);
-          const double rn = __drcp_rn(nd);
-          const double c1 = S1 * S1 * rn;
-          const double ssd = S2 - c1;
-          const double feat = (ssd > 0.0 ? ssd : 0.0) * rn;
-          const double x = feat * bin_scale;
-          const double k = rint(x);
-          if (k >= 1.0 && k <= bins_d - 1.0) {
-            const double tol = ((nd + 8.0) * 4.440892098500626e-16 * (S2 + c1) * rn +
-                                feat * 9.094947017729282e-13) * bin_scale + 1e-300;
-            if (fabs(x - k) <= tol) recheck = true;
-          }
-          const double f = floor(x);
-          bb = 1 + (f >= bins_d - 1.0 ? g.bins - 1 : (int)f);
-          dump_feat = feat;
-        } else {
-          const uint32_t n = ccnt[s];
-          ckey[s] = kEmpty32; ccnt[s] = 0u;
-          bb = n < (uint32_t)kCountLut ? (int)count_lut[n] : feature_bin((double)n, g.clamp, g.bins);
-          dump_feat = (double)n;
-        }
-        atomicAdd(&hist[ba4[u] * W + bb], 1u);
-        if (dump.keys) {  // debug export (vmi_fast_features): lin -> packed key, feature
-          const int j = atomicAdd(dump.n, 1);
-          if (j < dump.cap) {
-            const uint32_t l = lin4[u];
-            const uint32_t rz = l % A.ext[2], rxy = l / A.ext[2];
-            const uint32_t ry = rxy % A.ext[1], rx = rxy / A.ext[1];
-            const unsigned long long off = 1ull << 20;
-            dump.keys[j] = ((unsigned long long)(long long)((int)rx + A.amin[0]) + off) << 42 |
-                           ((unsigned long long)(long long)((int)ry + A.amin[1]) + off) << 21 |
-                           ((unsigned long long)(long long)((int)rz + A.amin[2]) + off);
-            dump.values[j] = dump_feat;
-          }
-        }
-      }
     }
     if (recheck) misc[8] = 1;
 
@@ -620,7 +643,7 @@ static cudaError_t launch_fast_t(const FastLaunch& fl, cudaStream_t st) {
   cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e != cudaSuccess) return e;
   k<<<fl.grid, THREADS, smem, st>>>(fl.g, fl.A, fl.B, fl.mats, fl.P, fl.cap, fl.mi, fl.status,
-                                    fl.hist, fl.total, fl.dump, fl.sums);
+                                    fl.hist, fl.total, fl.dump, fl.sums, fl.npass);
   return cudaGetLastError();
 }
 

@@ -55,6 +55,7 @@ struct vmi_ctx {
   int threads = kFastThreads;  // span-layout threads
   int streams = 1;             // spans per CUDA thread in the fast kernel
   int cap_override = 0;
+  int npass_override = 0;
 
   ExactScratch ex;
 
@@ -237,6 +238,16 @@ int launch_fast_eval(vmi_ctx* c, const double* mats_dev, int64_t P, double* mi, 
   fl.cap = table_cap(c);
   fl.grid = (int)(P < c->sm_count ? P : c->sm_count);
   fl.streams = c->streams;
+  // hash-partition passes so that each pass's voxels fill <= ~55% of the table
+  fl.npass = 1;
+  if (c->npass_override > 0) {
+    fl.npass = c->npass_override;
+  } else if (c->b_voxels > 0) {
+    const double per_pass = 0.55 * (double)fl.cap;
+    fl.npass = (int)std::ceil((double)c->b_voxels / per_pass);
+    if (fl.npass < 1) fl.npass = 1;
+    if (fl.npass > 64) fl.npass = 64;
+  }
   int rc = ensure_sums(c, fl.grid, fl.cap);
   if (rc) return rc;
   fl.sums = c->d_sums;
@@ -329,6 +340,13 @@ int vmi_set_tuning(vmi_ctx* c, int table_cap_, int threads) {
     return fail(c, VMI_ERR_ARG, "threads must be 0 (default) or 512");
   if (table_cap_ < 0) return fail(c, VMI_ERR_ARG, "table_cap must be >= 0");
   c->cap_override = (table_cap_ + 31) & ~31;  // the clear loop writes 16-byte words
+  return 0;
+}
+
+int vmi_set_passes(vmi_ctx* c, int npass) {
+  if (!c) return VMI_ERR_ARG;
+  if (npass < 0 || npass > 64) return fail(c, VMI_ERR_ARG, "npass must be in [0, 64]");
+  c->npass_override = npass;
   return 0;
 }
 

@@ -30,6 +30,7 @@ struct FastLaunch {
   FeatureDump dump;  // debug: B's per-voxel features from the fast path (P == 1)
   int streams = 1;   // spans per thread: 1 (CTA = B.threads) or 2 (CTA = B.threads / 2)
   double2* sums = nullptr;  // VARZ: grid * cap (S1, S2) scratch, L2-resident
+  int npass = 1;            // hash partitions of the voxel space (table capacity)
 };
 size_t fast_smem_bytes(int kind, int cap, int bins, int threads, int f32, int ns);
 cudaError_t launch_fast(const FastLaunch& fl, cudaStream_t st);

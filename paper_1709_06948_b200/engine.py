@@ -68,7 +68,7 @@ class MIEngine:
     """
 
     def __init__(self, grid=None, binning=None, kind=None, include_phi: bool = True,
-                 device: int = 0, threads: int = 0, table_cap: int = 0):
+                 device: int = 0, threads: int = 0, table_cap: int = 0, passes: int = 0):
         grid = grid if grid is not None else GridSpec()
         if binning is None:
             binning = BinningSpec(kind=as_kind(kind) if kind is not None else FeatureKind.VARZ)
@@ -82,6 +82,7 @@ class MIEngine:
         self.include_phi = bool(include_phi)
         self.ctx = _lib.Context(device)
         self.ctx.set_tuning(table_cap=table_cap, threads=threads)
+        self.ctx.set_passes(passes)
         self.ctx.set_params(self.origin, self.resolution, self.kind.code, self.bins, self.clamp,
                             self.include_phi)
         self._feat_a: FeatureMap | None = None

@@ -145,13 +145,28 @@ def test_fast_path_equals_exact_path_on_c2_batch(hdl):
 def test_table_overflow_falls_back_to_exact(hdl):
     a, b = hdl
     g = golden("hdl_golden.npz")
-    eng = engine(1.0, kind="varz", table_cap=256)  # far too small: every pose overflows
+    # far too small and a single pass forced: every pose overflows
+    eng = engine(1.0, kind="varz", table_cap=256, passes=1)
     eng.set_reference(a[:, :3].astype(np.float64))
     eng.set_query(b)
     mi, st, hist, total = eng.evaluate(g["poses"][:8], histograms=True)
     np.testing.assert_array_equal(st, g["v1_status"][:8])
     np.testing.assert_array_equal(hist, g["v1_hist"][:8].astype(np.int64))
     assert_mi_close(mi, g["v1_mi"][:8])
+
+
+@pytest.mark.parametrize("passes", [2, 5])
+def test_multipass_partitions_match_reference(hdl, passes):
+    """Hash-partitioned passes (the large-grid mode) give the same histograms."""
+    a, b = hdl
+    g = golden("hdl_golden.npz")
+    eng = engine(1.0, kind="varz", table_cap=2048, passes=passes)
+    eng.set_reference(a[:, :3].astype(np.float64))
+    eng.set_query(b)
+    mi, st, hist, _ = eng.evaluate(g["poses"], histograms=True)
+    np.testing.assert_array_equal(st, g["v1_status"])
+    np.testing.assert_array_equal(hist, g["v1_hist"].astype(np.int64))
+    assert_mi_close(mi, g["v1_mi"])
 
 
 @pytest.mark.parametrize("threads", [0, 512])
