@@ -14,7 +14,8 @@ import os
 import numpy as np
 
 HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(HERE, "_native", "libvmi.so")
+# VMI_LIB overrides the library path (A/B experiments with variant builds)
+LIB_PATH = os.environ.get("VMI_LIB") or os.path.join(HERE, "_native", "libvmi.so")
 
 VMI_OK, VMI_EMPTY_REGION, VMI_KEY_RANGE, VMI_PHI_OFF_EMPTY = 0, 1, 2, 3
 VMI_FLAG_RECHECK = 0x100

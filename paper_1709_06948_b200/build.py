@@ -44,7 +44,13 @@ def _stale(target: str, deps: list[str]) -> bool:
     return any(os.path.getmtime(d) > t for d in deps)
 
 
-def build(verbose: bool = False, force: bool = False) -> str:
+def build(verbose: bool = False, force: bool = False, out_dir: str | None = None,
+          defines: tuple = ()) -> str:
+    """Build libvmi.so; ``out_dir``/``defines`` produce variant builds for A/B runs."""
+    global BUILD_DIR, LIB
+    if out_dir:
+        BUILD_DIR = os.path.join(out_dir, "obj")
+        LIB = os.path.join(out_dir, "libvmi.so")
     os.makedirs(BUILD_DIR, exist_ok=True)
     nvcc = _nvcc()
     hdrs = [os.path.join(CSRC, h) for h in HEADERS]
@@ -56,7 +62,7 @@ def build(verbose: bool = False, force: bool = False) -> str:
         o = os.path.join(BUILD_DIR, src + ".o")
         objs.append(o)
         if force or _stale(o, [s] + hdrs):
-            cmd = [nvcc, *NVCC_FLAGS, "-c", s, "-o", o]
+            cmd = [nvcc, *NVCC_FLAGS, *[f"-D{d}" for d in defines], "-c", s, "-o", o]
             r = subprocess.run(cmd, capture_output=True, text=True)
             ptxas_log.append(r.stderr)
             if r.returncode != 0:
@@ -79,4 +85,7 @@ def build(verbose: bool = False, force: bool = False) -> str:
 
 
 if __name__ == "__main__":
-    print(build(verbose=True, force="--force" in sys.argv))
+    args = [a for a in sys.argv[1:] if not a.startswith("--")]
+    defs = tuple(a[2:] for a in sys.argv[1:] if a.startswith("-D"))
+    out = next((a.split("=", 1)[1] for a in sys.argv[1:] if a.startswith("--out=")), None)
+    print(build(verbose=True, force="--force" in sys.argv, out_dir=out, defines=defs))

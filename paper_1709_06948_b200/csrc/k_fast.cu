@@ -298,6 +298,9 @@ __global__ void __launch_bounds__(THREADS, 1)
     bool recheck = false;
     // npass > 1 only when scan B's voxels outgrow the table: pass k aggregates
     // the voxels of hash partition k, so every voxel is complete in one pass.
+#ifdef VMI_NO_MULTIPASS
+    npass = 1;
+#endif
     for (int pass = 0; pass < npass; ++pass) {
       // ---- pass over this thread's span(s) of scan B ------------------------
       // Each thread walks NS spans ("virtual threads" tid + k*THREADS of the
@@ -325,11 +328,16 @@ __global__ void __launch_bounds__(THREADS, 1)
       };
       auto store_rec = [&](uint32_t pos, int k) {
         const uint32_t a = qbase + (pos & (kQueue - 1)) * kRec;
-        if (KIND == 0) {  // scalar stores: no register shuffling into vector quads
+        if (KIND == 0) {
+#ifdef VMI_VEC_STORES
+          st_shared_v4(a, cur[k], (uint32_t)cn[k], dlo(cK[k]), dhi(cK[k]));
+          st_shared_v4(a + 16, dlo(cs1[k]), dhi(cs1[k]), dlo(cs2[k]), dhi(cs2[k]));
+#else  // scalar stores: no register shuffling into vector quads
           st_shared_v2(a, cur[k], (uint32_t)cn[k]);
           st_shared_f64(a + 8, cK[k]);
           st_shared_f64(a + 16, cs1[k]);
           st_shared_f64(a + 24, cs2[k]);
+#endif
         } else {
           st_shared_v2(a, cur[k], (uint32_t)cn[k]);
         }
@@ -435,12 +443,17 @@ __global__ void __launch_bounds__(THREADS, 1)
         }
         advance(lin, Z);
       };
+#ifdef VMI_DYN_SLOT
+      #pragma unroll 4
+      for (int r = 0; r < full; ++r) body(r, r % S);
+#else
       int r0 = 0;
       for (; r0 + S <= full; r0 += S) {
   #pragma unroll
         for (int u = 0; u < S; ++u) body(r0 + u, u);
       }
       for (int r = r0; r < full; ++r) body(r, r % S);
+#endif
       cp_async_wait<0>();
       {  // the ragged last iteration
         uint32_t lin[NS];

@@ -111,3 +111,54 @@ def as_pose_array(poses) -> np.ndarray:
     if not np.isfinite(arr).all():
         raise ValueError("poses contain non-finite components")
     return arr
+
+
+ORTHONORMAL_TOL = 1e-9
+GIMBAL_GUARD = math.pi / 2 - 1e-6
+
+
+def wrap_angle(a: float) -> float:
+    """Wrap into (-pi, pi]; exact no-op when already in range (geometry.py:26-33)."""
+    if -math.pi < a <= math.pi:
+        return a
+    w = math.remainder(a, math.tau)
+    if w <= -math.pi:
+        w += math.tau
+    return w
+
+
+def normalized(p: EulerPose) -> EulerPose:
+    """EulerPose with angles wrapped into (-pi, pi] (geometry.py:94-99)."""
+    return EulerPose(p.tx, p.ty, p.tz, wrap_angle(p.rx), wrap_angle(p.ry), wrap_angle(p.rz))
+
+
+def validate_transform(t) -> np.ndarray:
+    """Rigid-transform invariants (geometry.py:109-123): 4x4, finite, last row
+    [0,0,0,1], orthonormal rotation with det +1 (1e-9)."""
+    t = np.asarray(t, dtype=np.float64)
+    if t.shape != (4, 4):
+        raise ValueError(f"transform must be 4x4, got {t.shape}")
+    if not np.isfinite(t).all():
+        raise ValueError("transform contains non-finite entries")
+    if not np.array_equal(t[3], [0.0, 0.0, 0.0, 1.0]):
+        raise ValueError(f"last row must be [0, 0, 0, 1], got {t[3]}")
+    r = t[:3, :3]
+    if np.abs(r.T @ r - np.eye(3)).max() > ORTHONORMAL_TOL:
+        raise ValueError("rotation block is not orthonormal within 1e-9")
+    if abs(np.linalg.det(r) - 1.0) > ORTHONORMAL_TOL:
+        raise ValueError("rotation block determinant is not +1")
+    return t
+
+
+def transform_to_euler(t) -> EulerPose:
+    """ZYX Euler angles of a transform (geometry.py:141-159); raises near gimbal lock."""
+    from .errors import VoxmiError
+    t = validate_transform(t)
+    r = t[:3, :3]
+    sp = max(-1.0, min(1.0, -float(r[2, 0])))
+    ry = math.asin(sp)
+    if abs(ry) >= GIMBAL_GUARD:
+        raise VoxmiError(f"pitch {ry:.6f} rad is within 1e-6 of +/-pi/2")
+    rx = math.atan2(r[2, 1], r[2, 2])
+    rz = math.atan2(r[1, 0], r[0, 0])
+    return EulerPose(float(t[0, 3]), float(t[1, 3]), float(t[2, 3]), rx, ry, rz)

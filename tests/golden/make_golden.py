@@ -243,7 +243,33 @@ def make_bins():
     np.savez_compressed(os.path.join(HERE, "bins_golden.npz"), **out)
 
 
+def make_align():
+    """voxmi.align on the C1 scans: two configurations, every report field."""
+    from voxmi import AlignmentConfig, SimplexConfig, align
+    s = np.load(os.path.join(HERE, "c1_scans.npz"))
+    a, b = PointCloud(s["a"]), PointCloud(s["b"])
+    cases = {
+        "varz1": (AlignmentConfig(), EulerPose(0.6, 0.2, 0.0, 0.0, 0.0, 0.06)),
+        "count05": (AlignmentConfig(feature=FeatureKind.COUNT, grid=GridSpec(resolution=0.5),
+                                    simplex=SimplexConfig(initial_steps=(2.0, 2.0, 0.5, 0.05, 0.05, 0.2),
+                                                          max_iterations=150, restarts=1)),
+                    EulerPose()),
+    }
+    out = {}
+    for tag, (cfg, p0) in cases.items():
+        rep = align(a, b, euler_to_transform(p0), cfg)
+        out[f"{tag}_t0"] = p0.as_vector()
+        out[f"{tag}_pose"] = rep.estimated_pose.as_vector()
+        out[f"{tag}_matrix"] = rep.estimated
+        out[f"{tag}_final_mi"] = np.float64(rep.final_mi)
+        out[f"{tag}_trace"] = np.asarray(rep.mi_trace)
+        out[f"{tag}_iterations"] = np.int64(rep.iterations)
+        out[f"{tag}_termination"] = np.array(rep.termination)
+        print("align", tag, rep.iterations, rep.termination, rep.final_mi, rep.wall_time)
+    np.savez_compressed(os.path.join(HERE, "align_golden.npz"), **out)
+
+
 if __name__ == "__main__":
-    what = sys.argv[1:] or ["small", "mi", "bins", "hdl", "c1"]
+    what = sys.argv[1:] or ["small", "mi", "bins", "hdl", "c1", "align"]
     for w in what:
         globals()[f"make_{w}"]()

@@ -360,3 +360,27 @@ def test_fast_path_features_match_reference(tag, res, kind):
         np.testing.assert_allclose(vals, want, rtol=1e-6, atol=1e-18)
         rel = np.abs(vals - want) / np.maximum(np.abs(want), 1e-300)
         assert np.max(rel[want > 1e-12]) < 1e-11  # measured headroom, not the bar
+
+
+@pytest.mark.parametrize("tag", ["varz1", "count05"])
+def test_align_matches_reference_run(tag):
+    """align() (batched speculative Nelder-Mead on the GPU objective) reproduces
+    the reference's run decision for decision: same trace, iterations,
+    termination and estimated pose, bit for bit."""
+    g = golden("align_golden.npz")
+    s = golden("c1_scans.npz")
+    if tag == "varz1":
+        cfg = vmi.AlignmentConfig()
+    else:
+        cfg = vmi.AlignmentConfig(feature=FeatureKind.COUNT, grid=GridSpec(resolution=0.5),
+                                  simplex=vmi.SimplexConfig(initial_steps=(2.0, 2.0, 0.5, 0.05, 0.05, 0.2),
+                                                            max_iterations=150, restarts=1))
+    t0 = vmi.euler_to_transform(EulerPose.from_vector(g[f"{tag}_t0"]))
+    rep = vmi.align(s["a"], s["b"], t0, cfg)
+    assert rep.iterations == int(g[f"{tag}_iterations"])
+    assert rep.termination == str(g[f"{tag}_termination"])
+    np.testing.assert_array_equal(np.asarray(rep.mi_trace), g[f"{tag}_trace"])
+    np.testing.assert_array_equal(rep.estimated_pose.as_vector(), g[f"{tag}_pose"])
+    np.testing.assert_array_equal(rep.estimated, g[f"{tag}_matrix"])
+    assert rep.final_mi == float(g[f"{tag}_final_mi"])
+    assert rep.n_batches < rep.n_evaluations  # candidates were batched
