@@ -44,8 +44,15 @@ __device__ __forceinline__ uint32_t slot_of(uint32_t lin, uint32_t cap) {
 }
 
 // ---- cp.async staging of scan-B records (LDGSTS, L1 bypass) ---------------
+#ifndef VMI_UNROLL
+#define VMI_UNROLL 4
+#endif
+#ifndef VMI_STAGES
+#define VMI_STAGES 4
+#endif
+constexpr int kUnroll = VMI_UNROLL;  // main point loop unroll (A/B tunable)
 template <bool F32>
-__host__ __device__ constexpr int kStages() { return F32 ? 4 : 2; }
+__host__ __device__ constexpr int kStages() { return F32 ? VMI_STAGES : 2; }
 template <typename Rec>
 __device__ __forceinline__ void cp_async_rec(uint32_t dst, const Rec* src) {
   asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(dst), "l"(src) : "memory");
@@ -198,7 +205,7 @@ __device__ __forceinline__ double mkd(uint32_t lo, uint32_t hi) {
   return __hiloint2double((int)hi, (int)lo);
 }
 
-template <int THREADS, int NS, int KIND, bool F32, int MODE>
+template <int THREADS, int NS, int KIND, bool F32, int MODE, bool MULTI>
 __global__ void __launch_bounds__(THREADS, 1)
     k_pose_fast(GridParams g, RefView A, QueryView B, const double* __restrict__ mats, int64_t P,
                 int cap, double* __restrict__ mi_out, int32_t* __restrict__ status_out,
@@ -298,9 +305,7 @@ __global__ void __launch_bounds__(THREADS, 1)
     bool recheck = false;
     // npass > 1 only when scan B's voxels outgrow the table: pass k aggregates
     // the voxels of hash partition k, so every voxel is complete in one pass.
-#ifdef VMI_NO_MULTIPASS
-    npass = 1;
-#endif
+    if (!MULTI) npass = 1;  // single-pass instantiation: the pass loop folds away
     for (int pass = 0; pass < npass; ++pass) {
       // ---- pass over this thread's span(s) of scan B ------------------------
       // Each thread walks NS spans ("virtual threads" tid + k*THREADS of the
@@ -329,7 +334,7 @@ __global__ void __launch_bounds__(THREADS, 1)
       auto store_rec = [&](uint32_t pos, int k) {
         const uint32_t a = qbase + (pos & (kQueue - 1)) * kRec;
         if (KIND == 0) {
-#ifdef VMI_VEC_STORES
+#ifndef VMI_SCALAR_STORES
           st_shared_v4(a, cur[k], (uint32_t)cn[k], dlo(cK[k]), dhi(cK[k]));
           st_shared_v4(a + 16, dlo(cs1[k]), dhi(cs1[k]), dlo(cs2[k]), dhi(cs2[k]));
 #else  // scalar stores: no register shuffling into vector quads
@@ -443,8 +448,8 @@ __global__ void __launch_bounds__(THREADS, 1)
         }
         advance(lin, Z);
       };
-#ifdef VMI_DYN_SLOT
-      #pragma unroll 4
+#ifndef VMI_STATIC_SLOT
+      #pragma unroll kUnroll
       for (int r = 0; r < full; ++r) body(r, r % S);
 #else
       int r0 = 0;
@@ -649,9 +654,9 @@ __global__ void __launch_bounds__(THREADS, 1)
   }
 }
 
-template <int THREADS, int NS, int KIND, bool F32, int MODE>
+template <int THREADS, int NS, int KIND, bool F32, int MODE, bool MULTI>
 static cudaError_t launch_fast_t(const FastLaunch& fl, cudaStream_t st) {
-  auto k = k_pose_fast<THREADS, NS, KIND, F32, MODE>;
+  auto k = k_pose_fast<THREADS, NS, KIND, F32, MODE, MULTI>;
   size_t smem = fast_smem_bytes(KIND, fl.cap, fl.g.bins, THREADS, F32 ? 1 : 0, NS);
   cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e != cudaSuccess) return e;
@@ -660,13 +665,21 @@ static cudaError_t launch_fast_t(const FastLaunch& fl, cudaStream_t st) {
   return cudaGetLastError();
 }
 
+template <int T, int NS, int KIND, bool F32, bool MULTI>
+static cudaError_t launch_grid(const FastLaunch& fl, cudaStream_t st) {
+  switch (fl.g.mode) {
+    case kGridUnit: return launch_fast_t<T, NS, KIND, F32, kGridUnit, MULTI>(fl, st);
+    case kGridPow2: return launch_fast_t<T, NS, KIND, F32, kGridPow2, MULTI>(fl, st);
+    default: return launch_fast_t<T, NS, KIND, F32, kGridGeneral, MULTI>(fl, st);
+  }
+}
+
+// The multi-pass loop costs ~8% even at npass == 1 (measured), so single- and
+// multi-pass are separate instantiations.
 template <int T, int NS, int KIND, bool F32>
 static cudaError_t launch_mode(const FastLaunch& fl, cudaStream_t st) {
-  switch (fl.g.mode) {
-    case kGridUnit: return launch_fast_t<T, NS, KIND, F32, kGridUnit>(fl, st);
-    case kGridPow2: return launch_fast_t<T, NS, KIND, F32, kGridPow2>(fl, st);
-    default: return launch_fast_t<T, NS, KIND, F32, kGridGeneral>(fl, st);
-  }
+  return fl.npass > 1 ? launch_grid<T, NS, KIND, F32, true>(fl, st)
+                      : launch_grid<T, NS, KIND, F32, false>(fl, st);
 }
 
 template <int T, int NS>

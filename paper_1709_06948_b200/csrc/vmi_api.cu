@@ -6,6 +6,7 @@
 // and the float32-exactness test of uploaded coordinates.
 #include <cmath>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <string>
 #include <vector>
@@ -129,7 +130,12 @@ int table_cap(const vmi_ctx* c) {
   size_t cap = (c->smem_optin - fixed) / per;
   // every slot is walked once per pose: size for a ~40% load at the expected
   // occupancy (scan B's voxel count) rather than filling shared memory
-  const size_t want = ((size_t)(2.5 * (double)(c->b_voxels > 0 ? c->b_voxels : 4096)) + 31) & ~size_t(31);
+  static const double factor = [] {
+    const char* e = std::getenv("VMI_CAP_FACTOR");  // experiments only
+    return e ? std::atof(e) : 2.5;
+  }();
+  const size_t want =
+      ((size_t)(factor * (double)(c->b_voxels > 0 ? c->b_voxels : 4096)) + 31) & ~size_t(31);
   if (want < cap) cap = want < 2048 ? 2048 : want;
   cap &= ~size_t(31);
   return (int)cap;
