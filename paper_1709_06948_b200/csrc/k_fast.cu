@@ -609,8 +609,12 @@ __global__ void __launch_bounds__(THREADS, 1)
     if (recheck) misc[8] = 1;
 
     // ---- A marginal over the region --------------------------------------
+#ifdef VMI_TIMING_SKIP_MARG  // timing experiment only (wrong marginals)
+    const bool cover_all = true;
+#else
     const bool cover_all = rlo[0] == A.amin[0] && rlo[1] == A.amin[1] && rlo[2] == A.amin[2] &&
                       rhi[0] == A.amax[0] && rhi[1] == A.amax[1] && rhi[2] == A.amax[2];
+#endif
     if (cover_all) {
       for (int i = tid; i < W; i += THREADS) marg[i] = A.bin_total[i];
     } else {
@@ -639,7 +643,11 @@ __global__ void __launch_bounds__(THREADS, 1)
     __syncthreads();
 
     // ---- analytic phi cells + MI (fused K2) -------------------------------
+#ifdef VMI_TIMING_SKIP_FINAL  // timing experiment only (no MI)
+    MIOut r{};
+#else
     MIOut r = finalize_mi<THREADS>(hist, marg, W, n_region, g.include_phi, red, rows, cols, h00_s);
+#endif
     const bool flag = misc[7] || misc[8];
     if (tid == 0) {
       mi_out[p] = r.status == 0 ? r.mi : -1e300;

@@ -196,3 +196,44 @@ def grid_poses(center, axes: dict[str, np.ndarray]) -> np.ndarray:
             else np.array([center[i]]) for i, k in enumerate(names)]
     mesh = np.meshgrid(*cols, indexing="ij")
     return np.stack([m.ravel() for m in mesh], axis=1)
+
+
+def drive_sequence(n_frames: int, spec: LidarSceneSpec = LidarSceneSpec(), seed: int = 0,
+                   step: float = 1.0) -> tuple[list[np.ndarray], list[EulerPose]]:
+    """C5: a synthetic drive, ``n_frames`` HDL-64-shaped scans ~``step`` m apart.
+
+    The sensor follows the road (x axis) with a slow lateral / yaw drift
+    through a corridor of boxes; returns the scans (float32 records, each in
+    its own sensor frame) and the world sensor poses (planar).  The relative
+    pose mapping frame i+1 into frame i is ``relative_pose(poses[i], poses[i+1])``.
+    """
+    rng = np.random.default_rng(np.random.SeedSequence(seed).spawn(1)[0])
+    length = n_frames * step
+    corridor = LidarSceneSpec(seed=seed, extent=spec.extent, n_boxes=spec.n_boxes,
+                              n_points=spec.n_points, azimuths=spec.azimuths,
+                              max_range=spec.max_range, range_noise=spec.range_noise,
+                              box_height=spec.box_height, box_half_width=spec.box_half_width)
+    # boxes along the whole corridor: tile the square scene every `extent` metres
+    boxes = []
+    for k, x0 in enumerate(np.arange(-spec.extent / 2, length + spec.extent / 2, spec.extent)):
+        b = _boxes(corridor, np.random.default_rng([seed, k]))
+        b[:, [0, 3]] += x0 + spec.extent / 2
+        boxes.append(b)
+    boxes = np.concatenate(boxes)
+    poses, scans = [], []
+    for i in range(n_frames):
+        x = i * step
+        y = 0.6 * math.sin(x / 37.0)
+        yaw = 0.03 * math.sin(x / 23.0)
+        pose = EulerPose(x, y, 0.0, 0.0, 0.0, yaw)
+        near = boxes[(np.abs((boxes[:, 0] + boxes[:, 3]) / 2 - x) < spec.max_range + 10.0)]
+        scans.append(scan_from(spec, near, pose, np.random.default_rng([seed, 1000 + i])))
+        poses.append(pose)
+    return scans, poses
+
+
+def relative_pose(p_i: EulerPose, p_j: EulerPose) -> EulerPose:
+    """Planar pose of sensor j expressed in sensor i's frame (maps scan j into scan i)."""
+    c, s = math.cos(p_i.rz), math.sin(p_i.rz)
+    dx, dy = p_j.tx - p_i.tx, p_j.ty - p_i.ty
+    return EulerPose(c * dx + s * dy, -s * dx + c * dy, 0.0, 0.0, 0.0, p_j.rz - p_i.rz)
