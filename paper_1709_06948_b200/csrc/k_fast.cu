@@ -48,11 +48,17 @@ __device__ __forceinline__ uint32_t slot_of(uint32_t lin, uint32_t cap) {
 #define VMI_UNROLL 4
 #endif
 #ifndef VMI_STAGES
+#ifdef VMI_CPASYNC
 #define VMI_STAGES 4
+#else
+#define VMI_STAGES 8  // TMA: two groups of four records in flight per warp
 #endif
+#endif
+#ifdef VMI_CPASYNC
 constexpr int kUnroll = VMI_UNROLL;  // main point loop unroll (A/B tunable)
+#endif
 template <bool F32>
-__host__ __device__ constexpr int kStages() { return F32 ? VMI_STAGES : 2; }
+__host__ __device__ constexpr int kStages() { return F32 ? VMI_STAGES : VMI_STAGES / 2; }
 template <typename Rec>
 __device__ __forceinline__ void cp_async_rec(uint32_t dst, const Rec* src) {
   asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(dst), "l"(src) : "memory");
@@ -61,6 +67,37 @@ __device__ __forceinline__ void cp_async_rec(uint32_t dst, const Rec* src) {
                  "l"(reinterpret_cast<const char*>(src) + 16)
                  : "memory");
 }
+// ---- TMA bulk staging (cp.async.bulk + mbarrier) ------------------------------
+__device__ __forceinline__ void mbar_init(uint32_t bar, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(bar), "r"(count) : "memory");
+}
+__device__ __forceinline__ void mbar_arrive_expect_tx(uint32_t bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar), "r"(bytes)
+               : "memory");
+}
+__device__ __forceinline__ bool mbar_try_wait(uint32_t bar, uint32_t parity) {
+  uint32_t ok;
+  asm volatile(
+      "{\n .reg .pred p;\n mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n"
+      " selp.u32 %0, 1, 0, p;\n}"
+      : "=r"(ok)
+      : "r"(bar), "r"(parity)
+      : "memory");
+  return ok != 0;
+}
+__device__ __forceinline__ void bulk_g2s(uint32_t dst, const void* src, uint32_t bytes, uint32_t bar) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(dst),
+      "l"(src), "r"(bytes), "r"(bar)
+      : "memory");
+}
+__device__ __forceinline__ void fence_proxy_async() {
+  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+}
+__device__ __forceinline__ void fence_mbar_init() {
+  asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+}
+
 __device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
 template <int N>
 __device__ __forceinline__ void cp_async_wait() {
@@ -145,7 +182,7 @@ constexpr int kQueueMax = 128;  // entries per warp: a step pushes <= 32*NS, dra
 constexpr int kCountLut = 1024;  // COUNT bins precomputed for n < kCountLut
 
 struct FastSmem {
-  size_t stage, table, queue, hist, marg, red, rows, cols, misc, lut, total;
+  size_t stage, bars, table, queue, hist, marg, red, rows, cols, misc, lut, total;
 };
 __host__ __device__ inline FastSmem fast_layout(int kind, int cap, int W, int threads, int f32,
                                                 int ns) {
@@ -153,6 +190,8 @@ __host__ __device__ inline FastSmem fast_layout(int kind, int cap, int W, int th
   size_t off = 0;
   L.stage = off;
   off += (size_t)threads * ns * (f32 ? 16 * kStages<true>() : 32 * kStages<false>());
+  L.bars = off;  // two mbarriers per warp (TMA bulk staging)
+  off += (size_t)(threads / 32) * 16;
   L.table = off;
   off += (size_t)cap * (kind == 0 ? (8 + 4) : (4 + 4));
   off = (off + 15) & ~size_t(15);
@@ -245,6 +284,41 @@ __global__ void __launch_bounds__(THREADS, 1)
     ckey = reinterpret_cast<uint32_t*>(smem + L.table);
     ccnt = reinterpret_cast<uint32_t*>(smem + L.table + (size_t)cap * 4);
   }
+
+#ifndef VMI_CPASYNC
+  static_assert(NS == 1, "TMA staging assumes one span per thread");
+  using RecT = typename std::conditional<F32, float4, double4>::type;
+  constexpr int G = F32 ? 4 : 2;                              // iterations per group
+  constexpr uint32_t kChunk = 32u * (uint32_t)sizeof(RecT);  // one warp, one iteration
+  const uint32_t wstage = stage_base + (uint32_t)wid * 2u * G * kChunk;
+  const uint32_t wbar = (uint32_t)__cvta_generic_to_shared(smem + L.bars) + (uint32_t)wid * 16u;
+  const char* wsrc = reinterpret_cast<const char*>(B.pts) + (size_t)wid * kChunk;
+  const int full_it = B.span - 1;
+  const int ng = (full_it + G - 1) / G;  // groups per pass over the span
+  uint32_t gp = 0, gq = 0;               // groups produced / consumed (warp-uniform)
+  auto produce = [&]() {
+    if (ng == 0) return;
+    const int r0 = (int)(gp % (uint32_t)ng) * G;
+    const int cnt = min(G, full_it - r0);
+    const uint32_t slot = gp & 1u;
+    if (lane == 0) {
+      fence_proxy_async();  // prior generic reads of this buffer before the async write
+      mbar_arrive_expect_tx(wbar + slot * 8u, (uint32_t)cnt * kChunk);
+      for (int u = 0; u < cnt; ++u)
+        bulk_g2s(wstage + (slot * G + u) * kChunk,
+                 wsrc + (size_t)(r0 + u) * (size_t)THREADS * sizeof(RecT), kChunk, wbar + slot * 8u);
+    }
+    ++gp;
+  };
+  if (lane == 0) {
+    mbar_init(wbar, 1);
+    mbar_init(wbar + 8, 1);
+    fence_mbar_init();
+  }
+  __syncwarp();
+  produce();
+  produce();
+#endif
 
   // The table is cleared once here; afterwards the per-pose table walk resets
   // every slot it reads, so each pose starts from an empty table.
@@ -413,6 +487,7 @@ __global__ void __launch_bounds__(THREADS, 1)
       using Rec = typename std::conditional<F32, float4, double4>::type;
       const Rec* pts = reinterpret_cast<const Rec*>(B.pts) + tid;
       const int full = B.span - 1;  // iterations every span owns
+#ifdef VMI_CPASYNC
       // Scan-B records are staged through shared memory with cp.async: each
       // virtual thread streams its own span kStages-1 records ahead into a
       // private ring slot (no cross-thread dependency, so no barrier), then reads
@@ -460,6 +535,33 @@ __global__ void __launch_bounds__(THREADS, 1)
       for (int r = r0; r < full; ++r) body(r, r % S);
 #endif
       cp_async_wait<0>();
+#else
+      // Scan-B records are staged through shared memory by TMA bulk copies:
+      // in the span layout a warp's 32 records of one iteration are one
+      // contiguous 32*sizeof(Rec)-byte chunk, so lane 0 streams groups of G
+      // iterations (two groups in flight, one mbarrier each) and every lane
+      // reads its record back with one LDS.  The stream runs continuously
+      // across passes and poses (scan B is the same for every pose).
+      for (int q = 0; q < ng; ++q) {
+        const uint32_t slot = gq & 1u;
+        while (!mbar_try_wait(wbar + slot * 8u, (gq >> 1) & 1u)) {
+        }
+        const int r0 = q * G;
+#pragma unroll
+        for (int u = 0; u < G; ++u) {
+          if (r0 + u < full) {  // warp-uniform
+            uint32_t lin[NS];
+            double Z[NS];
+            const Rec v = lds_rec<Rec>(wstage + (slot * G + u) * kChunk + (uint32_t)lane * sizeof(Rec));
+            locate((double)v.x, (double)v.y, (double)v.z, true, lin[0], Z[0]);
+            advance(lin, Z);
+          }
+        }
+        __syncwarp();  // every lane has read this buffer: it may be refilled
+        ++gq;
+        produce();
+      }
+#endif
       {  // the ragged last iteration
         uint32_t lin[NS];
         double Z[NS];
@@ -660,6 +762,14 @@ __global__ void __launch_bounds__(THREADS, 1)
     }
     __syncthreads();
   }
+#ifndef VMI_CPASYNC
+  // retire the two groups still in flight (no bulk copy may outlive the CTA)
+  for (int i = 0; i < 2 && ng > 0; ++i) {
+    while (!mbar_try_wait(wbar + (gq & 1u) * 8u, (gq >> 1) & 1u)) {
+    }
+    ++gq;
+  }
+#endif
 }
 
 template <int THREADS, int NS, int KIND, bool F32, int MODE, bool MULTI>
