@@ -48,13 +48,13 @@ __device__ __forceinline__ uint32_t slot_of(uint32_t lin, uint32_t cap) {
 #define VMI_UNROLL 4
 #endif
 #ifndef VMI_STAGES
-#ifdef VMI_CPASYNC
+#ifndef VMI_TMA
 #define VMI_STAGES 4
 #else
 #define VMI_STAGES 8  // TMA: two groups of four records in flight per warp
 #endif
 #endif
-#ifdef VMI_CPASYNC
+#ifndef VMI_TMA
 constexpr int kUnroll = VMI_UNROLL;  // main point loop unroll (A/B tunable)
 #endif
 template <bool F32>
@@ -285,7 +285,7 @@ __global__ void __launch_bounds__(THREADS, 1)
     ccnt = reinterpret_cast<uint32_t*>(smem + L.table + (size_t)cap * 4);
   }
 
-#ifndef VMI_CPASYNC
+#ifdef VMI_TMA
   static_assert(NS == 1, "TMA staging assumes one span per thread");
   using RecT = typename std::conditional<F32, float4, double4>::type;
   constexpr int G = F32 ? 4 : 2;                              // iterations per group
@@ -487,7 +487,7 @@ __global__ void __launch_bounds__(THREADS, 1)
       using Rec = typename std::conditional<F32, float4, double4>::type;
       const Rec* pts = reinterpret_cast<const Rec*>(B.pts) + tid;
       const int full = B.span - 1;  // iterations every span owns
-#ifdef VMI_CPASYNC
+#ifndef VMI_TMA
       // Scan-B records are staged through shared memory with cp.async: each
       // virtual thread streams its own span kStages-1 records ahead into a
       // private ring slot (no cross-thread dependency, so no barrier), then reads
@@ -762,7 +762,7 @@ __global__ void __launch_bounds__(THREADS, 1)
     }
     __syncthreads();
   }
-#ifndef VMI_CPASYNC
+#ifdef VMI_TMA
   // retire the two groups still in flight (no bulk copy may outlive the CTA)
   for (int i = 0; i < 2 && ng > 0; ++i) {
     while (!mbar_try_wait(wbar + (gq & 1u) * 8u, (gq >> 1) & 1u)) {
