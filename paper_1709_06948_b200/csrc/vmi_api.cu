@@ -72,6 +72,10 @@ struct vmi_ctx {
   long long* d_best_idx = nullptr;
   double2* d_sums = nullptr;  // fast-path VARZ sums scratch (grid * cap)
   size_t sums_n = 0;
+  // grow-only capacities (bytes) of buffers reused across scan pairs
+  size_t cap_grid = 0, cap_avox = 0, cap_akeys = 0, cap_avalues = 0, cap_pts = 0, cap_upload = 0;
+  void* d_upload = nullptr;  // staging for host uploads
+  int64_t a_npts = 0;        // scan A's point count (0 when set from features)
 };
 
 namespace {
@@ -91,12 +95,30 @@ int cuda_fail(vmi_ctx* c, cudaError_t e, const char* where) {
     if (e_ != cudaSuccess) return cuda_fail(ctx, e_, #x); \
   } while (0)
 
+// Scan A's buffers are grow-only and reused by the next reference (a drive
+// re-sets scan A every pair); only the bookkeeping is reset here.
 void free_a(vmi_ctx* c) {
+  c->a_set = false; c->n_avox = 0; c->a_nvox = 0; c->grid_bytes = 0; c->a_npts = 0;
+}
+
+void release_a(vmi_ctx* c) {
   cudaFree(c->d_grid); cudaFree(c->d_avox); cudaFree(c->d_bin_total); cudaFree(c->d_cursor);
-  cudaFree(c->d_akeys); cudaFree(c->d_avalues);
+  cudaFree(c->d_akeys); cudaFree(c->d_avalues); cudaFree(c->d_upload);
   c->d_grid = nullptr; c->d_avox = nullptr; c->d_bin_total = nullptr; c->d_cursor = nullptr;
-  c->d_akeys = nullptr; c->d_avalues = nullptr;
-  c->a_set = false; c->n_avox = 0; c->a_nvox = 0; c->grid_bytes = 0;
+  c->d_akeys = nullptr; c->d_avalues = nullptr; c->d_upload = nullptr;
+  c->cap_grid = c->cap_avox = c->cap_akeys = c->cap_avalues = c->cap_upload = 0;
+  free_a(c);
+}
+
+template <typename T>
+cudaError_t grow(T** p, size_t& cap, size_t need) {
+  if (need <= cap && *p) return cudaSuccess;
+  cudaFree(*p);
+  *p = nullptr;
+  cap = 0;
+  cudaError_t e = cudaMalloc(p, need > 0 ? need : 16);
+  if (e == cudaSuccess) cap = need;
+  return e;
 }
 
 RefView ref_view(const vmi_ctx* c) {
@@ -161,9 +183,9 @@ int finish_reference(vmi_ctx* c, const int64_t bounds[6], int64_t V) {
     if (bounds[j] > bounds[3 + j]) c->a_empty = true;
   }
   c->a_nvox = V;
-  CK(c, cudaMalloc(&c->d_bin_total, 4 * kMaxW));
+  if (!c->d_bin_total) CK(c, cudaMalloc(&c->d_bin_total, 4 * kMaxW));
   CK(c, cudaMemsetAsync(c->d_bin_total, 0, 4 * kMaxW, c->stream));
-  CK(c, cudaMalloc(&c->d_cursor, 4 * kMaxW));
+  if (!c->d_cursor) CK(c, cudaMalloc(&c->d_cursor, 4 * kMaxW));
   if (c->a_empty) {
     c->a_set = true;
     return 0;
@@ -178,9 +200,9 @@ int finish_reference(vmi_ctx* c, const int64_t bounds[6], int64_t V) {
     return fail(c, VMI_ERR_UNSUPPORTED,
                 "scan A's occupied AABB exceeds 2^32-2 voxels (dense reference grid limit)");
   c->grid_bytes = (size_t)vol;
-  CK(c, cudaMalloc(&c->d_grid, c->grid_bytes));
+  CK(c, grow(&c->d_grid, c->cap_grid, c->grid_bytes));
   CK(c, cudaMemsetAsync(c->d_grid, 0, c->grid_bytes, c->stream));
-  CK(c, cudaMalloc(&c->d_avox, sizeof(int4) * (V > 0 ? V : 1)));
+  CK(c, grow(&c->d_avox, c->cap_avox, sizeof(int4) * (V > 0 ? V : 1)));
   CK(c, build_reference(c->d_akeys, c->d_avalues, (int)V, c->g, c->amin, c->ext, c->d_grid,
                         c->d_avox, c->d_bin_total, c->d_cursor, c->stream, &c->launches));
   std::vector<uint32_t> tot(kMaxW);
@@ -325,7 +347,7 @@ int vmi_destroy(vmi_ctx* c) {
   if (!c) return 0;
   cudaSetDevice(c->device);
   cudaStreamSynchronize(c->stream);
-  free_a(c);
+  release_a(c);
   cudaFree(c->d_pts);
   exact_free(c->ex);
   cudaFree(c->d_mats); cudaFree(c->d_mi); cudaFree(c->d_status); cudaFree(c->d_hist);
@@ -401,8 +423,8 @@ int vmi_set_reference_points(vmi_ctx* c, const double* xyz, int64_t n) {
   if (n > 0x7fffffff) return fail(c, VMI_ERR_UNSUPPORTED, "more than 2^31-1 points");
   cudaSetDevice(c->device);
   free_a(c);
-  double* d = nullptr;
-  CK(c, cudaMalloc(&d, n * 24));
+  CK(c, grow(&c->d_upload, c->cap_upload, (size_t)n * 24));
+  double* d = static_cast<double*>(c->d_upload);
   CK(c, cudaMemcpyAsync(d, xyz, n * 24, cudaMemcpyHostToDevice, c->stream));
   PointSource src{};
   src.xyz = d;
@@ -413,16 +435,17 @@ int vmi_set_reference_points(vmi_ctx* c, const double* xyz, int64_t n) {
   CK(c, cudaMemcpyAsync(h, c->ex.bounds, 7 * 4, cudaMemcpyDeviceToHost, c->stream));
   CK(c, cudaMemcpyAsync(&V, c->ex.nruns, 4, cudaMemcpyDeviceToHost, c->stream));
   CK(c, cudaStreamSynchronize(c->stream));
-  cudaFree(d);
   if (h[6]) return fail(c, VMI_ERR_RANGE, "a point of scan A maps outside the voxel key range");
-  CK(c, cudaMalloc(&c->d_akeys, 8 * (size_t)V));
-  CK(c, cudaMalloc(&c->d_avalues, 8 * (size_t)V));
+  CK(c, grow(&c->d_akeys, c->cap_akeys, 8 * (size_t)V));
+  CK(c, grow(&c->d_avalues, c->cap_avalues, 8 * (size_t)V));
   CK(c, cudaMemcpyAsync(c->d_akeys, c->ex.ukeys, 8 * (size_t)V, cudaMemcpyDeviceToDevice, c->stream));
   CK(c, cudaMemcpyAsync(c->d_avalues, c->ex.values, 8 * (size_t)V, cudaMemcpyDeviceToDevice,
                         c->stream));
   int64_t b64[6];
   for (int j = 0; j < 6; ++j) b64[j] = h[j];
-  return finish_reference(c, b64, V);
+  const int rc = finish_reference(c, b64, V);
+  c->a_npts = n;
+  return rc;
 }
 
 int vmi_set_reference_features(vmi_ctx* c, const int64_t* keys, const double* values, int64_t n,
@@ -436,8 +459,8 @@ int vmi_set_reference_features(vmi_ctx* c, const int64_t* keys, const double* va
   cudaSetDevice(c->device);
   free_a(c);
   const size_t m = n > 0 ? (size_t)n : 1;
-  CK(c, cudaMalloc(&c->d_akeys, 8 * m));
-  CK(c, cudaMalloc(&c->d_avalues, 8 * m));
+  CK(c, grow(&c->d_akeys, c->cap_akeys, 8 * m));
+  CK(c, grow(&c->d_avalues, c->cap_avalues, 8 * m));
   if (n > 0) {
     CK(c, cudaMemcpyAsync(c->d_akeys, keys, 8 * n, cudaMemcpyHostToDevice, c->stream));
     CK(c, cudaMemcpyAsync(c->d_avalues, values, 8 * n, cudaMemcpyHostToDevice, c->stream));
@@ -471,8 +494,6 @@ static int set_query(vmi_ctx* c, const void* host, int is_f32_src, int64_t n) {
   if (n <= 0 || !host) return fail(c, VMI_ERR_ARG, "cannot voxelize an empty cloud");
   if (n > 0x7fffffff) return fail(c, VMI_ERR_UNSUPPORTED, "more than 2^31-1 points");
   cudaSetDevice(c->device);
-  cudaFree(c->d_pts);
-  c->d_pts = nullptr;
   c->b_set = false;
   int as_f32 = 1;
   std::vector<float> f4;
@@ -505,23 +526,25 @@ static int set_query(vmi_ctx* c, const void* host, int is_f32_src, int64_t n) {
       mx = std::fmax(mx, std::fabs(v));
     }
   c->max_abs = mx;
-  void* tmp = nullptr;
-  CK(c, cudaMalloc(&tmp, up_bytes));
+  CK(c, grow(&c->d_upload, c->cap_upload, up_bytes));
+  void* tmp = c->d_upload;
   CK(c, cudaMemcpyAsync(tmp, up, up_bytes, cudaMemcpyHostToDevice, c->stream));
   c->span = (int)((n + c->threads - 1) / c->threads);
   c->rem = (int)(n - (int64_t)(c->span - 1) * c->threads);
   const size_t rec = as_f32 ? 16 : 32;
-  CK(c, cudaMalloc(&c->d_pts, (size_t)c->span * c->threads * rec));
+  CK(c, grow(&c->d_pts, c->cap_pts, (size_t)c->span * c->threads * rec));
   CK(c, launch_span_layout(tmp, as_f32, n, c->span, c->rem, c->threads, c->d_pts, c->stream));
   c->launches += 1;
   CK(c, cudaStreamSynchronize(c->stream));
-  cudaFree(tmp);
   c->is_f32 = as_f32;
   c->nb = n;
   c->b_set = true;
   // table sizing hint: scan B's occupied voxel count in its own frame
   c->b_voxels = 0;
-  if (c->params_set) {
+  if (c->a_set && c->a_npts > 0 && c->a_nvox > 0) {
+    // same sensor, same grid: scale scan A's voxel count (saves a voxelization)
+    c->b_voxels = (int64_t)((double)c->a_nvox * (double)n / (double)c->a_npts) + 1;
+  } else if (c->params_set) {
     PointSource src{};
     src.B = query_view(c);
     src.n = n;

@@ -88,15 +88,18 @@ class MIEngine:
         self._feat_a: FeatureMap | None = None
 
     # ---- scan A ---------------------------------------------------------------
-    def set_reference(self, scan_a) -> FeatureMap:
-        """Voxelize + featurize scan A on the GPU (bit-exact), keep it resident."""
+    def set_reference(self, scan_a, fetch: bool = True) -> FeatureMap | None:
+        """Voxelize + featurize scan A on the GPU (bit-exact), keep it resident.
+
+        Returns the FeatureMap (copied back to the host) unless ``fetch`` is
+        False; ``reference`` fetches it lazily later.
+        """
         pts = _points_of(scan_a)[:, :3]
         if pts.shape[0] == 0:
             raise ValueError("cannot voxelize an empty cloud")
-        self.ctx.set_reference_points(pts)
-        keys, vals, bounds = self.ctx.get_reference_features()
-        self._feat_a = FeatureMap(kind=self.kind, keys=keys, values=vals, bounds=bounds)
-        return self._feat_a
+        self.ctx.set_reference_points(np.ascontiguousarray(pts, dtype=np.float64))
+        self._feat_a = None
+        return self.reference if fetch else None
 
     def set_reference_features(self, feat_a) -> None:
         """Upload an existing FeatureMap (this package's or the reference's)."""
@@ -107,6 +110,9 @@ class MIEngine:
 
     @property
     def reference(self) -> FeatureMap | None:
+        if self._feat_a is None:
+            keys, vals, bounds = self.ctx.get_reference_features()
+            self._feat_a = FeatureMap(kind=self.kind, keys=keys, values=vals, bounds=bounds)
         return self._feat_a
 
     # ---- scan B ---------------------------------------------------------------
