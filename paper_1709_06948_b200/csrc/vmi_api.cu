@@ -495,11 +495,21 @@ static int set_query(vmi_ctx* c, const void* host, int is_f32_src, int64_t n) {
   if (n > 0x7fffffff) return fail(c, VMI_ERR_UNSUPPORTED, "more than 2^31-1 points");
   cudaSetDevice(c->device);
   c->b_set = false;
-  int as_f32 = 1;
+  // VMI_FORCE_F64 (experiments): keep double records even for float32-exact input
+  static const bool force_f64 = std::getenv("VMI_FORCE_F64") != nullptr;
+  int as_f32 = force_f64 ? 0 : 1;
   std::vector<float> f4;
+  std::vector<double> d3;
   const void* up = host;
   size_t up_bytes;
-  if (is_f32_src) {
+  if (is_f32_src && force_f64) {  // expand float records to (x, y, z) doubles
+    const float* r = static_cast<const float*>(host);
+    d3.resize((size_t)n * 3);
+    for (int64_t i = 0; i < n; ++i)
+      for (int j = 0; j < 3; ++j) d3[3 * i + j] = (double)r[4 * i + j];
+    up = d3.data();
+    up_bytes = (size_t)n * 24;
+  } else if (is_f32_src) {
     up_bytes = (size_t)n * 16;
   } else {
     const double* xyz = static_cast<const double*>(host);

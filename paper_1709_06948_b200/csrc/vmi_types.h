@@ -45,7 +45,10 @@ struct RefView {
 // the whole scan and every warp gets a similar share of voxel-run records
 // (far rings produce many more than near ones).  Element r of thread t's
 // span is stored at r*T + t: every warp load is 32 consecutive records.
-constexpr int kFastThreads = 512;  // spans per CTA (span layout "threads") of the fast kernel
+#ifndef VMI_FAST_THREADS
+#define VMI_FAST_THREADS 512
+#endif
+constexpr int kFastThreads = VMI_FAST_THREADS;  // spans per CTA (span layout "threads")
 
 struct QueryView {
   const void* pts;  // float4 (x, y, z, i) or double4 (x, y, z, pad)

@@ -269,7 +269,42 @@ def make_align():
     np.savez_compressed(os.path.join(HERE, "align_golden.npz"), **out)
 
 
+def nm_test_function(x):
+    """Smooth 6-D test objective with a unique maximum (for optimizer parity)."""
+    x = np.asarray(x, dtype=np.float64)
+    c = np.array([1.0, -2.0, 0.5, 0.1, -0.05, 0.3])
+    w = np.array([1.0, 0.5, 2.0, 10.0, 10.0, 4.0])
+    return float(np.exp(-np.sum(w * (x - c) ** 2)) + 0.1 * np.cos(x[0] - x[1]))
+
+
+def make_nm():
+    """voxmi.nelder_mead_maximize on a closed-form objective: every OptimResult field."""
+    from voxmi import SimplexConfig, nelder_mead_maximize
+    out = {}
+    cases = {
+        "default": (np.zeros(6), SimplexConfig()),
+        "restarts": (np.array([3.0, 1.0, 0.0, 0.0, 0.0, 0.0]),
+                     SimplexConfig(initial_steps=(1.0, 1.0, 0.5, 0.05, 0.05, 0.2),
+                                   max_iterations=400, restarts=2, f_tol=1e-9, x_tol=1e-7)),
+        "maxiter": (np.ones(6), SimplexConfig(max_iterations=25)),
+    }
+    for tag, (x0, cfg) in cases.items():
+        r = nelder_mead_maximize(nm_test_function, x0, cfg)
+        out[f"{tag}_x0"] = x0
+        out[f"{tag}_steps"] = np.asarray(cfg.initial_steps)
+        out[f"{tag}_cfg"] = np.array([cfg.max_iterations, cfg.f_tol, cfg.x_tol, cfg.restarts])
+        out[f"{tag}_best_x"] = r.best_x
+        out[f"{tag}_best_value"] = np.float64(r.best_value)
+        out[f"{tag}_iterations"] = np.int64(r.iterations)
+        out[f"{tag}_termination"] = np.array(r.termination)
+        out[f"{tag}_trace"] = np.asarray(r.trace)
+        out[f"{tag}_spread"] = np.asarray(r.trace_spread)
+        out[f"{tag}_n_eval"] = np.int64(r.n_evaluations)
+        print("nm", tag, r.iterations, r.termination, r.n_evaluations)
+    np.savez_compressed(os.path.join(HERE, "nm_golden.npz"), **out)
+
+
 if __name__ == "__main__":
-    what = sys.argv[1:] or ["small", "mi", "bins", "hdl", "c1", "align"]
+    what = sys.argv[1:] or ["small", "mi", "bins", "hdl", "c1", "align", "nm"]
     for w in what:
         globals()[f"make_{w}"]()
