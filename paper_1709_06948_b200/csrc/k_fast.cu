@@ -54,7 +54,7 @@ __device__ __forceinline__ uint32_t slot_of(uint32_t lin, uint32_t cap) {
 #define VMI_STAGES 8  // TMA: two groups of four records in flight per warp
 #endif
 #endif
-#ifndef VMI_TMA
+#if !defined(VMI_TMA) && !defined(VMI_PAIR_PUSH)
 constexpr int kUnroll = VMI_UNROLL;  // main point loop unroll (A/B tunable)
 #endif
 template <bool F32>
@@ -176,7 +176,12 @@ __device__ __forceinline__ void flush_count(uint32_t* key, uint32_t* cnt, uint32
 
 // Warp-private flush queue: run records pushed by any lane, drained 32 at a
 // time by the whole warp so the hash/atomic path always runs converged.
-constexpr int kQueueMax = 128;  // entries per warp: a step pushes <= 32*NS, drained at 32
+constexpr int kQueueMax = 128;
+#ifdef VMI_PAIR_PUSH
+constexpr bool kPairPush = true;   // one queue push per two points
+#else
+constexpr bool kPairPush = false;
+#endif  // entries per warp: a step pushes <= 32*NS, drained at 32
 
 // Shared-memory layout helper (bytes), mirrored by fast_smem_bytes() on the host.
 constexpr int kCountLut = 1024;  // COUNT bins precomputed for n < kCountLut
@@ -196,7 +201,8 @@ __host__ __device__ inline FastSmem fast_layout(int kind, int cap, int W, int th
   off += (size_t)cap * (kind == 0 ? (8 + 4) : (4 + 4));
   off = (off + 15) & ~size_t(15);
   L.queue = off;
-  off += (size_t)(threads / 32) * (ns == 1 ? 64 : kQueueMax) * (kind == 0 ? (4 + 4 + 8 + 8 + 8) : (4 + 4));
+  off += (size_t)(threads / 32) * (ns == 1 && !kPairPush ? 64 : kQueueMax) *
+         (kind == 0 ? (4 + 4 + 8 + 8 + 8) : (4 + 4));
   off = (off + 15) & ~size_t(15);
   L.hist = off; off += (size_t)W * W * 4; off = (off + 15) & ~size_t(15);
   L.marg = off; off += (size_t)W * 4; off = (off + 15) & ~size_t(15);
@@ -274,7 +280,7 @@ __global__ void __launch_bounds__(THREADS, 1)
   uint32_t* ccnt = nullptr;
   // warp queue: AoS records, VARZ 32 B {lin, n, K, S1, S2}, COUNT 8 B {lin, n}
   constexpr uint32_t kRec = KIND == 0 ? 32u : 8u;
-  constexpr int kQueue = NS == 1 ? 64 : 128;
+  constexpr int kQueue = (NS == 1 && !kPairPush) ? 64 : 128;
   const uint32_t qbase = (uint32_t)__cvta_generic_to_shared(smem + L.queue) + wid * kQueue * kRec;
   if (KIND == 0) {
     VT.key = reinterpret_cast<unsigned long long*>(smem + L.table);
@@ -523,7 +529,74 @@ __global__ void __launch_bounds__(THREADS, 1)
         }
         advance(lin, Z);
       };
-#ifndef VMI_STATIC_SLOT
+#if defined(VMI_PAIR_PUSH)
+      // two points per step: both located first (independent fp64 chains),
+      // then both run updates, then ONE warp-wide queue push for the up to
+      // two runs each lane finished
+      auto store_state = [&](uint32_t pos, uint32_t l, uint32_t n, double K, double a1, double a2) {
+        const uint32_t a = qbase + (pos & (kQueue - 1)) * kRec;
+        if (KIND == 0) {
+          st_shared_v4(a, l, n, dlo(K), dhi(K));
+          st_shared_v4(a + 16, dlo(a1), dhi(a1), dlo(a2), dhi(a2));
+        } else {
+          st_shared_v2(a, l, n);
+        }
+      };
+      auto step1 = [&](uint32_t lin, double Z, bool& pend, uint32_t& pl, uint32_t& pn, double& pK,
+                       double& p1, double& p2) {
+        const bool e = lin != cur[0];
+        pend = e && cur[0] != kNoVoxel;
+        pl = cur[0]; pn = (uint32_t)cn[0]; pK = cK[0]; p1 = cs1[0]; p2 = cs2[0];
+        if (e) {
+          cur[0] = lin; cn[0] = 1; cK[0] = Z; cs1[0] = 0.0; cs2[0] = 0.0;
+        } else {
+          const double d = Z - cK[0];
+          ++cn[0]; cs1[0] += d; cs2[0] = fma(d, d, cs2[0]);
+        }
+      };
+      auto pair_body = [&](int r) {
+        cp_async_wait<S - 2>();  // groups r and r+1 have landed
+        const Rec v0 = lds_rec<Rec>(my_stage + (uint32_t)(r % S) * kStageStride);
+        const Rec v1 = lds_rec<Rec>(my_stage + (uint32_t)((r + 1) % S) * kStageStride);
+        uint32_t l0, l1;
+        double Z0, Z1;
+        locate((double)v0.x, (double)v0.y, (double)v0.z, true, l0, Z0);
+        locate((double)v1.x, (double)v1.y, (double)v1.z, true, l1, Z1);
+        issue(r + S);      // refill the two slots just consumed
+        issue(r + S + 1);
+        bool pa, pb;
+        uint32_t la, na, lb, nb;
+        double Ka, a1, a2, Kb, b1, b2;
+        step1(l0, Z0, pa, la, na, Ka, a1, a2);
+        step1(l1, Z1, pb, lb, nb, Kb, b1, b2);
+        const unsigned ma = __ballot_sync(0xffffffffu, pa);
+        const unsigned mb = __ballot_sync(0xffffffffu, pb);
+        if ((ma | mb) != 0u) {
+          const uint32_t ca = __popc(ma);
+          if (pa) store_state(qt + __popc(ma & lt_mask), la, na, Ka, a1, a2);
+          if (pb) store_state(qt + ca + __popc(mb & lt_mask), lb, nb, Kb, b1, b2);
+          qt += ca + __popc(mb);
+          while (qt - qh >= 32) {
+            __syncwarp();
+            flush_rec(qh + lane);
+            qh += 32;
+            __syncwarp();
+          }
+        }
+      };
+      issue(S - 1);  // pair mode keeps S groups in flight
+      int rr = 0;
+#pragma unroll 2
+      for (; rr + 2 <= full; rr += 2) pair_body(rr);
+      if (rr < full) {  // odd leftover
+        cp_async_wait<0>();
+        uint32_t lin[NS];
+        double Z[NS];
+        const Rec v = lds_rec<Rec>(my_stage + (uint32_t)(rr % S) * kStageStride);
+        locate((double)v.x, (double)v.y, (double)v.z, true, lin[0], Z[0]);
+        advance(lin, Z);
+      }
+#elif !defined(VMI_STATIC_SLOT)
       #pragma unroll kUnroll
       for (int r = 0; r < full; ++r) body(r, r % S);
 #else
