@@ -54,7 +54,7 @@ __device__ __forceinline__ uint32_t slot_of(uint32_t lin, uint32_t cap) {
 #define VMI_STAGES 8  // TMA: two groups of four records in flight per warp
 #endif
 #endif
-#if !defined(VMI_TMA) && !defined(VMI_PAIR_PUSH)
+#if !defined(VMI_TMA) && defined(VMI_SINGLE_PUSH)
 constexpr int kUnroll = VMI_UNROLL;  // main point loop unroll (A/B tunable)
 #endif
 template <bool F32>
@@ -176,12 +176,16 @@ __device__ __forceinline__ void flush_count(uint32_t* key, uint32_t* cnt, uint32
 
 // Warp-private flush queue: run records pushed by any lane, drained 32 at a
 // time by the whole warp so the hash/atomic path always runs converged.
-constexpr int kQueueMax = 128;
-#ifdef VMI_PAIR_PUSH
-constexpr bool kPairPush = true;   // one queue push per two points
+constexpr int kQueueMax = 128;  // >= 32 * (kPG + 1)
+#ifndef VMI_SINGLE_PUSH
+constexpr bool kPairPush = true;   // one queue push per group of kPG points
 #else
 constexpr bool kPairPush = false;
-#endif  // entries per warp: a step pushes <= 32*NS, drained at 32
+#endif
+#ifndef VMI_PG
+#define VMI_PG 2
+#endif
+constexpr int kPG = VMI_PG;  // points per queue push (a lane finishes at most kPG runs)  // entries per warp: a step pushes <= 32*NS, drained at 32
 
 // Shared-memory layout helper (bytes), mirrored by fast_smem_bytes() on the host.
 constexpr int kCountLut = 1024;  // COUNT bins precomputed for n < kCountLut
@@ -243,6 +247,16 @@ __device__ __forceinline__ uint2 ld_shared_v2(uint32_t a) {
   uint2 v;
   asm volatile("ld.shared.v2.u32 {%0, %1}, [%2];" : "=r"(v.x), "=r"(v.y) : "r"(a) : "memory");
   return v;
+}
+__device__ __forceinline__ int pin_reg(int v) {
+  int r;
+  asm volatile("mov.b32 %0, %1;" : "=r"(r) : "r"(v));
+  return r;
+}
+__device__ __forceinline__ uint32_t pin_reg(uint32_t v) {
+  uint32_t r;
+  asm volatile("mov.b32 %0, %1;" : "=r"(r) : "r"(v));
+  return r;
 }
 __device__ __forceinline__ uint32_t dlo(double d) { return (uint32_t)__double2loint(d); }
 __device__ __forceinline__ uint32_t dhi(double d) { return (uint32_t)__double2hiint(d); }
@@ -449,6 +463,15 @@ __global__ void __launch_bounds__(THREADS, 1)
         }
       };
       // transform, voxel index, bounds, voxel inside A's AABB (pure per point)
+#ifdef VMI_PIN_CONSTS
+      // opaque copies: kept in registers instead of re-loaded from the
+      // constant bank on every point
+      const int am0 = pin_reg(A.amin[0]), am1 = pin_reg(A.amin[1]), am2 = pin_reg(A.amin[2]);
+      const uint32_t ex0 = pin_reg(A.ext[0]), ex1 = pin_reg(A.ext[1]), ex2 = pin_reg(A.ext[2]);
+#else
+      const int am0 = A.amin[0], am1 = A.amin[1], am2 = A.amin[2];
+      const uint32_t ex0 = A.ext[0], ex1 = A.ext[1], ex2 = A.ext[2];
+#endif
       auto locate = [&](double x, double y, double z, bool valid, uint32_t& lin, double& Z) {
         const double X = xform_row(x, y, z, m0, m1, m2, t0);
         const double Y = xform_row(x, y, z, m3, m4, m5, t1);
@@ -461,11 +484,11 @@ __global__ void __launch_bounds__(THREADS, 1)
           bmin0 = min(bmin0, ix); bmax0 = max(bmax0, ix);
           bmin1 = min(bmin1, iy); bmax1 = max(bmax1, iy);
           bmin2 = min(bmin2, iz); bmax2 = max(bmax2, iz);
-          const uint32_t rx = (uint32_t)(ix - A.amin[0]);
-          const uint32_t ry = (uint32_t)(iy - A.amin[1]);
-          const uint32_t rz = (uint32_t)(iz - A.amin[2]);
-          const bool inside = (rx < A.ext[0]) & (ry < A.ext[1]) & (rz < A.ext[2]);
-          lin = inside ? (rx * A.ext[1] + ry) * A.ext[2] + rz : kNoVoxel;
+          const uint32_t rx = (uint32_t)(ix - am0);
+          const uint32_t ry = (uint32_t)(iy - am1);
+          const uint32_t rz = (uint32_t)(iz - am2);
+          const bool inside = (rx < ex0) & (ry < ex1) & (rz < ex2);
+          lin = inside ? (rx * ex1 + ry) * ex2 + rz : kNoVoxel;
         if (npass > 1 && lin != kNoVoxel && __umulhi(lin * 0x85EBCA6Bu, (uint32_t)npass) != (uint32_t)pass)
           lin = kNoVoxel;  // another pass's partition
         }
@@ -529,7 +552,7 @@ __global__ void __launch_bounds__(THREADS, 1)
         }
         advance(lin, Z);
       };
-#if defined(VMI_PAIR_PUSH)
+#if !defined(VMI_SINGLE_PUSH)
       // two points per step: both located first (independent fp64 chains),
       // then both run updates, then ONE warp-wide queue push for the up to
       // two runs each lane finished
@@ -554,28 +577,34 @@ __global__ void __launch_bounds__(THREADS, 1)
           ++cn[0]; cs1[0] += d; cs2[0] = fma(d, d, cs2[0]);
         }
       };
-      auto pair_body = [&](int r) {
-        cp_async_wait<S - 2>();  // groups r and r+1 have landed
-        const Rec v0 = lds_rec<Rec>(my_stage + (uint32_t)(r % S) * kStageStride);
-        const Rec v1 = lds_rec<Rec>(my_stage + (uint32_t)((r + 1) % S) * kStageStride);
-        uint32_t l0, l1;
-        double Z0, Z1;
-        locate((double)v0.x, (double)v0.y, (double)v0.z, true, l0, Z0);
-        locate((double)v1.x, (double)v1.y, (double)v1.z, true, l1, Z1);
-        issue(r + S);      // refill the two slots just consumed
-        issue(r + S + 1);
-        bool pa, pb;
-        uint32_t la, na, lb, nb;
-        double Ka, a1, a2, Kb, b1, b2;
-        step1(l0, Z0, pa, la, na, Ka, a1, a2);
-        step1(l1, Z1, pb, lb, nb, Kb, b1, b2);
-        const unsigned ma = __ballot_sync(0xffffffffu, pa);
-        const unsigned mb = __ballot_sync(0xffffffffu, pb);
-        if ((ma | mb) != 0u) {
-          const uint32_t ca = __popc(ma);
-          if (pa) store_state(qt + __popc(ma & lt_mask), la, na, Ka, a1, a2);
-          if (pb) store_state(qt + ca + __popc(mb & lt_mask), lb, nb, Kb, b1, b2);
-          qt += ca + __popc(mb);
+      auto group_body = [&](int r) {
+        cp_async_wait<S - kPG>();  // groups r .. r+kPG-1 have landed
+        uint32_t l[kPG];
+        double Z[kPG];
+#pragma unroll
+        for (int u = 0; u < kPG; ++u) {
+          const Rec v = lds_rec<Rec>(my_stage + (uint32_t)((r + u) % S) * kStageStride);
+          locate((double)v.x, (double)v.y, (double)v.z, true, l[u], Z[u]);
+        }
+#pragma unroll
+        for (int u = 0; u < kPG; ++u) issue(r + S + u);  // refill the slots just consumed
+        bool pd[kPG];
+        uint32_t pl[kPG], pn[kPG];
+        double pK[kPG], p1[kPG], p2[kPG];
+#pragma unroll
+        for (int u = 0; u < kPG; ++u) step1(l[u], Z[u], pd[u], pl[u], pn[u], pK[u], p1[u], p2[u]);
+        unsigned m[kPG];
+        unsigned any = 0u;
+#pragma unroll
+        for (int u = 0; u < kPG; ++u) { m[u] = __ballot_sync(0xffffffffu, pd[u]); any |= m[u]; }
+        if (any != 0u) {
+          uint32_t base = qt;
+#pragma unroll
+          for (int u = 0; u < kPG; ++u) {
+            if (pd[u]) store_state(base + __popc(m[u] & lt_mask), pl[u], pn[u], pK[u], p1[u], p2[u]);
+            base += __popc(m[u]);
+          }
+          qt = base;
           while (qt - qh >= 32) {
             __syncwarp();
             flush_rec(qh + lane);
@@ -584,17 +613,17 @@ __global__ void __launch_bounds__(THREADS, 1)
           }
         }
       };
-      issue(S - 1);  // pair mode keeps S groups in flight
+      static_assert(S >= kPG, "ring must hold a full group");
+      issue(S - 1);  // group mode keeps S records in flight (invariant: 0..r+S-1 issued)
       int rr = 0;
-#pragma unroll 2
-      for (; rr + 2 <= full; rr += 2) pair_body(rr);
-      if (rr < full) {  // odd leftover
+      for (; rr + kPG <= full; rr += kPG) group_body(rr);
+      for (; rr < full; ++rr) {  // leftover (< kPG) points
         cp_async_wait<0>();
         uint32_t lin[NS];
-        double Z[NS];
+        double Zs[NS];
         const Rec v = lds_rec<Rec>(my_stage + (uint32_t)(rr % S) * kStageStride);
-        locate((double)v.x, (double)v.y, (double)v.z, true, lin[0], Z[0]);
-        advance(lin, Z);
+        locate((double)v.x, (double)v.y, (double)v.z, true, lin[0], Zs[0]);
+        advance(lin, Zs);
       }
 #elif !defined(VMI_STATIC_SLOT)
       #pragma unroll kUnroll
