@@ -49,7 +49,7 @@ __device__ __forceinline__ uint32_t slot_of(uint32_t lin, uint32_t cap) {
 #endif
 #ifndef VMI_STAGES
 #ifndef VMI_TMA
-#define VMI_STAGES 4
+#define VMI_STAGES 8  // cp.async ring: 8 records in flight per thread (>= 2 push groups)
 #else
 #define VMI_STAGES 8  // TMA: two groups of four records in flight per warp
 #endif
@@ -183,9 +183,13 @@ constexpr bool kPairPush = true;   // one queue push per group of kPG points
 constexpr bool kPairPush = false;
 #endif
 #ifndef VMI_PG
-#define VMI_PG 2
+#define VMI_PG 4
 #endif
-constexpr int kPG = VMI_PG;  // points per queue push (a lane finishes at most kPG runs)  // entries per warp: a step pushes <= 32*NS, drained at 32
+constexpr int kPG = VMI_PG;  // points per queue push (a lane finishes at most kPG runs)
+#ifndef VMI_GROUP_UNROLL
+#define VMI_GROUP_UNROLL 2
+#endif
+constexpr int kGroupUnroll = VMI_GROUP_UNROLL;  // entries per warp: a step pushes <= 32*NS, drained at 32
 
 // Shared-memory layout helper (bytes), mirrored by fast_smem_bytes() on the host.
 constexpr int kCountLut = 1024;  // COUNT bins precomputed for n < kCountLut
@@ -616,6 +620,7 @@ __global__ void __launch_bounds__(THREADS, 1)
       static_assert(S >= kPG, "ring must hold a full group");
       issue(S - 1);  // group mode keeps S records in flight (invariant: 0..r+S-1 issued)
       int rr = 0;
+#pragma unroll kGroupUnroll
       for (; rr + kPG <= full; rr += kPG) group_body(rr);
       for (; rr < full; ++rr) {  // leftover (< kPG) points
         cp_async_wait<0>();

@@ -271,7 +271,9 @@ int launch_fast_eval(vmi_ctx* c, const double* mats_dev, int64_t P, double* mi, 
   if (c->npass_override > 0) {
     fl.npass = c->npass_override;
   } else if (c->b_voxels > 0) {
-    const double per_pass = 0.55 * (double)fl.cap;
+    // the estimate counts all of scan B's voxels; only those inside A's AABB
+    // enter the table, so ~70% nominal load leaves real loads near 50-60%
+    const double per_pass = 0.70 * (double)fl.cap;
     fl.npass = (int)std::ceil((double)c->b_voxels / per_pass);
     if (fl.npass < 1) fl.npass = 1;
     if (fl.npass > 64) fl.npass = 64;
