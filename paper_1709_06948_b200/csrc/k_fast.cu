@@ -57,8 +57,14 @@ __device__ __forceinline__ uint32_t slot_of(uint32_t lin, uint32_t cap) {
 #if !defined(VMI_TMA) && defined(VMI_SINGLE_PUSH)
 constexpr int kUnroll = VMI_UNROLL;  // main point loop unroll (A/B tunable)
 #endif
-template <bool F32>
-__host__ __device__ constexpr int kStages() { return F32 ? VMI_STAGES : VMI_STAGES / 2; }
+// Pipeline shape per instantiation.  Single-pass poses: kPG points per queue
+// push with an S-record cp.async ring (two push groups in flight).  Multi-pass
+// (large grids): shared memory goes to the table instead (more capacity =
+// fewer passes), so one point per push and a 4-record ring.
+template <bool F32, bool MULTI = false>
+__host__ __device__ constexpr int kStages() {
+  return MULTI ? 4 : (F32 ? VMI_STAGES : VMI_STAGES / 2);
+}
 template <typename Rec>
 __device__ __forceinline__ void cp_async_rec(uint32_t dst, const Rec* src) {
   asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(dst), "l"(src) : "memory");
@@ -185,7 +191,14 @@ constexpr bool kPairPush = false;
 #ifndef VMI_PG
 #define VMI_PG 4
 #endif
-constexpr int kPG = VMI_PG;  // points per queue push (a lane finishes at most kPG runs)
+template <bool F32, bool MULTI>
+__host__ __device__ constexpr int kPGt() {  // points per queue push
+  return (MULTI || !kPairPush) ? 1 : (F32 ? VMI_PG : VMI_PG / 2);
+}
+template <bool F32, bool MULTI>
+__host__ __device__ constexpr int kQueueT() {  // warp queue entries: >= 32*(kPG+1), pow2
+  return kPGt<F32, MULTI>() == 1 ? 64 : 128;
+}
 #ifndef VMI_GROUP_UNROLL
 #define VMI_GROUP_UNROLL 2
 #endif
@@ -198,19 +211,21 @@ struct FastSmem {
   size_t stage, bars, table, queue, hist, marg, red, rows, cols, misc, lut, total;
 };
 __host__ __device__ inline FastSmem fast_layout(int kind, int cap, int W, int threads, int f32,
-                                                int ns) {
+                                                int ns, int multi) {
   FastSmem L;
   size_t off = 0;
   L.stage = off;
-  off += (size_t)threads * ns * (f32 ? 16 * kStages<true>() : 32 * kStages<false>());
+  const int stages = multi ? kStages<true, true>() : (f32 ? kStages<true>() : kStages<false>());
+  off += (size_t)threads * ns * (f32 ? 16 : 32) * stages;
   L.bars = off;  // two mbarriers per warp (TMA bulk staging)
   off += (size_t)(threads / 32) * 16;
   L.table = off;
   off += (size_t)cap * (kind == 0 ? (8 + 4) : (4 + 4));
   off = (off + 15) & ~size_t(15);
   L.queue = off;
-  off += (size_t)(threads / 32) * (ns == 1 && !kPairPush ? 64 : kQueueMax) *
-         (kind == 0 ? (4 + 4 + 8 + 8 + 8) : (4 + 4));
+  const int queue = ns != 1 ? kQueueMax
+                    : (multi ? kQueueT<true, true>() : (f32 ? kQueueT<true, false>() : kQueueT<false, false>()));
+  off += (size_t)(threads / 32) * queue * (kind == 0 ? (4 + 4 + 8 + 8 + 8) : (4 + 4));
   off = (off + 15) & ~size_t(15);
   L.hist = off; off += (size_t)W * W * 4; off = (off + 15) & ~size_t(15);
   L.marg = off; off += (size_t)W * 4; off = (off + 15) & ~size_t(15);
@@ -224,8 +239,8 @@ __host__ __device__ inline FastSmem fast_layout(int kind, int cap, int W, int th
   return L;
 }
 
-size_t fast_smem_bytes(int kind, int cap, int bins, int threads, int f32, int ns) {
-  return fast_layout(kind, cap, bins + 1, threads, f32, ns).total;
+size_t fast_smem_bytes(int kind, int cap, int bins, int threads, int f32, int ns, int multi) {
+  return fast_layout(kind, cap, bins + 1, threads, f32, ns, multi).total;
 }
 
 __device__ __forceinline__ void st_shared_v4(uint32_t a, uint32_t x, uint32_t y, uint32_t z,
@@ -276,7 +291,8 @@ __global__ void __launch_bounds__(THREADS, 1)
                 FeatureDump dump, double2* __restrict__ gsums, int npass) {
   extern __shared__ __align__(16) unsigned char smem[];
   const int W = g.bins + 1;
-  const FastSmem L = fast_layout(KIND, cap, W, THREADS, F32 ? 1 : 0, NS);
+  const FastSmem L = fast_layout(KIND, cap, W, THREADS, F32 ? 1 : 0, NS, MULTI ? 1 : 0);
+  constexpr int kPG = kPGt<F32, MULTI>();
   const uint32_t stage_base = (uint32_t)__cvta_generic_to_shared(smem + L.stage);
   uint32_t* hist = reinterpret_cast<uint32_t*>(smem + L.hist);
   uint32_t* marg = reinterpret_cast<uint32_t*>(smem + L.marg);
@@ -298,7 +314,7 @@ __global__ void __launch_bounds__(THREADS, 1)
   uint32_t* ccnt = nullptr;
   // warp queue: AoS records, VARZ 32 B {lin, n, K, S1, S2}, COUNT 8 B {lin, n}
   constexpr uint32_t kRec = KIND == 0 ? 32u : 8u;
-  constexpr int kQueue = (NS == 1 && !kPairPush) ? 64 : 128;
+  constexpr int kQueue = NS == 1 ? kQueueT<F32, MULTI>() : kQueueMax;
   const uint32_t qbase = (uint32_t)__cvta_generic_to_shared(smem + L.queue) + wid * kQueue * kRec;
   if (KIND == 0) {
     VT.key = reinterpret_cast<unsigned long long*>(smem + L.table);
@@ -527,7 +543,7 @@ __global__ void __launch_bounds__(THREADS, 1)
       // the record back with one LDS when it is its turn.  Keeping the prefetch
       // out of the register file stops the compiler from hoisting conversions of
       // in-flight data (which turned a register prefetch into stalls).
-      constexpr int S = kStages<F32>();
+      constexpr int S = kStages<F32, MULTI>();
       const uint32_t my_stage = stage_base + (uint32_t)tid * (uint32_t)sizeof(Rec);
       constexpr uint32_t kStageStride = (uint32_t)(VTH * sizeof(Rec));
       constexpr uint32_t kStreamOff = (uint32_t)(THREADS * sizeof(Rec));
@@ -882,7 +898,7 @@ __global__ void __launch_bounds__(THREADS, 1)
 template <int THREADS, int NS, int KIND, bool F32, int MODE, bool MULTI>
 static cudaError_t launch_fast_t(const FastLaunch& fl, cudaStream_t st) {
   auto k = k_pose_fast<THREADS, NS, KIND, F32, MODE, MULTI>;
-  size_t smem = fast_smem_bytes(KIND, fl.cap, fl.g.bins, THREADS, F32 ? 1 : 0, NS);
+  size_t smem = fast_smem_bytes(KIND, fl.cap, fl.g.bins, THREADS, F32 ? 1 : 0, NS, MULTI ? 1 : 0);
   cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e != cudaSuccess) return e;
   k<<<fl.grid, THREADS, smem, st>>>(fl.g, fl.A, fl.B, fl.mats, fl.P, fl.cap, fl.mi, fl.status,

@@ -6,6 +6,7 @@
 // and the float32-exactness test of uploaded coordinates.
 #include <cmath>
 #include <cstdio>
+#include <algorithm>
 #include <cstdlib>
 #include <cstring>
 #include <string>
@@ -144,23 +145,43 @@ QueryView query_view(const vmi_ctx* c) {
   return B;
 }
 
-int table_cap(const vmi_ctx* c) {
-  if (c->cap_override > 0) return c->cap_override;
+// Largest table that fits shared memory next to the kernel's other buffers.
+size_t max_table_cap(const vmi_ctx* c, bool multi) {
   const size_t fixed = fast_smem_bytes(c->g.kind, 0, c->g.bins, c->threads / c->streams,
-                                       c->is_f32, c->streams);
+                                       c->is_f32, c->streams, multi ? 1 : 0);
   const size_t per = c->g.kind == 0 ? 12 : 8;
-  size_t cap = (c->smem_optin - fixed) / per;
-  // every slot is walked once per pose: size for a ~40% load at the expected
-  // occupancy (scan B's voxel count) rather than filling shared memory
+  return ((c->smem_optin - fixed) / per) & ~size_t(31);
+}
+
+// Table capacity and pass count for the current scan pair.  Every slot is
+// walked once per pose, so a single-pass table is sized for a ~40% load at
+// scan B's expected occupancy rather than filling shared memory; when even a
+// full table cannot hold it, the multi-pass layout (bigger table) is used.
+void plan_table(const vmi_ctx* c, int* cap_out, int* npass_out) {
   static const double factor = [] {
     const char* e = std::getenv("VMI_CAP_FACTOR");  // experiments only
     return e ? std::atof(e) : 2.5;
   }();
-  const size_t want =
-      ((size_t)(factor * (double)(c->b_voxels > 0 ? c->b_voxels : 4096)) + 31) & ~size_t(31);
-  if (want < cap) cap = want < 2048 ? 2048 : want;
-  cap &= ~size_t(31);
-  return (int)cap;
+  const double est = (double)(c->b_voxels > 0 ? c->b_voxels : 4096);
+  if (c->cap_override > 0) {
+    *cap_out = c->cap_override;
+    *npass_out = c->npass_override > 0 ? c->npass_override
+                                       : std::max(1, (int)std::ceil(est / (0.70 * c->cap_override)));
+    return;
+  }
+  const size_t cap1 = max_table_cap(c, false);
+  if (c->npass_override <= 1 && (c->npass_override == 1 || est <= 0.70 * (double)cap1)) {
+    size_t want = ((size_t)(factor * est) + 31) & ~size_t(31);
+    if (want < 2048) want = 2048;
+    *cap_out = (int)std::min(cap1, want);
+    *npass_out = 1;
+    return;
+  }
+  const size_t capm = max_table_cap(c, true);
+  *cap_out = (int)capm;
+  *npass_out = c->npass_override > 1
+                   ? c->npass_override
+                   : std::min(64, std::max(2, (int)std::ceil(est / (0.70 * (double)capm))));
 }
 
 int ensure_sums(vmi_ctx* c, int grid, int cap) {
@@ -263,21 +284,9 @@ int launch_fast_eval(vmi_ctx* c, const double* mats_dev, int64_t P, double* mi, 
   fl.B = query_view(c);
   fl.mats = mats_dev;
   fl.P = P;
-  fl.cap = table_cap(c);
   fl.grid = (int)(P < c->sm_count ? P : c->sm_count);
   fl.streams = c->streams;
-  // hash-partition passes so that each pass's voxels fill <= ~55% of the table
-  fl.npass = 1;
-  if (c->npass_override > 0) {
-    fl.npass = c->npass_override;
-  } else if (c->b_voxels > 0) {
-    // the estimate counts all of scan B's voxels; only those inside A's AABB
-    // enter the table, so ~70% nominal load leaves real loads near 50-60%
-    const double per_pass = 0.70 * (double)fl.cap;
-    fl.npass = (int)std::ceil((double)c->b_voxels / per_pass);
-    if (fl.npass < 1) fl.npass = 1;
-    if (fl.npass > 64) fl.npass = 64;
-  }
+  plan_table(c, &fl.cap, &fl.npass);
   int rc = ensure_sums(c, fl.grid, fl.cap);
   if (rc) return rc;
   fl.sums = c->d_sums;
@@ -698,7 +707,7 @@ int vmi_fast_features(vmi_ctx* c, const double mat[12], int64_t* keys, double* v
   fl.B = query_view(c);
   fl.mats = c->d_mats;
   fl.P = 1;
-  fl.cap = table_cap(c);
+  plan_table(c, &fl.cap, &fl.npass);
   fl.grid = 1;
   fl.streams = c->streams;
   if ((rc = ensure_sums(c, 1, fl.cap))) return rc;

@@ -32,7 +32,7 @@ struct FastLaunch {
   double2* sums = nullptr;  // VARZ: grid * cap (S1, S2) scratch, L2-resident
   int npass = 1;            // hash partitions of the voxel space (table capacity)
 };
-size_t fast_smem_bytes(int kind, int cap, int bins, int threads, int f32, int ns);
+size_t fast_smem_bytes(int kind, int cap, int bins, int threads, int f32, int ns, int multi);
 cudaError_t launch_fast(const FastLaunch& fl, cudaStream_t st);
 
 // ---- exact sort-based path (k_exact.cu) -------------------------------------
