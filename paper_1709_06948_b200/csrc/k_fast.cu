@@ -579,8 +579,15 @@ __global__ void __launch_bounds__(THREADS, 1)
       auto store_state = [&](uint32_t pos, uint32_t l, uint32_t n, double K, double a1, double a2) {
         const uint32_t a = qbase + (pos & (kQueue - 1)) * kRec;
         if (KIND == 0) {
+#ifdef VMI_STS64
+          st_shared_v2(a, l, n);
+          st_shared_f64(a + 8, K);
+          st_shared_f64(a + 16, a1);
+          st_shared_f64(a + 24, a2);
+#else
           st_shared_v4(a, l, n, dlo(K), dhi(K));
           st_shared_v4(a + 16, dlo(a1), dhi(a1), dlo(a2), dhi(a2));
+#endif
         } else {
           st_shared_v2(a, l, n);
         }
@@ -590,12 +597,24 @@ __global__ void __launch_bounds__(THREADS, 1)
         const bool e = lin != cur[0];
         pend = e && cur[0] != kNoVoxel;
         pl = cur[0]; pn = (uint32_t)cn[0]; pK = cK[0]; p1 = cs1[0]; p2 = cs2[0];
+#ifdef VMI_BRANCHLESS_STEP
+        // reset folds into the update: on a new run cK = Z makes d = 0 and the
+        // 0/1 factor clears the sums (DP pipe has headroom; no branches/moves)
+        cur[0] = lin;  // equal to the old value when the run continues
+        cK[0] = e ? Z : cK[0];
+        cn[0] = e ? 1 : cn[0] + 1;
+        const double keep = e ? 0.0 : 1.0;
+        const double d = Z - cK[0];
+        cs1[0] = fma(cs1[0], keep, d);
+        cs2[0] = fma(d, d, cs2[0] * keep);
+#else
         if (e) {
           cur[0] = lin; cn[0] = 1; cK[0] = Z; cs1[0] = 0.0; cs2[0] = 0.0;
         } else {
           const double d = Z - cK[0];
           ++cn[0]; cs1[0] += d; cs2[0] = fma(d, d, cs2[0]);
         }
+#endif
       };
       auto group_body = [&](int r) {
         cp_async_wait<S - kPG>();  // groups r .. r+kPG-1 have landed
