@@ -61,9 +61,12 @@ constexpr int kUnroll = VMI_UNROLL;  // main point loop unroll (A/B tunable)
 // push with an S-record cp.async ring (two push groups in flight).  Multi-pass
 // (large grids): shared memory goes to the table instead (more capacity =
 // fewer passes), so one point per push and a 4-record ring.
+#ifndef VMI_STAGES64
+#define VMI_STAGES64 2  // double records: a small ring leaves room for the table (A/B: C1)
+#endif
 template <bool F32, bool MULTI = false>
 __host__ __device__ constexpr int kStages() {
-  return MULTI ? 4 : (F32 ? VMI_STAGES : VMI_STAGES / 2);
+  return MULTI ? 4 : (F32 ? VMI_STAGES : VMI_STAGES64);
 }
 template <typename Rec>
 __device__ __forceinline__ void cp_async_rec(uint32_t dst, const Rec* src) {
@@ -191,9 +194,12 @@ constexpr bool kPairPush = false;
 #ifndef VMI_PG
 #define VMI_PG 4
 #endif
+#ifndef VMI_PG64
+#define VMI_PG64 1
+#endif
 template <bool F32, bool MULTI>
 __host__ __device__ constexpr int kPGt() {  // points per queue push
-  return (MULTI || !kPairPush) ? 1 : (F32 ? VMI_PG : VMI_PG / 2);
+  return (MULTI || !kPairPush) ? 1 : (F32 ? VMI_PG : VMI_PG64);
 }
 template <bool F32, bool MULTI>
 __host__ __device__ constexpr int kQueueT() {  // warp queue entries: >= 32*(kPG+1), pow2
