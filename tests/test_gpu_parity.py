@@ -384,3 +384,37 @@ def test_align_matches_reference_run(tag):
     np.testing.assert_array_equal(rep.estimated, g[f"{tag}_matrix"])
     assert rep.final_mi == float(g[f"{tag}_final_mi"])
     assert rep.n_batches < rep.n_evaluations  # candidates were batched
+
+
+def test_varz_bin_edge_is_rechecked_exactly():
+    """A voxel whose z-variance sits exactly on a bin edge (two points 0.5 m
+    apart: var = 0.0625 = 2.0/32) must be flagged by the fast path and scored
+    by the exact path; the histogram then equals the oracle's bit for bit."""
+    import torch
+    rng = np.random.default_rng(8)
+    a = rng.uniform(-6, 6, size=(3000, 3))
+    edge = np.array([[10.25, 10.25, 0.125], [10.75, 10.25, 0.625]])  # alone in a 1 m voxel, dz = 0.5
+    a = np.concatenate([a, edge])
+    b = a.copy()
+    eng = engine(1.0, kind="varz")
+    eng.set_reference(a)
+    eng.set_query(b)
+    poses = np.zeros((3, 6))
+    poses[1, 0] = 0.0  # identity twice plus a shift that keeps the pair together
+    poses[2, 0] = 2.0
+    mats = torch.from_numpy(vmi.poses_to_mats(poses)).cuda()
+    mi = torch.empty(3, dtype=torch.float64, device="cuda")
+    st = torch.empty(3, dtype=torch.int32, device="cuda")
+    eng.ctx.eval_device(mats.data_ptr(), 3, mi.data_ptr(), st.data_ptr())
+    torch.cuda.synchronize()
+    flags = st.cpu().numpy()
+    assert (flags & 0x100).any(), flags  # the edge voxel was flagged
+    n_fixed = eng.ctx.eval_fixups(mats.data_ptr(), 3, mi.data_ptr(), st.data_ptr())
+    assert n_fixed == int(((flags & 0x100) != 0).sum())
+    got_mi, got_st, hist, _ = eng.evaluate(poses, histograms=True)
+    fa = oracle.feature_map(a, (0, 0, 0), 1.0, "varz")
+    for k in range(3):
+        omi, ost, oc, _ = oracle.mi_objective_full(fa, b, vmi.poses_to_mats(poses[k])[0])
+        assert ost == got_st[k]
+        np.testing.assert_array_equal(hist[k], oc)
+        assert got_mi[k] == pytest.approx(omi, rel=MI_RTOL, abs=MI_ATOL)
