@@ -137,8 +137,8 @@ int vmi_argmax_device(vmi_ctx* ctx, const double* mi_dev, int64_t P, double* bes
 /* Number of kernel launches issued by this context so far (bench accounting). */
 int64_t vmi_launch_count(const vmi_ctx* ctx);
 
-/* Fast-path configuration knobs (tests/bench): table capacity (0 = max that
-   fits shared memory) and CUDA threads per CTA (0 = default = 512, one scan-B span per
+/* Fast-path configuration knobs (tests/bench): table capacity (0 = sized from
+   scan B's occupancy; larger than fits shared memory = clamped) and CUDA threads per CTA (0 = default = 512, one scan-B span per
    thread). */
 int vmi_set_tuning(vmi_ctx* ctx, int table_cap, int threads);
 

@@ -230,17 +230,14 @@ __global__ void k_scatter_by_bin(const int4* avox_tmp, int V, int* cursor, int4*
 
 cudaError_t build_reference(const unsigned long long* keys, const double* values, int V,
                             const GridParams& g, const int amin[3], const uint32_t ext[3],
-                            uint8_t* grid, int4* avox, uint32_t* bin_total, int* cursor,
-                            cudaStream_t st, int64_t* launches) {
+                            uint8_t* grid, int4* tmp, int4* avox, uint32_t* bin_total,
+                            int* cursor, cudaStream_t st, int64_t* launches) {
   if (V <= 0) return cudaSuccess;
-  int4* tmp = nullptr;
-  VMI_TRY(cudaMallocAsync(&tmp, (size_t)V * sizeof(int4), st));
   const int T = 256, blocks = (V + T - 1) / T;
   k_build_grid<<<blocks, T, 0, st>>>(keys, values, V, g, make_int3(amin[0], amin[1], amin[2]),
                                      make_uint3(ext[0], ext[1], ext[2]), grid, tmp, bin_total);
   k_bin_offsets<<<1, 32, 0, st>>>(bin_total, g.bins + 1, cursor);
   k_scatter_by_bin<<<blocks, T, 0, st>>>(tmp, V, cursor, avox);
-  VMI_TRY(cudaFreeAsync(tmp, st));
   if (launches) *launches += 3;
   return cudaGetLastError();
 }

@@ -924,7 +924,20 @@ template <int THREADS, int NS, int KIND, bool F32, int MODE, bool MULTI>
 static cudaError_t launch_fast_t(const FastLaunch& fl, cudaStream_t st) {
   auto k = k_pose_fast<THREADS, NS, KIND, F32, MODE, MULTI>;
   size_t smem = fast_smem_bytes(KIND, fl.cap, fl.g.bins, THREADS, F32 ? 1 : 0, NS, MULTI ? 1 : 0);
-  cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  // The opt-in is set to the device maximum, never to this launch's size:
+  // contexts on other host threads launch the same instantiation with other
+  // table sizes, and a smaller per-launch value could land between another
+  // thread's attribute call and its launch.
+  static const int optin = [k] {
+    int dev = 0, v = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&v, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev);
+    cudaFuncAttributes fa{};
+    if (cudaFuncGetAttributes(&fa, k) == cudaSuccess) v -= (int)fa.sharedSizeBytes;
+    return v;
+  }();
+  if ((int)smem > optin) return cudaErrorInvalidValue;
+  cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, optin);
   if (e != cudaSuccess) return e;
   k<<<fl.grid, THREADS, smem, st>>>(fl.g, fl.A, fl.B, fl.mats, fl.P, fl.cap, fl.mi, fl.status,
                                     fl.hist, fl.total, fl.dump, fl.sums, fl.npass);

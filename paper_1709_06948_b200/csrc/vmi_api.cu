@@ -38,6 +38,7 @@ struct vmi_ctx {
   uint8_t* d_grid = nullptr;
   size_t grid_bytes = 0;
   int4* d_avox = nullptr;
+  int4* d_avox_tmp = nullptr;  // unsorted voxel list of build_reference
   int n_avox = 0;
   uint32_t* d_bin_total = nullptr;
   int* d_cursor = nullptr;
@@ -74,7 +75,7 @@ struct vmi_ctx {
   double2* d_sums = nullptr;  // fast-path VARZ sums scratch (grid * cap)
   size_t sums_n = 0;
   // grow-only capacities (bytes) of buffers reused across scan pairs
-  size_t cap_grid = 0, cap_avox = 0, cap_akeys = 0, cap_avalues = 0, cap_pts = 0, cap_upload = 0;
+  size_t cap_grid = 0, cap_avox = 0, cap_avox_tmp = 0, cap_akeys = 0, cap_avalues = 0, cap_pts = 0, cap_upload = 0;
   void* d_upload = nullptr;  // staging for host uploads
   int64_t a_npts = 0;        // scan A's point count (0 when set from features)
 };
@@ -103,11 +104,11 @@ void free_a(vmi_ctx* c) {
 }
 
 void release_a(vmi_ctx* c) {
-  cudaFree(c->d_grid); cudaFree(c->d_avox); cudaFree(c->d_bin_total); cudaFree(c->d_cursor);
+  cudaFree(c->d_grid); cudaFree(c->d_avox); cudaFree(c->d_avox_tmp); cudaFree(c->d_bin_total); cudaFree(c->d_cursor);
   cudaFree(c->d_akeys); cudaFree(c->d_avalues); cudaFree(c->d_upload);
-  c->d_grid = nullptr; c->d_avox = nullptr; c->d_bin_total = nullptr; c->d_cursor = nullptr;
+  c->d_grid = nullptr; c->d_avox = nullptr; c->d_avox_tmp = nullptr; c->d_bin_total = nullptr; c->d_cursor = nullptr;
   c->d_akeys = nullptr; c->d_avalues = nullptr; c->d_upload = nullptr;
-  c->cap_grid = c->cap_avox = c->cap_akeys = c->cap_avalues = c->cap_upload = 0;
+  c->cap_grid = c->cap_avox = c->cap_avox_tmp = c->cap_akeys = c->cap_avalues = c->cap_upload = 0;
   free_a(c);
 }
 
@@ -164,9 +165,12 @@ void plan_table(const vmi_ctx* c, int* cap_out, int* npass_out) {
   }();
   const double est = (double)(c->b_voxels > 0 ? c->b_voxels : 4096);
   if (c->cap_override > 0) {
-    *cap_out = c->cap_override;
-    *npass_out = c->npass_override > 0 ? c->npass_override
-                                       : std::max(1, (int)std::ceil(est / (0.70 * c->cap_override)));
+    // a requested table larger than shared memory holds is clamped to the largest that fits
+    const int np = c->npass_override > 0
+                       ? c->npass_override
+                       : std::max(1, (int)std::ceil(est / (0.70 * c->cap_override)));
+    *cap_out = (int)std::min((size_t)c->cap_override, max_table_cap(c, np > 1));
+    *npass_out = np;
     return;
   }
   const size_t cap1 = max_table_cap(c, false);
@@ -224,8 +228,9 @@ int finish_reference(vmi_ctx* c, const int64_t bounds[6], int64_t V) {
   CK(c, grow(&c->d_grid, c->cap_grid, c->grid_bytes));
   CK(c, cudaMemsetAsync(c->d_grid, 0, c->grid_bytes, c->stream));
   CK(c, grow(&c->d_avox, c->cap_avox, sizeof(int4) * (V > 0 ? V : 1)));
+  CK(c, grow(&c->d_avox_tmp, c->cap_avox_tmp, sizeof(int4) * (V > 0 ? V : 1)));
   CK(c, build_reference(c->d_akeys, c->d_avalues, (int)V, c->g, c->amin, c->ext, c->d_grid,
-                        c->d_avox, c->d_bin_total, c->d_cursor, c->stream, &c->launches));
+                        c->d_avox_tmp, c->d_avox, c->d_bin_total, c->d_cursor, c->stream, &c->launches));
   std::vector<uint32_t> tot(kMaxW);
   CK(c, cudaMemcpyAsync(tot.data(), c->d_bin_total, 4 * kMaxW, cudaMemcpyDeviceToHost, c->stream));
   CK(c, cudaStreamSynchronize(c->stream));

@@ -73,11 +73,12 @@ cudaError_t exact_voxelize(ExactScratch& s, const PointSource& src, const double
                            const GridParams& g, cudaStream_t st, int64_t* launches);
 
 // Build A's dense bin grid and sorted voxel list from V feature-map entries
-// (keys + values on device).  grid must be zeroed, ext-sized.
+// (keys + values on device).  grid must be zeroed, ext-sized; tmp and avox
+// hold V entries each.
 cudaError_t build_reference(const unsigned long long* keys, const double* values, int V,
                             const GridParams& g, const int amin[3], const uint32_t ext[3],
-                            uint8_t* grid, int4* avox, uint32_t* bin_total, int* cursor,
-                            cudaStream_t st, int64_t* launches);
+                            uint8_t* grid, int4* tmp, int4* avox, uint32_t* bin_total,
+                            int* cursor, cudaStream_t st, int64_t* launches);
 
 // Histogram + finalisation + MI for pose p from an exact voxelization held in
 // s (after exact_voxelize).  Writes mi[p], status[p], hist[p], total[p].

@@ -418,3 +418,33 @@ def test_varz_bin_edge_is_rechecked_exactly():
         assert ost == got_st[k]
         np.testing.assert_array_equal(hist[k], oc)
         assert got_mi[k] == pytest.approx(omi, rel=MI_RTOL, abs=MI_ATOL)
+
+
+def test_concurrent_engines_with_different_tables(hdl):
+    """Engines on several host threads launch the same kernel instantiation
+    with different shared-memory table sizes (the C5 bench pattern); every
+    launch must succeed and every result must equal the single-thread one."""
+    from concurrent.futures import ThreadPoolExecutor
+    from paper_1709_06948_b200.synth import candidate_batch
+    a, b = hdl
+    poses = candidate_batch(EulerPose(1.5, 0.3, 0, 0, 0, 0.05), 512, seed=5)
+    caps = [2048, 4096, 1 << 20, 0]  # 1 << 20: clamped to what fits
+    engines = []
+    for cap in caps:
+        e = engine(1.0, kind="varz", table_cap=cap)
+        e.set_reference(a[:, :3].astype(np.float64))
+        e.set_query(b)
+        engines.append(e)
+    want, _ = engines[-1].evaluate(poses)
+
+    def work(i):
+        out = []
+        for _ in range(6):
+            mi, _ = engines[i].evaluate(poses)
+            out.append(mi)
+        return out
+
+    with ThreadPoolExecutor(len(engines)) as pool:
+        for res in pool.map(work, range(len(engines))):
+            for mi in res:
+                np.testing.assert_array_equal(mi, want)
