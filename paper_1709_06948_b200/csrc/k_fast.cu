@@ -49,7 +49,7 @@ __device__ __forceinline__ uint32_t slot_of(uint32_t lin, uint32_t cap) {
 #endif
 #ifndef VMI_STAGES
 #ifndef VMI_TMA
-#define VMI_STAGES 8  // cp.async ring: 8 records in flight per thread (>= 2 push groups)
+#define VMI_STAGES 6  // cp.async ring: 6 records in flight per thread (2 push groups)
 #else
 #define VMI_STAGES 8  // TMA: two groups of four records in flight per warp
 #endif
@@ -185,14 +185,14 @@ __device__ __forceinline__ void flush_count(uint32_t* key, uint32_t* cnt, uint32
 
 // Warp-private flush queue: run records pushed by any lane, drained 32 at a
 // time by the whole warp so the hash/atomic path always runs converged.
-constexpr int kQueueMax = 128;  // >= 32 * (kPG + 1)
+constexpr int kQueueMax = 128;  // >= 32 * kPG (a group's pushes; the pending partial round is flushed first when needed)
 #ifndef VMI_SINGLE_PUSH
 constexpr bool kPairPush = true;   // one queue push per group of kPG points
 #else
 constexpr bool kPairPush = false;
 #endif
 #ifndef VMI_PG
-#define VMI_PG 4
+#define VMI_PG 3  // A/B (C2): 3 > 4 (which needs a queue-overrun guard) > 2
 #endif
 #ifndef VMI_PG64
 #define VMI_PG64 1
@@ -202,7 +202,7 @@ __host__ __device__ constexpr int kPGt() {  // points per queue push
   return (MULTI || !kPairPush) ? 1 : (F32 ? VMI_PG : VMI_PG64);
 }
 template <bool F32, bool MULTI>
-__host__ __device__ constexpr int kQueueT() {  // warp queue entries: >= 32*(kPG+1), pow2
+__host__ __device__ constexpr int kQueueT() {  // warp queue entries: >= 32*max(kPG, 2), pow2
   return kPGt<F32, MULTI>() == 1 ? 64 : 128;
 }
 #ifndef VMI_GROUP_UNROLL
@@ -281,6 +281,11 @@ __device__ __forceinline__ int pin_reg(int v) {
 __device__ __forceinline__ uint32_t pin_reg(uint32_t v) {
   uint32_t r;
   asm volatile("mov.b32 %0, %1;" : "=r"(r) : "r"(v));
+  return r;
+}
+__device__ __forceinline__ double pin_reg(double v) {
+  double r;
+  asm volatile("mov.b64 %0, %1;" : "=d"(r) : "d"(v));
   return r;
 }
 __device__ __forceinline__ uint32_t dlo(double d) { return (uint32_t)__double2loint(d); }
@@ -498,21 +503,28 @@ __global__ void __launch_bounds__(THREADS, 1)
       const int am0 = A.amin[0], am1 = A.amin[1], am2 = A.amin[2];
       const uint32_t ex0 = A.ext[0], ex1 = A.ext[1], ex2 = A.ext[2];
 #endif
+      // floor(q) - amin straight from DADD.RM against 1.5*2^52 - amin (an
+      // integer in [2^52, 2^53), so the sum rounds down to kc + floor(q) and
+      // its low word is floor(q) - amin); bounds are tracked relative to amin
+      // (opaque copies: otherwise they are recomputed from amin on every step)
+      const double kc0 = pin_reg(6755399441055744.0 - (double)am0);
+      const double kc1 = pin_reg(6755399441055744.0 - (double)am1);
+      const double kc2 = pin_reg(6755399441055744.0 - (double)am2);
       auto locate = [&](double x, double y, double z, bool valid, uint32_t& lin, double& Z) {
         const double X = xform_row(x, y, z, m0, m1, m2, t0);
         const double Y = xform_row(x, y, z, m3, m4, m5, t1);
         Z = xform_row(x, y, z, m6, m7, m8, t2);
-        const int ix = floor_i32(grid_q<MODE>(X, g.origin[0], g.res, g.inv_res));
-        const int iy = floor_i32(grid_q<MODE>(Y, g.origin[1], g.res, g.inv_res));
-        const int iz = floor_i32(grid_q<MODE>(Z, g.origin[2], g.res, g.inv_res));
+        const int ix = __double2loint(__dadd_rd(grid_q<MODE>(X, g.origin[0], g.res, g.inv_res), kc0));
+        const int iy = __double2loint(__dadd_rd(grid_q<MODE>(Y, g.origin[1], g.res, g.inv_res), kc1));
+        const int iz = __double2loint(__dadd_rd(grid_q<MODE>(Z, g.origin[2], g.res, g.inv_res), kc2));
         lin = kNoVoxel;
         if (valid) {
           bmin0 = min(bmin0, ix); bmax0 = max(bmax0, ix);
           bmin1 = min(bmin1, iy); bmax1 = max(bmax1, iy);
           bmin2 = min(bmin2, iz); bmax2 = max(bmax2, iz);
-          const uint32_t rx = (uint32_t)(ix - am0);
-          const uint32_t ry = (uint32_t)(iy - am1);
-          const uint32_t rz = (uint32_t)(iz - am2);
+          const uint32_t rx = (uint32_t)ix;
+          const uint32_t ry = (uint32_t)iy;
+          const uint32_t rz = (uint32_t)iz;
           const bool inside = (rx < ex0) & (ry < ex1) & (rz < ex2);
           lin = inside ? (rx * ex1 + ry) * ex2 + rz : kNoVoxel;
         if (npass > 1 && lin != kNoVoxel && __umulhi(lin * 0x85EBCA6Bu, (uint32_t)npass) != (uint32_t)pass)
@@ -562,8 +574,10 @@ __global__ void __launch_bounds__(THREADS, 1)
         }
         cp_async_commit();
       };
+#if defined(VMI_SINGLE_PUSH)
   #pragma unroll
       for (int r = 0; r < S - 1; ++r) issue(r);
+#endif
       // body for record r held in ring slot `slot` (a compile-time constant in
       // the unrolled main loop, so every shared address is base + immediate)
       auto body = [&](int r, int slot) {
@@ -622,8 +636,24 @@ __global__ void __launch_bounds__(THREADS, 1)
         }
 #endif
       };
+      // Group staging: rows are issued kPG at a time as one commit group from a
+      // running pointer.  The span layout is padded with kStagePadRows rows, so
+      // rows past the span are issued unconditionally (and never read back).
+      static_assert(S % kPG == 0, "ring holds whole groups");
+      static_assert(S <= kStagePadRows, "span layout padding covers the ring");
+      constexpr int kGroups = S / kPG;  // commit groups in flight
+      constexpr size_t kRowBytes = (size_t)VTH * sizeof(Rec);
+      const char* src = reinterpret_cast<const char*>(pts);
+      auto issue_group = [&](int slot0) {
+#pragma unroll
+        for (int u = 0; u < kPG; ++u)
+          cp_async_rec<Rec>(my_stage + (uint32_t)(slot0 + u) * kStageStride,
+                            reinterpret_cast<const Rec*>(src + u * kRowBytes));
+        src += kPG * kRowBytes;
+        cp_async_commit();
+      };
       auto group_body = [&](int r) {
-        cp_async_wait<S - kPG>();  // groups r .. r+kPG-1 have landed
+        cp_async_wait<kGroups - 1>();  // rows r .. r+kPG-1 have landed
         uint32_t l[kPG];
         double Z[kPG];
 #pragma unroll
@@ -631,8 +661,7 @@ __global__ void __launch_bounds__(THREADS, 1)
           const Rec v = lds_rec<Rec>(my_stage + (uint32_t)((r + u) % S) * kStageStride);
           locate((double)v.x, (double)v.y, (double)v.z, true, l[u], Z[u]);
         }
-#pragma unroll
-        for (int u = 0; u < kPG; ++u) issue(r + S + u);  // refill the slots just consumed
+        issue_group(r % S);  // refill the slots just consumed with rows r+S ..
         bool pd[kPG];
         uint32_t pl[kPG], pn[kPG];
         double pK[kPG], p1[kPG], p2[kPG];
@@ -643,6 +672,19 @@ __global__ void __launch_bounds__(THREADS, 1)
 #pragma unroll
         for (int u = 0; u < kPG; ++u) { m[u] = __ballot_sync(0xffffffffu, pd[u]); any |= m[u]; }
         if (any != 0u) {
+          // A group can push up to 32*kPG records on top of < 32 unflushed ones:
+          // when that would overrun the ring, flush the partial round first.
+          uint32_t n = 0;
+#pragma unroll
+          for (int u = 0; u < kPG; ++u) n += __popc(m[u]);
+#ifndef VMI_NO_QUEUE_GUARD  // A/B timing experiment only (unsafe for dense pushes)
+          if (32 * kPG + 31 > kQueue && qt - qh + n > (uint32_t)kQueue) {
+            __syncwarp();
+            if ((uint32_t)lane < qt - qh) flush_rec(qh + lane);
+            qh = qt;
+            __syncwarp();
+          }
+#endif
           uint32_t base = qt;
 #pragma unroll
           for (int u = 0; u < kPG; ++u) {
@@ -659,7 +701,8 @@ __global__ void __launch_bounds__(THREADS, 1)
         }
       };
       static_assert(S >= kPG, "ring must hold a full group");
-      issue(S - 1);  // group mode keeps S records in flight (invariant: 0..r+S-1 issued)
+#pragma unroll
+      for (int gi = 0; gi < kGroups; ++gi) issue_group(gi * kPG);  // rows 0 .. S-1 in flight
       int rr = 0;
 #pragma unroll kGroupUnroll
       for (; rr + kPG <= full; rr += kPG) group_body(rr);
@@ -741,9 +784,11 @@ __global__ void __launch_bounds__(THREADS, 1)
         bmax0 = __reduce_max_sync(0xffffffffu, bmax0);
         bmax1 = __reduce_max_sync(0xffffffffu, bmax1);
         bmax2 = __reduce_max_sync(0xffffffffu, bmax2);
-        if (lane == 0) {
-          atomicMin(&misc[0], bmin0); atomicMin(&misc[1], bmin1); atomicMin(&misc[2], bmin2);
-          atomicMax(&misc[3], bmax0); atomicMax(&misc[4], bmax1); atomicMax(&misc[5], bmax2);
+        if (lane == 0 && bmin0 != INT_MAX) {  // relative to amin (locate); a warp may have no points
+          atomicMin(&misc[0], bmin0 + am0); atomicMin(&misc[1], bmin1 + am1);
+          atomicMin(&misc[2], bmin2 + am2);
+          atomicMax(&misc[3], bmax0 + am0); atomicMax(&misc[4], bmax1 + am1);
+          atomicMax(&misc[5], bmax2 + am2);
         }
         __syncthreads();
         // voxel.py:200-206: any index outside [-2^20, 2^20-1] -> OutOfBoundsError

@@ -54,6 +54,7 @@ struct vmi_ctx {
   int span = 0;
   int rem = 0;
   double max_abs = 0.0;
+  double b_lo[3] = {0, 0, 0}, b_hi[3] = {0, 0, 0};  // scan B's AABB
   int64_t b_voxels = 0;  // scan B's occupied voxels at the identity pose (table sizing)
   int threads = kFastThreads;  // span-layout threads
   int streams = 1;             // spans per CUDA thread in the fast kernel
@@ -143,6 +144,7 @@ QueryView query_view(const vmi_ctx* c) {
   B.rem = c->rem;
   B.threads = c->threads;
   B.max_abs = c->max_abs;
+  for (int j = 0; j < 3; ++j) { B.lo[j] = c->b_lo[j]; B.hi[j] = c->b_hi[j]; }
   return B;
 }
 
@@ -545,12 +547,19 @@ static int set_query(vmi_ctx* c, const void* host, int is_f32_src, int64_t n) {
     }
   }
   double mx = 0.0;
+  double lo[3] = {INFINITY, INFINITY, INFINITY}, hi[3] = {-INFINITY, -INFINITY, -INFINITY};
   for (int64_t i = 0; i < n; ++i)
     for (int j = 0; j < 3; ++j) {
       const double v = is_f32_src ? (double)static_cast<const float*>(host)[4 * i + j]
                                   : static_cast<const double*>(host)[3 * i + j];
-      mx = std::fmax(mx, std::fabs(v));
+      lo[j] = std::fmin(lo[j], v);
+      hi[j] = std::fmax(hi[j], v);
     }
+  for (int j = 0; j < 3; ++j) {
+    mx = std::fmax(mx, std::fmax(std::fabs(lo[j]), std::fabs(hi[j])));
+    c->b_lo[j] = lo[j];
+    c->b_hi[j] = hi[j];
+  }
   c->max_abs = mx;
   CK(c, grow(&c->d_upload, c->cap_upload, up_bytes));
   void* tmp = c->d_upload;
@@ -558,7 +567,7 @@ static int set_query(vmi_ctx* c, const void* host, int is_f32_src, int64_t n) {
   c->span = (int)((n + c->threads - 1) / c->threads);
   c->rem = (int)(n - (int64_t)(c->span - 1) * c->threads);
   const size_t rec = as_f32 ? 16 : 32;
-  CK(c, grow(&c->d_pts, c->cap_pts, (size_t)c->span * c->threads * rec));
+  CK(c, grow(&c->d_pts, c->cap_pts, (size_t)(c->span + kStagePadRows) * c->threads * rec));
   CK(c, launch_span_layout(tmp, as_f32, n, c->span, c->rem, c->threads, c->d_pts, c->stream));
   c->launches += 1;
   CK(c, cudaStreamSynchronize(c->stream));

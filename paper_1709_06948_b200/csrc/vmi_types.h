@@ -50,6 +50,10 @@ struct RefView {
 #endif
 constexpr int kFastThreads = VMI_FAST_THREADS;  // spans per CTA (span layout "threads")
 
+// Extra rows allocated after the span layout: the fast kernel's staging ring
+// streams up to this many rows past the span without bounds checks.
+constexpr int kStagePadRows = 16;
+
 struct QueryView {
   const void* pts;  // float4 (x, y, z, i) or double4 (x, y, z, pad)
   int is_f32;
@@ -58,6 +62,8 @@ struct QueryView {
   int rem;
   int threads;
   double max_abs;  // max |coordinate| of scan B (pose safety bound)
+  double lo[3];    // scan B's AABB in its own frame (per-pose key box, k_fast.cu)
+  double hi[3];
 };
 
 __host__ __device__ inline int span_of_thread(int t, int threads) {

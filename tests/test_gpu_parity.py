@@ -448,3 +448,30 @@ def test_concurrent_engines_with_different_tables(hdl):
         for res in pool.map(work, range(len(engines))):
             for mi in res:
                 np.testing.assert_array_equal(mi, want)
+
+
+@pytest.mark.parametrize("kind", ["varz", "count"])
+def test_sparse_scan_run_queue_pressure(kind):
+    """Scan B where almost every point opens a new voxel run: warps push up
+    to one record per lane per point, so the run queue runs at capacity.  Histograms must still
+    match the reference exactly."""
+    rng = np.random.default_rng(17)
+    base = rng.uniform(-20.0, 20.0, size=(3000, 3)).astype(np.float32)
+    # 60k points drawn from 3k locations: nearly every point opens a new run,
+    # yet the occupied voxels fit one shared-memory table
+    pts_b = base[rng.integers(0, base.shape[0], size=60000)].astype(np.float64)
+    pts_a = rng.uniform(-20.0, 20.0, size=(6000, 3)).astype(np.float32).astype(np.float64)
+    eng = engine(0.5, kind=kind, passes=1)
+    eng.set_reference(pts_a)
+    eng.set_query(pts_b)
+    poses = np.array([[0.0, 0.0, 0.0, 0.0, 0.0, 0.0], [0.3, -0.2, 0.1, 0.01, 0.02, 0.3],
+                      [1.0, 1.0, 0.0, 0.0, 0.0, -0.5], [-2.0, 0.5, 0.25, 0.0, 0.0, 1.0]])
+    mi, st, hist, total = eng.evaluate(poses, histograms=True)
+    fa = oracle.feature_map(pts_a, (0, 0, 0), 0.5, kind)
+    mats = vmi.poses_to_mats(poses)
+    for i in range(len(poses)):
+        omi, ost, ohist, ototal = oracle.mi_objective_full(fa, pts_b, mats[i], res=0.5)
+        assert st[i] == ost
+        np.testing.assert_array_equal(hist[i], ohist)
+        assert total[i] == ototal
+        assert_mi_close([mi[i]], [omi])
