@@ -260,6 +260,25 @@ __device__ __forceinline__ void st_shared_v2(uint32_t a, uint32_t x, uint32_t y)
 __device__ __forceinline__ void st_shared_f64(uint32_t a, double x) {
   asm volatile("st.shared.f64 [%0], %1;" ::"r"(a), "d"(x) : "memory");
 }
+// predicated queue-record stores (no divergent branch around them)
+__device__ __forceinline__ void st_rec32_if(bool p, uint32_t a, uint32_t l, uint32_t n, double K,
+                                            double s1, double s2) {
+  asm volatile(
+      "{\n .reg .pred q;\n setp.ne.b32 q, %0, 0;\n"
+      " @q st.shared.v4.u32 [%1], {%2, %3, %4, %5};\n"
+      " @q st.shared.v4.u32 [%1+16], {%6, %7, %8, %9};\n}" ::"r"((int)p),
+      "r"(a), "r"(l), "r"(n), "r"(__double2loint(K)), "r"(__double2hiint(K)),
+      "r"(__double2loint(s1)), "r"(__double2hiint(s1)), "r"(__double2loint(s2)),
+      "r"(__double2hiint(s2))
+      : "memory");
+}
+__device__ __forceinline__ void st_rec8_if(bool p, uint32_t a, uint32_t l, uint32_t n) {
+  asm volatile(
+      "{\n .reg .pred q;\n setp.ne.b32 q, %0, 0;\n @q st.shared.v2.u32 [%1], {%2, %3};\n}" ::"r"(
+          (int)p),
+      "r"(a), "r"(l), "r"(n)
+      : "memory");
+}
 __device__ __forceinline__ uint4 ld_shared_v4(uint32_t a) {
   uint4 v;
   asm volatile("ld.shared.v4.u32 {%0, %1, %2, %3}, [%4];"
@@ -662,6 +681,36 @@ __global__ void __launch_bounds__(THREADS, 1)
           locate((double)v.x, (double)v.y, (double)v.z, true, l[u], Z[u]);
         }
         issue_group(r % S);  // refill the slots just consumed with rows r+S ..
+#ifndef VMI_BATCH_PUSH  // (batched ballots + branchy stores: A/B measured 0.8% slower)
+        // per point: ballot, predicated store of the finished run straight from
+        // the run registers, then the run update (no pending copies, no branches).
+        // A group adds <= 32*kPG records to < 32 unflushed ones.
+        static_assert(32 * kPG + 31 <= kQueue, "a push group must fit the run queue");
+#pragma unroll
+        for (int u = 0; u < kPG; ++u) {
+          const bool e = l[u] != cur[0];
+          const bool pdu = e && cur[0] != kNoVoxel;
+          const unsigned mu = __ballot_sync(0xffffffffu, pdu);
+          const uint32_t a = qbase + ((qt + __popc(mu & lt_mask)) & (kQueue - 1)) * kRec;
+          if (KIND == 0)
+            st_rec32_if(pdu, a, cur[0], (uint32_t)cn[0], cK[0], cs1[0], cs2[0]);
+          else
+            st_rec8_if(pdu, a, cur[0], (uint32_t)cn[0]);
+          qt += __popc(mu);
+          if (e) {
+            cur[0] = l[u]; cn[0] = 1; cK[0] = Z[u]; cs1[0] = 0.0; cs2[0] = 0.0;
+          } else {
+            const double d = Z[u] - cK[0];
+            ++cn[0]; cs1[0] += d; cs2[0] = fma(d, d, cs2[0]);
+          }
+        }
+        while (qt - qh >= 32) {
+          __syncwarp();
+          flush_rec(qh + lane);
+          qh += 32;
+          __syncwarp();
+        }
+#else
         bool pd[kPG];
         uint32_t pl[kPG], pn[kPG];
         double pK[kPG], p1[kPG], p2[kPG];
@@ -699,6 +748,7 @@ __global__ void __launch_bounds__(THREADS, 1)
             __syncwarp();
           }
         }
+#endif
       };
       static_assert(S >= kPG, "ring must hold a full group");
 #pragma unroll
