@@ -263,6 +263,18 @@ __device__ __forceinline__ void st_shared_f64(uint32_t a, double x) {
 // predicated queue-record stores (no divergent branch around them)
 __device__ __forceinline__ void st_rec32_if(bool p, uint32_t a, uint32_t l, uint32_t n, double K,
                                             double s1, double s2) {
+#ifndef VMI_SEQ_STS128  // 64-bit stores straight from the run registers: no moves into
+                         // aligned quads (A/B: -1.5 % vs two st.shared.v4)
+  asm volatile(
+      "{\n .reg .pred q;\n setp.ne.b32 q, %0, 0;\n"
+      " @q st.shared.v2.u32 [%1], {%2, %3};\n"
+      " @q st.shared.f64 [%1+8], %4;\n"
+      " @q st.shared.f64 [%1+16], %5;\n"
+      " @q st.shared.f64 [%1+24], %6;\n}" ::"r"((int)p),
+      "r"(a), "r"(l), "r"(n), "d"(K), "d"(s1), "d"(s2)
+      : "memory");
+  return;
+#endif
   asm volatile(
       "{\n .reg .pred q;\n setp.ne.b32 q, %0, 0;\n"
       " @q st.shared.v4.u32 [%1], {%2, %3, %4, %5};\n"
