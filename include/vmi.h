@@ -134,6 +134,14 @@ int vmi_fast_features(vmi_ctx* ctx, const double mat[12], int64_t* keys, double*
 int vmi_argmax_device(vmi_ctx* ctx, const double* mi_dev, int64_t P, double* best_mi,
                       int64_t* best_idx, void* stream);
 
+/* Device-side top-K over mi: the min(K, P) largest values in descending
+   order with their candidate indices; equal values keep ascending index order,
+   so entry 0 is np.argmax's first maximum (cli.py:202).  The per-rank
+   exchange unit of a sharded search (top-K (mi, idx) per GPU,
+   then one all-gather).  Writes K doubles and K indices to host. */
+int vmi_topk_device(vmi_ctx* ctx, const double* mi_dev, int64_t P, int64_t K, double* top_mi,
+                    int64_t* top_idx, void* stream);
+
 /* Number of kernel launches issued by this context so far (bench accounting). */
 int64_t vmi_launch_count(const vmi_ctx* ctx);
 

@@ -6,8 +6,8 @@ kernels behind a C ABI (include/vmi.h, libvmi.so).  See DESIGN.md.
 """
 
 from .api import (SWEEP_AXES, SearchResult, clear_cache, compute_feature_map, engine_for,
-                  grid_search, joint_histogram_at, mi_at, mi_objective, mi_objective_batch,
-                  sweep_axis)
+                  grid_search, grid_search_sharded, joint_histogram_at, mi_at, mi_objective,
+                  mi_objective_batch, sweep_axis)
 from .align import AlignmentReport, align
 from .engine import MIEngine, entropy_exact, mutual_information_exact
 from .optim import OptimResult, SimplexConfig, nelder_mead_maximize_batched
@@ -23,7 +23,8 @@ __all__ = [
     "AlignmentReport", "align", "OptimResult", "SimplexConfig", "nelder_mead_maximize_batched",
     "normalized", "transform_to_euler", "validate_transform",
     "SWEEP_AXES", "SearchResult", "clear_cache", "compute_feature_map", "engine_for",
-    "grid_search", "joint_histogram_at", "mi_at", "mi_objective", "mi_objective_batch",
+    "grid_search", "grid_search_sharded", "joint_histogram_at", "mi_at", "mi_objective",
+    "mi_objective_batch",
     "sweep_axis", "MIEngine", "entropy_exact", "mutual_information_exact", "EmptyOverlapError",
     "NoOverlapError", "OutOfBoundsError", "VoxmiError", "EulerPose", "PointCloud",
     "as_pose_array", "euler_to_transform", "DEFAULT_BIN_COUNT", "DEFAULT_UPPER_CLAMP",

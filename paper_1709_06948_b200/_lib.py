@@ -28,7 +28,7 @@ EXPORTS = (
     "vmi_set_query_points", "vmi_set_query_records_f32", "vmi_poses_to_mats", "vmi_eval",
     "vmi_eval_device", "vmi_eval_fixups", "vmi_eval_exact", "vmi_query_features",
     "vmi_fast_features",
-    "vmi_argmax_device", "vmi_launch_count", "vmi_set_tuning", "vmi_set_passes",
+    "vmi_argmax_device", "vmi_topk_device", "vmi_launch_count", "vmi_set_tuning", "vmi_set_passes",
 )
 
 
@@ -76,6 +76,7 @@ def load(path: str = LIB_PATH):
     L.vmi_query_features.argtypes = [_ctx, _d, _i64, _d, ctypes.c_int64, _i64, _i64, _i32]
     L.vmi_fast_features.argtypes = [_ctx, _d, _i64, _d, ctypes.c_int64, _i64, _i32]
     L.vmi_argmax_device.argtypes = [_ctx, _vp, ctypes.c_int64, _d, _i64, _vp]
+    L.vmi_topk_device.argtypes = [_ctx, _vp, ctypes.c_int64, ctypes.c_int64, _d, _i64, _vp]
     L.vmi_launch_count.argtypes = [_ctx]
     L.vmi_launch_count.restype = ctypes.c_int64
     L.vmi_set_tuning.argtypes = [_ctx, ctypes.c_int, ctypes.c_int]
@@ -224,6 +225,16 @@ class Context:
         self.check(self._L.vmi_argmax_device(self._h, mi_ptr, P, ctypes.byref(v), ctypes.byref(i),
                                              stream or None), "vmi_argmax_device")
         return float(v.value), int(i.value)
+
+    def topk_device(self, mi_ptr: int, P: int, k: int, stream: int = 0):
+        """The min(k, P) largest MI values on the device (descending, ties in
+        ascending index order) -> (mi[k], idx[k]) on the host."""
+        n = max(0, min(int(k), int(P)))
+        vals = np.empty(max(n, 1), dtype=np.float64)
+        idx = np.empty(max(n, 1), dtype=np.int64)
+        self.check(self._L.vmi_topk_device(self._h, mi_ptr, P, k, ptr(vals, _d), ptr(idx, _i64),
+                                           stream or None), "vmi_topk_device")
+        return vals[:n], idx[:n]
 
     def fast_features(self, mat12: np.ndarray, cap: int):
         """B's features at one pose from the fast path (inside A's AABB), sorted by key."""

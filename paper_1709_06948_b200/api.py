@@ -195,3 +195,49 @@ def grid_search(scan_a, scan_b, poses=None, cfg: AlignmentConfig | None = None, 
     return SearchResult(best_pose=EulerPose.from_vector(poses[idx]), best_mi=best, best_index=idx,
                         mi=mi, status=st, n_poses=poses.shape[0])
 
+
+def grid_search_sharded(scan_a, scan_b, poses=None, cfg: AlignmentConfig | None = None,
+                        center=None, axes: dict | None = None, device: int | None = None,
+                        group=None) -> SearchResult:
+    """``grid_search`` across the ranks of a torch.distributed group
+    (SURVEY.md 8(e)): every rank holds the same candidate list and both scans,
+    scores its contiguous shard on its own GPU, re-scores its shard winner
+    exactly from the bit-exact histogram, and one all-gather of (mi, global
+    index) per rank picks np.argmax's first maximum.  ``mi``/``status`` of the
+    result are this rank's shard; ``best_*`` are global and identical on every
+    rank (and to ``grid_search`` on one GPU).
+    """
+    import torch
+    import torch.distributed as dist
+
+    from .shard import all_gather_winner, shard_bounds
+    cfg = cfg or AlignmentConfig()
+    if poses is None:
+        if axes is None:
+            raise ValueError("give poses or axes")
+        c = center.as_vector() if hasattr(center, "as_vector") else (
+            np.zeros(6) if center is None else np.asarray(center, dtype=np.float64))
+        poses = grid_poses(c, axes)
+    poses = as_pose_array(poses)
+    world, rank = dist.get_world_size(group), dist.get_rank(group)
+    if device is None:
+        device = torch.cuda.current_device()
+    lo, hi = shard_bounds(poses.shape[0], world, rank)
+    mi = np.empty(0)
+    st = np.empty(0, dtype=np.int32)
+    value, index = float("-inf"), np.iinfo(np.int64).max
+    if hi > lo:
+        eng = _prepare(scan_a, scan_b, cfg, device=device)
+        try:
+            mi, st = eng.evaluate(poses[lo:hi])
+            k, value = eng.best(poses[lo:hi], mi, exact_value=True)
+            index = lo + k
+        finally:
+            eng.close()
+    xdev = torch.device("cuda", device) if dist.get_backend(group) == "nccl" else torch.device("cpu")
+    best, idx = all_gather_winner(value, index, dist, xdev)
+    if best <= NO_OVERLAP_SENTINEL:
+        raise NoOverlapError("no candidate pose produced overlapping occupied bounds")
+    return SearchResult(best_pose=EulerPose.from_vector(poses[idx]), best_mi=best, best_index=idx,
+                        mi=mi, status=st, n_poses=poses.shape[0])
+

@@ -360,6 +360,24 @@ cudaError_t launch_argmax(const double* v, int64_t P, double* out_val, long long
   return cudaGetLastError();
 }
 
+// ---- top-K: stable descending radix sort of (mi, index) -----------------------
+__global__ void k_iota(int* a, int n) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < n) a[i] = i;
+}
+
+cudaError_t topk_sort(const double* mi, int P, double* keys_out, int* idx_in, int* idx_out,
+                      void* tmp, size_t* tmp_bytes, cudaStream_t st) {
+  if (!tmp)  // size query
+    return cub::DeviceRadixSort::SortPairsDescending(nullptr, *tmp_bytes, mi, keys_out, idx_in,
+                                                     idx_out, P, 0, 64, st);
+  k_iota<<<(P + 255) / 256, 256, 0, st>>>(idx_in, P);
+  // CUB's radix sort is stable: equal MI keep ascending candidate order, so
+  // the first entry is np.argmax's first maximum
+  return cub::DeviceRadixSort::SortPairsDescending(tmp, *tmp_bytes, mi, keys_out, idx_in, idx_out,
+                                                   P, 0, 64, st);
+}
+
 // ---- span layout (see QueryView) ------------------------------------------------
 __global__ void k_span_layout(const void* src, int is_f32, int64_t n, int span, int rem,
                               int threads, void* dst) {

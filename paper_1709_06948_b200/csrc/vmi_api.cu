@@ -73,6 +73,12 @@ struct vmi_ctx {
   bool hist_alloc = false;
   double* d_best = nullptr;
   long long* d_best_idx = nullptr;
+  // top-K scratch (grow-only)
+  double* d_tk_keys = nullptr;
+  int* d_tk_idx = nullptr;
+  int* d_tk_out = nullptr;
+  void* d_tk_tmp = nullptr;
+  size_t cap_tk_keys = 0, cap_tk_idx = 0, cap_tk_out = 0, cap_tk_tmp = 0;
   double2* d_sums = nullptr;  // fast-path VARZ sums scratch (grid * cap)
   size_t sums_n = 0;
   // grow-only capacities (bytes) of buffers reused across scan pairs
@@ -370,6 +376,7 @@ int vmi_destroy(vmi_ctx* c) {
   exact_free(c->ex);
   cudaFree(c->d_mats); cudaFree(c->d_mi); cudaFree(c->d_status); cudaFree(c->d_hist);
   cudaFree(c->d_total); cudaFree(c->d_best); cudaFree(c->d_best_idx); cudaFree(c->d_sums);
+  cudaFree(c->d_tk_keys); cudaFree(c->d_tk_idx); cudaFree(c->d_tk_out); cudaFree(c->d_tk_tmp);
   cudaStreamDestroy(c->stream);
   delete c;
   return 0;
@@ -759,6 +766,30 @@ int vmi_argmax_device(vmi_ctx* c, const double* mi_dev, int64_t P, double* best_
   CK(c, cudaMemcpyAsync(best_mi, c->d_best, 8, cudaMemcpyDeviceToHost, st));
   CK(c, cudaMemcpyAsync(best_idx, c->d_best_idx, 8, cudaMemcpyDeviceToHost, st));
   CK(c, cudaStreamSynchronize(st));
+  return 0;
+}
+
+int vmi_topk_device(vmi_ctx* c, const double* mi_dev, int64_t P, int64_t K, double* top_mi,
+                    int64_t* top_idx, void* stream) {
+  if (!c || !mi_dev || P <= 0 || K <= 0 || !top_mi || !top_idx) return VMI_ERR_ARG;
+  if (P > 0x7fffffff) return fail(c, VMI_ERR_UNSUPPORTED, "top-K over more than 2^31-1 values");
+  cudaSetDevice(c->device);
+  cudaStream_t st = stream ? (cudaStream_t)stream : c->stream;
+  const int n = (int)P;
+  size_t bytes = 0;
+  CK(c, topk_sort(mi_dev, n, nullptr, nullptr, nullptr, nullptr, &bytes, st));
+  CK(c, grow(&c->d_tk_keys, c->cap_tk_keys, 8 * (size_t)n));
+  CK(c, grow(&c->d_tk_idx, c->cap_tk_idx, 4 * (size_t)n));
+  CK(c, grow(&c->d_tk_out, c->cap_tk_out, 4 * (size_t)n));
+  CK(c, grow(&c->d_tk_tmp, c->cap_tk_tmp, bytes));
+  CK(c, topk_sort(mi_dev, n, c->d_tk_keys, c->d_tk_idx, c->d_tk_out, c->d_tk_tmp, &bytes, st));
+  c->launches += 2;
+  const int64_t k = K < P ? K : P;
+  std::vector<int> idx((size_t)k);
+  CK(c, cudaMemcpyAsync(top_mi, c->d_tk_keys, 8 * (size_t)k, cudaMemcpyDeviceToHost, st));
+  CK(c, cudaMemcpyAsync(idx.data(), c->d_tk_out, 4 * (size_t)k, cudaMemcpyDeviceToHost, st));
+  CK(c, cudaStreamSynchronize(st));
+  for (int64_t i = 0; i < k; ++i) top_idx[i] = idx[(size_t)i];
   return 0;
 }
 

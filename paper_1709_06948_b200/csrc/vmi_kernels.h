@@ -90,6 +90,11 @@ cudaError_t exact_score(ExactScratch& s, const GridParams& g, const RefView& A, 
 cudaError_t launch_argmax(const double* v, int64_t P, double* out_val, long long* out_idx,
                           cudaStream_t st);
 
+// Stable descending sort of P MI values with their indices (tmp == nullptr:
+// *tmp_bytes receives the scratch size).  Two launches (iota + CUB sort).
+cudaError_t topk_sort(const double* mi, int P, double* keys_out, int* idx_in, int* idx_out,
+                      void* tmp, size_t* tmp_bytes, cudaStream_t st);
+
 // Reorder contiguous points into the fast path's span layout.
 cudaError_t launch_span_layout(const void* src, int is_f32, int64_t n, int span, int rem,
                                int threads, void* dst, cudaStream_t st);

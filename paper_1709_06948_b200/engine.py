@@ -143,14 +143,41 @@ class MIEngine:
         mi, st, hist, total = self.ctx.eval(mats, want_hist=histograms, bins=self.bins, exact=exact)
         return (mi, st, hist, total) if histograms else (mi, st)
 
-    def best(self, poses, mi: np.ndarray | None = None, rel_tie: float = 1e-12):
+    def evaluate_device(self, poses):
+        """Score P poses leaving the results on the GPU: (mi, status) torch
+        tensors on this engine's device (flagged poses already re-run on the
+        exact path).  For device-side consumers (top-K, argmax)."""
+        import torch
+        mats_h = self.mats(poses)
+        P = mats_h.shape[0]
+        dev = torch.device("cuda", self.ctx.device)
+        mats = torch.from_numpy(mats_h).to(dev)
+        mi = torch.empty(P, dtype=torch.float64, device=dev)
+        st = torch.empty(P, dtype=torch.int32, device=dev)
+        s = torch.cuda.current_stream(dev).cuda_stream
+        self.ctx.eval_device(mats.data_ptr(), P, mi.data_ptr(), st.data_ptr(), stream=s)
+        self.ctx.eval_fixups(mats.data_ptr(), P, mi.data_ptr(), st.data_ptr(), stream=s)
+        return mi, st
+
+    def topk(self, poses, k: int):
+        """The k best candidates by GPU MI: (mi[k] descending, index[k]);
+        equal MI keep candidate order, so entry 0 is np.argmax's pick
+        (before the near-tie re-score that ``best`` applies)."""
+        mi, _ = self.evaluate_device(poses)
+        s = __import__("torch").cuda.current_stream(mi.device).cuda_stream
+        return self.ctx.topk_device(mi.data_ptr(), mi.numel(), k, stream=s)
+
+    def best(self, poses, mi: np.ndarray | None = None, rel_tie: float = 1e-12,
+             exact_value: bool = False):
         """np.argmax over the candidates' MI with the reference's tie semantics.
 
         GPU MI agrees with the reference to ~1e-15; the order of two poses can
         only differ when their MI values are that close.  Every candidate
         within ``rel_tie`` of the maximum is re-scored on the host from its
         bit-exact GPU histogram with the reference's own formula, and the
-        first maximum in candidate order wins.  Returns (index, mi).
+        first maximum in candidate order wins.  Returns (index, mi); with
+        ``exact_value`` the winner's MI is always the host re-score (what a
+        sharded search compares across ranks).
         """
         poses = as_pose_array(poses)
         if mi is None:
@@ -159,7 +186,7 @@ class MIEngine:
         if top <= NO_OVERLAP_SENTINEL:
             return int(np.argmax(mi)), top
         tied = np.nonzero(mi >= top - abs(top) * rel_tie)[0]
-        if tied.size == 1:
+        if tied.size == 1 and not exact_value:
             return int(tied[0]), float(mi[tied[0]])
         _, _, hist, _ = self.evaluate(poses[tied], histograms=True)
         exact = np.array([mutual_information_exact(h, self.include_phi)[0] for h in hist])
