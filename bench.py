@@ -56,7 +56,7 @@ def parse():
     ap.add_argument("--c5-mode", default="grid", choices=["grid", "nm"],
                     help="c5: 4,096-pose grid search per pair, or align() (batched "
                          "Nelder-Mead, reference-identical decisions) from the prior")
-    ap.add_argument("--c5-workers", type=int, default=3,
+    ap.add_argument("--c5-workers", type=int, default=6,
                     help="c5: host threads, each with its own engine/stream, so one pair's "
                          "A-grid build and uploads overlap another pair's pose scoring")
     return ap.parse_args()
