@@ -134,9 +134,26 @@ __device__ __forceinline__ double4 lds_rec<double4>(uint32_t a) {
 // sums (S1, S2) in a per-CTA, L2-resident global array updated with native
 // fire-and-forget f64 reductions (RED.ADD.F64) -- a shared-memory f64
 // atomicAdd is a CAS loop on sm_100 and was ~30% of the kernel's stalls.
+// VARZ slot counts live in shared memory (12-byte slots) for single-pass
+// poses, but in the L2 scratch next to the sums (8-byte slots: ~50 % more
+// capacity, hence fewer passes) for the multi-pass large-grid mode.  A/B:
+// C2 33.4 vs 35.3 ms (global counts slower), C4 314k vs 383k pose-evals/s.
+template <bool MULTI>
+__host__ __device__ constexpr bool kGlobalCounts() {
+#ifdef VMI_GCNT
+  return true;
+#else
+  return MULTI;
+#endif
+}
+__host__ __device__ inline int slot_bytes(int kind, int multi) {
+  if (kind != 0) return 4 + 4;
+  return (multi ? kGlobalCounts<true>() : kGlobalCounts<false>()) ? 8 : 8 + 4;
+}
+
 struct VarzTable {
   unsigned long long* key;  // (lin << 32) | float32 bits of the slot pivot
-  uint32_t* cnt;
+  uint32_t* cnt;            // shared memory, or (VMI_GCNT) the per-CTA global scratch
   double2* sums;            // global: this CTA's [cap] (S1, S2)
 };
 
@@ -226,7 +243,7 @@ __host__ __device__ inline FastSmem fast_layout(int kind, int cap, int W, int th
   L.bars = off;  // two mbarriers per warp (TMA bulk staging)
   off += (size_t)(threads / 32) * 16;
   L.table = off;
-  off += (size_t)cap * (kind == 0 ? (8 + 4) : (4 + 4));
+  off += (size_t)cap * slot_bytes(kind, multi);
   off = (off + 15) & ~size_t(15);
   L.queue = off;
   const int queue = ns != 1 ? kQueueMax
@@ -248,6 +265,8 @@ __host__ __device__ inline FastSmem fast_layout(int kind, int cap, int W, int th
 size_t fast_smem_bytes(int kind, int cap, int bins, int threads, int f32, int ns, int multi) {
   return fast_layout(kind, cap, bins + 1, threads, f32, ns, multi).total;
 }
+
+int fast_slot_bytes(int kind, int multi) { return slot_bytes(kind, multi); }
 
 __device__ __forceinline__ void st_shared_v4(uint32_t a, uint32_t x, uint32_t y, uint32_t z,
                                              uint32_t w) {
@@ -360,7 +379,10 @@ __global__ void __launch_bounds__(THREADS, 1)
   const uint32_t qbase = (uint32_t)__cvta_generic_to_shared(smem + L.queue) + wid * kQueue * kRec;
   if (KIND == 0) {
     VT.key = reinterpret_cast<unsigned long long*>(smem + L.table);
-    VT.cnt = reinterpret_cast<uint32_t*>(smem + L.table + (size_t)cap * 8);
+    if (kGlobalCounts<MULTI>())  // counts next to the sums in L2 (native RED.ADD.U32)
+      VT.cnt = reinterpret_cast<uint32_t*>(gsums + (size_t)gridDim.x * cap) + (size_t)blockIdx.x * cap;
+    else
+      VT.cnt = reinterpret_cast<uint32_t*>(smem + L.table + (size_t)cap * 8);
     VT.sums = gsums + (size_t)blockIdx.x * cap;
   } else {
     ckey = reinterpret_cast<uint32_t*>(smem + L.table);
@@ -412,6 +434,8 @@ __global__ void __launch_bounds__(THREADS, 1)
     for (int i = tid; i < all_words; i += THREADS) t4[i] = i < key_words ? ones : zero;
     if (KIND == 0)
       for (int i = tid; i < cap; i += THREADS) VT.sums[i] = make_double2(0.0, 0.0);
+    if (KIND == 0 && kGlobalCounts<MULTI>())
+      for (int i = tid; i < cap; i += THREADS) VT.cnt[i] = 0u;
   };
   clear_table();
   // COUNT features are small integers: their bins (mi.py:72-79) come from a LUT
@@ -897,7 +921,7 @@ __global__ void __launch_bounds__(THREADS, 1)
         int bb;
         double dump_feat = 0.0;
         if (KIND == 0) {
-          const double nd = (double)VT.cnt[s];
+          const double nd = (double)(kGlobalCounts<MULTI>() ? __ldcg(&VT.cnt[s]) : VT.cnt[s]);
           const double S1 = sum.x, S2 = sum.y;
           VT.key[s] = kEmpty64; VT.cnt[s] = 0u;
           VT.sums[s] = make_double2(0.0, 0.0);

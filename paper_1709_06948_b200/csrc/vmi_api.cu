@@ -158,7 +158,7 @@ QueryView query_view(const vmi_ctx* c) {
 size_t max_table_cap(const vmi_ctx* c, bool multi) {
   const size_t fixed = fast_smem_bytes(c->g.kind, 0, c->g.bins, c->threads / c->streams,
                                        c->is_f32, c->streams, multi ? 1 : 0);
-  const size_t per = c->g.kind == 0 ? 12 : 8;
+  const size_t per = (size_t)fast_slot_bytes(c->g.kind, multi ? 1 : 0);
   return ((c->smem_optin - fixed) / per) & ~size_t(31);
 }
 
@@ -202,7 +202,7 @@ int ensure_sums(vmi_ctx* c, int grid, int cap) {
   if (need <= c->sums_n) return 0;
   cudaFree(c->d_sums);
   c->d_sums = nullptr;
-  CK(c, cudaMalloc(&c->d_sums, need * sizeof(double2)));
+  CK(c, cudaMalloc(&c->d_sums, need * (sizeof(double2) + 4)));  // sums, then (multi-pass) u32 counts
   c->sums_n = need;
   return 0;
 }

@@ -33,6 +33,7 @@ struct FastLaunch {
   int npass = 1;            // hash partitions of the voxel space (table capacity)
 };
 size_t fast_smem_bytes(int kind, int cap, int bins, int threads, int f32, int ns, int multi);
+int fast_slot_bytes(int kind, int multi);  // shared-memory bytes per table slot
 cudaError_t launch_fast(const FastLaunch& fl, cudaStream_t st);
 
 // ---- exact sort-based path (k_exact.cu) -------------------------------------
