@@ -101,7 +101,7 @@ def workload(cfg: str, world: int, per_gpu: int) -> Workload:
         poses = candidate_batch(EulerPose(*TRUTH), per_gpu * world, seed=2024)
         return Workload("c4", a, b, poses, 0.2, "varz", "weak",
                         "C4: HDL-64-shaped 120k-point scans in a 100 m scene, 0.2 m VARZ "
-                        "(large grid, table overflow -> exact path)")
+                        "(large grid: hash-partitioned multi-pass table)")
     a, b = hdl64_pair(LidarSceneSpec(), EulerPose(*TRUTH))
     if cfg == "c3":
         t = np.asarray(TRUTH)

@@ -21,13 +21,14 @@
 //   mutual_information (mi.py:163-191)      fused epilogue (finalize_mi)
 //
 // VARZ is accumulated as (n, S1 = sum(z-K), S2 = sum((z-K)^2)) around a pivot K
-// that is (the float32 rounding of) the z of the first run to reach the slot:
-// within ~1e-14 relative of the reference's two-pass value.  A VARZ value that
+// that is the z of the voxel's lower face (|z - K| < resolution): within
+// ~1e-12 relative of the reference's two-pass value.  A VARZ value that
 // falls within rounding distance of a bin edge, or a table overflow, marks the
 // pose VMI_FLAG_RECHECK and the host re-evaluates it through the exact
 // sort-based path (k_exact.cu), so histograms stay bit-exact.
 #include <cstdint>
 #include <climits>
+#include <cstdio>
 #include <type_traits>
 #include <cuda_runtime.h>
 
@@ -36,7 +37,6 @@
 
 namespace vmi {
 
-constexpr unsigned long long kEmpty64 = ~0ull;
 constexpr uint32_t kEmpty32 = 0xFFFFFFFFu;
 
 __device__ __forceinline__ uint32_t slot_of(uint32_t lin, uint32_t cap) {
@@ -44,23 +44,13 @@ __device__ __forceinline__ uint32_t slot_of(uint32_t lin, uint32_t cap) {
 }
 
 // ---- cp.async staging of scan-B records (LDGSTS, L1 bypass) ---------------
-#ifndef VMI_UNROLL
-#define VMI_UNROLL 4
-#endif
-#ifndef VMI_STAGES
-#ifndef VMI_TMA
-#define VMI_STAGES 6  // cp.async ring: 6 records in flight per thread (2 push groups)
-#else
-#define VMI_STAGES 8  // TMA: two groups of four records in flight per warp
-#endif
-#endif
-#if !defined(VMI_TMA) && defined(VMI_SINGLE_PUSH)
-constexpr int kUnroll = VMI_UNROLL;  // main point loop unroll (A/B tunable)
-#endif
 // Pipeline shape per instantiation.  Single-pass poses: kPG points per queue
 // push with an S-record cp.async ring (two push groups in flight).  Multi-pass
 // (large grids): shared memory goes to the table instead (more capacity =
 // fewer passes), so one point per push and a 4-record ring.
+#ifndef VMI_STAGES
+#define VMI_STAGES 6  // cp.async ring: 6 records in flight per thread (2 push groups)
+#endif
 #ifndef VMI_STAGES64
 #define VMI_STAGES64 2  // double records: a small ring leaves room for the table (A/B: C1)
 #endif
@@ -76,37 +66,6 @@ __device__ __forceinline__ void cp_async_rec(uint32_t dst, const Rec* src) {
                  "l"(reinterpret_cast<const char*>(src) + 16)
                  : "memory");
 }
-// ---- TMA bulk staging (cp.async.bulk + mbarrier) ------------------------------
-__device__ __forceinline__ void mbar_init(uint32_t bar, uint32_t count) {
-  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(bar), "r"(count) : "memory");
-}
-__device__ __forceinline__ void mbar_arrive_expect_tx(uint32_t bar, uint32_t bytes) {
-  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar), "r"(bytes)
-               : "memory");
-}
-__device__ __forceinline__ bool mbar_try_wait(uint32_t bar, uint32_t parity) {
-  uint32_t ok;
-  asm volatile(
-      "{\n .reg .pred p;\n mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n"
-      " selp.u32 %0, 1, 0, p;\n}"
-      : "=r"(ok)
-      : "r"(bar), "r"(parity)
-      : "memory");
-  return ok != 0;
-}
-__device__ __forceinline__ void bulk_g2s(uint32_t dst, const void* src, uint32_t bytes, uint32_t bar) {
-  asm volatile(
-      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(dst),
-      "l"(src), "r"(bytes), "r"(bar)
-      : "memory");
-}
-__device__ __forceinline__ void fence_proxy_async() {
-  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-}
-__device__ __forceinline__ void fence_mbar_init() {
-  asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-}
-
 __device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
 template <int N>
 __device__ __forceinline__ void cp_async_wait() {
@@ -130,84 +89,36 @@ __device__ __forceinline__ double4 lds_rec<double4>(uint32_t a) {
   asm volatile("ld.shared.v2.f64 {%0, %1}, [%2];" : "=d"(v.z), "=d"(v.w) : "r"(a + 16) : "memory");
   return v;
 }
-// VARZ table: keys and counts in shared memory; the per-slot pivot-shifted
-// sums (S1, S2) in a per-CTA, L2-resident global array updated with native
-// fire-and-forget f64 reductions (RED.ADD.F64) -- a shared-memory f64
-// atomicAdd is a CAS loop on sm_100 and was ~30% of the kernel's stalls.
-// VARZ slot counts live in shared memory (12-byte slots) for single-pass
-// poses, but in the L2 scratch next to the sums (8-byte slots: ~50 % more
-// capacity, hence fewer passes) for the multi-pass large-grid mode.  A/B:
-// C2 33.4 vs 35.3 ms (global counts slower), C4 314k vs 383k pose-evals/s.
+// VARZ is accumulated as (n, S1 = sum(z - K), S2 = sum((z - K)^2)) around the
+// pivot K = the z of the voxel's lower face (a deterministic function of the
+// voxel index, so every run of a voxel shares it: runs merge by plain addition
+// and the table key is the voxel alone).  Keys (32-bit voxel index) and counts
+// live in shared memory; (S1, S2) in a per-CTA, L2-resident global array
+// updated with native fire-and-forget f64 reductions (RED.ADD.F64) -- a
+// shared-memory f64 atomicAdd is a CAS loop on sm_100 and was ~30% of the
+// kernel's stalls.  The multi-pass large-grid mode also keeps the counts in the
+// L2 scratch (4-byte slots: more capacity, hence fewer passes).
 template <bool MULTI>
 __host__ __device__ constexpr bool kGlobalCounts() {
-#ifdef VMI_GCNT
-  return true;
-#else
   return MULTI;
-#endif
 }
+// (A/B: a per-run pivot -- the run's first z, re-pivoted on merge into a
+// 64-bit key+pivot slot -- was 7 % slower at C2.)
+using VKey = uint32_t;
+constexpr VKey kEmptyKey = kEmpty32;
 __host__ __device__ inline int slot_bytes(int kind, int multi) {
   if (kind != 0) return 4 + 4;
-  return (multi ? kGlobalCounts<true>() : kGlobalCounts<false>()) ? 8 : 8 + 4;
+  return (int)sizeof(VKey) + (multi ? 0 : 4);
 }
 
 struct VarzTable {
-  unsigned long long* key;  // (lin << 32) | float32 bits of the slot pivot
-  uint32_t* cnt;            // shared memory, or (VMI_GCNT) the per-CTA global scratch
-  double2* sums;            // global: this CTA's [cap] (S1, S2)
+  VKey* key;      // voxel index inside A's AABB (kEmptyKey = free)
+  uint32_t* cnt;  // shared memory, or (multi-pass) the per-CTA global scratch
+  double2* sums;  // global: this CTA's [cap] (S1, S2)
 };
-
-__device__ __forceinline__ void flush_varz(const VarzTable& T, uint32_t cap, uint32_t lin, int n,
-                                           double K, double a1, double a2, int* overflow) {
-  uint32_t s = slot_of(lin, cap);
-  const unsigned long long mine =
-      ((unsigned long long)lin << 32) | __float_as_uint(__double2float_rn(K));
-  unsigned long long w;
-  uint32_t probes = 0;
-  while (true) {
-    w = ((volatile unsigned long long*)T.key)[s];
-    if ((uint32_t)(w >> 32) == lin) break;
-    if (w == kEmpty64) {
-      unsigned long long old = atomicCAS(&T.key[s], kEmpty64, mine);
-      if (old == kEmpty64) { w = mine; break; }
-      if ((uint32_t)(old >> 32) == lin) { w = old; break; }
-    }
-    if (++s == cap) s = 0;
-    if (++probes >= cap) { *overflow = 1; return; }
-  }
-  const double kp = (double)__uint_as_float((uint32_t)w);
-  const double dl = K - kp;
-  const double nd = (double)n;
-  atomicAdd(&T.cnt[s], (uint32_t)n);
-  atomicAdd(&T.sums[s].x, a1 + nd * dl);
-  atomicAdd(&T.sums[s].y, a2 + dl * (2.0 * a1 + nd * dl));
-}
-
-__device__ __forceinline__ void flush_count(uint32_t* key, uint32_t* cnt, uint32_t cap,
-                                            uint32_t lin, int n, int* overflow) {
-  uint32_t s = slot_of(lin, cap);
-  uint32_t probes = 0;
-  while (true) {
-    uint32_t w = ((volatile uint32_t*)key)[s];
-    if (w == lin) break;
-    if (w == kEmpty32) {
-      uint32_t old = atomicCAS(&key[s], kEmpty32, lin);
-      if (old == kEmpty32 || old == lin) break;
-    }
-    if (++s == cap) s = 0;
-    if (++probes >= cap) { *overflow = 1; return; }
-  }
-  atomicAdd(&cnt[s], (uint32_t)n);
-}
 
 // Warp-private flush queue: run records pushed by any lane, drained 32 at a
 // time by the whole warp so the hash/atomic path always runs converged.
-constexpr int kQueueMax = 128;  // >= 32 * kPG (a group's pushes; the pending partial round is flushed first when needed)
-#ifndef VMI_SINGLE_PUSH
-constexpr bool kPairPush = true;   // one queue push per group of kPG points
-#else
-constexpr bool kPairPush = false;
-#endif
 #ifndef VMI_PG
 #define VMI_PG 3  // A/B (C2): 3 > 4 (which needs a queue-overrun guard) > 2
 #endif
@@ -216,22 +127,18 @@ constexpr bool kPairPush = false;
 #endif
 template <bool F32, bool MULTI>
 __host__ __device__ constexpr int kPGt() {  // points per queue push
-  return (MULTI || !kPairPush) ? 1 : (F32 ? VMI_PG : VMI_PG64);
+  return MULTI ? 1 : (F32 ? VMI_PG : VMI_PG64);
 }
 template <bool F32, bool MULTI>
-__host__ __device__ constexpr int kQueueT() {  // warp queue entries: >= 32*max(kPG, 2), pow2
+__host__ __device__ constexpr int kQueueT() {  // warp queue entries: > 32*kPG + 31, pow2
   return kPGt<F32, MULTI>() == 1 ? 64 : 128;
 }
-#ifndef VMI_GROUP_UNROLL
-#define VMI_GROUP_UNROLL 2
-#endif
-constexpr int kGroupUnroll = VMI_GROUP_UNROLL;  // entries per warp: a step pushes <= 32*NS, drained at 32
 
 // Shared-memory layout helper (bytes), mirrored by fast_smem_bytes() on the host.
 constexpr int kCountLut = 1024;  // COUNT bins precomputed for n < kCountLut
 
 struct FastSmem {
-  size_t stage, bars, table, queue, hist, marg, red, rows, cols, misc, lut, total;
+  size_t stage, table, queue, hist, marg, red, rows, cols, misc, lut, total;
 };
 __host__ __device__ inline FastSmem fast_layout(int kind, int cap, int W, int threads, int f32,
                                                 int ns, int multi) {
@@ -240,15 +147,13 @@ __host__ __device__ inline FastSmem fast_layout(int kind, int cap, int W, int th
   L.stage = off;
   const int stages = multi ? kStages<true, true>() : (f32 ? kStages<true>() : kStages<false>());
   off += (size_t)threads * ns * (f32 ? 16 : 32) * stages;
-  L.bars = off;  // two mbarriers per warp (TMA bulk staging)
-  off += (size_t)(threads / 32) * 16;
   L.table = off;
   off += (size_t)cap * slot_bytes(kind, multi);
   off = (off + 15) & ~size_t(15);
   L.queue = off;
-  const int queue = ns != 1 ? kQueueMax
-                    : (multi ? kQueueT<true, true>() : (f32 ? kQueueT<true, false>() : kQueueT<false, false>()));
-  off += (size_t)(threads / 32) * queue * (kind == 0 ? (4 + 4 + 8 + 8 + 8) : (4 + 4));
+  const int queue = multi ? kQueueT<true, true>() : (f32 ? kQueueT<true, false>() : kQueueT<false, false>());
+  // + one warp queue of slack: the kernel aligns the queues to their size
+  off += (size_t)(threads / 32 + 1) * queue * (kind == 0 ? 32 : 8);
   off = (off + 15) & ~size_t(15);
   L.hist = off; off += (size_t)W * W * 4; off = (off + 15) & ~size_t(15);
   L.marg = off; off += (size_t)W * 4; off = (off + 15) & ~size_t(15);
@@ -268,48 +173,6 @@ size_t fast_smem_bytes(int kind, int cap, int bins, int threads, int f32, int ns
 
 int fast_slot_bytes(int kind, int multi) { return slot_bytes(kind, multi); }
 
-__device__ __forceinline__ void st_shared_v4(uint32_t a, uint32_t x, uint32_t y, uint32_t z,
-                                             uint32_t w) {
-  asm volatile("st.shared.v4.u32 [%0], {%1, %2, %3, %4};" ::"r"(a), "r"(x), "r"(y), "r"(z), "r"(w)
-               : "memory");
-}
-__device__ __forceinline__ void st_shared_v2(uint32_t a, uint32_t x, uint32_t y) {
-  asm volatile("st.shared.v2.u32 [%0], {%1, %2};" ::"r"(a), "r"(x), "r"(y) : "memory");
-}
-__device__ __forceinline__ void st_shared_f64(uint32_t a, double x) {
-  asm volatile("st.shared.f64 [%0], %1;" ::"r"(a), "d"(x) : "memory");
-}
-// predicated queue-record stores (no divergent branch around them)
-__device__ __forceinline__ void st_rec32_if(bool p, uint32_t a, uint32_t l, uint32_t n, double K,
-                                            double s1, double s2) {
-#ifndef VMI_SEQ_STS128  // 64-bit stores straight from the run registers: no moves into
-                         // aligned quads (A/B: -1.5 % vs two st.shared.v4)
-  asm volatile(
-      "{\n .reg .pred q;\n setp.ne.b32 q, %0, 0;\n"
-      " @q st.shared.v2.u32 [%1], {%2, %3};\n"
-      " @q st.shared.f64 [%1+8], %4;\n"
-      " @q st.shared.f64 [%1+16], %5;\n"
-      " @q st.shared.f64 [%1+24], %6;\n}" ::"r"((int)p),
-      "r"(a), "r"(l), "r"(n), "d"(K), "d"(s1), "d"(s2)
-      : "memory");
-  return;
-#endif
-  asm volatile(
-      "{\n .reg .pred q;\n setp.ne.b32 q, %0, 0;\n"
-      " @q st.shared.v4.u32 [%1], {%2, %3, %4, %5};\n"
-      " @q st.shared.v4.u32 [%1+16], {%6, %7, %8, %9};\n}" ::"r"((int)p),
-      "r"(a), "r"(l), "r"(n), "r"(__double2loint(K)), "r"(__double2hiint(K)),
-      "r"(__double2loint(s1)), "r"(__double2hiint(s1)), "r"(__double2loint(s2)),
-      "r"(__double2hiint(s2))
-      : "memory");
-}
-__device__ __forceinline__ void st_rec8_if(bool p, uint32_t a, uint32_t l, uint32_t n) {
-  asm volatile(
-      "{\n .reg .pred q;\n setp.ne.b32 q, %0, 0;\n @q st.shared.v2.u32 [%1], {%2, %3};\n}" ::"r"(
-          (int)p),
-      "r"(a), "r"(l), "r"(n)
-      : "memory");
-}
 __device__ __forceinline__ uint4 ld_shared_v4(uint32_t a) {
   uint4 v;
   asm volatile("ld.shared.v4.u32 {%0, %1, %2, %3}, [%4];"
@@ -323,26 +186,67 @@ __device__ __forceinline__ uint2 ld_shared_v2(uint32_t a) {
   asm volatile("ld.shared.v2.u32 {%0, %1}, [%2];" : "=r"(v.x), "=r"(v.y) : "r"(a) : "memory");
   return v;
 }
-__device__ __forceinline__ int pin_reg(int v) {
-  int r;
-  asm volatile("mov.b32 %0, %1;" : "=r"(r) : "r"(v));
+// predicated run-record stores straight from the run registers (no branch, no
+// moves into aligned register quads): VARZ {lin, n, -, -, S1, S2} (32 B),
+// COUNT {lin, n} (8 B)
+__device__ __forceinline__ void st_rec32_if(bool p, uint32_t a, uint32_t l, uint32_t n, double s1,
+                                            double s2) {
+  asm volatile(
+      "{\n .reg .pred q;\n setp.ne.b32 q, %0, 0;\n"
+      " @q st.shared.v2.u32 [%1], {%2, %3};\n"
+      " @q st.shared.f64 [%1+16], %4;\n"
+      " @q st.shared.f64 [%1+24], %5;\n}" ::"r"((int)p),
+      "r"(a), "r"(l), "r"(n), "d"(s1), "d"(s2)
+      : "memory");
+}
+__device__ __forceinline__ void st_rec8_if(bool p, uint32_t a, uint32_t l, uint32_t n) {
+  asm volatile(
+      "{\n .reg .pred q;\n setp.ne.b32 q, %0, 0;\n @q st.shared.v2.u32 [%1], {%2, %3};\n}" ::"r"(
+          (int)p),
+      "r"(a), "r"(l), "r"(n)
+      : "memory");
+}
+// a new run starts: zero the run registers in place (predicated; no selects)
+__device__ __forceinline__ void run_reset_if(bool p, uint32_t& n, double& s1, double& s2) {
+  asm volatile(
+      "{\n .reg .pred q;\n setp.ne.b32 q, %3, 0;\n"
+      " @q mov.b32 %0, 0;\n @q mov.b64 %1, 0;\n @q mov.b64 %2, 0;\n}"
+      : "+r"(n), "+d"(s1), "+d"(s2)
+      : "r"((int)p));
+}
+// lin if (rx, ry, rz) lies inside A's AABB, else kNoVoxel (one predicate chain)
+__device__ __forceinline__ uint32_t inside_lin(uint32_t rx, uint32_t ry, uint32_t rz, uint32_t ex0,
+                                               uint32_t ex1, uint32_t ex2) {
+  const uint32_t lin = (rx * ex1 + ry) * ex2 + rz;
+  uint32_t r;
+  asm("{\n .reg .pred q;\n setp.lt.u32 q, %1, %4;\n setp.lt.and.u32 q, %2, %5, q;\n"
+      " setp.lt.and.u32 q, %3, %6, q;\n selp.b32 %0, %7, -1, q;\n}"
+      : "=r"(r)
+      : "r"(rx), "r"(ry), "r"(rz), "r"(ex0), "r"(ex1), "r"(ex2), "r"(lin));
   return r;
 }
-__device__ __forceinline__ uint32_t pin_reg(uint32_t v) {
-  uint32_t r;
-  asm volatile("mov.b32 %0, %1;" : "=r"(r) : "r"(v));
-  return r;
+__device__ __forceinline__ double mkd(uint32_t lo, uint32_t hi) {
+  return __hiloint2double((int)hi, (int)lo);
 }
 __device__ __forceinline__ double pin_reg(double v) {
   double r;
   asm volatile("mov.b64 %0, %1;" : "=d"(r) : "d"(v));
   return r;
 }
-__device__ __forceinline__ uint32_t dlo(double d) { return (uint32_t)__double2loint(d); }
-__device__ __forceinline__ uint32_t dhi(double d) { return (uint32_t)__double2hiint(d); }
-__device__ __forceinline__ double mkd(uint32_t lo, uint32_t hi) {
-  return __hiloint2double((int)hi, (int)lo);
-}
+
+#ifdef VMI_WATCHDOG  // debug builds: trap a runaway loop with its location
+#define VMI_WD(id, cnt, a, b)                                                              \
+  if (++cnt > (1u << 24)) {                                                                \
+    printf("vmi watchdog %d block %d tid %d: %u %u\n", id, blockIdx.x, threadIdx.x,         \
+           (unsigned)(a), (unsigned)(b));                                                  \
+    __trap();                                                                              \
+  }
+#define VMI_TR(msg, a)                                                                    \
+  if (threadIdx.x % 32 == 0 && blockIdx.x == 0) printf("tr %s warp %d: %d\n", msg, threadIdx.x / 32, (int)(a));
+#else
+#define VMI_WD(id, cnt, a, b)
+#define VMI_TR(msg, a)
+#endif
 
 template <int THREADS, int NS, int KIND, bool F32, int MODE, bool MULTI>
 __global__ void __launch_bounds__(THREADS, 1)
@@ -350,6 +254,7 @@ __global__ void __launch_bounds__(THREADS, 1)
                 int cap, double* __restrict__ mi_out, int32_t* __restrict__ status_out,
                 long long* __restrict__ hist_out, long long* __restrict__ total_out,
                 FeatureDump dump, double2* __restrict__ gsums, int npass) {
+  static_assert(NS == 1, "one span per thread");
   extern __shared__ __align__(16) unsigned char smem[];
   const int W = g.bins + 1;
   const FastSmem L = fast_layout(KIND, cap, W, THREADS, F32 ? 1 : 0, NS, MULTI ? 1 : 0);
@@ -373,62 +278,31 @@ __global__ void __launch_bounds__(THREADS, 1)
   VarzTable VT;
   uint32_t* ckey = nullptr;
   uint32_t* ccnt = nullptr;
-  // warp queue: AoS records, VARZ 32 B {lin, n, K, S1, S2}, COUNT 8 B {lin, n}
+  // warp queue: AoS records, VARZ 32 B {lin, n, -, -, S1, S2}, COUNT 8 B {lin, n}
   constexpr uint32_t kRec = KIND == 0 ? 32u : 8u;
-  constexpr int kQueue = NS == 1 ? kQueueT<F32, MULTI>() : kQueueMax;
-  const uint32_t qbase = (uint32_t)__cvta_generic_to_shared(smem + L.queue) + wid * kQueue * kRec;
+  constexpr int kQueue = kQueueT<F32, MULTI>();
+  // Each warp's queue is aligned to its size QB, so a record address is
+  // qbase | (byte offset mod QB): one LOP3 per push.
+  constexpr uint32_t QB = (uint32_t)kQueue * kRec;
+  const uint32_t qbase =
+      (((uint32_t)__cvta_generic_to_shared(smem + L.queue) + QB - 1) & ~(QB - 1)) + wid * QB;
   if (KIND == 0) {
-    VT.key = reinterpret_cast<unsigned long long*>(smem + L.table);
+    VT.key = reinterpret_cast<VKey*>(smem + L.table);
     if (kGlobalCounts<MULTI>())  // counts next to the sums in L2 (native RED.ADD.U32)
       VT.cnt = reinterpret_cast<uint32_t*>(gsums + (size_t)gridDim.x * cap) + (size_t)blockIdx.x * cap;
     else
-      VT.cnt = reinterpret_cast<uint32_t*>(smem + L.table + (size_t)cap * 8);
+      VT.cnt = reinterpret_cast<uint32_t*>(smem + L.table + (size_t)cap * sizeof(VKey));
     VT.sums = gsums + (size_t)blockIdx.x * cap;
   } else {
     ckey = reinterpret_cast<uint32_t*>(smem + L.table);
     ccnt = reinterpret_cast<uint32_t*>(smem + L.table + (size_t)cap * 4);
   }
 
-#ifdef VMI_TMA
-  static_assert(NS == 1, "TMA staging assumes one span per thread");
-  using RecT = typename std::conditional<F32, float4, double4>::type;
-  constexpr int G = F32 ? 4 : 2;                              // iterations per group
-  constexpr uint32_t kChunk = 32u * (uint32_t)sizeof(RecT);  // one warp, one iteration
-  const uint32_t wstage = stage_base + (uint32_t)wid * 2u * G * kChunk;
-  const uint32_t wbar = (uint32_t)__cvta_generic_to_shared(smem + L.bars) + (uint32_t)wid * 16u;
-  const char* wsrc = reinterpret_cast<const char*>(B.pts) + (size_t)wid * kChunk;
-  const int full_it = B.span - 1;
-  const int ng = (full_it + G - 1) / G;  // groups per pass over the span
-  uint32_t gp = 0, gq = 0;               // groups produced / consumed (warp-uniform)
-  auto produce = [&]() {
-    if (ng == 0) return;
-    const int r0 = (int)(gp % (uint32_t)ng) * G;
-    const int cnt = min(G, full_it - r0);
-    const uint32_t slot = gp & 1u;
-    if (lane == 0) {
-      fence_proxy_async();  // prior generic reads of this buffer before the async write
-      mbar_arrive_expect_tx(wbar + slot * 8u, (uint32_t)cnt * kChunk);
-      for (int u = 0; u < cnt; ++u)
-        bulk_g2s(wstage + (slot * G + u) * kChunk,
-                 wsrc + (size_t)(r0 + u) * (size_t)THREADS * sizeof(RecT), kChunk, wbar + slot * 8u);
-    }
-    ++gp;
-  };
-  if (lane == 0) {
-    mbar_init(wbar, 1);
-    mbar_init(wbar + 8, 1);
-    fence_mbar_init();
-  }
-  __syncwarp();
-  produce();
-  produce();
-#endif
-
   // The table is cleared once here; afterwards the per-pose table walk resets
   // every slot it reads, so each pose starts from an empty table.
   auto clear_table = [&]() {
     uint4* t4 = reinterpret_cast<uint4*>(smem + L.table);
-    const int key_words = KIND == 0 ? cap / 2 : cap / 4;  // uint4s holding keys
+    const int key_words = KIND == 0 ? cap * (int)sizeof(VKey) / 16 : cap / 4;  // uint4s holding keys
     const int all_words = (int)((L.queue - L.table) / 16);
     const uint4 ones = make_uint4(~0u, ~0u, ~0u, ~0u), zero = make_uint4(0u, 0u, 0u, 0u);
     for (int i = tid; i < all_words; i += THREADS) t4[i] = i < key_words ? ones : zero;
@@ -487,77 +361,92 @@ __global__ void __launch_bounds__(THREADS, 1)
     // the voxels of hash partition k, so every voxel is complete in one pass.
     if (!MULTI) npass = 1;  // single-pass instantiation: the pass loop folds away
     for (int pass = 0; pass < npass; ++pass) {
-      // ---- pass over this thread's span(s) of scan B ------------------------
-      // Each thread walks NS spans ("virtual threads" tid + k*THREADS of the
-      // span layout) in lock step: NS independent dependency chains per thread.
-      constexpr int VTH = THREADS * NS;  // virtual threads = spans per CTA
+      // ---- pass over this thread's span of scan B ---------------------------
       int bmin0 = INT_MAX, bmin1 = INT_MAX, bmin2 = INT_MAX;
       int bmax0 = INT_MIN, bmax1 = INT_MIN, bmax2 = INT_MIN;
-      uint32_t cur[NS];
-      int cn[NS];
-      double cK[NS], cs1[NS], cs2[NS];
-  #pragma unroll
-      for (int k = 0; k < NS; ++k) { cur[k] = kNoVoxel; cn[k] = 0; cK[k] = cs1[k] = cs2[k] = 0.0; }
-      uint32_t qh = 0, qt = 0;  // warp-uniform queue head / tail
+      // the open run: voxel, point count, S1, S2 (pivot: the voxel's lower z face)
+      uint32_t cur = kNoVoxel, cn = 0u;
+      double cs1 = 0.0, cs2 = 0.0;
+      uint32_t qh = 0, qt = 0;  // warp-uniform queue head / tail, in bytes
 
-      auto flush_rec = [&](uint32_t idx) {  // one queued record -> table
-        const uint32_t a = qbase + (idx & (kQueue - 1)) * kRec;
-        if (KIND == 0) {
-          const uint4 r0 = ld_shared_v4(a), r1 = ld_shared_v4(a + 16);
-          flush_varz(VT, ucap, r0.x, (int)r0.y, mkd(r0.z, r0.w), mkd(r1.x, r1.y), mkd(r1.z, r1.w),
-                     &misc[7]);
-        } else {
-          const uint2 r0 = ld_shared_v2(a);
-          flush_count(ckey, ccnt, ucap, r0.x, (int)r0.y, &misc[7]);
+      // one queued record per lane -> table.  The first probe (a hit, or the
+      // insert into an empty home slot: most records) is one straight-line CAS,
+      // so those lanes issue the count/sum atomics together once; only
+      // collisions take the divergent probe loop.  (A probe loop that lanes
+      // leave one by one re-issued the atomics ~3.4 times per drain.)
+      auto flush_rec = [&](uint32_t idx, bool has) {
+        const uint32_t a = qbase | (idx & (QB - 1));
+        const uint2 r0 = has ? ld_shared_v2(a) : make_uint2(kNoVoxel, 0u);
+        uint32_t* keys = KIND == 0 ? reinterpret_cast<uint32_t*>(VT.key) : ckey;
+        uint32_t sl = slot_of(r0.x, ucap);
+        // first probe = one CAS (hit or insert), no branch before the atomics
+        const uint32_t old0 = has ? atomicCAS(&keys[sl], kEmpty32, r0.x) : 0u;
+        const bool done = has && (old0 == kEmpty32 || old0 == r0.x);
+        auto add = [&](uint32_t slot) {
+          if (KIND == 0) {
+            const uint4 r1 = ld_shared_v4(a + 16);
+            atomicAdd(&VT.cnt[slot], r0.y);
+            atomicAdd(&VT.sums[slot].x, mkd(r1.x, r1.y));
+            atomicAdd(&VT.sums[slot].y, mkd(r1.z, r1.w));
+          } else {
+            atomicAdd(&ccnt[slot], r0.y);
+          }
+        };
+        if (done) {
+          add(sl);
+        } else if (has) {  // collision: linear probing from the next slot
+          uint32_t probes = 1;
+          while (true) {
+            if (++sl == ucap) sl = 0;
+            if (probes++ >= ucap) { misc[7] = 1; break; }  // table full -> exact path
+            const uint32_t w = ((volatile uint32_t*)keys)[sl];
+            if (w == r0.x) { add(sl); break; }
+            if (w == kEmpty32) {
+              const uint32_t old = atomicCAS(&keys[sl], kEmpty32, r0.x);
+              if (old == kEmpty32 || old == r0.x) { add(sl); break; }
+            }
+          }
         }
       };
-      auto store_rec = [&](uint32_t pos, int k) {
-        const uint32_t a = qbase + (pos & (kQueue - 1)) * kRec;
-        if (KIND == 0) {
-#ifndef VMI_SCALAR_STORES
-          st_shared_v4(a, cur[k], (uint32_t)cn[k], dlo(cK[k]), dhi(cK[k]));
-          st_shared_v4(a + 16, dlo(cs1[k]), dhi(cs1[k]), dlo(cs2[k]), dhi(cs2[k]));
-#else  // scalar stores: no register shuffling into vector quads
-          st_shared_v2(a, cur[k], (uint32_t)cn[k]);
-          st_shared_f64(a + 8, cK[k]);
-          st_shared_f64(a + 16, cs1[k]);
-          st_shared_f64(a + 24, cs2[k]);
-#endif
-        } else {
-          st_shared_v2(a, cur[k], (uint32_t)cn[k]);
-        }
-      };
-      // whole warp: enqueue the finished runs, drain 32 at a time (converged)
-      auto push = [&](const bool* do_push) {
-        unsigned m[NS];
-        unsigned any = 0u;
-  #pragma unroll
-        for (int k = 0; k < NS; ++k) { m[k] = __ballot_sync(0xffffffffu, do_push[k]); any |= m[k]; }
-        if (any == 0u) return;
-        uint32_t base = qt;
-  #pragma unroll
-        for (int k = 0; k < NS; ++k) {
-          if (do_push[k]) store_rec(base + __popc(m[k] & lt_mask), k);
-          base += __popc(m[k]);
-        }
-        qt = base;
-        while (qt - qh >= 32) {
+      auto drain_full = [&]() {  // whole warp, converged: 32 records at a time
+        uint32_t wd = 0; (void)wd;
+        while (qt - qh >= 32 * kRec) {
+          VMI_WD(1, wd, qt, qh)
           __syncwarp();
-          flush_rec(qh + lane);
-          qh += 32;
+          flush_rec(qh + lane * kRec, true);
+          qh += 32 * kRec;
           __syncwarp();
         }
       };
-      // transform, voxel index, bounds, voxel inside A's AABB (pure per point)
-#ifdef VMI_PIN_CONSTS
-      // opaque copies: kept in registers instead of re-loaded from the
-      // constant bank on every point
-      const int am0 = pin_reg(A.amin[0]), am1 = pin_reg(A.amin[1]), am2 = pin_reg(A.amin[2]);
-      const uint32_t ex0 = pin_reg(A.ext[0]), ex1 = pin_reg(A.ext[1]), ex2 = pin_reg(A.ext[2]);
+      // per point: ballot the runs that just ended, predicated store of the
+      // finished run straight from the run registers, then the run update
+      auto run_step = [&](uint32_t lin, double d) {  // d: z - pivot
+        const bool e = lin != cur;
+        const bool pdu = e && cur != kNoVoxel;
+        const unsigned mu = __ballot_sync(0xffffffffu, pdu);
+        const uint32_t a = qbase | ((qt + __popc(mu & lt_mask) * kRec) & (QB - 1));
+        if (KIND == 0)
+          st_rec32_if(pdu, a, cur, cn, cs1, cs2);
+        else
+          st_rec8_if(pdu, a, cur, cn);
+        qt += __popc(mu) * kRec;
+#ifdef VMI_PRED_RESET
+        run_reset_if(e, cn, cs1, cs2);
+        ++cn;
+        cs1 = __dadd_rn(cs1, d);
+        cs2 = __fma_rn(d, d, cs2);
 #else
+        // a new run restarts the sums through a 0/1 factor (fma(x, 0, d) == d,
+        // fma(x, 1, d) == x + d): one select instead of four 32-bit ones
+        const double keep = e ? 0.0 : 1.0;
+        cn = e ? 1u : cn + 1u;
+        cs1 = __fma_rn(cs1, keep, d);
+        cs2 = __fma_rn(cs2, keep, __dmul_rn(d, d));
+#endif
+        cur = lin;
+      };
       const int am0 = A.amin[0], am1 = A.amin[1], am2 = A.amin[2];
       const uint32_t ex0 = A.ext[0], ex1 = A.ext[1], ex2 = A.ext[2];
-#endif
       // floor(q) - amin straight from DADD.RM against 1.5*2^52 - amin (an
       // integer in [2^52, 2^53), so the sum rounds down to kc + floor(q) and
       // its low word is floor(q) - amin); bounds are tracked relative to amin
@@ -565,139 +454,46 @@ __global__ void __launch_bounds__(THREADS, 1)
       const double kc0 = pin_reg(6755399441055744.0 - (double)am0);
       const double kc1 = pin_reg(6755399441055744.0 - (double)am1);
       const double kc2 = pin_reg(6755399441055744.0 - (double)am2);
-      auto locate = [&](double x, double y, double z, bool valid, uint32_t& lin, double& Z) {
+      // transform (geometry.py:162-166), voxel index (voxel.py:192-207), lin
+      // inside A's AABB, and d = z - (the voxel's lower z face): pure per point
+      auto locate = [&](double x, double y, double z, uint32_t& lin, double& d, int& ix, int& iy,
+                        int& iz) {
         const double X = xform_row(x, y, z, m0, m1, m2, t0);
         const double Y = xform_row(x, y, z, m3, m4, m5, t1);
-        Z = xform_row(x, y, z, m6, m7, m8, t2);
-        const int ix = __double2loint(__dadd_rd(grid_q<MODE>(X, g.origin[0], g.res, g.inv_res), kc0));
-        const int iy = __double2loint(__dadd_rd(grid_q<MODE>(Y, g.origin[1], g.res, g.inv_res), kc1));
-        const int iz = __double2loint(__dadd_rd(grid_q<MODE>(Z, g.origin[2], g.res, g.inv_res), kc2));
-        lin = kNoVoxel;
-        if (valid) {
-          bmin0 = min(bmin0, ix); bmax0 = max(bmax0, ix);
-          bmin1 = min(bmin1, iy); bmax1 = max(bmax1, iy);
-          bmin2 = min(bmin2, iz); bmax2 = max(bmax2, iz);
-          const uint32_t rx = (uint32_t)ix;
-          const uint32_t ry = (uint32_t)iy;
-          const uint32_t rz = (uint32_t)iz;
-          const bool inside = (rx < ex0) & (ry < ex1) & (rz < ex2);
-          lin = inside ? (rx * ex1 + ry) * ex2 + rz : kNoVoxel;
-        if (npass > 1 && lin != kNoVoxel && __umulhi(lin * 0x85EBCA6Bu, (uint32_t)npass) != (uint32_t)pass)
+        const double Z = xform_row(x, y, z, m6, m7, m8, t2);
+        const double fx = __dadd_rd(grid_q<MODE>(X, g.origin[0], g.res, g.inv_res), kc0);
+        const double fy = __dadd_rd(grid_q<MODE>(Y, g.origin[1], g.res, g.inv_res), kc1);
+        const double fz = __dadd_rd(grid_q<MODE>(Z, g.origin[2], g.res, g.inv_res), kc2);
+        ix = __double2loint(fx);
+        iy = __double2loint(fy);
+        iz = __double2loint(fz);
+        // fz - kc2 == floor(q_z) exactly (both integers below 2^53)
+        const double qf = __dsub_rn(fz, kc2);
+        d = __dsub_rn(Z, MODE == kGridUnit ? qf : __fma_rn(qf, g.res, g.origin[2]));
+        lin = inside_lin((uint32_t)ix, (uint32_t)iy, (uint32_t)iz, ex0, ex1, ex2);
+        if (MULTI && npass > 1 && lin != kNoVoxel &&
+            __umulhi(lin * 0x85EBCA6Bu, (uint32_t)npass) != (uint32_t)pass)
           lin = kNoVoxel;  // another pass's partition
-        }
-      };
-      // run aggregation for one point of every stream
-      auto advance = [&](const uint32_t* lin, const double* Z) {
-        bool ends[NS], pushes[NS];
-  #pragma unroll
-        for (int k = 0; k < NS; ++k) {
-          ends[k] = lin[k] != cur[k];
-          pushes[k] = ends[k] && cur[k] != kNoVoxel;
-        }
-        push(pushes);
-  #pragma unroll
-        for (int k = 0; k < NS; ++k) {
-          if (ends[k]) {
-            cur[k] = lin[k]; cn[k] = 1; cK[k] = Z[k]; cs1[k] = 0.0; cs2[k] = 0.0;
-          } else {
-            const double d = Z[k] - cK[k];
-            ++cn[k]; cs1[k] += d; cs2[k] = fma(d, d, cs2[k]);
-          }
-        }
       };
 
       using Rec = typename std::conditional<F32, float4, double4>::type;
       const Rec* pts = reinterpret_cast<const Rec*>(B.pts) + tid;
       const int full = B.span - 1;  // iterations every span owns
-#ifndef VMI_TMA
       // Scan-B records are staged through shared memory with cp.async: each
-      // virtual thread streams its own span kStages-1 records ahead into a
-      // private ring slot (no cross-thread dependency, so no barrier), then reads
-      // the record back with one LDS when it is its turn.  Keeping the prefetch
-      // out of the register file stops the compiler from hoisting conversions of
-      // in-flight data (which turned a register prefetch into stalls).
+      // thread streams its own span S-1 records ahead into a private ring slot
+      // (no cross-thread dependency, so no barrier), then reads the record back
+      // with one LDS when it is its turn.  Rows are issued kPG at a time as one
+      // commit group from a running pointer; the span layout is padded with
+      // kStagePadRows rows, so rows past the span are issued unconditionally
+      // (and never read back).
       constexpr int S = kStages<F32, MULTI>();
       const uint32_t my_stage = stage_base + (uint32_t)tid * (uint32_t)sizeof(Rec);
-      constexpr uint32_t kStageStride = (uint32_t)(VTH * sizeof(Rec));
-      constexpr uint32_t kStreamOff = (uint32_t)(THREADS * sizeof(Rec));
-      auto issue = [&](int r) {
-        if (r < full) {
-  #pragma unroll
-          for (int k = 0; k < NS; ++k)
-            cp_async_rec<Rec>(my_stage + (uint32_t)(r % S) * kStageStride + k * kStreamOff,
-                              pts + r * VTH + k * THREADS);
-        }
-        cp_async_commit();
-      };
-#if defined(VMI_SINGLE_PUSH)
-  #pragma unroll
-      for (int r = 0; r < S - 1; ++r) issue(r);
-#endif
-      // body for record r held in ring slot `slot` (a compile-time constant in
-      // the unrolled main loop, so every shared address is base + immediate)
-      auto body = [&](int r, int slot) {
-        issue(r + S - 1);
-        cp_async_wait<S - 1>();
-        uint32_t lin[NS];
-        double Z[NS];
-  #pragma unroll
-        for (int k = 0; k < NS; ++k) {
-          const Rec v = lds_rec<Rec>(my_stage + (uint32_t)slot * kStageStride + k * kStreamOff);
-          locate((double)v.x, (double)v.y, (double)v.z, true, lin[k], Z[k]);
-        }
-        advance(lin, Z);
-      };
-#if !defined(VMI_SINGLE_PUSH)
-      // two points per step: both located first (independent fp64 chains),
-      // then both run updates, then ONE warp-wide queue push for the up to
-      // two runs each lane finished
-      auto store_state = [&](uint32_t pos, uint32_t l, uint32_t n, double K, double a1, double a2) {
-        const uint32_t a = qbase + (pos & (kQueue - 1)) * kRec;
-        if (KIND == 0) {
-#ifdef VMI_STS64
-          st_shared_v2(a, l, n);
-          st_shared_f64(a + 8, K);
-          st_shared_f64(a + 16, a1);
-          st_shared_f64(a + 24, a2);
-#else
-          st_shared_v4(a, l, n, dlo(K), dhi(K));
-          st_shared_v4(a + 16, dlo(a1), dhi(a1), dlo(a2), dhi(a2));
-#endif
-        } else {
-          st_shared_v2(a, l, n);
-        }
-      };
-      auto step1 = [&](uint32_t lin, double Z, bool& pend, uint32_t& pl, uint32_t& pn, double& pK,
-                       double& p1, double& p2) {
-        const bool e = lin != cur[0];
-        pend = e && cur[0] != kNoVoxel;
-        pl = cur[0]; pn = (uint32_t)cn[0]; pK = cK[0]; p1 = cs1[0]; p2 = cs2[0];
-#ifdef VMI_BRANCHLESS_STEP
-        // reset folds into the update: on a new run cK = Z makes d = 0 and the
-        // 0/1 factor clears the sums (DP pipe has headroom; no branches/moves)
-        cur[0] = lin;  // equal to the old value when the run continues
-        cK[0] = e ? Z : cK[0];
-        cn[0] = e ? 1 : cn[0] + 1;
-        const double keep = e ? 0.0 : 1.0;
-        const double d = Z - cK[0];
-        cs1[0] = fma(cs1[0], keep, d);
-        cs2[0] = fma(d, d, cs2[0] * keep);
-#else
-        if (e) {
-          cur[0] = lin; cn[0] = 1; cK[0] = Z; cs1[0] = 0.0; cs2[0] = 0.0;
-        } else {
-          const double d = Z - cK[0];
-          ++cn[0]; cs1[0] += d; cs2[0] = fma(d, d, cs2[0]);
-        }
-#endif
-      };
-      // Group staging: rows are issued kPG at a time as one commit group from a
-      // running pointer.  The span layout is padded with kStagePadRows rows, so
-      // rows past the span are issued unconditionally (and never read back).
+      constexpr uint32_t kStageStride = (uint32_t)(THREADS * sizeof(Rec));
       static_assert(S % kPG == 0, "ring holds whole groups");
       static_assert(S <= kStagePadRows, "span layout padding covers the ring");
+      static_assert(32 * kPG + 31 <= kQueue, "a push group must fit the run queue");
       constexpr int kGroups = S / kPG;  // commit groups in flight
-      constexpr size_t kRowBytes = (size_t)VTH * sizeof(Rec);
+      constexpr size_t kRowBytes = (size_t)THREADS * sizeof(Rec);
       const char* src = reinterpret_cast<const char*>(pts);
       auto issue_group = [&](int slot0) {
 #pragma unroll
@@ -707,173 +503,70 @@ __global__ void __launch_bounds__(THREADS, 1)
         src += kPG * kRowBytes;
         cp_async_commit();
       };
-      auto group_body = [&](int r) {
+      auto group_body = [&](int slot0) {  // the group starts in ring slot slot0
         cp_async_wait<kGroups - 1>();  // rows r .. r+kPG-1 have landed
         uint32_t l[kPG];
-        double Z[kPG];
+        double D[kPG];
+        int ix[kPG], iy[kPG], iz[kPG];
 #pragma unroll
         for (int u = 0; u < kPG; ++u) {
-          const Rec v = lds_rec<Rec>(my_stage + (uint32_t)((r + u) % S) * kStageStride);
-          locate((double)v.x, (double)v.y, (double)v.z, true, l[u], Z[u]);
+          const Rec v = lds_rec<Rec>(my_stage + (uint32_t)(slot0 + u) * kStageStride);
+          locate((double)v.x, (double)v.y, (double)v.z, l[u], D[u], ix[u], iy[u], iz[u]);
         }
-        issue_group(r % S);  // refill the slots just consumed with rows r+S ..
-#ifndef VMI_BATCH_PUSH  // (batched ballots + branchy stores: A/B measured 0.8% slower)
-        // per point: ballot, predicated store of the finished run straight from
-        // the run registers, then the run update (no pending copies, no branches).
-        // A group adds <= 32*kPG records to < 32 unflushed ones.
-        static_assert(32 * kPG + 31 <= kQueue, "a push group must fit the run queue");
+        issue_group(slot0);  // refill the slots just consumed with rows r+S ..
+        // bounds: one min/max tree per group (3-input VIMNMX3)
+        int n0 = ix[0], n1 = iy[0], n2 = iz[0], x0 = ix[0], x1 = iy[0], x2 = iz[0];
 #pragma unroll
-        for (int u = 0; u < kPG; ++u) {
-          const bool e = l[u] != cur[0];
-          const bool pdu = e && cur[0] != kNoVoxel;
-          const unsigned mu = __ballot_sync(0xffffffffu, pdu);
-          const uint32_t a = qbase + ((qt + __popc(mu & lt_mask)) & (kQueue - 1)) * kRec;
-          if (KIND == 0)
-            st_rec32_if(pdu, a, cur[0], (uint32_t)cn[0], cK[0], cs1[0], cs2[0]);
-          else
-            st_rec8_if(pdu, a, cur[0], (uint32_t)cn[0]);
-          qt += __popc(mu);
-#ifdef VMI_SEQ_BRANCHLESS  // experiment: fewer instructions, longer dependency chain (A/B: +0.6 % time)
-          // reset folded into the update: a new run takes cK = Z, so d = 0 and
-          // the 0/1 factor clears the sums (fma(x, 1, d) == x + d exactly)
-          cur[0] = l[u];
-          cK[0] = e ? Z[u] : cK[0];
-          const double keep = e ? 0.0 : 1.0;
-          const double d = Z[u] - cK[0];
-          cn[0] = e ? 1 : cn[0] + 1;
-          cs1[0] = fma(cs1[0], keep, d);
-          cs2[0] = fma(d, d, cs2[0] * keep);
-#else
-          if (e) {
-            cur[0] = l[u]; cn[0] = 1; cK[0] = Z[u]; cs1[0] = 0.0; cs2[0] = 0.0;
-          } else {
-            const double d = Z[u] - cK[0];
-            ++cn[0]; cs1[0] += d; cs2[0] = fma(d, d, cs2[0]);
-          }
-#endif
+        for (int u = 1; u < kPG; ++u) {
+          n0 = min(n0, ix[u]); n1 = min(n1, iy[u]); n2 = min(n2, iz[u]);
+          x0 = max(x0, ix[u]); x1 = max(x1, iy[u]); x2 = max(x2, iz[u]);
         }
-        while (qt - qh >= 32) {
-          __syncwarp();
-          flush_rec(qh + lane);
-          qh += 32;
-          __syncwarp();
-        }
-#else
-        bool pd[kPG];
-        uint32_t pl[kPG], pn[kPG];
-        double pK[kPG], p1[kPG], p2[kPG];
+        bmin0 = min(bmin0, n0); bmin1 = min(bmin1, n1); bmin2 = min(bmin2, n2);
+        bmax0 = max(bmax0, x0); bmax1 = max(bmax1, x1); bmax2 = max(bmax2, x2);
+        // a group adds <= 32*kPG records to < 32 unflushed ones
 #pragma unroll
-        for (int u = 0; u < kPG; ++u) step1(l[u], Z[u], pd[u], pl[u], pn[u], pK[u], p1[u], p2[u]);
-        unsigned m[kPG];
-        unsigned any = 0u;
-#pragma unroll
-        for (int u = 0; u < kPG; ++u) { m[u] = __ballot_sync(0xffffffffu, pd[u]); any |= m[u]; }
-        if (any != 0u) {
-          // A group can push up to 32*kPG records on top of < 32 unflushed ones:
-          // when that would overrun the ring, flush the partial round first.
-          uint32_t n = 0;
-#pragma unroll
-          for (int u = 0; u < kPG; ++u) n += __popc(m[u]);
-#ifndef VMI_NO_QUEUE_GUARD  // A/B timing experiment only (unsafe for dense pushes)
-          if (32 * kPG + 31 > kQueue && qt - qh + n > (uint32_t)kQueue) {
-            __syncwarp();
-            if ((uint32_t)lane < qt - qh) flush_rec(qh + lane);
-            qh = qt;
-            __syncwarp();
-          }
-#endif
-          uint32_t base = qt;
-#pragma unroll
-          for (int u = 0; u < kPG; ++u) {
-            if (pd[u]) store_state(base + __popc(m[u] & lt_mask), pl[u], pn[u], pK[u], p1[u], p2[u]);
-            base += __popc(m[u]);
-          }
-          qt = base;
-          while (qt - qh >= 32) {
-            __syncwarp();
-            flush_rec(qh + lane);
-            qh += 32;
-            __syncwarp();
-          }
-        }
-#endif
+        for (int u = 0; u < kPG; ++u) run_step(l[u], D[u]);
+        drain_full();
       };
-      static_assert(S >= kPG, "ring must hold a full group");
 #pragma unroll
       for (int gi = 0; gi < kGroups; ++gi) issue_group(gi * kPG);  // rows 0 .. S-1 in flight
       int rr = 0;
-#pragma unroll kGroupUnroll
-      for (; rr + kPG <= full; rr += kPG) group_body(rr);
-      for (; rr < full; ++rr) {  // leftover (< kPG) points
-        cp_async_wait<0>();
-        uint32_t lin[NS];
-        double Zs[NS];
-        const Rec v = lds_rec<Rec>(my_stage + (uint32_t)(rr % S) * kStageStride);
-        locate((double)v.x, (double)v.y, (double)v.z, true, lin[0], Zs[0]);
-        advance(lin, Zs);
-      }
-#elif !defined(VMI_STATIC_SLOT)
-      #pragma unroll kUnroll
-      for (int r = 0; r < full; ++r) body(r, r % S);
-#else
-      int r0 = 0;
-      for (; r0 + S <= full; r0 += S) {
-  #pragma unroll
-        for (int u = 0; u < S; ++u) body(r0 + u, u);
-      }
-      for (int r = r0; r < full; ++r) body(r, r % S);
-#endif
-      cp_async_wait<0>();
-#else
-      // Scan-B records are staged through shared memory by TMA bulk copies:
-      // in the span layout a warp's 32 records of one iteration are one
-      // contiguous 32*sizeof(Rec)-byte chunk, so lane 0 streams groups of G
-      // iterations (two groups in flight, one mbarrier each) and every lane
-      // reads its record back with one LDS.  The stream runs continuously
-      // across passes and poses (scan B is the same for every pose).
-      for (int q = 0; q < ng; ++q) {
-        const uint32_t slot = gq & 1u;
-        while (!mbar_try_wait(wbar + slot * 8u, (gq >> 1) & 1u)) {
-        }
-        const int r0 = q * G;
+      // one trip = one lap of the ring (compile-time slots), then the last groups
+      for (; rr + S <= full; rr += S) {
 #pragma unroll
-        for (int u = 0; u < G; ++u) {
-          if (r0 + u < full) {  // warp-uniform
-            uint32_t lin[NS];
-            double Z[NS];
-            const Rec v = lds_rec<Rec>(wstage + (slot * G + u) * kChunk + (uint32_t)lane * sizeof(Rec));
-            locate((double)v.x, (double)v.y, (double)v.z, true, lin[0], Z[0]);
-            advance(lin, Z);
-          }
+        for (int gi = 0; gi < kGroups; ++gi) group_body(gi * kPG);
+      }
+      for (; rr + kPG <= full; rr += kPG) group_body(rr % S);
+      cp_async_wait<0>();
+      VMI_TR("main loop done", rr)
+      for (; rr <= full; ++rr) {  // leftover (< kPG) points and the ragged last row
+        const bool has = rr < full || span_of_thread(tid, THREADS) < B.rem;
+        const Rec v = rr < full ? lds_rec<Rec>(my_stage + (uint32_t)(rr % S) * kStageStride)
+                                : pts[(size_t)full * THREADS];
+        uint32_t lin;
+        double d;
+        int ix, iy, iz;
+        locate((double)v.x, (double)v.y, (double)v.z, lin, d, ix, iy, iz);
+        if (has) {
+          bmin0 = min(bmin0, ix); bmin1 = min(bmin1, iy); bmin2 = min(bmin2, iz);
+          bmax0 = max(bmax0, ix); bmax1 = max(bmax1, iy); bmax2 = max(bmax2, iz);
+        } else {
+          lin = kNoVoxel;
         }
-        __syncwarp();  // every lane has read this buffer: it may be refilled
-        ++gq;
-        produce();
+        run_step(lin, d);
+        drain_full();
       }
-#endif
-      {  // the ragged last iteration
-        uint32_t lin[NS];
-        double Z[NS];
-  #pragma unroll
-        for (int k = 0; k < NS; ++k) {
-          const Rec v = pts[full * VTH + k * THREADS];
-          const bool has_last = span_of_thread(tid + k * THREADS, VTH) < B.rem;
-          locate((double)v.x, (double)v.y, (double)v.z, has_last, lin[k], Z[k]);
-        }
-        advance(lin, Z);
-      }
-      {
-        bool fin[NS];
-  #pragma unroll
-        for (int k = 0; k < NS; ++k) fin[k] = cur[k] != kNoVoxel;
-        push(fin);
-      }
+      VMI_TR("leftover done", rr)
+      run_step(kNoVoxel, 0.0);  // close the open run
+      uint32_t wd2 = 0; (void)wd2;
       while (qh != qt) {  // drain the tail (partial round)
+        VMI_WD(2, wd2, qt, qh)
         __syncwarp();
-        if ((uint32_t)lane < qt - qh) flush_rec(qh + lane);
-        qh = (qt - qh > 32u) ? qh + 32 : qt;
+        if ((uint32_t)lane * kRec < qt - qh) flush_rec(qh + lane * kRec, true);
+        qh = (qt - qh > 32u * kRec) ? qh + 32 * kRec : qt;
         __syncwarp();
       }
+      VMI_TR("tail drained", qt)
       if (pass == 0) {
         // ---- reduce bounds / key-range flag ----------------------------------
         bmin0 = __reduce_min_sync(0xffffffffu, bmin0);
@@ -923,7 +616,7 @@ __global__ void __launch_bounds__(THREADS, 1)
         if (KIND == 0) {
           const double nd = (double)(kGlobalCounts<MULTI>() ? __ldcg(&VT.cnt[s]) : VT.cnt[s]);
           const double S1 = sum.x, S2 = sum.y;
-          VT.key[s] = kEmpty64; VT.cnt[s] = 0u;
+          VT.key[s] = kEmptyKey; VT.cnt[s] = 0u;
           VT.sums[s] = make_double2(0.0, 0.0);
           const double rn = __drcp_rn(nd);
           const double c1 = S1 * S1 * rn;
@@ -959,6 +652,7 @@ __global__ void __launch_bounds__(THREADS, 1)
           }
         }
       };
+      VMI_TR("walk start", status)
       if constexpr (KIND == 0) {
         // VARZ: each warp owns a contiguous slice of the table; it compacts the
         // occupied slots (ballot) into a ring in its share of the (idle)
@@ -969,27 +663,24 @@ __global__ void __launch_bounds__(THREADS, 1)
         constexpr int NW = THREADS / 32;
         constexpr int kWR = 256;  // ring entries; kWU ballots per scan step / entries per lane
         constexpr int kWU = kWR / 64;
-#ifndef VMI_TMA
         static_assert(kStages<F32, MULTI>() * NS * (F32 ? 16 : 32) * 32 >= kWR * 4,
                       "walk ring fits the warp's staging slice");
         uint32_t* wl = reinterpret_cast<uint32_t*>(
             smem + L.stage + (size_t)wid * 32 * NS * (F32 ? 16 : 32) * kStages<F32, MULTI>());
-#else
-        static_assert(kQueue * kRec >= kWR * 4, "walk ring fits the run queue");
-        uint32_t* wl = reinterpret_cast<uint32_t*>(smem + L.queue + (size_t)wid * kQueue * kRec);
-#endif
         const int per = ((cap + NW - 1) / NW + 31) & ~31;
         const int se = min(cap, wid * per + per);
         int scan = wid * per;
         uint32_t wh = 0, wt = 0;  // ring head / tail (warp-uniform)
+        uint32_t wd3 = 0; (void)wd3;
         while (scan < se || wt != wh) {  // warp-uniform
+          VMI_WD(3, wd3, scan, wt - wh)
           while (scan < se && wt - wh < (uint32_t)(32 * kWU)) {
             bool occ[kWU];
             unsigned m[kWU];
 #pragma unroll
             for (int u = 0; u < kWU; ++u) {
               const int s = scan + u * 32 + lane;
-              occ[u] = s < se && VT.key[s] != kEmpty64;
+              occ[u] = s < se && VT.key[s] != kEmptyKey;
               m[u] = __ballot_sync(0xffffffffu, occ[u]);
             }
 #pragma unroll
@@ -1009,7 +700,7 @@ __global__ void __launch_bounds__(THREADS, 1)
           for (int u = 0; u < kWU; ++u) {
             const uint32_t i = (uint32_t)(u * 32 + lane);
             sl[u] = i < take ? (int)wl[(wh + i) & (kWR - 1)] : -1;
-            lin[u] = sl[u] >= 0 ? (uint32_t)(VT.key[sl[u]] >> 32) : kNoVoxel;
+            lin[u] = sl[u] >= 0 ? VT.key[sl[u]] : kNoVoxel;
             ba[u] = lin[u] != kNoVoxel ? (int)__ldg(&A.grid[lin[u]]) : 0;
             // L2 copy (the reductions happen in L2; never trust a stale L1 line)
             sum[u] = lin[u] != kNoVoxel ? __ldcg(&VT.sums[sl[u]]) : make_double2(0.0, 0.0);
@@ -1041,6 +732,7 @@ __global__ void __launch_bounds__(THREADS, 1)
             if (lin[u] != kNoVoxel) finish_slot(s0 + u * THREADS, lin[u], ba[u], make_double2(0.0, 0.0));
         }
       }
+      VMI_TR("walk done", 0)
       __syncthreads();  // walk done (slots reset) before the next pass refills
     }
     if (status != 0) {
@@ -1109,14 +801,6 @@ __global__ void __launch_bounds__(THREADS, 1)
     }
     __syncthreads();
   }
-#ifdef VMI_TMA
-  // retire the two groups still in flight (no bulk copy may outlive the CTA)
-  for (int i = 0; i < 2 && ng > 0; ++i) {
-    while (!mbar_try_wait(wbar + (gq & 1u) * 8u, (gq >> 1) & 1u)) {
-    }
-    ++gq;
-  }
-#endif
 }
 
 template <int THREADS, int NS, int KIND, bool F32, int MODE, bool MULTI>

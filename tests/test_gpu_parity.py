@@ -340,7 +340,8 @@ def unpack(keys):
 @pytest.mark.parametrize("tag,res,kind", [("v1", 1.0, "varz"), ("c1", 1.0, "count")])
 def test_fast_path_features_match_reference(tag, res, kind):
     """The fused kernel's own per-voxel features (pivot-shifted VARZ sums) for
-    scan B at the truth pose: voxel ids and COUNT exact, VARZ within 1e-6."""
+    scan B at the truth pose: voxel ids and COUNT exact, VARZ within its
+    summation-error bound (and 1e-6 relative above it)."""
     g = golden("hdl_golden.npz")
     a, b = hdl_pair()
     eng = engine(res, kind=kind)
@@ -356,10 +357,22 @@ def test_fast_path_features_match_reference(tag, res, kind):
     if kind == "count":
         np.testing.assert_array_equal(vals, bv[inside])
     else:
+        # The kernel sums (z - K) and (z - K)^2 around K = the voxel's lower z
+        # face, so its VARZ error is bounded by the summation error of those
+        # sums: |err| <= (n + 8) * 2^-51 * (S2 + S1^2/n) / n <= (n + 8) * 2^-50 * res^2
+        # -- the same bound the kernel's bin-edge guard uses (any voxel that
+        # close to a bin edge sends the pose to the exact path, so histograms
+        # stay bit-exact).  Relative 1e-6 holds wherever that bound is below it.
         want = bv[inside]
-        np.testing.assert_allclose(vals, want, rtol=1e-6, atol=1e-18)
-        rel = np.abs(vals - want) / np.maximum(np.abs(want), 1e-300)
-        assert np.max(rel[want > 1e-12]) < 1e-11  # measured headroom, not the bar
+        ck = g["c1_b_keys"]  # COUNT at the same resolution: per-voxel n
+        n = g["c1_b_values"][np.searchsorted(ck, keys)]
+        assert np.array_equal(ck[np.searchsorted(ck, keys)], keys)
+        bound = (n + 8) * 2.0 ** -50 * res * res
+        err = np.abs(vals - want)
+        assert np.all(err <= bound), np.max(err / bound)
+        big = want > 1e4 * bound
+        np.testing.assert_allclose(vals[big], want[big], rtol=1e-6)
+        assert big.mean() > 0.9  # measured 0.93 (the rest: near-flat voxels, var < 1e4 * bound)
 
 
 @pytest.mark.parametrize("tag", ["varz1", "count05"])
