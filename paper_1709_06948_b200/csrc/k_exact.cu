@@ -35,8 +35,12 @@ __device__ __forceinline__ void point_at(const PointSource& src, int64_t i, doub
   }
   const int64_t li = span_slot(i, src.B.span, src.B.rem, src.B.threads);
   if (src.B.is_f32) {
+#if VMI_SPLITREC
+    split_decode(reinterpret_cast<const uint4*>(src.B.pts)[li], x, y, z);
+#else
     float4 v = reinterpret_cast<const float4*>(src.B.pts)[li];
     x = v.x; y = v.y; z = v.z;
+#endif
   } else {
     const double* d = reinterpret_cast<const double*>(src.B.pts) + 4 * li;
     x = d[0]; y = d[1]; z = d[2];
@@ -392,7 +396,12 @@ __global__ void k_span_layout(const void* src, int is_f32, int64_t n, int span, 
   }
   const int64_t li = span_slot(i, span, rem, threads);
   if (is_f32) {
-    reinterpret_cast<float4*>(dst)[li] = reinterpret_cast<const float4*>(src)[i];
+    const float4 v = reinterpret_cast<const float4*>(src)[i];
+#if VMI_SPLITREC
+    reinterpret_cast<uint4*>(dst)[li] = split_encode(v.x, v.y, v.z);  // (the intensity is unused)
+#else
+    reinterpret_cast<float4*>(dst)[li] = v;
+#endif
   } else {
     const double* s = reinterpret_cast<const double*>(src);
     reinterpret_cast<double4*>(dst)[li] = make_double4(s[3 * i], s[3 * i + 1], s[3 * i + 2], 0.0);

@@ -71,6 +71,20 @@ template <int N>
 __device__ __forceinline__ void cp_async_wait() {
   asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory");
 }
+// a staged record's coordinates as doubles (float4 records are split doubles,
+// vmi_device.cuh, unless VMI_SPLITREC=0)
+__device__ __forceinline__ void rec_xyz(const float4& v, double& x, double& y, double& z) {
+#if VMI_SPLITREC
+  split_decode(make_uint4(__float_as_uint(v.x), __float_as_uint(v.y), __float_as_uint(v.z),
+                          __float_as_uint(v.w)),
+               x, y, z);
+#else
+  x = v.x; y = v.y; z = v.z;
+#endif
+}
+__device__ __forceinline__ void rec_xyz(const double4& v, double& x, double& y, double& z) {
+  x = v.x; y = v.y; z = v.z;
+}
 template <typename Rec>
 __device__ __forceinline__ Rec lds_rec(uint32_t a);
 template <>
@@ -511,7 +525,9 @@ __global__ void __launch_bounds__(THREADS, 1)
 #pragma unroll
         for (int u = 0; u < kPG; ++u) {
           const Rec v = lds_rec<Rec>(my_stage + (uint32_t)(slot0 + u) * kStageStride);
-          locate((double)v.x, (double)v.y, (double)v.z, l[u], D[u], ix[u], iy[u], iz[u]);
+          double x, y, z;
+          rec_xyz(v, x, y, z);
+          locate(x, y, z, l[u], D[u], ix[u], iy[u], iz[u]);
         }
         issue_group(slot0);  // refill the slots just consumed with rows r+S ..
         // bounds: one min/max tree per group (3-input VIMNMX3)
@@ -546,7 +562,9 @@ __global__ void __launch_bounds__(THREADS, 1)
         uint32_t lin;
         double d;
         int ix, iy, iz;
-        locate((double)v.x, (double)v.y, (double)v.z, lin, d, ix, iy, iz);
+        double x, y, z;
+        rec_xyz(v, x, y, z);
+        locate(x, y, z, lin, d, ix, iy, iz);
         if (has) {
           bmin0 = min(bmin0, ix); bmin1 = min(bmin1, iy); bmin2 = min(bmin2, iz);
           bmax0 = max(bmax0, ix); bmax1 = max(bmax1, iy); bmax2 = max(bmax2, iz);

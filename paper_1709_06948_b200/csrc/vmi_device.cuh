@@ -14,6 +14,32 @@ constexpr uint32_t kNoVoxel = 0xFFFFFFFFu;
 constexpr int kKeyMin = -(1 << 20);
 constexpr int kKeyMax = (1 << 20) - 1;
 
+// ---- float32 scan-B records, stored pre-widened ("split doubles") -----------
+// (double)f of a float has a 24-bit significand: the double's low word holds
+// only its top 3 bits.  Words 0-2 of a record are the high words of (double)x,
+// (double)y, (double)z; word 3 packs the three low words' top bits (x in bits
+// 31..29, y in 28..26, z in 25..23).  Decoding is 4 integer ops instead of 3
+// F2F.F64.F32 conversions (XU pipe, variable latency) per point.
+#ifndef VMI_SPLITREC
+#define VMI_SPLITREC 1
+#endif
+__device__ __forceinline__ uint4 split_encode(float x, float y, float z) {
+  const double d[3] = {(double)x, (double)y, (double)z};
+  uint4 r;
+  r.x = (uint32_t)__double2hiint(d[0]);
+  r.y = (uint32_t)__double2hiint(d[1]);
+  r.z = (uint32_t)__double2hiint(d[2]);
+  r.w = ((uint32_t)__double2loint(d[0]) & 0xE0000000u) |
+        (((uint32_t)__double2loint(d[1]) & 0xE0000000u) >> 3) |
+        (((uint32_t)__double2loint(d[2]) & 0xE0000000u) >> 6);
+  return r;
+}
+__device__ __forceinline__ void split_decode(uint4 v, double& x, double& y, double& z) {
+  x = __hiloint2double((int)v.x, (int)(v.w & 0xE0000000u));
+  y = __hiloint2double((int)v.y, (int)((v.w << 3) & 0xE0000000u));
+  z = __hiloint2double((int)v.z, (int)(v.w << 6));
+}
+
 
 // ---- geometry.py:162-166: numpy `points @ R.T + t` through OpenBLAS dgemm is,
 // bit for bit, fma(z, R[j][2], fma(y, R[j][1], x * R[j][0])) + t[j].
