@@ -48,6 +48,9 @@ __device__ __forceinline__ uint32_t slot_of(uint32_t lin, uint32_t cap) {
 // push with an S-record cp.async ring (two push groups in flight).  Multi-pass
 // (large grids): shared memory goes to the table instead (more capacity =
 // fewer passes), so one point per push and a 4-record ring.
+#ifndef VMI_NEAR_FIX  // 0: teeth check of the near-integer test only (wrong floors)
+#define VMI_NEAR_FIX 1
+#endif
 #ifndef VMI_STAGES
 #define VMI_STAGES 6  // cp.async ring: 6 records in flight per thread (2 push groups)
 #endif
@@ -348,7 +351,9 @@ __global__ void __launch_bounds__(THREADS, 1)
     // checked exactly on the reduced bounds.  Poses beyond that (translations
     // of ~1e9 voxels) go to the exact path, which reports KEY_RANGE.
     {
-      const double lim = 1073741824.0 * g.res;
+      // kGridGeneral's fast floor needs |q - amin| < 2^22 (locate): 2^21 - max|amin|
+      const int amx = max(max(abs(A.amin[0]), abs(A.amin[1])), abs(A.amin[2]));
+      const double lim = (MODE == kGridGeneral ? 2097152.0 - (double)amx : 1073741824.0) * g.res;
       const double mx = B.max_abs;
       const bool unsafe =
           fabs(t0 - g.origin[0]) + (fabs(m0) + fabs(m1) + fabs(m2)) * mx >= lim ||
@@ -468,6 +473,17 @@ __global__ void __launch_bounds__(THREADS, 1)
       const double kc0 = pin_reg(6755399441055744.0 - (double)am0);
       const double kc1 = pin_reg(6755399441055744.0 - (double)am1);
       const double kc2 = pin_reg(6755399441055744.0 - (double)am2);
+      // General resolutions (kGridGeneral): q' = (p - o) * RN(1/res) is within
+      // |q'| * 2^-51 of numpy's RN((p - o) / res), i.e. < 2^-30 voxel for the
+      // |q'| < 2^21 this pose is guaranteed (see `unsafe` above).  q' is
+      // floored on a 2^-29 grid by DADD.RM against 1.5*2^23 - amin: the
+      // mantissa >> 29 is 2^22 + floor(q') - amin and the low 29 bits are the
+      // fraction.  Only a fraction within 4 grid steps of an integer can floor
+      // differently from the reference; such a point (about 1 in 10^8) takes
+      // the IEEE division.
+      const double kf0 = pin_reg(12582912.0 - (double)am0);
+      const double kf1 = pin_reg(12582912.0 - (double)am1);
+      const double kf2 = pin_reg(12582912.0 - (double)am2);
       // transform (geometry.py:162-166), voxel index (voxel.py:192-207), lin
       // inside A's AABB, and d = z - (the voxel's lower z face): pure per point
       auto locate = [&](double x, double y, double z, uint32_t& lin, double& d, int& ix, int& iy,
@@ -475,6 +491,34 @@ __global__ void __launch_bounds__(THREADS, 1)
         const double X = xform_row(x, y, z, m0, m1, m2, t0);
         const double Y = xform_row(x, y, z, m3, m4, m5, t1);
         const double Z = xform_row(x, y, z, m6, m7, m8, t2);
+        if constexpr (MODE == kGridGeneral) {
+          const double qx = __dmul_rn(__dsub_rn(X, g.origin[0]), g.inv_res);
+          const double qy = __dmul_rn(__dsub_rn(Y, g.origin[1]), g.inv_res);
+          const double qz = __dmul_rn(__dsub_rn(Z, g.origin[2]), g.inv_res);
+          const double rx = __dadd_rd(qx, kf0), ry = __dadd_rd(qy, kf1), rz = __dadd_rd(qz, kf2);
+          const uint32_t lx = (uint32_t)__double2loint(rx), ly = (uint32_t)__double2loint(ry),
+                         lz = (uint32_t)__double2loint(rz);
+          constexpr uint32_t kFB = 0x0B400000u;  // (hi(2^23) << 3) + 2^22
+          ix = (int)(__funnelshift_r(lx, (uint32_t)__double2hiint(rx), 29) - kFB);
+          iy = (int)(__funnelshift_r(ly, (uint32_t)__double2hiint(ry), 29) - kFB);
+          iz = (int)(__funnelshift_r(lz, (uint32_t)__double2hiint(rz), 29) - kFB);
+          const bool near = ((lx + 4u) & 0x1FFFFFFFu) < 8u || ((ly + 4u) & 0x1FFFFFFFu) < 8u ||
+                            ((lz + 4u) & 0x1FFFFFFFu) < 8u;
+          double qf = __dsub_rn(__dadd_rd(qz, 6755399441055744.0), 6755399441055744.0);
+          if (VMI_NEAR_FIX && __builtin_expect(near, 0)) {  // the reference's IEEE quotient
+            ix = __double2loint(__dadd_rd(grid_q<MODE>(X, g.origin[0], g.res, g.inv_res), kc0));
+            iy = __double2loint(__dadd_rd(grid_q<MODE>(Y, g.origin[1], g.res, g.inv_res), kc1));
+            const double fz = __dadd_rd(grid_q<MODE>(Z, g.origin[2], g.res, g.inv_res), kc2);
+            iz = __double2loint(fz);
+            qf = __dsub_rn(fz, kc2);
+          }
+          d = __dsub_rn(Z, __fma_rn(qf, g.res, g.origin[2]));
+          lin = inside_lin((uint32_t)ix, (uint32_t)iy, (uint32_t)iz, ex0, ex1, ex2);
+          if (MULTI && npass > 1 && lin != kNoVoxel &&
+              __umulhi(lin * 0x85EBCA6Bu, (uint32_t)npass) != (uint32_t)pass)
+            lin = kNoVoxel;  // another pass's partition
+          return;
+        }
         const double fx = __dadd_rd(grid_q<MODE>(X, g.origin[0], g.res, g.inv_res), kc0);
         const double fy = __dadd_rd(grid_q<MODE>(Y, g.origin[1], g.res, g.inv_res), kc1);
         const double fz = __dadd_rd(grid_q<MODE>(Z, g.origin[2], g.res, g.inv_res), kc2);
@@ -628,11 +672,11 @@ __global__ void __launch_bounds__(THREADS, 1)
       // var * (B / clamp): our VARZ is itself within ~1e-14 of the reference's,
       // and any value within rounding distance of a bin edge marks the pose for
       // the exact path.
-      auto finish_slot = [&](int s, uint32_t lin, int ba, double2 sum) {
+      auto finish_slot = [&](int s, uint32_t lin, int ba, double2 sum, uint32_t cnt) {
         int bb;
         double dump_feat = 0.0;
         if (KIND == 0) {
-          const double nd = (double)(kGlobalCounts<MULTI>() ? __ldcg(&VT.cnt[s]) : VT.cnt[s]);
+          const double nd = (double)cnt;
           const double S1 = sum.x, S2 = sum.y;
           VT.key[s] = kEmptyKey; VT.cnt[s] = 0u;
           VT.sums[s] = make_double2(0.0, 0.0);
@@ -714,6 +758,7 @@ __global__ void __launch_bounds__(THREADS, 1)
           uint32_t lin[kWU];
           int ba[kWU];
           double2 sum[kWU];
+          uint32_t cnt[kWU];
 #pragma unroll
           for (int u = 0; u < kWU; ++u) {
             const uint32_t i = (uint32_t)(u * 32 + lane);
@@ -722,12 +767,14 @@ __global__ void __launch_bounds__(THREADS, 1)
             ba[u] = lin[u] != kNoVoxel ? (int)__ldg(&A.grid[lin[u]]) : 0;
             // L2 copy (the reductions happen in L2; never trust a stale L1 line)
             sum[u] = lin[u] != kNoVoxel ? __ldcg(&VT.sums[sl[u]]) : make_double2(0.0, 0.0);
+            // (multi-pass: the counts live in L2 too; load them with the sums)
+            cnt[u] = lin[u] == kNoVoxel ? 0u : kGlobalCounts<MULTI>() ? __ldcg(&VT.cnt[sl[u]]) : VT.cnt[sl[u]];
           }
           wh += take;
           __syncwarp();  // entries read: the ring may be refilled
 #pragma unroll
           for (int u = 0; u < kWU; ++u)
-            if (lin[u] != kNoVoxel) finish_slot(sl[u], lin[u], ba[u], sum[u]);
+            if (lin[u] != kNoVoxel) finish_slot(sl[u], lin[u], ba[u], sum[u], cnt[u]);
         }
       } else {
         // COUNT: four slots per thread per step, four A-grid loads in flight
@@ -747,7 +794,7 @@ __global__ void __launch_bounds__(THREADS, 1)
           }
 #pragma unroll
           for (int u = 0; u < 4; ++u)
-            if (lin[u] != kNoVoxel) finish_slot(s0 + u * THREADS, lin[u], ba[u], make_double2(0.0, 0.0));
+            if (lin[u] != kNoVoxel) finish_slot(s0 + u * THREADS, lin[u], ba[u], make_double2(0.0, 0.0), 0u);
         }
       }
       VMI_TR("walk done", 0)

@@ -422,7 +422,7 @@ int vmi_set_params(vmi_ctx* c, const double origin[3], double res, int kind, int
   const bool pow2 = mant == 0.5;
   const bool zero_origin = origin[0] == 0.0 && origin[1] == 0.0 && origin[2] == 0.0;
   g.mode = (zero_origin && res == 1.0) ? kGridUnit : (pow2 ? kGridPow2 : kGridGeneral);
-  g.inv_res = pow2 ? 1.0 / res : 0.0;
+  g.inv_res = 1.0 / res;  // exact for pow2; RN(1/res) for the general fast floor (k_fast.cu)
   g.kind = kind;
   g.bins = bins;
   g.clamp = clamp;

@@ -488,3 +488,46 @@ def test_sparse_scan_run_queue_pressure(kind):
         np.testing.assert_array_equal(hist[i], ohist)
         assert total[i] == ototal
         assert_mi_close([mi[i]], [omi])
+
+
+@pytest.mark.parametrize("res,kind", [(0.7, "count"), (0.7, "varz"), (0.2, "count")])
+def test_general_resolution_near_integer_quotients(res, kind):
+    """Non-power-of-two resolutions: the kernel floors (p - o) * RN(1/res) and
+    falls back to the IEEE quotient only when that product lies within a few
+    2^-29 steps of an integer.  Dyadic coordinates under identity rotations
+    and dyadic translations land exactly on those cases (at res 0.7, 26 of 8000
+    multiples of 1/8 floor differently through the product than through
+    numpy's division), so voxel ids and histograms must match the reference."""
+    xs = np.arange(-4000, 4000) / 8.0
+    assert (np.floor(xs / 0.7) != np.floor(xs * (1.0 / 0.7))).sum() > 0  # the test has teeth
+    rng = np.random.default_rng(23)
+    # (sized so scan B's voxels fit one table: no pose is sent to the exact path)
+    pts_b = np.stack([rng.choice(xs[np.abs(xs) < 12], 10000),
+                      rng.choice(xs[np.abs(xs) < 12], 10000),
+                      rng.choice(xs[np.abs(xs) < 3], 10000)], axis=1)
+    pts_a = np.concatenate([pts_b[::3] + rng.normal(0, 0.05, size=pts_b[::3].shape),
+                            rng.uniform(-16, 16, size=(2000, 3))]).astype(np.float32).astype(np.float64)
+    eng = engine(res, kind=kind, passes=1)
+    eng.set_reference(pts_a)
+    eng.set_query(pts_b)  # float32-exact: split-double records
+    poses = np.array([[0.0, 0.0, 0.0, 0.0, 0.0, 0.0], [0.875, -0.5, 0.125, 0.0, 0.0, 0.0],
+                      [-2.25, 1.5, 0.0, 0.0, 0.0, 0.0], [0.3, 0.1, 0.0, 0.0, 0.0, 0.02]])
+    mats = vmi.poses_to_mats(poses)
+    mi, st, hist, total = eng.evaluate(poses, histograms=True)
+    fa = oracle.feature_map(pts_a, (0, 0, 0), res, kind)
+    for i in range(len(poses)):
+        omi, ost, ohist, ototal = oracle.mi_objective_full(fa, pts_b, mats[i], res=res)
+        assert st[i] == ost
+        np.testing.assert_array_equal(hist[i], ohist)
+        assert total[i] == ototal
+        assert_mi_close([mi[i]], [omi])
+    if kind == "count":  # voxel ids and counts of the fused kernel itself
+        for i in range(len(poses)):
+            keys, vals, fst = eng.ctx.fast_features(mats[i], 200000)
+            assert fst == 0
+            fb = oracle.feature_map(oracle.transform(pts_b, mats[i]), (0, 0, 0), res, kind)
+            ijk = unpack(fb.keys)
+            lo, hi = fa.bounds
+            inside = ((ijk >= lo) & (ijk <= hi)).all(axis=1)
+            np.testing.assert_array_equal(keys, fb.keys[inside])
+            np.testing.assert_array_equal(vals, fb.values[inside])
