@@ -902,11 +902,13 @@ static cudaError_t launch_grid(const FastLaunch& fl, cudaStream_t st) {
 }
 
 // The multi-pass loop costs ~8% even at npass == 1 (measured), so single- and
-// multi-pass are separate instantiations.
+// multi-pass are separate instantiations; the multi-pass layout (a ~3x bigger
+// table) also runs single-pass when scan B's voxels fit it but not the
+// single-pass table.
 template <int T, int NS, int KIND, bool F32>
 static cudaError_t launch_mode(const FastLaunch& fl, cudaStream_t st) {
-  return fl.npass > 1 ? launch_grid<T, NS, KIND, F32, true>(fl, st)
-                      : launch_grid<T, NS, KIND, F32, false>(fl, st);
+  return fl.multi ? launch_grid<T, NS, KIND, F32, true>(fl, st)
+                  : launch_grid<T, NS, KIND, F32, false>(fl, st);
 }
 
 template <int T, int NS>

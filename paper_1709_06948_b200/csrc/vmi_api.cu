@@ -166,7 +166,7 @@ size_t max_table_cap(const vmi_ctx* c, bool multi) {
 // walked once per pose, so a single-pass table is sized for a ~40% load at
 // scan B's expected occupancy rather than filling shared memory; when even a
 // full table cannot hold it, the multi-pass layout (bigger table) is used.
-void plan_table(const vmi_ctx* c, int* cap_out, int* npass_out) {
+void plan_table(const vmi_ctx* c, int* cap_out, int* npass_out, int* multi_out) {
   static const double factor = [] {
     const char* e = std::getenv("VMI_CAP_FACTOR");  // experiments only
     return e ? std::atof(e) : 2.5;
@@ -179,6 +179,7 @@ void plan_table(const vmi_ctx* c, int* cap_out, int* npass_out) {
                        : std::max(1, (int)std::ceil(est / (0.70 * c->cap_override)));
     *cap_out = (int)std::min((size_t)c->cap_override, max_table_cap(c, np > 1));
     *npass_out = np;
+    *multi_out = np > 1;
     return;
   }
   const size_t cap1 = max_table_cap(c, false);
@@ -187,13 +188,17 @@ void plan_table(const vmi_ctx* c, int* cap_out, int* npass_out) {
     if (want < 2048) want = 2048;
     *cap_out = (int)std::min(cap1, want);
     *npass_out = 1;
+    *multi_out = 0;
     return;
   }
+  // multi-pass layout: as many passes as keep each partition at <= 70 % load
+  // (one pass when scan B fits the bigger table)
   const size_t capm = max_table_cap(c, true);
   *cap_out = (int)capm;
+  *multi_out = 1;
   *npass_out = c->npass_override > 1
                    ? c->npass_override
-                   : std::min(64, std::max(2, (int)std::ceil(est / (0.70 * (double)capm))));
+                   : std::min(64, std::max(1, (int)std::ceil(est / (0.70 * (double)capm))));
 }
 
 int ensure_sums(vmi_ctx* c, int grid, int cap) {
@@ -299,7 +304,7 @@ int launch_fast_eval(vmi_ctx* c, const double* mats_dev, int64_t P, double* mi, 
   fl.P = P;
   fl.grid = (int)(P < c->sm_count ? P : c->sm_count);
   fl.streams = c->streams;
-  plan_table(c, &fl.cap, &fl.npass);
+  plan_table(c, &fl.cap, &fl.npass, &fl.multi);
   int rc = ensure_sums(c, fl.grid, fl.cap);
   if (rc) return rc;
   fl.sums = c->d_sums;
@@ -728,7 +733,7 @@ int vmi_fast_features(vmi_ctx* c, const double mat[12], int64_t* keys, double* v
   fl.B = query_view(c);
   fl.mats = c->d_mats;
   fl.P = 1;
-  plan_table(c, &fl.cap, &fl.npass);
+  plan_table(c, &fl.cap, &fl.npass, &fl.multi);
   fl.grid = 1;
   fl.streams = c->streams;
   if ((rc = ensure_sums(c, 1, fl.cap))) return rc;

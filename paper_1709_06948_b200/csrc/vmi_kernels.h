@@ -31,6 +31,7 @@ struct FastLaunch {
   int streams = 1;   // spans per thread: 1 (CTA = B.threads) or 2 (CTA = B.threads / 2)
   double2* sums = nullptr;  // VARZ: grid * cap (S1, S2) scratch, L2-resident
   int npass = 1;            // hash partitions of the voxel space (table capacity)
+  int multi = 0;            // multi-pass layout (4-byte slots, counts in L2), any npass
 };
 size_t fast_smem_bytes(int kind, int cap, int bins, int threads, int f32, int ns, int multi);
 int fast_slot_bytes(int kind, int multi);  // shared-memory bytes per table slot
