@@ -100,6 +100,15 @@ int vmi_poses_to_mats(const double* poses, int64_t n, double* mats, int threads)
 int vmi_eval(vmi_ctx* ctx, const double* mats, int64_t P, double* mi_out, int32_t* status_out,
              int64_t* hist_out, int64_t* total_out);
 
+/* vmi_eval from poses: P x 6 float64 (tx, ty, tz, roll, pitch, yaw), the
+   reference's EulerPose fields (geometry.py:68-102).  The pose -> matrix step
+   (euler_to_transform, geometry.py:126-138, glibc sin/cos) runs on the host
+   and is overlapped with the GPU: the first poses are launched while the rest
+   are converted and uploaded (pinned staging, second stream).  Results are
+   identical to vmi_poses_to_mats + vmi_eval.  Synchronous. */
+int vmi_eval_poses(vmi_ctx* ctx, const double* poses, int64_t P, double* mi_out,
+                   int32_t* status_out, int64_t* hist_out, int64_t* total_out);
+
 /* Same with device pointers on a caller stream (cudaStream_t as void*);
    asynchronous: no host sync, no fix-up pass (see vmi_eval_fixups). */
 int vmi_eval_device(vmi_ctx* ctx, const double* mats_dev, int64_t P, double* mi_dev,

@@ -26,7 +26,7 @@ EXPORTS = (
     "vmi_create", "vmi_destroy", "vmi_last_error", "vmi_version", "vmi_set_params",
     "vmi_set_reference_points", "vmi_set_reference_features", "vmi_get_reference_features",
     "vmi_set_query_points", "vmi_set_query_records_f32", "vmi_poses_to_mats", "vmi_eval",
-    "vmi_eval_device", "vmi_eval_fixups", "vmi_eval_exact", "vmi_query_features",
+    "vmi_eval_poses", "vmi_eval_device", "vmi_eval_fixups", "vmi_eval_exact", "vmi_query_features",
     "vmi_fast_features",
     "vmi_argmax_device", "vmi_topk_device", "vmi_launch_count", "vmi_set_tuning", "vmi_set_passes",
 )
@@ -70,6 +70,7 @@ def load(path: str = LIB_PATH):
     L.vmi_set_query_records_f32.argtypes = [_ctx, _f, ctypes.c_int64]
     L.vmi_poses_to_mats.argtypes = [_d, ctypes.c_int64, _d, ctypes.c_int]
     L.vmi_eval.argtypes = [_ctx, _d, ctypes.c_int64, _d, _i32, _i64, _i64]
+    L.vmi_eval_poses.argtypes = [_ctx, _d, ctypes.c_int64, _d, _i32, _i64, _i64]
     L.vmi_eval_device.argtypes = [_ctx, _vp, ctypes.c_int64, _vp, _vp, _vp, _vp, _vp]
     L.vmi_eval_fixups.argtypes = [_ctx, _vp, ctypes.c_int64, _vp, _vp, _vp, _vp, _vp, _i64]
     L.vmi_eval_exact.argtypes = [_ctx, _d, ctypes.c_int64, _d, _i32, _i64, _i64]
@@ -204,6 +205,20 @@ class Context:
         fn = self._L.vmi_eval_exact if exact else self._L.vmi_eval
         self.check(fn(self._h, ptr(mats, _d), P, ptr(mi, _d), ptr(st, _i32),
                       ptr(hist, _i64) if want_hist else None, ptr(total, _i64)), "vmi_eval")
+        return mi, st, hist, total
+
+    def eval_poses(self, poses: np.ndarray, want_hist: bool = False, bins: int = 32):
+        """vmi_eval_poses: (P, 6) EulerPose rows in, host pose->matrix overlapped
+        with the GPU (same results as poses_to_mats + eval)."""
+        poses = np.ascontiguousarray(poses, dtype=np.float64).reshape(-1, 6)
+        P = poses.shape[0]
+        mi = np.empty(P, dtype=np.float64)
+        st = np.empty(P, dtype=np.int32)
+        total = np.empty(P, dtype=np.int64)
+        hist = np.empty((P, bins + 1, bins + 1), dtype=np.int64) if want_hist else None
+        self.check(self._L.vmi_eval_poses(self._h, ptr(poses, _d), P, ptr(mi, _d), ptr(st, _i32),
+                                          ptr(hist, _i64) if want_hist else None, ptr(total, _i64)),
+                   "vmi_eval_poses")
         return mi, st, hist, total
 
     def eval_device(self, mats_ptr: int, P: int, mi_ptr: int, st_ptr: int, stream: int = 0,

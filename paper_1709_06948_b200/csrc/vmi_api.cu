@@ -64,6 +64,10 @@ struct vmi_ctx {
   ExactScratch ex;
 
   // host-API staging
+  cudaStream_t copy_stream = nullptr;  // vmi_eval_poses: tail-chunk upload beside the head kernel
+  cudaEvent_t copy_done = nullptr;
+  double* h_mats = nullptr;  // pinned pose matrices (vmi_eval_poses), grow-only
+  int64_t h_mats_cap = 0;
   double* d_mats = nullptr;
   double* d_mi = nullptr;
   int32_t* d_status = nullptr;
@@ -382,6 +386,9 @@ int vmi_destroy(vmi_ctx* c) {
   cudaFree(c->d_mats); cudaFree(c->d_mi); cudaFree(c->d_status); cudaFree(c->d_hist);
   cudaFree(c->d_total); cudaFree(c->d_best); cudaFree(c->d_best_idx); cudaFree(c->d_sums);
   cudaFree(c->d_tk_keys); cudaFree(c->d_tk_idx); cudaFree(c->d_tk_out); cudaFree(c->d_tk_tmp);
+  if (c->h_mats) cudaFreeHost(c->h_mats);
+  if (c->copy_done) cudaEventDestroy(c->copy_done);
+  if (c->copy_stream) cudaStreamDestroy(c->copy_stream);
   cudaStreamDestroy(c->stream);
   delete c;
   return 0;
@@ -653,6 +660,63 @@ int vmi_eval(vmi_ctx* c, const double* mats, int64_t P, double* mi_out, int32_t*
     const int W = c->g.bins + 1;
     CK(c, cudaMemcpyAsync(hist_out, dh, (size_t)P * W * W * 8, cudaMemcpyDeviceToHost, c->stream));
   }
+  if (total_out) CK(c, cudaMemcpyAsync(total_out, c->d_total, P * 8, cudaMemcpyDeviceToHost, c->stream));
+  CK(c, cudaStreamSynchronize(c->stream));
+  return 0;
+}
+
+extern "C" int vmi_poses_to_mats(const double* poses, int64_t n, double* mats, int threads);
+
+// Poses in, MI out, with the host work hidden behind the GPU: the first
+// `head` poses are converted (glibc sin/cos, pose_host.cpp) into pinned
+// memory, uploaded and launched; the host converts the rest while that kernel
+// runs, and their upload runs on a second stream beside it.  Same results as
+// vmi_poses_to_mats + vmi_eval.
+int vmi_eval_poses(vmi_ctx* c, const double* poses, int64_t P, double* mi_out, int32_t* status_out,
+                   int64_t* hist_out, int64_t* total_out) {
+  int rc = check_ready(c);
+  if (rc) return rc;
+  if (P < 0 || (P > 0 && (!poses || !mi_out || !status_out))) return fail(c, VMI_ERR_ARG, "bad arguments");
+  if (P == 0) return 0;
+  cudaSetDevice(c->device);
+  if ((rc = ensure_P(c, P, hist_out != nullptr))) return rc;
+  if (P > c->h_mats_cap) {
+    if (c->h_mats) cudaFreeHost(c->h_mats);
+    c->h_mats = nullptr;
+    c->h_mats_cap = 0;
+    CK(c, cudaMallocHost(&c->h_mats, (size_t)P * 96));
+    c->h_mats_cap = P;
+  }
+  if (!c->copy_stream) CK(c, cudaStreamCreateWithFlags(&c->copy_stream, cudaStreamNonBlocking));
+  if (!c->copy_done) CK(c, cudaEventCreateWithFlags(&c->copy_done, cudaEventDisableTiming));
+  const int W = c->g.bins + 1;
+  long long* dh = hist_out ? c->d_hist : nullptr;
+  // head: long enough for its kernel (~0.5 us/pose at C2) to cover the host
+  // conversion of the rest (~25 ns/pose on one thread, less with threads)
+  const int64_t head = P < 8192 ? P : std::max<int64_t>(2048, P / 16);
+  if (vmi_poses_to_mats(poses, head, c->h_mats, 0)) return fail(c, VMI_ERR_ARG, "poses_to_mats");
+  CK(c, cudaMemcpyAsync(c->d_mats, c->h_mats, head * 96, cudaMemcpyHostToDevice, c->stream));
+  if ((rc = launch_fast_eval(c, c->d_mats, head, c->d_mi, c->d_status, dh, c->d_total, c->stream))) return rc;
+  if (P > head) {
+    const int64_t n = P - head;
+    if (vmi_poses_to_mats(poses + 6 * head, n, c->h_mats + 12 * head, 0)) {
+      cudaStreamSynchronize(c->stream);
+      return fail(c, VMI_ERR_ARG, "poses_to_mats");
+    }
+    CK(c, cudaMemcpyAsync(c->d_mats + 12 * head, c->h_mats + 12 * head, n * 96,
+                          cudaMemcpyHostToDevice, c->copy_stream));
+    CK(c, cudaEventRecord(c->copy_done, c->copy_stream));
+    CK(c, cudaStreamWaitEvent(c->stream, c->copy_done, 0));
+    if ((rc = launch_fast_eval(c, c->d_mats + 12 * head, n, c->d_mi + head, c->d_status + head,
+                               dh ? dh + (size_t)head * W * W : nullptr, c->d_total + head,
+                               c->stream)))
+      return rc;
+  }
+  if ((rc = do_fixups(c, c->d_mats, P, c->d_mi, c->d_status, dh, c->d_total, c->stream, nullptr))) return rc;
+  CK(c, cudaMemcpyAsync(mi_out, c->d_mi, P * 8, cudaMemcpyDeviceToHost, c->stream));
+  CK(c, cudaMemcpyAsync(status_out, c->d_status, P * 4, cudaMemcpyDeviceToHost, c->stream));
+  if (hist_out)
+    CK(c, cudaMemcpyAsync(hist_out, dh, (size_t)P * W * W * 8, cudaMemcpyDeviceToHost, c->stream));
   if (total_out) CK(c, cudaMemcpyAsync(total_out, c->d_total, P * 8, cudaMemcpyDeviceToHost, c->stream));
   CK(c, cudaStreamSynchronize(c->stream));
   return 0;

@@ -133,8 +133,12 @@ class MIEngine:
     def evaluate(self, poses, histograms: bool = False, exact: bool = False):
         """Score P poses.  Returns (mi[P], status[P]) or, with histograms=True,
         (mi, status, counts[P, B+1, B+1], total[P])."""
-        mats = self.mats(poses)
-        mi, st, hist, total = self.ctx.eval(mats, want_hist=histograms, bins=self.bins, exact=exact)
+        if exact:
+            mi, st, hist, total = self.ctx.eval(self.mats(poses), want_hist=histograms,
+                                                bins=self.bins, exact=True)
+        else:  # pose -> matrix on the host, overlapped with the GPU (vmi_eval_poses)
+            mi, st, hist, total = self.ctx.eval_poses(as_pose_array(poses), want_hist=histograms,
+                                                      bins=self.bins)
         if histograms:
             return mi, st, hist, total
         return mi, st

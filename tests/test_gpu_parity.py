@@ -531,3 +531,30 @@ def test_general_resolution_near_integer_quotients(res, kind):
             inside = ((ijk >= lo) & (ijk <= hi)).all(axis=1)
             np.testing.assert_array_equal(keys, fb.keys[inside])
             np.testing.assert_array_equal(vals, fb.values[inside])
+
+
+def test_eval_poses_two_chunk_pipeline_equals_eval():
+    """vmi_eval_poses (host pose->matrix overlapped with a head launch, tail
+    uploaded on a second stream) returns exactly what vmi_poses_to_mats +
+    vmi_eval return, histograms included, across the head/tail split."""
+    rng = np.random.default_rng(5)
+    a = rng.uniform(-15, 15, size=(6000, 3))
+    a[:, 2] = rng.uniform(0, 2, size=6000)
+    b = (a + rng.normal(0, 0.05, size=a.shape)).astype(np.float32).astype(np.float64)
+    eng = engine(1.0, kind="varz")
+    eng.set_reference(a)
+    eng.set_query(b)
+    from paper_1709_06948_b200.synth import candidate_batch
+    poses = candidate_batch(EulerPose(), 20000, seed=3,
+                            half_width=(2.0, 2.0, 0.2, 0.02, 0.02, 0.3))
+    mi, st, hist, total = eng.evaluate(poses, histograms=True)  # vmi_eval_poses
+    mi2, st2, hist2, total2 = eng.ctx.eval(vmi.poses_to_mats(poses), want_hist=True, bins=32)
+    np.testing.assert_array_equal(st, st2)
+    np.testing.assert_array_equal(mi, mi2)
+    np.testing.assert_array_equal(hist, hist2)
+    np.testing.assert_array_equal(total, total2)
+    for k in (0, 2047, 2048, 19999):  # both sides of the head (2048 poses) and the ends
+        omi, ost, ohist, ototal = oracle.mi_objective_full(
+            oracle.feature_map(a, (0, 0, 0), 1.0, "varz"), b, vmi.poses_to_mats(poses[k:k + 1])[0])
+        assert st[k] == ost
+        np.testing.assert_array_equal(hist[k], ohist)
