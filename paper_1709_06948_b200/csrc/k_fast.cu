@@ -336,12 +336,18 @@ __global__ void __launch_bounds__(THREADS, 1)
       count_lut[n] = (uint8_t)feature_bin((double)n, g.clamp, g.bins);
   const double bin_scale = (double)g.bins / g.clamp;
 
+  // the next pose's matrix is loaded one pose ahead (its L2 latency hides
+  // behind the current pose instead of stalling the whole CTA at pose start)
+  double mat_next = (tid < 12 && blockIdx.x < P) ? mats[(int64_t)blockIdx.x * 12 + tid] : 0.0;
   for (int64_t p = blockIdx.x; p < P; p += gridDim.x) {
     for (int i = tid; i < W * W; i += THREADS) hist[i] = 0u;
     for (int i = tid; i < W; i += THREADS) marg[i] = 0u;
     if (tid < 3) { misc[tid] = INT_MAX; misc[3 + tid] = INT_MIN; }
     if (tid >= 6 && tid < 9) misc[tid] = 0;
-    if (tid < 12) mat_s[tid] = mats[p * 12 + tid];
+    if (tid < 12) {
+      mat_s[tid] = mat_next;
+      if (p + gridDim.x < P) mat_next = mats[(p + gridDim.x) * 12 + tid];
+    }
     __syncthreads();
     const double m0 = mat_s[0], m1 = mat_s[1], m2 = mat_s[2], m3 = mat_s[3], m4 = mat_s[4],
                  m5 = mat_s[5], m6 = mat_s[6], m7 = mat_s[7], m8 = mat_s[8], t0 = mat_s[9],

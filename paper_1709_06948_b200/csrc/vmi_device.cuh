@@ -211,8 +211,12 @@ __device__ MIOut finalize_mi(uint32_t* hist, const uint32_t* marg, int W, long l
     if (lane == 0) (is_row ? rows : cols)[x - o] = v;
   }
   __syncthreads();
-  long long total = 0;
-  for (int a = 0; a < m; ++a) total += rows[a];
+  // total = sum of the row marginals: every warp reduces the (<= 65) rows
+  // itself (two per lane, one shuffle tree) instead of a 33-deep serial chain
+  long long total = (lane < m ? rows[lane] : 0LL) + (lane + 32 < m ? rows[lane + 32] : 0LL) +
+                    (lane + 64 < m ? rows[lane + 64] : 0LL);
+#pragma unroll
+  for (int off = 16; off > 0; off >>= 1) total += __shfl_xor_sync(0xffffffffu, total, off);
   MIOut out;
   out.h00 = h00;
   if (total <= 0) {  // entropy of an all-zero block raises -> sentinel (mi.py:215-219)
@@ -239,8 +243,13 @@ __device__ MIOut finalize_mi(uint32_t* hist, const uint32_t* marg, int W, long l
   sxy = warp_sum(sxy);
   if (lane == 0) { red[wid] = sx; red[NW + wid] = sy; red[2 * NW + wid] = sxy; }
   __syncthreads();
-  double hx = 0.0, hy = 0.0, hxy = 0.0;
-  for (int w = 0; w < NW; ++w) { hx += red[w]; hy += red[NW + w]; hxy += red[2 * NW + w]; }
+  // per-warp partials -> totals by one fixed-order shuffle tree (deterministic)
+  static_assert(NW <= 32, "one partial per lane");
+  double hx = lane < NW ? red[lane] : 0.0, hy = lane < NW ? red[NW + lane] : 0.0,
+         hxy = lane < NW ? red[2 * NW + lane] : 0.0;
+  hx = warp_sum(hx);
+  hy = warp_sum(hy);
+  hxy = warp_sum(hxy);
   hx = -hx; hy = -hy; hxy = -hxy;
   double mi = hx + hy - hxy;
   if (mi >= -1e-12 && mi < 0.0) mi = 0.0;  // mi.py:189-190
