@@ -48,6 +48,9 @@ __device__ __forceinline__ uint32_t slot_of(uint32_t lin, uint32_t cap) {
 // push with an S-record cp.async ring (two push groups in flight).  Multi-pass
 // (large grids): shared memory goes to the table instead (more capacity =
 // fewer passes), so one point per push and a 4-record ring.
+#ifndef VMI_MAT_PREFETCH  // A/B switch: pose matrices loaded one pose ahead
+#define VMI_MAT_PREFETCH 1
+#endif
 #ifndef VMI_NEAR_FIX  // 0: teeth check of the near-integer test only (wrong floors)
 #define VMI_NEAR_FIX 1
 #endif
@@ -345,8 +348,13 @@ __global__ void __launch_bounds__(THREADS, 1)
     if (tid < 3) { misc[tid] = INT_MAX; misc[3 + tid] = INT_MIN; }
     if (tid >= 6 && tid < 9) misc[tid] = 0;
     if (tid < 12) {
+#if VMI_MAT_PREFETCH
       mat_s[tid] = mat_next;
       if (p + gridDim.x < P) mat_next = mats[(p + gridDim.x) * 12 + tid];
+#else
+      mat_s[tid] = mats[p * 12 + tid];
+      (void)mat_next;
+#endif
     }
     __syncthreads();
     const double m0 = mat_s[0], m1 = mat_s[1], m2 = mat_s[2], m3 = mat_s[3], m4 = mat_s[4],
