@@ -197,12 +197,20 @@ void plan_table(const vmi_ctx* c, int* cap_out, int* npass_out, int* multi_out) 
   }
   // multi-pass layout: as many passes as keep each partition at <= 70 % load
   // (one pass when scan B fits the bigger table)
+  static const double factor_m = [] {
+    const char* e = std::getenv("VMI_CAPM_FACTOR");  // experiments only
+    // C4 (A/B): 1.4 -> 91.4 ms, 1.5 -> 93.8, 1.6 -> 95.4, full table -> 96.3;
+    // 1.2 overflows on some poses (exact-path fix-ups)
+    return e ? std::atof(e) : 1.4;
+  }();
   const size_t capm = max_table_cap(c, true);
   *cap_out = (int)capm;
   *multi_out = 1;
   *npass_out = c->npass_override > 1
                    ? c->npass_override
                    : std::min(64, std::max(1, (int)std::ceil(est / (0.70 * (double)capm))));
+  if (*npass_out == 1 && factor_m > 0.0)  // a smaller L2 scratch (grid * cap * 20 B)
+    *cap_out = (int)std::min(capm, (((size_t)(factor_m * est) + 31) & ~size_t(31)));
 }
 
 int ensure_sums(vmi_ctx* c, int grid, int cap) {
