@@ -6,7 +6,9 @@
 // -ffp-contract=off (see build.py) and calls glibc's sin/cos, so every entry
 // is bit-identical; CUDA's device sin/cos carry no such guarantee, which is
 // why this O(P) step stays on the host.
+#include <algorithm>
 #include <cmath>
+#include <cstdlib>
 #include <cstdint>
 #include <thread>
 #include <vector>
@@ -35,7 +37,12 @@ extern "C" int vmi_poses_to_mats(const double* poses, int64_t n, double* mats, i
     }
   };
   int hw = (int)std::thread::hardware_concurrency();
-  if (threads <= 0) threads = hw > 0 ? hw : 1;
+  if (threads <= 0) {
+    // one process per GPU (torchrun): share the host cores between the local ranks
+    const char* lws = std::getenv("LOCAL_WORLD_SIZE");
+    const int ranks = lws ? std::max(1, std::atoi(lws)) : 1;
+    threads = hw > 0 ? std::max(1, hw / ranks) : 1;
+  }
   if (n < 4096 || threads == 1) {
     work(0, n);
     return 0;
