@@ -48,6 +48,15 @@ __device__ __forceinline__ uint32_t slot_of(uint32_t lin, uint32_t cap) {
 // push with an S-record cp.async ring (two push groups in flight).  Multi-pass
 // (large grids): shared memory goes to the table instead (more capacity =
 // fewer passes), so one point per push and a 4-record ring.
+// VARZ walk: compaction ring entries (loads in flight per lane = ring / 64).
+// A/B: single-pass C2 512 -> 28.87 ms, 256 -> 28.97, 128 -> 29.34; multi-layout
+// C4 128 -> 87.3 ms, 256 -> 91.9, 512 -> 97.2.
+#ifndef VMI_WALK_RING
+#define VMI_WALK_RING 512
+#endif
+#ifndef VMI_WALK_RING_M
+#define VMI_WALK_RING_M 128
+#endif
 #ifndef VMI_MAT_PREFETCH  // A/B switch: pose matrices loaded one pose ahead
 #define VMI_MAT_PREFETCH 1
 #endif
@@ -737,7 +746,7 @@ __global__ void __launch_bounds__(THREADS, 1)
         // load round (the whole CTA is in this phase at once: nothing else
         // hides the latency).  A/B: -3 % kernel time at C2.
         constexpr int NW = THREADS / 32;
-        constexpr int kWR = 256;  // ring entries; kWU ballots per scan step / entries per lane
+        constexpr int kWR = MULTI ? VMI_WALK_RING_M : VMI_WALK_RING;  // ring entries; kWU ballots per scan step / entries per lane
         constexpr int kWU = kWR / 64;
         static_assert(kStages<F32, MULTI>() * NS * (F32 ? 16 : 32) * 32 >= kWR * 4,
                       "walk ring fits the warp's staging slice");
