@@ -66,12 +66,21 @@ __device__ __forceinline__ uint32_t slot_of(uint32_t lin, uint32_t cap) {
 #ifndef VMI_STAGES
 #define VMI_STAGES 6  // cp.async ring: 6 records in flight per thread (2 push groups)
 #endif
+// multi-pass layout: ring depth / points per push.  A/B (C4, 1 point per
+// push): 2 stages 80.4 ms, 3 stages 90.2, 4 stages 87.7; 2 points per push
+// (4 stages) 107.3, 3 points (6 stages) 109.1.
+#ifndef VMI_STAGESM
+#define VMI_STAGESM 2
+#endif
+#ifndef VMI_PGM
+#define VMI_PGM 1
+#endif
 #ifndef VMI_STAGES64
 #define VMI_STAGES64 2  // double records: a small ring leaves room for the table (A/B: C1)
 #endif
 template <bool F32, bool MULTI = false>
 __host__ __device__ constexpr int kStages() {
-  return MULTI ? 4 : (F32 ? VMI_STAGES : VMI_STAGES64);
+  return MULTI ? VMI_STAGESM : (F32 ? VMI_STAGES : VMI_STAGES64);
 }
 template <typename Rec>
 __device__ __forceinline__ void cp_async_rec(uint32_t dst, const Rec* src) {
@@ -156,7 +165,7 @@ struct VarzTable {
 #endif
 template <bool F32, bool MULTI>
 __host__ __device__ constexpr int kPGt() {  // points per queue push
-  return MULTI ? 1 : (F32 ? VMI_PG : VMI_PG64);
+  return MULTI ? VMI_PGM : (F32 ? VMI_PG : VMI_PG64);
 }
 template <bool F32, bool MULTI>
 __host__ __device__ constexpr int kQueueT() {  // warp queue entries: > 32*kPG + 31, pow2
