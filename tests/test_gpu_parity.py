@@ -558,3 +558,32 @@ def test_eval_poses_two_chunk_pipeline_equals_eval():
             oracle.feature_map(a, (0, 0, 0), 1.0, "varz"), b, vmi.poses_to_mats(poses[k:k + 1])[0])
         assert st[k] == ost
         np.testing.assert_array_equal(hist[k], ohist)
+
+
+@pytest.mark.parametrize("kind", ["varz", "count"])
+@pytest.mark.parametrize("nb", [1, 2, 31, 511, 512, 513, 1024, 1543, 3073])
+def test_ragged_query_sizes_match_oracle(nb, kind):
+    """Scan-B sizes around the span layout's row of 512 spans (n = 512*(span-1)
+    + rem, 0 < rem <= 512): fewer points than spans (no full row: only the
+    leftover path runs), exactly one row, one past it, and sizes whose full
+    rows end mid-ring / mid-push-group.  Every pose must equal the oracle
+    bit for bit (status, histogram, region total) and MI within 1e-6."""
+    a = small_case("s0")["a"] if kind == "varz" else small_case("s1")["a"]
+    res = 1.0 if kind == "varz" else 0.5
+    rng = np.random.default_rng(nb)
+    b = a[rng.permutation(a.shape[0])[:nb]] + rng.normal(0, 0.02, size=(nb, 3))
+    eng = engine(res, kind=kind)
+    eng.set_reference(a)
+    eng.set_query(b)
+    poses = np.array([[0.0, 0.0, 0.0, 0.0, 0.0, 0.0], [0.4, -0.3, 0.05, 0.01, -0.02, 0.1],
+                      [-1.5, 2.0, 0.0, 0.0, 0.0, -0.3], [3.0, 0.0, 0.2, 0.05, 0.0, 0.0]])
+    mats = vmi.poses_to_mats(poses)
+    mi, st, hist, total = eng.evaluate(poses, histograms=True)
+    fa = oracle.feature_map(a, (0, 0, 0), res, kind)
+    for i in range(len(poses)):
+        omi, ost, ohist, ototal = oracle.mi_objective_full(fa, b, mats[i], res=res)
+        assert st[i] == ost
+        if ost in (0, 3):
+            np.testing.assert_array_equal(hist[i], ohist)
+            assert total[i] == ototal
+        assert_mi_close([mi[i]], [omi])
