@@ -52,7 +52,8 @@ def parse():
     ap.add_argument("--e2e-steps", type=int, default=3)
     ap.add_argument("--config", default="c2", choices=["c1", "c2", "c3", "c4", "c5"],
                     help="SURVEY.md 8(d) workload (c2 = the headline)")
-    ap.add_argument("--frames", type=int, default=24, help="c5: frames in the synthetic drive")
+    ap.add_argument("--frames", type=int, default=1001,
+                    help="c5: frames in the synthetic drive (1001 frames = the 1000-pair sequence)")
     ap.add_argument("--c5-mode", default="grid", choices=["grid", "nm"],
                     help="c5: 4,096-pose grid search per pair, or align() (batched "
                          "Nelder-Mead, reference-identical decisions) from the prior")
@@ -439,9 +440,13 @@ def run_c5(args, world, rank, local):
     from paper_1709_06948_b200.synth import drive_sequence, grid_poses, relative_pose
     local = local % max(1, torch.cuda.device_count())
     torch.cuda.set_device(local)
-    scans, world_poses = drive_sequence(args.frames)
-    pairs = list(range(len(scans) - 1))
+    # each rank builds only the frames of its pair shard (frame generation is
+    # host work outside the timed region; spawned processes, cores shared by ranks)
+    n_frames = args.frames
+    pairs = list(range(n_frames - 1))
     lo, hi = shard_bounds(len(pairs), world, rank)
+    gen_workers = max(1, (os.cpu_count() or 1) // int(os.environ.get("LOCAL_WORLD_SIZE", "1")))
+    scans, world_poses = drive_sequence(n_frames, workers=min(32, gen_workers), subset=(lo, hi + 1))
     rng = np.random.default_rng(5)
     priors, truths = [], []
     for i in pairs:
@@ -505,7 +510,7 @@ def run_c5(args, world, rank, local):
             "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
             "ms_per_step": 1e3 * dt / args.steps, "higher_is_better": True, "scaling": "strong",
             "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-            "config": {"workload": f"C5: {len(scans)}-frame synthetic drive (HDL-64-shaped "
+            "config": {"workload": f"C5: {n_frames}-frame synthetic drive (HDL-64-shaped "
                                    "120k-point scans ~1 m apart), consecutive pairs, 1 m VARZ; per "
                                    "pair: GPU A-grid build + 16x16x16 (tx, ty, yaw) grid around a "
                                    "prior perturbed by 0.5 m / 1 deg",

@@ -198,14 +198,22 @@ def grid_poses(center, axes: dict[str, np.ndarray]) -> np.ndarray:
     return np.stack([m.ravel() for m in mesh], axis=1)
 
 
+def _frame_job(job):
+    spec, near, pose, seed, i = job
+    return scan_from(spec, near, pose, np.random.default_rng([seed, 1000 + i]))
+
+
 def drive_sequence(n_frames: int, spec: LidarSceneSpec = LidarSceneSpec(), seed: int = 0,
-                   step: float = 1.0) -> tuple[list[np.ndarray], list[EulerPose]]:
+                   step: float = 1.0, workers: int = 1,
+                   subset: tuple[int, int] | None = None) -> tuple[list, list[EulerPose]]:
     """C5: a synthetic drive, ``n_frames`` HDL-64-shaped scans ~``step`` m apart.
 
     The sensor follows the road (x axis) with a slow lateral / yaw drift
     through a corridor of boxes; returns the scans (float32 records, each in
     its own sensor frame) and the world sensor poses (planar).  The relative
     pose mapping frame i+1 into frame i is ``relative_pose(poses[i], poses[i+1])``.
+    ``workers`` > 1 builds the frames in that many spawned processes (same scans);
+    ``subset=(lo, hi)`` builds only frames lo..hi-1 (the others are None).
     """
     rng = np.random.default_rng(np.random.SeedSequence(seed).spawn(1)[0])
     length = n_frames * step
@@ -225,10 +233,29 @@ def drive_sequence(n_frames: int, spec: LidarSceneSpec = LidarSceneSpec(), seed:
         x = i * step
         y = 0.6 * math.sin(x / 37.0)
         yaw = 0.03 * math.sin(x / 23.0)
-        pose = EulerPose(x, y, 0.0, 0.0, 0.0, yaw)
+        poses.append(EulerPose(x, y, 0.0, 0.0, 0.0, yaw))
+
+    def frame(i):  # every frame has its own generator: independent of the order
+        x = poses[i].tx
         near = boxes[(np.abs((boxes[:, 0] + boxes[:, 3]) / 2 - x) < spec.max_range + 10.0)]
-        scans.append(scan_from(spec, near, pose, np.random.default_rng([seed, 1000 + i])))
-        poses.append(pose)
+        return scan_from(spec, near, poses[i], np.random.default_rng([seed, 1000 + i]))
+
+    idx = range(*subset) if subset is not None else range(n_frames)
+    if workers > 1 and len(idx) > 1:  # spawned processes (scan_from holds the GIL)
+        import multiprocessing as mp
+        from concurrent.futures import ProcessPoolExecutor
+        jobs = []
+        for i in idx:
+            x = poses[i].tx
+            near = boxes[(np.abs((boxes[:, 0] + boxes[:, 3]) / 2 - x) < spec.max_range + 10.0)]
+            jobs.append((spec, near, poses[i], seed, i))
+        with ProcessPoolExecutor(workers, mp_context=mp.get_context("spawn")) as pool:
+            built = list(pool.map(_frame_job, jobs, chunksize=max(1, len(idx) // (4 * workers))))
+    else:
+        built = [frame(i) for i in idx]
+    scans = [None] * n_frames
+    for i, sc in zip(idx, built):
+        scans[i] = sc
     return scans, poses
 
 
