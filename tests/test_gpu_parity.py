@@ -587,3 +587,20 @@ def test_ragged_query_sizes_match_oracle(nb, kind):
             np.testing.assert_array_equal(hist[i], ohist)
             assert total[i] == ototal
         assert_mi_close([mi[i]], [omi])
+
+
+def test_count_voxel_order_changes_nothing(monkeypatch):
+    """COUNT scans that arrive unordered are regrouped by voxel before upload
+    (engine.MIEngine._voxel_order); every output must be bit-identical to the
+    input-order upload."""
+    c = small_case("s1")  # COUNT, 0.5 m, unordered synthetic scene
+    out = []
+    for flag in ("0", "1"):
+        monkeypatch.setenv("VMI_COUNT_ORDER", flag)
+        eng = engine(c["res"], c["origin"], c["kind"], c["phi"])
+        eng.set_reference(c["a"])
+        eng.set_query(c["b"])
+        out.append(eng.evaluate(c["poses"], histograms=True))
+    for x, y in zip(*out):
+        np.testing.assert_array_equal(x, y)
+    assert_mi_close(out[1][0], c["mi"])
