@@ -83,7 +83,10 @@ int vmi_get_reference_features(vmi_ctx* ctx, int64_t* keys, double* values, int6
                                int64_t* n_out, int64_t bounds[6]);
 
 /* Scan B (PointCloud, geometry.py:36-65): host (n, 3) float64.  Stored as
-   float4 when every coordinate is float32-exact (KITTI input), else double. */
+   float4 when every coordinate is float32-exact (KITTI input), else double.
+   Point order never changes a result; the fused kernel aggregates runs of
+   consecutive points in one voxel, so ring-ordered (or, for COUNT,
+   voxel-grouped) scans run fastest. */
 int vmi_set_query_points(vmi_ctx* ctx, const double* xyz, int64_t n);
 /* Scan B as KITTI .bin records (x, y, z, intensity float32; scan_io.py:57-75). */
 int vmi_set_query_records_f32(vmi_ctx* ctx, const float* xyzi, int64_t n);
