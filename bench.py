@@ -22,6 +22,8 @@ import argparse
 import json
 import math
 import os
+import platform
+import socket
 from dataclasses import dataclass
 import subprocess
 import sys
@@ -57,6 +59,12 @@ def parse():
     ap.add_argument("--c5-mode", default="grid", choices=["grid", "nm"],
                     help="c5: 4,096-pose grid search per pair, or align() (batched "
                          "Nelder-Mead, reference-identical decisions) from the prior")
+    ap.add_argument("--parity-sample", type=int, default=2048,
+                    help="poses of the batch (strided) re-scored by the CPU oracle for the "
+                         "line's `parity` object (0 = skip)")
+    ap.add_argument("--dist-selftest", action="store_true",
+                    help="launch plumbing only (CPU, gloo): ranks exchange synthetic shard "
+                         "winners and rank 0 prints the pick; no GPU work")
     ap.add_argument("--c5-workers", type=int, default=6,
                     help="c5: host threads, each with its own engine/stream, so one pair's "
                          "A-grid build and uploads overlap another pair's pose scoring")
@@ -68,6 +76,109 @@ def dist_env():
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
     return world, rank, local
+
+
+def _free_port() -> int:
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        return s.getsockname()[1]
+
+
+def self_launch(args) -> int | None:
+    """`bench.py --gpus N` outside torchrun: re-exec this command under
+    torch.distributed.run with N local ranks (one per GPU) and return its exit
+    code.  Under torchrun (WORLD_SIZE set) the world must equal --gpus."""
+    if "WORLD_SIZE" in os.environ:
+        world = int(os.environ["WORLD_SIZE"])
+        if world != args.gpus:
+            raise SystemExit(f"bench.py: --gpus {args.gpus} but WORLD_SIZE={world}")
+        return None
+    if args.gpus <= 1:
+        return None
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1",
+           f"--nproc-per-node={args.gpus}", "--master-addr=127.0.0.1",
+           f"--master-port={_free_port()}", os.path.abspath(__file__), *sys.argv[1:]]
+    return subprocess.run(cmd).returncode
+
+
+def init_dist(world: int, local: int):
+    """One process group per run: NCCL over the GPUs (VMI_DIST_BACKEND=gloo for
+    functional checks on fewer GPUs / CPU).  Returns (dist | None, collective device)."""
+    import torch
+    backend = os.environ.get("VMI_DIST_BACKEND", "nccl")
+    if world <= 1:
+        return None, "cpu"
+    import torch.distributed as dist
+    if backend == "nccl":
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        return dist, f"cuda:{local}"
+    dist.init_process_group(backend)
+    return dist, "cpu"
+
+
+def exchange_winner(dist, cdev, value: float, index: int):
+    """Per-rank (mi, global index) -> np.argmax's pick over all ranks (the one
+    data-path collective: 8 + 8 bytes per rank, index as int64)."""
+    from paper_1709_06948_b200.shard import all_gather_winner
+    return all_gather_winner(value, index, dist, cdev)
+
+
+def max_over_ranks(dist, cdev, x: float) -> float:
+    if dist is None:
+        return x
+    import torch
+    t = torch.tensor([x], dtype=torch.float64, device=cdev)
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    return float(t.item())
+
+
+def sum_over_ranks(dist, cdev, x: float) -> float:
+    if dist is None:
+        return x
+    import torch
+    t = torch.tensor([x], dtype=torch.float64, device=cdev)
+    dist.all_reduce(t, op=dist.ReduceOp.SUM)
+    return float(t.item())
+
+
+def run_dist_selftest(args, world, rank, local):
+    """CPU check of the N-rank launch: contiguous shards of a synthetic MI
+    vector, one winner exchange, rank 0 prints the pick (tests/test_bench.py)."""
+    from paper_1709_06948_b200.shard import local_winner, shard_bounds
+    os.environ.setdefault("VMI_DIST_BACKEND", "gloo")
+    dist, cdev = init_dist(world, local)
+    mi = np.random.default_rng(3).uniform(0, 1, size=args.poses)
+    lo, hi = shard_bounds(mi.size, world, rank)
+    v, i = local_winner(mi[lo:hi], lo)
+    best, idx = exchange_winner(dist, cdev, v, i) if dist else (v, i)
+    if rank == 0:
+        print(json.dumps({"dist_selftest": True, "n_gpus": world, "best": best, "index": idx,
+                          "want_index": int(np.argmax(mi))}), flush=True)
+    if dist:
+        dist.destroy_process_group()
+
+
+def host_info(cores: int) -> dict:
+    """CPU model, core count, numpy and BLAS build of the host running a CPU
+    baseline (BASELINE.md 2 / SURVEY 8(d))."""
+    model = platform.processor() or "unknown"
+    try:
+        with open("/proc/cpuinfo") as fh:
+            model = next((ln.split(":", 1)[1].strip() for ln in fh if ln.startswith("model name")),
+                         model)
+    except OSError:
+        pass
+    blas = None
+    try:
+        import threadpoolctl
+        b = [x for x in threadpoolctl.threadpool_info() if x.get("user_api") == "blas"]
+        if b:
+            blas = f"{b[0].get('internal_api')} {b[0].get('version')} ({b[0].get('architecture')})"
+    except Exception:
+        pass
+    return {"cpu_model": model, "host_cpus": os.cpu_count(), "threads_used": cores,
+            "numpy": np.__version__, "blas": blas,
+            "oracle_build": "gcc -O2 -ffp-contract=off -fopenmp (oracle/Makefile)"}
 
 
 @dataclass
@@ -193,21 +304,39 @@ def measured_peak():
         return FALLBACK_HBM, "fallback (B200_PROFILING.md)"
 
 
-def profiled_traffic():
-    p = os.path.join(ROOT, "profiles", "roofline_traffic.json")
+def profiled_ceilings(cfg: str):
+    """This config's ncu-derived figures (profiles/ceilings.json, written by
+    tools/make_ceilings.py from that config's own capture), or None."""
+    p = os.path.join(ROOT, "profiles", "ceilings.json")
     try:
         with open(p) as fh:
-            d = json.load(fh)
-        return d
+            return json.load(fh).get(cfg)
     except Exception:
         return None
+
+
+def ceilings(c, value: float, sm_mhz: float | None):
+    """Issue and FP64 ceilings (pose-evals/s) from this config's capture."""
+    if not c:
+        return None, None
+    clk = (sm_mhz or 1965.0) * 1e6
+    issue_rate = 148 * 4 * clk  # warp-instructions/s: 4 schedulers per SM, 1 issue/clk
+    ic = issue_rate / c["warp_inst_per_pose"]
+    fc = c["poses_per_launch"] / (c["ncu_kernel_ms"] * 1e-3 * c["fp64_pipe_active_frac"])
+    issue = {"ceiling": ic, "unit": UNIT, "frac": value / ic,
+             "warp_inst_per_pose": c["warp_inst_per_pose"],
+             "issue_rate": issue_rate, "source": c["source"]}
+    fp64 = {"ceiling": fc, "unit": UNIT, "frac": value / fc,
+            "fp64_pipe_active_frac": c["fp64_pipe_active_frac"], "source": c["source"],
+            "note": "rate if the FP64 pipe (DFMA 62 lanes/clk/SM measured, "
+                    "profiles/r01_microbench_b200.txt) were busy every cycle"}
+    return issue, fp64
 
 
 def cpu_port_baseline(wl: Workload, poses, threads: int, budget_s: float = 15.0):
     """The reference algorithm's CPU port (oracle/, test infrastructure) on a
     bounded sample of the same batch; returns (poses/s, n_poses, cores)."""
     import oracle
-    from paper_1709_06948_b200 import _lib
     fa = oracle.feature_map(wl.a[:, :3].astype(np.float64), (0, 0, 0), wl.res, wl.kind)
     pts = wl.b[:, :3].astype(np.float64)
     cores = threads if threads > 0 else oracle.max_threads()
@@ -215,11 +344,11 @@ def cpu_port_baseline(wl: Workload, poses, threads: int, budget_s: float = 15.0)
     stride = max(1, poses.shape[0] // 4096)
     sample = poses[::stride]
     t0 = time.perf_counter()
-    oracle.mi_objective_batch(fa, pts, _lib.poses_to_mats(sample[:cores]), res=wl.res,
+    oracle.mi_objective_batch(fa, pts, oracle.poses_to_mats(sample[:cores]), res=wl.res,
                               threads=cores)
     per = (time.perf_counter() - t0) / cores
     n = int(min(sample.shape[0], max(cores, budget_s / max(per, 1e-6) * cores)))
-    mats = _lib.poses_to_mats(sample[:n])
+    mats = oracle.poses_to_mats(sample[:n])
     t0 = time.perf_counter()
     oracle.mi_objective_batch(fa, pts, mats, res=wl.res, threads=cores)
     dt = time.perf_counter() - t0
@@ -233,12 +362,11 @@ def run_reference(args, world, rank):
     poses = wl.poses
     import oracle
     cores = oracle.max_threads()
-    from paper_1709_06948_b200 import _lib
     fa = oracle.feature_map(wl.a[:, :3].astype(np.float64), (0, 0, 0), wl.res, wl.kind)
     pts = wl.b[:, :3].astype(np.float64)
     # each step: a bounded, strided sample of the batch (~1-2 s of all-core CPU work)
     t0 = time.perf_counter()
-    oracle.mi_objective_batch(fa, pts, _lib.poses_to_mats(poses[:cores]), res=wl.res,
+    oracle.mi_objective_batch(fa, pts, oracle.poses_to_mats(poses[:cores]), res=wl.res,
                               threads=cores)
     per_pose = (time.perf_counter() - t0) / cores
     n = max(cores, int(1.5 / max(per_pose, 1e-6)) // cores * cores)
@@ -246,7 +374,7 @@ def run_reference(args, world, rank):
     times = []
     for s in range(args.warmup + args.steps):
         sel = poses[(s % stride)::stride][:n]
-        mats = _lib.poses_to_mats(sel)
+        mats = oracle.poses_to_mats(sel)
         t0 = time.perf_counter()
         mi, st = oracle.mi_objective_batch(fa, pts, mats, res=wl.res, threads=cores)
         int(np.argmax(mi))
@@ -261,7 +389,8 @@ def run_reference(args, world, rank):
         "data": "synthetic", "config": config(args, 1, wl, args.poses),
         "cpu_baseline": {"value": value, "unit": UNIT, "cores": cores, "kind": "port",
                          "sample": f"{n} strided poses of the {wl.name.upper()} batch per step, "
-                                   f"OpenMP over {cores} host threads (oracle/voxmi_oracle.c)"},
+                                   f"OpenMP over {cores} host threads (oracle/voxmi_oracle.c)",
+                         "host": host_info(cores)},
         "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line), flush=True)
@@ -271,34 +400,60 @@ def l2_flush(buf):
     buf.fill_(1)
 
 
+def parity_check(eng, wl: Workload, poses, mi_gpu, st_gpu, n: int, n_hist: int = 16):
+    """The CPU oracle (test infrastructure) on a strided sample of this step's
+    batch, against the GPU's MI / status from the timed run: statuses equal,
+    max relative MI error, the sample's argmax identical; histograms bit-exact
+    on the first ``n_hist`` sampled poses."""
+    import oracle
+    P = poses.shape[0]
+    stride = max(1, P // n)
+    sel = np.arange(0, P, stride)[:n]
+    fa = oracle.feature_map(wl.a[:, :3].astype(np.float64), (0, 0, 0), wl.res, wl.kind)
+    pts = wl.b[:, :3].astype(np.float64)
+    mats = oracle.poses_to_mats(poses[sel])
+    t0 = time.perf_counter()
+    omi, ost = oracle.mi_objective_batch(fa, pts, mats, res=wl.res, threads=0)
+    dt = time.perf_counter() - t0
+    g_mi, g_st = mi_gpu[sel], st_gpu[sel] & 0xFF
+    ok = ost == 0
+    rel = np.abs(g_mi[ok] - omi[ok]) / np.maximum(np.abs(omi[ok]), 1e-300)
+    # np.argmax over the sample, GPU side with the library's near-tie re-score
+    k_gpu, _ = eng.best(poses[sel], g_mi)
+    _, h_st, hist, _ = eng.evaluate(poses[sel[:n_hist]], histograms=True)
+    hist_ok = True
+    for j in range(min(n_hist, sel.size)):
+        _, s_o, c_o, _ = oracle.mi_objective_full(fa, pts, mats[j], res=wl.res)
+        hist_ok &= bool(s_o == h_st[j] and np.array_equal(c_o, hist[j]))
+    return {"sample": int(sel.size), "stride": int(stride),
+            "status_equal": bool(np.array_equal(g_st, ost)),
+            "max_rel_mi_err": float(rel.max()) if rel.size else 0.0,
+            "argmax_equal": bool(k_gpu == int(np.argmax(omi))),
+            "hist_bit_exact": f"{min(n_hist, sel.size)} poses: {'yes' if hist_ok else 'NO'}",
+            "oracle_s": round(dt, 2),
+            "checker": "oracle/voxmi_oracle.c (pinned to reference golden vectors)"}
+
+
 def run_ours(args, world, rank, local):
     import torch
     import paper_1709_06948_b200 as vmi
     from paper_1709_06948_b200 import _lib
+    from paper_1709_06948_b200.shard import shard_bounds
 
     # one rank per GPU; VMI_DIST_BACKEND=gloo exercises the N>1 code path on a
     # box with fewer GPUs (functional check only: ranks then share devices)
-    backend = os.environ.get("VMI_DIST_BACKEND", "nccl")
     local = local % max(1, torch.cuda.device_count())
     torch.cuda.set_device(local)
-    dist = None
-    if world > 1:
-        import torch.distributed as dist
-        if backend == "nccl":
-            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
-        else:
-            dist.init_process_group(backend)
-    cdev = f"cuda:{local}" if backend == "nccl" else "cpu"  # collective tensors
+    dist, cdev = init_dist(world, local)
     wl = workload(args.config, world, args.poses)
     a, b, poses_all = wl.a, wl.b, wl.poses
-    from paper_1709_06948_b200.shard import pick_global, shard_bounds
     lo, hi = shard_bounds(poses_all.shape[0], world, rank)
     poses = poses_all[lo:hi]
     P = poses.shape[0]
     eng = vmi.MIEngine(grid=vmi.GridSpec(resolution=wl.res),
                        binning=vmi.BinningSpec(kind=vmi.FeatureKind.from_name(wl.kind)),
                        device=local, threads=args.threads)
-    eng.set_reference(a[:, :3].astype(np.float64))
+    eng.set_reference(a[:, :3].astype(np.float64), fetch=False)
     eng.set_query(b)
     ctx = eng.ctx
 
@@ -316,8 +471,6 @@ def run_ours(args, world, rank, local):
     mi = torch.empty(P, dtype=torch.float64, device=f"cuda:{local}")
     st = torch.empty(P, dtype=torch.int32, device=f"cuda:{local}")
     flush = torch.empty(256 * 1024 * 1024 // 4, dtype=torch.float32, device=f"cuda:{local}")
-    winner = torch.empty(2, dtype=torch.float64, device=cdev)
-    gathered = [torch.empty(2, dtype=torch.float64, device=cdev) for _ in range(world)]
 
     fixups_total = 0
 
@@ -331,13 +484,9 @@ def run_ours(args, world, rank, local):
             ev[1].record(stream)
         fixups_total += ctx.eval_fixups(mats.data_ptr(), P, mi.data_ptr(), st.data_ptr(), stream=s)
         best, idx = ctx.argmax_device(mi.data_ptr(), P, stream=s)
-        if world > 1:
+        if dist is not None:
             with torch.cuda.stream(stream):
-                winner[0] = best
-                winner[1] = float(lo + idx)
-                dist.all_gather(gathered, winner)
-                g = torch.stack(gathered).cpu().numpy()
-            return pick_global(g)
+                return exchange_winner(dist, cdev, best, lo + idx)
         return best, lo + idx
 
     for _ in range(args.warmup):
@@ -362,17 +511,16 @@ def run_ours(args, world, rank, local):
             kern_ms.append(e[0].elapsed_time(e[1]))
     torch.cuda.synchronize()
     launches = ctx.launches - launches0
-    total_ms = float(sum(step_ms))
+    total_ms = max_over_ranks(dist, cdev, float(sum(step_ms)))
     if dist:
-        t = torch.tensor([total_ms], dtype=torch.float64, device=cdev)
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        total_ms = float(t.item())
         dist.barrier()
     n_total = poses_all.shape[0]  # all ranks' poses (shards cover the global list)
     value = n_total * args.steps / (total_ms / 1e3)
+    mi_h = mi.cpu().numpy()
+    st_h = st.cpu().numpy()
 
     # end to end through the public API: host poses in (pose->matrix on host,
-    # H2D), host MI out (D2H), host argmax; wall clock, synchronised.
+    # H2D), host MI out (D2H), host argmax + near-tie re-score (best); max over ranks
     e2e_times = []
     eng.evaluate(poses)  # untimed: first call allocates the host-API staging buffers
     for _ in range(args.e2e_steps):
@@ -380,20 +528,18 @@ def run_ours(args, world, rank, local):
         if dist:
             dist.barrier()
         t0 = time.perf_counter()
-        mi_h, st_h = eng.evaluate(poses)
-        int(np.argmax(mi_h))
+        mi_e, _ = eng.evaluate(poses)
+        eng.best(poses, mi_e)
         e2e_times.append(time.perf_counter() - t0)
-    e2e_s = float(np.mean(e2e_times))
-    if dist:
-        t = torch.tensor([e2e_s], dtype=torch.float64, device=cdev)
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        e2e_s = float(t.item())
+    e2e_s = max_over_ranks(dist, cdev, float(np.mean(e2e_times)))
     e2e_value = n_total / e2e_s
 
     kern_s = float(np.mean(kern_ms)) / 1e3
     achieved = bytes_per_pose * P / kern_s / 1e9
     peak, peak_src = measured_peak()
-    traffic = profiled_traffic()
+    clk = clocks.summary()
+    prof = profiled_ceilings(wl.name)
+    issue_c, fp64_c = ceilings(prof, P / kern_s, clk.get("sm_mhz"))
     line = {
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": total_ms / args.steps, "higher_is_better": True,
@@ -402,25 +548,35 @@ def run_ours(args, world, rank, local):
         "roofline": {
             "bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
             "frac": achieved / peak, "peak_source": peak_src,
-            "traffic": (traffic or {}).get("dram_bytes_per_launch"),
+            "traffic": prof["dram_bytes_per_launch"] if prof else None,
+            "traffic_source": (f"{prof['source']} ({prof['poses_per_launch']} poses per launch)"
+                               if prof else "no ncu capture of this config"),
             "kernel": "k_pose_fast (K1, fused transform/voxelize/aggregate/histogram/MI)",
             "kernel_ms": kern_s * 1e3,
             "algorithmic_bytes_per_pose": bytes_per_pose,
             "mean_vb_in_aabb_a": vb,
             "bytes_formula": f"{int(rec_bytes)}*N_B + |V_B in AABB_A| + 8",
+            "issue_ceiling": issue_c,
+            "fp64_ceiling": fp64_c,
         },
         "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": int(P * 96),
                 "d2h_bytes_per_step": int(P * 12),
-                "path": "MIEngine.evaluate(poses) -> host MI, np.argmax"},
+                "path": "MIEngine.evaluate(host poses P x 6 f64) -> host MI + status, "
+                        "MIEngine.best (np.argmax + near-tie re-score); H2D = the P x 12 f64 "
+                        "pose matrices built on the host (pinned staging), D2H = MI f64 + "
+                        "status i32"},
         "gpu_launches": int(launches),
         "fixups_per_step": fixups_total / args.steps,
-        "clocks": clocks.summary(),
+        "clocks": clk,
     }
+    if rank == 0 and world == 1 and args.parity_sample > 0:
+        line["parity"] = parity_check(eng, wl, poses, mi_h, st_h, args.parity_sample)
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         v, n, cores = cpu_port_baseline(wl, poses, threads=1)
         line["cpu_baseline"] = {"value": v, "unit": UNIT, "cores": cores, "kind": "port",
                                 "sample": f"{n} strided poses of the {wl.name.upper()} batch, "
-                                          "single thread (oracle/voxmi_oracle.c)"}
+                                          "single thread (oracle/voxmi_oracle.c)",
+                                "host": host_info(cores)}
     if rank == 0:
         print(json.dumps(line), flush=True)
     eng.close()
@@ -437,9 +593,10 @@ def run_c5(args, world, rank, local):
     import torch
     import paper_1709_06948_b200 as vmi
     from paper_1709_06948_b200.shard import shard_bounds
-    from paper_1709_06948_b200.synth import drive_sequence, grid_poses, relative_pose
+    from paper_1709_06948_b200.synth import C5_SIMPLEX_STEPS, c5_grid, c5_priors, drive_sequence
     local = local % max(1, torch.cuda.device_count())
     torch.cuda.set_device(local)
+    dist, cdev = init_dist(world, local)
     # each rank builds only the frames of its pair shard (frame generation is
     # host work outside the timed region; spawned processes, cores shared by ranks)
     n_frames = args.frames
@@ -447,16 +604,7 @@ def run_c5(args, world, rank, local):
     lo, hi = shard_bounds(len(pairs), world, rank)
     gen_workers = max(1, (os.cpu_count() or 1) // int(os.environ.get("LOCAL_WORLD_SIZE", "1")))
     scans, world_poses = drive_sequence(n_frames, workers=min(32, gen_workers), subset=(lo, hi + 1))
-    rng = np.random.default_rng(5)
-    priors, truths = [], []
-    for i in pairs:
-        t = relative_pose(world_poses[i], world_poses[i + 1])
-        h = rng.uniform(0, 2 * np.pi)
-        truths.append(t)
-        priors.append(np.array([t.tx + 0.5 * np.cos(h), t.ty + 0.5 * np.sin(h), 0.0, 0.0, 0.0,
-                                t.rz + np.radians(1.0) * (1 if rng.random() < 0.5 else -1)]))
-    offs = np.linspace(-0.75, 0.75, 16)
-    yaw_offs = np.radians(np.linspace(-1.5, 1.5, 16))
+    priors, truths = c5_priors(world_poses)
 
     nm_evals = []
 
@@ -468,11 +616,10 @@ def run_c5(args, world, rank, local):
             from paper_1709_06948_b200.align import exact_objective
             from paper_1709_06948_b200.optim import SimplexConfig, nelder_mead_maximize_batched
             res = nelder_mead_maximize_batched(
-                exact_objective(eng), c,
-                SimplexConfig(initial_steps=(1.0, 1.0, 0.1, 0.01, 0.01, 0.05)))
+                exact_objective(eng), c, SimplexConfig(initial_steps=C5_SIMPLEX_STEPS))
             nm_evals.append(res.n_evaluations)
             return res.best_x
-        poses = grid_poses(c, {"tx": c[0] + offs, "ty": c[1] + offs, "rz": c[5] + yaw_offs})
+        poses = c5_grid(c)
         mi, _ = eng.evaluate(poses)
         k, best = eng.best(poses, mi)
         return poses[k]
@@ -496,6 +643,8 @@ def run_c5(args, world, rank, local):
         for _ in range(max(1, args.warmup)):
             list(pool.map(lambda w: [align_pair(engines[w], i) for i in mine[w::nw][:1]], range(nw)))
         torch.cuda.synchronize()
+        if dist:
+            dist.barrier()
         errs = []
         t0 = time.perf_counter()
         for _ in range(args.steps):
@@ -503,10 +652,14 @@ def run_c5(args, world, rank, local):
                 errs.extend(r)
         torch.cuda.synchronize()
         dt = time.perf_counter() - t0
-    n = (hi - lo) * args.steps
+    # every rank's wall time (max) and pair count (sum): the job's alignments/s
+    dt = max_over_ranks(dist, cdev, dt)
+    n = int(sum_over_ranks(dist, cdev, float((hi - lo) * args.steps)))
+    n_evals = sum_over_ranks(dist, cdev, float(np.sum(nm_evals[-(hi - lo) * args.steps:]))
+                             if nm_evals else 0.0)
     if rank == 0:
         line = {
-            "metric": "scan-pair alignments/sec", "value": n * world / dt, "unit": "alignments/s",
+            "metric": "scan-pair alignments/sec", "value": n / dt, "unit": "alignments/s",
             "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
             "ms_per_step": 1e3 * dt / args.steps, "higher_is_better": True, "scaling": "strong",
             "vs_baseline": None, "dtype": "f64", "data": "synthetic",
@@ -517,8 +670,7 @@ def run_c5(args, world, rank, local):
                        "pairs": len(pairs),
                        "poses_per_pair": 4096 if args.c5_mode == "grid" else "Nelder-Mead",
                        "timing": "wall clock"},
-            "pose_evals_per_s": (n * world * 4096 / dt) if args.c5_mode == "grid"
-                                else float(np.sum(nm_evals[-n:]) * world / dt),
+            "pose_evals_per_s": (n * 4096 / dt) if args.c5_mode == "grid" else n_evals / dt,
             "mode": args.c5_mode,
             "median_translation_error_m": float(np.median(errs)),
             "host_workers": nw,
@@ -526,12 +678,19 @@ def run_c5(args, world, rank, local):
         print(json.dumps(line), flush=True)
     for e in engines:
         e.close()
+    if dist:
+        dist.destroy_process_group()
 
 
 def main():
     args = parse()
+    rc = self_launch(args)
+    if rc is not None:  # --gpus N outside torchrun: the ranks ran as children
+        sys.exit(rc)
     world, rank, local = dist_env()
-    if args.config == "c5" and args.impl != "reference":
+    if args.dist_selftest:
+        run_dist_selftest(args, world, rank, local)
+    elif args.config == "c5" and args.impl != "reference":
         run_c5(args, world, rank, local)
     elif args.impl == "reference":
         run_reference(args, world, rank)

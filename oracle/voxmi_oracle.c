@@ -329,13 +329,15 @@ double orc_mi_objective(const int64_t* ka, const double* va, int64_t na, const i
   return result;
 }
 
-/* Batch driver over P pose matrices; nthreads <= 0 means all (OpenMP). */
+/* Batch driver over P pose matrices; nthreads <= 0 means every host CPU
+   (OpenMP; omp_get_num_procs, so torchrun's OMP_NUM_THREADS=1 does not
+   silently serialise the CPU baseline). */
 void orc_mi_objective_batch(const int64_t* ka, const double* va, int64_t na, const int64_t* bounds_a,
                             const double* pts_b, int64_t nb, const double* mats, int64_t P,
                             const double* origin, double res, int kind, int bins, double clamp,
                             int include_phi, int nthreads, double* mi_out, int32_t* status_out) {
 #ifdef _OPENMP
-  if (nthreads <= 0) nthreads = omp_get_max_threads();
+  if (nthreads <= 0) nthreads = omp_get_num_procs();
 #pragma omp parallel for schedule(dynamic, 1) num_threads(nthreads)
 #endif
   for (int64_t p = 0; p < P; ++p)
@@ -345,7 +347,7 @@ void orc_mi_objective_batch(const int64_t* ka, const double* va, int64_t na, con
 
 int orc_max_threads(void) {
 #ifdef _OPENMP
-  return omp_get_max_threads();
+  return omp_get_num_procs();
 #else
   return 1;
 #endif

@@ -235,7 +235,7 @@ def grid_search_sharded(scan_a, scan_b, poses=None, cfg: AlignmentConfig | None 
         finally:
             eng.close()
     xdev = torch.device("cuda", device) if dist.get_backend(group) == "nccl" else torch.device("cpu")
-    best, idx = all_gather_winner(value, index, dist, xdev)
+    best, idx = all_gather_winner(value, index, dist, xdev, group=group)
     if best <= NO_OVERLAP_SENTINEL:
         raise NoOverlapError("no candidate pose produced overlapping occupied bounds")
     return SearchResult(best_pose=EulerPose.from_vector(poses[idx]), best_mi=best, best_index=idx,

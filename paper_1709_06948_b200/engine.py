@@ -195,13 +195,15 @@ class MIEngine:
         s = __import__("torch").cuda.current_stream(mi.device).cuda_stream
         return self.ctx.topk_device(mi.data_ptr(), mi.numel(), k, stream=s)
 
-    def best(self, poses, mi: np.ndarray | None = None, rel_tie: float = 1e-12,
+    def best(self, poses, mi: np.ndarray | None = None, rel_tie: float = 1e-9,
              exact_value: bool = False):
         """np.argmax over the candidates' MI with the reference's tie semantics.
 
-        GPU MI agrees with the reference to ~1e-15; the order of two poses can
-        only differ when their MI values are that close.  Every candidate
-        within ``rel_tie`` of the maximum is re-scored on the host from its
+        GPU MI agrees with the reference to ~1e-14 relative (measured over the
+        full C2 batch and a C3 slice: tests/test_gpu_headline_parity.py); the
+        order of two poses can only differ when their MI values are that
+        close.  Every candidate within ``rel_tie`` (1e-9, a wide margin over
+        that bound) of the maximum is re-scored on the host from its
         bit-exact GPU histogram with the reference's own formula, and the
         first maximum in candidate order wins.  Returns (index, mi); with
         ``exact_value`` the winner's MI is always the host re-score (what a

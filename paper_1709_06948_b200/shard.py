@@ -35,11 +35,25 @@ def pick_global(winners: np.ndarray) -> tuple[float, int]:
     return float(w[k, 0]), int(w[k, 1])
 
 
-def all_gather_winner(value: float, index: int, dist, device) -> tuple[float, int]:
-    """Exchange per-rank winners with torch.distributed (NCCL or gloo)."""
+def all_gather_winner(value: float, index: int, dist, device, group=None) -> tuple[float, int]:
+    """Exchange per-rank winners over ``group`` (default: WORLD) with
+    torch.distributed (NCCL or gloo).  The global index travels as an int64
+    (the MI as a float64 in a separate tensor), so it is exact at any size."""
     import torch
-    world = dist.get_world_size()
-    mine = torch.tensor([value, float(index)], dtype=torch.float64, device=device)
-    out = torch.empty(2 * world, dtype=torch.float64, device=device)
-    dist.all_gather_into_tensor(out, mine)
-    return pick_global(out.cpu().numpy())
+    world = dist.get_world_size(group)
+    mine_v = torch.tensor([value], dtype=torch.float64, device=device)
+    mine_i = torch.tensor([index], dtype=torch.int64, device=device)
+    out_v = torch.empty(world, dtype=torch.float64, device=device)
+    out_i = torch.empty(world, dtype=torch.int64, device=device)
+    dist.all_gather_into_tensor(out_v, mine_v, group=group)
+    dist.all_gather_into_tensor(out_i, mine_i, group=group)
+    return pick_global_pairs(out_v.cpu().numpy(), out_i.cpu().numpy())
+
+
+def pick_global_pairs(values: np.ndarray, indices: np.ndarray) -> tuple[float, int]:
+    """pick_global on separate (mi, int64 index) arrays: largest MI, lowest
+    global index among equal maxima (np.argmax's rule, cli.py:202)."""
+    v = np.asarray(values, dtype=np.float64).ravel()
+    i = np.asarray(indices, dtype=np.int64).ravel()
+    k = int(np.lexsort((i, -v))[0])
+    return float(v[k]), int(i[k])

@@ -264,3 +264,29 @@ def relative_pose(p_i: EulerPose, p_j: EulerPose) -> EulerPose:
     c, s = math.cos(p_i.rz), math.sin(p_i.rz)
     dx, dy = p_j.tx - p_i.tx, p_j.ty - p_i.ty
     return EulerPose(c * dx + s * dy, -s * dx + c * dy, 0.0, 0.0, 0.0, p_j.rz - p_i.rz)
+
+
+C5_SIMPLEX_STEPS = (1.0, 1.0, 0.1, 0.01, 0.01, 0.05)  # C5 --c5-mode nm initial simplex
+
+
+def c5_priors(world_poses, seed: int = 5) -> tuple[list, list[EulerPose]]:
+    """C5 per-pair priors: the true relative pose of (i, i+1) perturbed by
+    0.5 m in a random planar direction and +-1 deg of yaw (bench.py:203-224
+    `perturb_pose` style).  Returns (priors as (6,) arrays, truths)."""
+    rng = np.random.default_rng(seed)
+    priors, truths = [], []
+    for i in range(len(world_poses) - 1):
+        t = relative_pose(world_poses[i], world_poses[i + 1])
+        h = rng.uniform(0, 2 * np.pi)
+        truths.append(t)
+        priors.append(np.array([t.tx + 0.5 * np.cos(h), t.ty + 0.5 * np.sin(h), 0.0, 0.0, 0.0,
+                                t.rz + np.radians(1.0) * (1 if rng.random() < 0.5 else -1)]))
+    return priors, truths
+
+
+def c5_grid(prior) -> np.ndarray:
+    """C5 grid mode: 16 x 16 x 16 (tx, ty, yaw) candidates around a prior."""
+    c = np.asarray(prior, dtype=np.float64)
+    offs = np.linspace(-0.75, 0.75, 16)
+    yaw_offs = np.radians(np.linspace(-1.5, 1.5, 16))
+    return grid_poses(c, {"tx": c[0] + offs, "ty": c[1] + offs, "rz": c[5] + yaw_offs})

@@ -19,6 +19,13 @@ time.  Outputs (all .npz, committed):
                  several grids incl. non-zero origin and phi excluded, sentinels
   mi_golden.npz  300 random 33x33 histograms -> mutual_information (crit. 1)
   bins_golden.npz bin_features on random values + the test_mi.py known answers
+  c4_golden.npz  bench.py's C4 scene (100 m, HDL-64-shaped, 0.2 m VARZ): 16 poses'
+                 MI / status / histogram / total
+  c2ref_golden.npz bench.py's C2 batch (65,536 poses, seed 2024): the reference's MI
+                 and status for every 16th pose (4,096 poses)
+  c5_golden.npz  the first 20 pairs of bench.py's C5 drive: per pair the reference's
+                 pick over the 4,096-pose grid (np.argmax, MI) and voxmi.align from the
+                 prior (pose, final MI, iterations, termination)
 """
 
 from __future__ import annotations
@@ -304,7 +311,101 @@ def make_nm():
     np.savez_compressed(os.path.join(HERE, "nm_golden.npz"), **out)
 
 
+def _mi_worker(job):
+    fa, scan_b, grid, spec, chunk = job
+    out = []
+    for p in chunk:
+        m, s, _, _ = full_eval(fa, scan_b, p, grid, spec)
+        out.append((m, s))
+    return out
+
+
+def make_c4():
+    """bench.py C4 workload: 100 m scene, 0.2 m VARZ, 16 poses."""
+    from paper_1709_06948_b200.synth import candidate_batch
+    spec_scene = LidarSceneSpec(extent=100.0, n_boxes=120, box_height=(1.0, 10.0))
+    a_rec, b_rec = hdl64_pair(spec_scene, EulerPose(*HDL_TRUTH))
+    a = PointCloud(a_rec[:, :3].astype(np.float64))
+    b = PointCloud(b_rec[:, :3].astype(np.float64))
+    batch = candidate_batch(EulerPose(*HDL_TRUTH), 65536, seed=2024)
+    idx = np.arange(0, 65536, 4681)[:14]
+    poses = np.concatenate([np.asarray([HDL_TRUTH, (0, 0, 0, 0, 0, 0)]), batch[idx]])
+    grid = GridSpec(resolution=0.2)
+    spec = BinningSpec(kind=FeatureKind.VARZ)
+    fa = compute_feature_map(voxelize(a, grid), a, FeatureKind.VARZ)
+    mis, sts, hs, ts = [], [], [], []
+    for p in poses:
+        m, st, c, t = full_eval(fa, b, p, grid, spec)
+        mis.append(m); sts.append(st); hs.append(c); ts.append(t)
+    np.savez_compressed(os.path.join(HERE, "c4_golden.npz"), a_digest=digest(a_rec),
+                        b_digest=digest(b_rec), poses=poses, batch_idx=idx, mi=np.asarray(mis),
+                        status=np.asarray(sts, np.int32), hist=np.asarray(hs, np.int32),
+                        total=np.asarray(ts), a_nvox=np.int64(len(fa.keys)))
+    print("C4: |VA|", len(fa.keys), "mi", mis[:3])
+
+
+def make_c2ref():
+    """bench.py C2 batch: the reference's MI for every 16th of the 65,536 poses."""
+    from paper_1709_06948_b200.synth import candidate_batch
+    a_rec, b_rec = hdl64_pair(LidarSceneSpec(), EulerPose(*HDL_TRUTH))
+    a = PointCloud(a_rec[:, :3].astype(np.float64))
+    b = PointCloud(b_rec[:, :3].astype(np.float64))
+    batch = candidate_batch(EulerPose(*HDL_TRUTH), 65536, seed=2024)
+    sel = np.arange(0, 65536, 16)
+    grid = GridSpec(resolution=1.0)
+    spec = BinningSpec(kind=FeatureKind.VARZ)
+    fa = compute_feature_map(voxelize(a, grid), a, FeatureKind.VARZ)
+    jobs = [(fa, b, grid, spec, c) for c in np.array_split(batch[sel], 64)]
+    with ProcessPoolExecutor(8) as ex:
+        res = [r for part in ex.map(_mi_worker, jobs) for r in part]
+    np.savez_compressed(os.path.join(HERE, "c2ref_golden.npz"), a_digest=digest(a_rec),
+                        b_digest=digest(b_rec), sel=sel, mi=np.array([r[0] for r in res]),
+                        status=np.array([r[1] for r in res], np.int32))
+    print("C2ref:", len(res), "poses; argmax", sel[int(np.argmax([r[0] for r in res]))])
+
+
+def _c5_pair(job):
+    from voxmi import AlignmentConfig, SimplexConfig, align
+    a_rec, b_rec, prior, steps = job
+    from paper_1709_06948_b200.synth import c5_grid
+    a = PointCloud(a_rec[:, :3].astype(np.float64))
+    b = PointCloud(b_rec[:, :3].astype(np.float64))
+    grid = GridSpec(resolution=1.0)
+    spec = BinningSpec(kind=FeatureKind.VARZ)
+    fa = compute_feature_map(voxelize(a, grid), a, FeatureKind.VARZ)
+    poses = c5_grid(prior)
+    mi = np.array([mi_objective(fa, b, EulerPose.from_vector(p), grid, spec) for p in poses])
+    rep = align(a, b, euler_to_transform(EulerPose.from_vector(prior)),
+                AlignmentConfig(simplex=SimplexConfig(initial_steps=steps)))
+    return (int(np.argmax(mi)), float(mi.max()), mi[::64].copy(), rep.estimated_pose.as_vector(),
+            float(rep.final_mi), int(rep.iterations), str(rep.termination),
+            np.asarray(rep.mi_trace))
+
+
+def make_c5():
+    """First 20 pairs of bench.py's C5 drive: grid picks + voxmi.align results."""
+    from paper_1709_06948_b200.synth import C5_SIMPLEX_STEPS, c5_priors, drive_sequence
+    n = 20
+    scans, wp = drive_sequence(1001, workers=8, subset=(0, n + 1))
+    priors, _ = c5_priors(wp)
+    jobs = [(scans[i], scans[i + 1], priors[i], C5_SIMPLEX_STEPS) for i in range(n)]
+    with ProcessPoolExecutor(8) as ex:
+        res = list(ex.map(_c5_pair, jobs))
+    out = {"digests": np.array([digest(scans[i]) for i in range(n + 1)]),
+           "priors": np.asarray(priors[:n]),
+           "grid_argmax": np.array([r[0] for r in res]), "grid_best_mi": np.array([r[1] for r in res]),
+           "grid_mi_sub": np.stack([r[2] for r in res]),
+           "align_pose": np.stack([r[3] for r in res]), "align_final_mi": np.array([r[4] for r in res]),
+           "align_iterations": np.array([r[5] for r in res]),
+           "align_termination": np.array([r[6] for r in res])}
+    for i, r in enumerate(res):
+        out[f"align_trace_{i}"] = r[7]
+    np.savez_compressed(os.path.join(HERE, "c5_golden.npz"), **out)
+    print("C5: picks", out["grid_argmax"], "align iters", out["align_iterations"])
+
+
 if __name__ == "__main__":
-    what = sys.argv[1:] or ["small", "mi", "bins", "hdl", "c1", "align", "nm"]
+    what = sys.argv[1:] or ["small", "mi", "bins", "hdl", "c1", "align", "nm", "c4", "c2ref",
+                            "c5"]
     for w in what:
         globals()[f"make_{w}"]()

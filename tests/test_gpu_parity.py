@@ -136,7 +136,7 @@ def test_fast_path_equals_exact_path_on_c2_batch(hdl):
     np.testing.assert_allclose(mi_f, mi_e, rtol=1e-12, atol=1e-14)
     # and the oracle agrees on a subsample
     fa = oracle.feature_map(a[:, :3].astype(np.float64), (0, 0, 0), 1.0, "varz")
-    mats = vmi.poses_to_mats(poses[:12])
+    mats = oracle.poses_to_mats(poses[:12])
     omi, ost = oracle.mi_objective_batch(fa, b[:, :3].astype(np.float64), mats, threads=0)
     np.testing.assert_array_equal(ost, st_f[:12])
     assert_mi_close(mi_f[:12], omi)
@@ -255,7 +255,7 @@ def test_reference_feature_map_injection_and_phi_off_empty():
     assert mi_off == vmi.NO_OVERLAP_SENTINEL
     # the same through the oracle on the same maps
     ofa = oracle.OracleFeatureMap("count", fa.keys, fa.values, fa.bounds)
-    omi, ost = oracle.mi_objective_batch(ofa, cloud.points, vmi.poses_to_mats([[0, 0, 0, 0, 0, 0],
+    omi, ost = oracle.mi_objective_batch(ofa, cloud.points, oracle.poses_to_mats([[0, 0, 0, 0, 0, 0],
                                                                               [1, 0, 0, 0, 0, 0]]),
                                          include_phi=False)
     assert omi[1] == vmi.NO_OVERLAP_SENTINEL and ost[1] == 3
@@ -292,7 +292,7 @@ def test_bins_limits():
     mi, st, hist, _ = eng.evaluate(c["poses"][:6], histograms=True)
     ofa = oracle.feature_map(c["a"], (0, 0, 0), 1.0, "varz")
     for k in range(6):
-        omi, ost, oc, _ = oracle.mi_objective_full(ofa, c["b"], vmi.poses_to_mats(c["poses"][k])[0],
+        omi, ost, oc, _ = oracle.mi_objective_full(ofa, c["b"], oracle.poses_to_mats(c["poses"][k])[0],
                                                    bins=64)
         assert ost == st[k]
         if ost == 0:
@@ -315,7 +315,7 @@ def test_mi_at_breakdown_matches_oracle():
     pose = EulerPose(0.8, 0.6, 0.0, 0.0, 0.0, 0.09)
     r = vmi.mi_at(s["a"], s["b"], pose, cfg)
     fa = oracle.feature_map(s["a"], (0, 0, 0), 0.5, "count")
-    _, _, counts, _ = oracle.mi_objective_full(fa, s["b"], vmi.poses_to_mats(pose.as_vector())[0],
+    _, _, counts, _ = oracle.mi_objective_full(fa, s["b"], oracle.poses_to_mats(pose.as_vector())[0],
                                                res=0.5)
     want = oracle.mutual_information(counts)
     np.testing.assert_allclose([r.mi, r.h_x, r.h_y, r.h_xy], want, rtol=1e-12, atol=1e-14)
@@ -427,7 +427,7 @@ def test_varz_bin_edge_is_rechecked_exactly():
     got_mi, got_st, hist, _ = eng.evaluate(poses, histograms=True)
     fa = oracle.feature_map(a, (0, 0, 0), 1.0, "varz")
     for k in range(3):
-        omi, ost, oc, _ = oracle.mi_objective_full(fa, b, vmi.poses_to_mats(poses[k])[0])
+        omi, ost, oc, _ = oracle.mi_objective_full(fa, b, oracle.poses_to_mats(poses[k])[0])
         assert ost == got_st[k]
         np.testing.assert_array_equal(hist[k], oc)
         assert got_mi[k] == pytest.approx(omi, rel=MI_RTOL, abs=MI_ATOL)
@@ -481,7 +481,7 @@ def test_sparse_scan_run_queue_pressure(kind):
                       [1.0, 1.0, 0.0, 0.0, 0.0, -0.5], [-2.0, 0.5, 0.25, 0.0, 0.0, 1.0]])
     mi, st, hist, total = eng.evaluate(poses, histograms=True)
     fa = oracle.feature_map(pts_a, (0, 0, 0), 0.5, kind)
-    mats = vmi.poses_to_mats(poses)
+    mats = oracle.poses_to_mats(poses)
     for i in range(len(poses)):
         omi, ost, ohist, ototal = oracle.mi_objective_full(fa, pts_b, mats[i], res=0.5)
         assert st[i] == ost
@@ -512,7 +512,7 @@ def test_general_resolution_near_integer_quotients(res, kind):
     eng.set_query(pts_b)  # float32-exact: split-double records
     poses = np.array([[0.0, 0.0, 0.0, 0.0, 0.0, 0.0], [0.875, -0.5, 0.125, 0.0, 0.0, 0.0],
                       [-2.25, 1.5, 0.0, 0.0, 0.0, 0.0], [0.3, 0.1, 0.0, 0.0, 0.0, 0.02]])
-    mats = vmi.poses_to_mats(poses)
+    mats = oracle.poses_to_mats(poses)
     mi, st, hist, total = eng.evaluate(poses, histograms=True)
     fa = oracle.feature_map(pts_a, (0, 0, 0), res, kind)
     for i in range(len(poses)):
@@ -555,7 +555,7 @@ def test_eval_poses_two_chunk_pipeline_equals_eval():
     np.testing.assert_array_equal(total, total2)
     for k in (0, 2047, 2048, 19999):  # both sides of the head (2048 poses) and the ends
         omi, ost, ohist, ototal = oracle.mi_objective_full(
-            oracle.feature_map(a, (0, 0, 0), 1.0, "varz"), b, vmi.poses_to_mats(poses[k:k + 1])[0])
+            oracle.feature_map(a, (0, 0, 0), 1.0, "varz"), b, oracle.poses_to_mats(poses[k:k + 1])[0])
         assert st[k] == ost
         np.testing.assert_array_equal(hist[k], ohist)
 
@@ -577,7 +577,7 @@ def test_ragged_query_sizes_match_oracle(nb, kind):
     eng.set_query(b)
     poses = np.array([[0.0, 0.0, 0.0, 0.0, 0.0, 0.0], [0.4, -0.3, 0.05, 0.01, -0.02, 0.1],
                       [-1.5, 2.0, 0.0, 0.0, 0.0, -0.3], [3.0, 0.0, 0.2, 0.05, 0.0, 0.0]])
-    mats = vmi.poses_to_mats(poses)
+    mats = oracle.poses_to_mats(poses)
     mi, st, hist, total = eng.evaluate(poses, histograms=True)
     fa = oracle.feature_map(a, (0, 0, 0), res, kind)
     for i in range(len(poses)):

@@ -53,6 +53,11 @@ def full(rep: str, out: str) -> None:
         "l1tex__data_pipe_lsu_wavefronts_mem_shared_op_atom.sum",
         "l1tex__data_bank_conflicts_pipe_lsu_mem_shared_op_atom.sum",
         "smsp__inst_executed.sum", "sm__cycles_elapsed.avg",
+        "smsp__sass_thread_inst_executed_op_dfma_pred_on.sum",
+        "smsp__sass_thread_inst_executed_op_dadd_pred_on.sum",
+        "smsp__sass_thread_inst_executed_op_dmul_pred_on.sum",
+        "smsp__sass_inst_executed_op_shared_atom.sum", "smsp__sass_inst_executed_op_global_red.sum",
+        "smsp__sass_inst_executed_op_global_atom.sum",
     ]
     d = {k: (raw[k][0] if k == "Kernel Name" else _num(raw[k][0])) for k in pick if k in raw}
     d["units"] = {k: raw[k][1] for k in pick if k in raw and raw[k][1]}
