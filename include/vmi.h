@@ -70,6 +70,13 @@ int vmi_set_params(vmi_ctx* ctx, const double origin[3], double resolution, int 
    point leaves the key range (the reference raises OutOfBoundsError). */
 int vmi_set_reference_points(vmi_ctx* ctx, const double* xyz, int64_t n);
 
+/* Scan A as KITTI .bin records (x, y, z, intensity float32; scan_io.py:57-75),
+   uploaded as they are (16 B/point; no float64 upcast on the host) and widened
+   exactly on the GPU -- the reference loads them as PointCloud(data[:, :3]
+   .astype(float64)) (scan_io.py:74).  Same results as vmi_set_reference_points
+   on the widened coordinates. */
+int vmi_set_reference_records_f32(vmi_ctx* ctx, const float* xyzi, int64_t n);
+
 /* Scan A from an existing FeatureMap (voxel.py:129-164): packed keys
    (pack_keys, voxel.py:65-73) sorted ascending, values >= 0, bounds =
    [xmin, ymin, zmin, xmax, ymax, zmax].  The injection point the reference's

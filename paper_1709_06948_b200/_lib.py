@@ -24,7 +24,7 @@ SENTINEL = -1e300
 # every exported symbol of include/vmi.h (checked by tests/test_boundary.py)
 EXPORTS = (
     "vmi_create", "vmi_destroy", "vmi_last_error", "vmi_version", "vmi_set_params",
-    "vmi_set_reference_points", "vmi_set_reference_features", "vmi_get_reference_features",
+    "vmi_set_reference_points", "vmi_set_reference_records_f32", "vmi_set_reference_features", "vmi_get_reference_features",
     "vmi_set_query_points", "vmi_set_query_records_f32", "vmi_poses_to_mats", "vmi_eval",
     "vmi_eval_poses", "vmi_eval_device", "vmi_eval_fixups", "vmi_eval_exact", "vmi_query_features",
     "vmi_fast_features",
@@ -64,6 +64,7 @@ def load(path: str = LIB_PATH):
     L.vmi_set_params.argtypes = [_ctx, _d, ctypes.c_double, ctypes.c_int, ctypes.c_int,
                                  ctypes.c_double, ctypes.c_int]
     L.vmi_set_reference_points.argtypes = [_ctx, _d, ctypes.c_int64]
+    L.vmi_set_reference_records_f32.argtypes = [_ctx, _f, ctypes.c_int64]
     L.vmi_set_reference_features.argtypes = [_ctx, _i64, _d, ctypes.c_int64, _i64]
     L.vmi_get_reference_features.argtypes = [_ctx, _i64, _d, ctypes.c_int64, _i64, _i64]
     L.vmi_set_query_points.argtypes = [_ctx, _d, ctypes.c_int64]
@@ -163,6 +164,16 @@ class Context:
             from .errors import OutOfBoundsError
             raise OutOfBoundsError(self._L.vmi_last_error(self._h).decode())
         self.check(rc, "vmi_set_reference_points")
+
+    def set_reference_records(self, rec: np.ndarray):
+        rec = np.ascontiguousarray(rec, dtype=np.float32)
+        if rec.ndim != 2 or rec.shape[1] != 4:
+            raise ValueError("records must be (N, 4) float32")
+        rc = self._L.vmi_set_reference_records_f32(self._h, ptr(rec, _f), rec.shape[0])
+        if rc == -5:
+            from .errors import OutOfBoundsError
+            raise OutOfBoundsError(self._L.vmi_last_error(self._h).decode())
+        self.check(rc, "vmi_set_reference_records_f32")
 
     def set_reference_features(self, keys, values, bounds):
         k = np.ascontiguousarray(keys, dtype=np.int64)

@@ -29,6 +29,11 @@ namespace vmi {
 
 __device__ __forceinline__ void point_at(const PointSource& src, int64_t i, double& x, double& y,
                                          double& z) {
+  if (src.rec) {  // float32 records widen exactly (the reference's astype(float64))
+    const float4 v = src.rec[i];
+    x = v.x; y = v.y; z = v.z;
+    return;
+  }
   if (src.xyz) {
     x = src.xyz[3 * i]; y = src.xyz[3 * i + 1]; z = src.xyz[3 * i + 2];
     return;

@@ -145,9 +145,12 @@ __host__ __device__ constexpr bool kGlobalCounts() {
 using VKey = uint32_t;
 constexpr VKey kEmptyKey = kEmpty32;
 __host__ __device__ inline int slot_bytes(int kind, int multi) {
+  if (kind == kKindOcc) return 4;  // key only
   if (kind != 0) return 4 + 4;
   return (int)sizeof(VKey) + (multi ? 0 : 4);
 }
+// queued run record: VARZ {lin, n, -, -, S1, S2}, COUNT {lin, n}, occupancy {lin}
+__host__ __device__ constexpr int rec_bytes(int kind) { return kind == 0 ? 32 : kind == 1 ? 8 : 4; }
 
 struct VarzTable {
   VKey* key;      // voxel index inside A's AABB (kEmptyKey = free)
@@ -191,7 +194,7 @@ __host__ __device__ inline FastSmem fast_layout(int kind, int cap, int W, int th
   L.queue = off;
   const int queue = multi ? kQueueT<true, true>() : (f32 ? kQueueT<true, false>() : kQueueT<false, false>());
   // + one warp queue of slack: the kernel aligns the queues to their size
-  off += (size_t)(threads / 32 + 1) * queue * (kind == 0 ? 32 : 8);
+  off += (size_t)(threads / 32 + 1) * queue * rec_bytes(kind);
   off = (off + 15) & ~size_t(15);
   L.hist = off; off += (size_t)W * W * 4; off = (off + 15) & ~size_t(15);
   L.marg = off; off += (size_t)W * 4; off = (off + 15) & ~size_t(15);
@@ -219,6 +222,11 @@ __device__ __forceinline__ uint4 ld_shared_v4(uint32_t a) {
                : "memory");
   return v;
 }
+__device__ __forceinline__ uint32_t ld_shared_u32(uint32_t a) {
+  uint32_t v;
+  asm volatile("ld.shared.u32 %0, [%1];" : "=r"(v) : "r"(a) : "memory");
+  return v;
+}
 __device__ __forceinline__ uint2 ld_shared_v2(uint32_t a) {
   uint2 v;
   asm volatile("ld.shared.v2.u32 {%0, %1}, [%2];" : "=r"(v.x), "=r"(v.y) : "r"(a) : "memory");
@@ -236,6 +244,11 @@ __device__ __forceinline__ void st_rec32_if(bool p, uint32_t a, uint32_t l, uint
       " @q st.shared.f64 [%1+24], %5;\n}" ::"r"((int)p),
       "r"(a), "r"(l), "r"(n), "d"(s1), "d"(s2)
       : "memory");
+}
+__device__ __forceinline__ void st_rec4_if(bool p, uint32_t a, uint32_t l) {
+  asm volatile("{\n .reg .pred q;\n setp.ne.b32 q, %0, 0;\n @q st.shared.u32 [%1], %2;\n}" ::"r"((int)p),
+               "r"(a), "r"(l)
+               : "memory");
 }
 __device__ __forceinline__ void st_rec8_if(bool p, uint32_t a, uint32_t l, uint32_t n) {
   asm volatile(
@@ -316,8 +329,9 @@ __global__ void __launch_bounds__(THREADS, 1)
   VarzTable VT;
   uint32_t* ckey = nullptr;
   uint32_t* ccnt = nullptr;
-  // warp queue: AoS records, VARZ 32 B {lin, n, -, -, S1, S2}, COUNT 8 B {lin, n}
-  constexpr uint32_t kRec = KIND == 0 ? 32u : 8u;
+  // warp queue: AoS records, VARZ 32 B {lin, n, -, -, S1, S2}, COUNT 8 B {lin, n},
+  // occupancy 4 B {lin}
+  constexpr uint32_t kRec = (uint32_t)rec_bytes(KIND);
   constexpr int kQueue = kQueueT<F32, MULTI>();
   // Each warp's queue is aligned to its size QB, so a record address is
   // qbase | (byte offset mod QB): one LOP3 per push.
@@ -333,7 +347,7 @@ __global__ void __launch_bounds__(THREADS, 1)
     VT.sums = gsums + (size_t)blockIdx.x * cap;
   } else {
     ckey = reinterpret_cast<uint32_t*>(smem + L.table);
-    ccnt = reinterpret_cast<uint32_t*>(smem + L.table + (size_t)cap * 4);
+    if (KIND == kKindCount) ccnt = reinterpret_cast<uint32_t*>(smem + L.table + (size_t)cap * 4);
   }
 
   // The table is cleared once here; afterwards the per-pose table walk resets
@@ -427,7 +441,12 @@ __global__ void __launch_bounds__(THREADS, 1)
       // leave one by one re-issued the atomics ~3.4 times per drain.)
       auto flush_rec = [&](uint32_t idx, bool has) {
         const uint32_t a = qbase | (idx & (QB - 1));
-        const uint2 r0 = has ? ld_shared_v2(a) : make_uint2(kNoVoxel, 0u);
+        uint2 r0 = make_uint2(kNoVoxel, 0u);
+        if (KIND == kKindOcc) {
+          if (has) r0.x = ld_shared_u32(a);
+        } else if (has) {
+          r0 = ld_shared_v2(a);
+        }
         uint32_t* keys = KIND == 0 ? reinterpret_cast<uint32_t*>(VT.key) : ckey;
         uint32_t sl = slot_of(r0.x, ucap);
         // first probe = one CAS (hit or insert), no branch before the atomics
@@ -439,9 +458,9 @@ __global__ void __launch_bounds__(THREADS, 1)
             atomicAdd(&VT.cnt[slot], r0.y);
             atomicAdd(&VT.sums[slot].x, mkd(r1.x, r1.y));
             atomicAdd(&VT.sums[slot].y, mkd(r1.z, r1.w));
-          } else {
+          } else if (KIND == kKindCount) {
             atomicAdd(&ccnt[slot], r0.y);
-          }
+          }  // occupancy: the key is all there is
         };
         if (done) {
           add(sl);
@@ -478,8 +497,10 @@ __global__ void __launch_bounds__(THREADS, 1)
         const uint32_t a = qbase | ((qt + __popc(mu & lt_mask) * kRec) & (QB - 1));
         if (KIND == 0)
           st_rec32_if(pdu, a, cur, cn, cs1, cs2);
-        else
+        else if (KIND == kKindCount)
           st_rec8_if(pdu, a, cur, cn);
+        else
+          st_rec4_if(pdu, a, cur);
         qt += __popc(mu) * kRec;
 #ifdef VMI_PRED_RESET
         run_reset_if(e, cn, cs1, cs2);
@@ -726,11 +747,15 @@ __global__ void __launch_bounds__(THREADS, 1)
           const double f = floor(x);
           bb = 1 + (f >= bins_d - 1.0 ? g.bins - 1 : (int)f);
           dump_feat = feat;
-        } else {
+        } else if (KIND == kKindCount) {
           const uint32_t n = ccnt[s];
           ckey[s] = kEmpty32; ccnt[s] = 0u;
           bb = n < (uint32_t)kCountLut ? (int)count_lut[n] : feature_bin((double)n, g.clamp, g.bins);
           dump_feat = (double)n;
+        } else {  // occupancy: every occupied voxel has the same bin
+          ckey[s] = kEmpty32;
+          bb = g.occ_bin;
+          dump_feat = __longlong_as_double(0x7ff8000000000000LL);  // no feature value (NaN)
         }
         atomicAdd(&hist[ba * W + bb], 1u);
         if (dump.keys) {  // debug export (vmi_fast_features): lin -> packed key, feature
@@ -809,8 +834,8 @@ __global__ void __launch_bounds__(THREADS, 1)
             if (lin[u] != kNoVoxel) finish_slot(sl[u], lin[u], ba[u], sum[u], cnt[u]);
         }
       } else {
-        // COUNT: four slots per thread per step, four A-grid loads in flight
-        // (no L2 sums to fetch: compaction measured slower here)
+        // COUNT / occupancy: four slots per thread per step, four A-grid loads
+        // in flight (no L2 sums to fetch: compaction measured slower here)
         for (int s0 = tid; s0 < cap; s0 += 4 * THREADS) {
           uint32_t lin[4];
           int ba[4];
@@ -946,9 +971,11 @@ static cudaError_t launch_mode(const FastLaunch& fl, cudaStream_t st) {
 template <int T, int NS>
 static cudaError_t launch_threads(const FastLaunch& fl, cudaStream_t st) {
   const bool f32 = fl.B.is_f32 != 0;
-  if (fl.g.kind == 0)
+  if (fl.g.kind == kKindVarz)
     return f32 ? launch_mode<T, NS, 0, true>(fl, st) : launch_mode<T, NS, 0, false>(fl, st);
-  return f32 ? launch_mode<T, NS, 1, true>(fl, st) : launch_mode<T, NS, 1, false>(fl, st);
+  if (fl.g.kind == kKindCount)
+    return f32 ? launch_mode<T, NS, 1, true>(fl, st) : launch_mode<T, NS, 1, false>(fl, st);
+  return f32 ? launch_mode<T, NS, 2, true>(fl, st) : launch_mode<T, NS, 2, false>(fl, st);
 }
 
 // NS = 2 (two spans per thread at 256 threads) compiles and is exact, but was

@@ -29,6 +29,7 @@ struct vmi_ctx {
 
   bool params_set = false;
   GridParams g{};
+  int occ = 0;  // fast kernel runs the occupancy kind (every occupied voxel in one bin)
 
   // scan A
   bool a_set = false;
@@ -158,11 +159,15 @@ QueryView query_view(const vmi_ctx* c) {
   return B;
 }
 
+// The fast kernel's feature kind: the user's, or occupancy when every occupied
+// voxel provably takes one bin (vmi_set_params).
+int kernel_kind(const vmi_ctx* c) { return c->occ ? kKindOcc : c->g.kind; }
+
 // Largest table that fits shared memory next to the kernel's other buffers.
-size_t max_table_cap(const vmi_ctx* c, bool multi) {
-  const size_t fixed = fast_smem_bytes(c->g.kind, 0, c->g.bins, c->threads / c->streams,
+size_t max_table_cap(const vmi_ctx* c, int kind, bool multi) {
+  const size_t fixed = fast_smem_bytes(kind, 0, c->g.bins, c->threads / c->streams,
                                        c->is_f32, c->streams, multi ? 1 : 0);
-  const size_t per = (size_t)fast_slot_bytes(c->g.kind, multi ? 1 : 0);
+  const size_t per = (size_t)fast_slot_bytes(kind, multi ? 1 : 0);
   return ((c->smem_optin - fixed) / per) & ~size_t(31);
 }
 
@@ -170,7 +175,7 @@ size_t max_table_cap(const vmi_ctx* c, bool multi) {
 // walked once per pose, so a single-pass table is sized for a ~40% load at
 // scan B's expected occupancy rather than filling shared memory; when even a
 // full table cannot hold it, the multi-pass layout (bigger table) is used.
-void plan_table(const vmi_ctx* c, int* cap_out, int* npass_out, int* multi_out) {
+void plan_table(const vmi_ctx* c, int kind, int* cap_out, int* npass_out, int* multi_out) {
   static const double factor = [] {
     const char* e = std::getenv("VMI_CAP_FACTOR");  // experiments only
     // C2 (A/B, reproduced): 2.2 -> 28.98 ms, 2.0 -> 29.25, 2.5 -> 29.48; C1 flat
@@ -182,12 +187,12 @@ void plan_table(const vmi_ctx* c, int* cap_out, int* npass_out, int* multi_out) 
     const int np = c->npass_override > 0
                        ? c->npass_override
                        : std::max(1, (int)std::ceil(est / (0.70 * c->cap_override)));
-    *cap_out = (int)std::min((size_t)c->cap_override, max_table_cap(c, np > 1));
+    *cap_out = (int)std::min((size_t)c->cap_override, max_table_cap(c, kind, np > 1));
     *npass_out = np;
     *multi_out = np > 1;
     return;
   }
-  const size_t cap1 = max_table_cap(c, false);
+  const size_t cap1 = max_table_cap(c, kind, false);
   if (c->npass_override <= 1 && (c->npass_override == 1 || est <= 0.70 * (double)cap1)) {
     size_t want = ((size_t)(factor * est) + 31) & ~size_t(31);
     if (want < 2048) want = 2048;
@@ -204,7 +209,7 @@ void plan_table(const vmi_ctx* c, int* cap_out, int* npass_out, int* multi_out) 
     // 1.2 overflows on some poses (exact-path fix-ups)
     return e ? std::atof(e) : 1.4;
   }();
-  const size_t capm = max_table_cap(c, true);
+  const size_t capm = max_table_cap(c, kind, true);
   *cap_out = (int)capm;
   *multi_out = 1;
   *npass_out = c->npass_override > 1
@@ -214,8 +219,8 @@ void plan_table(const vmi_ctx* c, int* cap_out, int* npass_out, int* multi_out) 
     *cap_out = (int)std::min(capm, (((size_t)(factor_m * est) + 31) & ~size_t(31)));
 }
 
-int ensure_sums(vmi_ctx* c, int grid, int cap) {
-  if (c->g.kind != 0) return 0;
+int ensure_sums(vmi_ctx* c, int kind, int grid, int cap) {
+  if (kind != kKindVarz) return 0;
   const size_t need = (size_t)grid * cap;
   if (need <= c->sums_n) return 0;
   cudaFree(c->d_sums);
@@ -311,14 +316,15 @@ int launch_fast_eval(vmi_ctx* c, const double* mats_dev, int64_t P, double* mi, 
   if (P <= 0) return 0;
   FastLaunch fl{};
   fl.g = c->g;
+  fl.g.kind = kernel_kind(c);
   fl.A = ref_view(c);
   fl.B = query_view(c);
   fl.mats = mats_dev;
   fl.P = P;
   fl.grid = (int)(P < c->sm_count ? P : c->sm_count);
   fl.streams = c->streams;
-  plan_table(c, &fl.cap, &fl.npass, &fl.multi);
-  int rc = ensure_sums(c, fl.grid, fl.cap);
+  plan_table(c, fl.g.kind, &fl.cap, &fl.npass, &fl.multi);
+  int rc = ensure_sums(c, fl.g.kind, fl.grid, fl.cap);
   if (rc) return rc;
   fl.sums = c->d_sums;
   fl.mi = mi;
@@ -448,6 +454,29 @@ int vmi_set_params(vmi_ctx* c, const double origin[3], double res, int kind, int
   g.bins = bins;
   g.clamp = clamp;
   g.include_phi = include_phi ? 1 : 0;
+  // Occupancy specialisation (exact, not an approximation).  bin_feature
+  // (mi.py:62-69) maps v -> 1 + min(B-1, floor(v / clamp * B)).
+  //  * VARZ: a voxel's points have z within one voxel height (z in [o+k*res,
+  //    o+(k+1)*res) up to rounding), and the variance of values spread over an
+  //    interval of length L is at most L^2/4.  If res^2/4 * B/clamp <= 1/2,
+  //    every VARZ value bins to 1 with a margin no rounding can cross: the
+  //    joint histogram only depends on WHICH voxels B occupies (C4: 0.2 m,
+  //    B = 32, clamp 2 -> 0.16).
+  //  * COUNT: n >= 1 for an occupied voxel; if n = 1 already saturates
+  //    (floor(B / clamp) >= B - 1), every voxel bins to B.
+  // The fast kernel then keeps voxel keys only (no counts / sums); the exact
+  // path and the feature dumps keep computing the features themselves.
+  g.occ_bin = 0;
+  int occ = 0;
+  if (kind == VMI_VARZ && res * res / 4.0 * (double)bins / clamp <= 0.5) {
+    occ = 1;
+    g.occ_bin = 1;
+  } else if (kind == VMI_COUNT && std::floor(1.0 / clamp * (double)bins) >= (double)(bins - 1)) {
+    occ = 1;
+    g.occ_bin = bins;
+  }
+  if (std::getenv("VMI_NO_OCC")) occ = 0;  // A/B and parity cross-checks only
+  c->occ = occ;
   const bool grid_changed = !c->params_set || std::memcmp(&c->g, &g, sizeof(double) * 5) != 0 ||
                             c->g.kind != g.kind || c->g.bins != g.bins || c->g.clamp != g.clamp;
   c->g = g;
@@ -462,18 +491,29 @@ int vmi_set_params(vmi_ctx* c, const double origin[3], double res, int kind, int
   return 0;
 }
 
-int vmi_set_reference_points(vmi_ctx* c, const double* xyz, int64_t n) {
+// Scan A from host points: (n, 3) float64, or (n, 4) float32 KITTI records
+// uploaded as they are (16 B/point, widened exactly on the GPU).
+static int set_reference(vmi_ctx* c, const void* host, int is_rec, int64_t n) {
   if (!c) return VMI_ERR_ARG;
   if (!c->params_set) return fail(c, VMI_ERR_STATE, "vmi_set_params not called");
-  if (n <= 0 || !xyz) return fail(c, VMI_ERR_ARG, "cannot voxelize an empty cloud");
+  if (n <= 0 || !host) return fail(c, VMI_ERR_ARG, "cannot voxelize an empty cloud");
   if (n > 0x7fffffff) return fail(c, VMI_ERR_UNSUPPORTED, "more than 2^31-1 points");
+  if (is_rec) {  // PointCloud validation (geometry.py:36-65): finite coordinates
+    const float* r = static_cast<const float*>(host);
+    for (int64_t i = 0; i < n; ++i)
+      if (!(std::isfinite(r[4 * i]) && std::isfinite(r[4 * i + 1]) && std::isfinite(r[4 * i + 2])))
+        return fail(c, VMI_ERR_ARG, "points contain non-finite coordinates");
+  }
   cudaSetDevice(c->device);
   free_a(c);
-  CK(c, grow(&c->d_upload, c->cap_upload, (size_t)n * 24));
-  double* d = static_cast<double*>(c->d_upload);
-  CK(c, cudaMemcpyAsync(d, xyz, n * 24, cudaMemcpyHostToDevice, c->stream));
+  const size_t bytes = (size_t)n * (is_rec ? 16 : 24);
+  CK(c, grow(&c->d_upload, c->cap_upload, bytes));
+  CK(c, cudaMemcpyAsync(c->d_upload, host, bytes, cudaMemcpyHostToDevice, c->stream));
   PointSource src{};
-  src.xyz = d;
+  if (is_rec)
+    src.rec = static_cast<const float4*>(c->d_upload);
+  else
+    src.xyz = static_cast<const double*>(c->d_upload);
   src.n = n;
   CK(c, exact_voxelize(c->ex, src, nullptr, c->g, c->stream, &c->launches));
   int h[8];
@@ -492,6 +532,14 @@ int vmi_set_reference_points(vmi_ctx* c, const double* xyz, int64_t n) {
   const int rc = finish_reference(c, b64, V);
   c->a_npts = n;
   return rc;
+}
+
+int vmi_set_reference_points(vmi_ctx* c, const double* xyz, int64_t n) {
+  return set_reference(c, xyz, 0, n);
+}
+
+int vmi_set_reference_records_f32(vmi_ctx* c, const float* xyzi, int64_t n) {
+  return set_reference(c, xyzi, 1, n);
 }
 
 int vmi_set_reference_features(vmi_ctx* c, const int64_t* keys, const double* values, int64_t n,
@@ -576,13 +624,27 @@ static int set_query(vmi_ctx* c, const void* host, int is_f32_src, int64_t n) {
   }
   double mx = 0.0;
   double lo[3] = {INFINITY, INFINITY, INFINITY}, hi[3] = {-INFINITY, -INFINITY, -INFINITY};
-  for (int64_t i = 0; i < n; ++i)
-    for (int j = 0; j < 3; ++j) {
-      const double v = is_f32_src ? (double)static_cast<const float*>(host)[4 * i + j]
-                                  : static_cast<const double*>(host)[3 * i + j];
-      lo[j] = std::fmin(lo[j], v);
-      hi[j] = std::fmax(hi[j], v);
-    }
+  if (is_f32_src) {  // one pass: PointCloud validation (finite) + AABB
+    const float* r = static_cast<const float*>(host);
+    float flo[3] = {INFINITY, INFINITY, INFINITY}, fhi[3] = {-INFINITY, -INFINITY, -INFINITY};
+    bool finite = true;
+    for (int64_t i = 0; i < n; ++i)
+      for (int j = 0; j < 3; ++j) {
+        const float v = r[4 * i + j];
+        finite &= std::isfinite(v);
+        flo[j] = std::fmin(flo[j], v);
+        fhi[j] = std::fmax(fhi[j], v);
+      }
+    if (!finite) return fail(c, VMI_ERR_ARG, "points contain non-finite coordinates");
+    for (int j = 0; j < 3; ++j) { lo[j] = flo[j]; hi[j] = fhi[j]; }
+  } else {
+    for (int64_t i = 0; i < n; ++i)
+      for (int j = 0; j < 3; ++j) {
+        const double v = static_cast<const double*>(host)[3 * i + j];
+        lo[j] = std::fmin(lo[j], v);
+        hi[j] = std::fmax(hi[j], v);
+      }
+  }
   for (int j = 0; j < 3; ++j) {
     mx = std::fmax(mx, std::fmax(std::fabs(lo[j]), std::fabs(hi[j])));
     c->b_lo[j] = lo[j];
@@ -623,11 +685,6 @@ static int set_query(vmi_ctx* c, const void* host, int is_f32_src, int64_t n) {
 int vmi_set_query_points(vmi_ctx* c, const double* xyz, int64_t n) { return set_query(c, xyz, 0, n); }
 
 int vmi_set_query_records_f32(vmi_ctx* c, const float* xyzi, int64_t n) {
-  if (c && xyzi) {
-    for (int64_t i = 0; i < n; ++i)
-      for (int j = 0; j < 3; ++j)
-        if (!std::isfinite(xyzi[4 * i + j])) return fail(c, VMI_ERR_ARG, "points contain non-finite coordinates");
-  }
   return set_query(c, xyzi, 1, n);
 }
 
@@ -806,10 +863,10 @@ int vmi_fast_features(vmi_ctx* c, const double mat[12], int64_t* keys, double* v
   fl.B = query_view(c);
   fl.mats = c->d_mats;
   fl.P = 1;
-  plan_table(c, &fl.cap, &fl.npass, &fl.multi);
+  plan_table(c, fl.g.kind, &fl.cap, &fl.npass, &fl.multi);  // the user's kind: dumps need features
   fl.grid = 1;
   fl.streams = c->streams;
-  if ((rc = ensure_sums(c, 1, fl.cap))) return rc;
+  if ((rc = ensure_sums(c, fl.g.kind, 1, fl.cap))) return rc;
   fl.sums = c->d_sums;
   fl.mi = c->d_mi;
   fl.status = c->d_status;

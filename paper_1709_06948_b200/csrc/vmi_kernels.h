@@ -62,7 +62,8 @@ void exact_free(ExactScratch& s);
 
 // Point sources for the exact path.
 struct PointSource {
-  const double* xyz;  // contiguous (n, 3) doubles, or nullptr to use B
+  const float4* rec = nullptr;  // contiguous KITTI (x, y, z, i) float32 records, or
+  const double* xyz;  // contiguous (n, 3) doubles, or nullptr (both) to use B
   QueryView B;
   int64_t n;
 };

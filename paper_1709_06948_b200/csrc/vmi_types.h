@@ -13,15 +13,21 @@ enum GridMode : int {
   kGridGeneral = 2,  // IEEE division
 };
 
+// Fast-kernel feature kinds.  kKindOcc is internal: chosen by the host when
+// every occupied voxel provably lands in one feature bin (see vmi_set_params),
+// so the histogram needs only which voxels are occupied, not their features.
+constexpr int kKindVarz = 0, kKindCount = 1, kKindOcc = 2;
+
 struct GridParams {
   double origin[3];
   double res;
   double inv_res;
   int mode;
-  int kind;  // 0 varz, 1 count
+  int kind;  // 0 varz, 1 count (exact path / user); fast kernel: + 2 occupancy
   int bins;
   int include_phi;
   double clamp;
+  int occ_bin;  // kKindOcc: the one B-side bin every occupied voxel takes
 };
 
 // Scan A as the kernels see it: a dense u8 bin grid over A's occupied AABB

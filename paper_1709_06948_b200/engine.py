@@ -28,6 +28,11 @@ from .types import (NO_OVERLAP_SENTINEL, BinningSpec, FeatureKind, FeatureMap, G
 
 
 def _points_of(cloud) -> np.ndarray:
+    """(N, 3|4) array of a cloud: a PointCloud's KITTI records when it carries
+    them (scan_io.load_kitti_bin), else its points, else the array itself."""
+    rec = getattr(cloud, "records", None)
+    if rec is not None:
+        return rec
     pts = getattr(cloud, "points", cloud)
     pts = np.asarray(pts)
     if pts.ndim != 2 or pts.shape[1] not in (3, 4):
@@ -96,10 +101,13 @@ class MIEngine:
         Returns the FeatureMap (copied back to the host) unless ``fetch`` is
         False; ``reference`` fetches it lazily later.
         """
-        pts = _points_of(scan_a)[:, :3]
+        pts = _points_of(scan_a)
         if pts.shape[0] == 0:
             raise ValueError("cannot voxelize an empty cloud")
-        self.ctx.set_reference_points(np.ascontiguousarray(pts, dtype=np.float64))
+        if pts.dtype == np.float32 and pts.shape[1] == 4:
+            self.ctx.set_reference_records(pts)  # KITTI records, 16 B/point, widened on the GPU
+        else:
+            self.ctx.set_reference_points(np.ascontiguousarray(pts[:, :3], dtype=np.float64))
         self._feat_a = None
         return self.reference if fetch else None
 

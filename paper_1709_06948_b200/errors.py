@@ -17,3 +17,18 @@ class EmptyOverlapError(VoxmiError):
 
 class NoOverlapError(VoxmiError):
     """No probed pose produced any overlap (errors.py:43)."""
+
+
+class FormatError(VoxmiError):
+    """A file does not conform to its declared format (errors.py:9-27): the
+    path, the reason, and the line or byte offset of the offending record."""
+
+    def __init__(self, path, reason: str, line: int | None = None,
+                 byte_offset: int | None = None):
+        self.path = str(path)
+        self.reason = reason
+        self.line = line
+        self.byte_offset = byte_offset
+        loc = f", line {line}" if line is not None else (
+            f", byte {byte_offset}" if byte_offset is not None else "")
+        super().__init__(f"{self.path}{loc}: {reason}")

@@ -12,7 +12,7 @@ reference's ``math.sin``/``math.cos`` products (`geometry.py:126-138`).
 from __future__ import annotations
 
 import math
-from dataclasses import dataclass
+from dataclasses import dataclass, field
 
 import numpy as np
 
@@ -27,6 +27,9 @@ class PointCloud:
 
     points: np.ndarray
     intensity: np.ndarray | None = None
+    # the (N, 4) float32 KITTI records the cloud was read from, when it was
+    # (scan_io.load_kitti_bin): the engine uploads those as they are
+    records: np.ndarray | None = field(default=None, compare=False, repr=False)
 
     def __post_init__(self):
         pts = np.ascontiguousarray(self.points, dtype=np.float64)

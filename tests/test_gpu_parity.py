@@ -604,3 +604,74 @@ def test_count_voxel_order_changes_nothing(monkeypatch):
     for x, y in zip(*out):
         np.testing.assert_array_equal(x, y)
     assert_mi_close(out[1][0], c["mi"])
+
+
+@pytest.mark.parametrize("res,kind,clamp", [(0.2, "varz", None), (0.3, "varz", None),
+                                            (0.5, "count", 1.0), (0.2, "varz", 0.5)])
+def test_occupancy_specialisation_is_exact(monkeypatch, res, kind, clamp):
+    """When every occupied voxel provably lands in one feature bin (VARZ at
+    res^2/4 * B/clamp <= 1/2; COUNT with n = 1 already saturating), the fast
+    kernel keeps voxel keys only.  Histograms, totals and statuses must equal
+    the general kernel's (VMI_NO_OCC=1) and the oracle's bit for bit.  The
+    last case (clamp 0.5 at 0.2 m) is NOT degenerate and runs the general
+    kernel both times."""
+    a, b = hdl_pair()
+    a3 = a[:, :3].astype(np.float64)
+    from paper_1709_06948_b200.synth import candidate_batch
+    poses = candidate_batch(EulerPose(1.5, 0.3, 0, 0, 0, 0.05), 40, seed=21)
+    poses[0] = (1.5, 0.3, 0, 0, 0, 0.05)
+    spec = BinningSpec(kind=FeatureKind.from_name(kind)) if clamp is None else \
+        BinningSpec(kind=FeatureKind.from_name(kind), upper_clamp=clamp)
+    out = []
+    for flag in (None, "1"):
+        if flag:
+            monkeypatch.setenv("VMI_NO_OCC", flag)
+        else:
+            monkeypatch.delenv("VMI_NO_OCC", raising=False)
+        eng = MIEngine(grid=GridSpec(resolution=res), binning=spec)
+        eng.set_reference(a3, fetch=False)
+        eng.set_query(b)
+        out.append(eng.evaluate(poses, histograms=True))
+        eng.close()
+    (mi0, st0, h0, t0), (mi1, st1, h1, t1) = out
+    np.testing.assert_array_equal(st0, st1)
+    np.testing.assert_array_equal(h0, h1)
+    np.testing.assert_array_equal(t0, t1)
+    np.testing.assert_array_equal(mi0, mi1)
+    fa = oracle.feature_map(a3, (0, 0, 0), res, kind)
+    mats = oracle.poses_to_mats(poses[:6])
+    for k in range(6):
+        _, ost, oc, otot = oracle.mi_objective_full(fa, b[:, :3].astype(np.float64), mats[k],
+                                                    res=res, clamp=spec.upper_clamp)
+        assert ost == st0[k]
+        np.testing.assert_array_equal(h0[k], oc)
+        assert otot == t0[k]
+
+
+def test_kitti_records_reference_and_pinned_ingest(tmp_path):
+    """Scan A and B from KITTI .bin files (scan_io.load_kitti_bin, pinned):
+    scan A's feature map from the float32 records (16 B/point upload, widened
+    on the GPU) equals the float64 path bit for bit, and so do histograms."""
+    from paper_1709_06948_b200.scan_io import load_kitti_bin, save_kitti_bin
+    a, b = hdl_pair()
+    save_kitti_bin(a, tmp_path / "a.bin")
+    save_kitti_bin(b, tmp_path / "b.bin")
+    ca, cb = load_kitti_bin(tmp_path / "a.bin", pinned=True), load_kitti_bin(tmp_path / "b.bin",
+                                                                             pinned=True)
+    import torch
+    assert torch.from_numpy(ca.records).is_pinned()
+    from paper_1709_06948_b200.synth import candidate_batch
+    poses = candidate_batch(EulerPose(1.5, 0.3, 0, 0, 0, 0.05), 24, seed=3)
+    out = []
+    for src_a, src_b in ((ca, cb), (a[:, :3].astype(np.float64), b)):
+        eng = engine(1.0, kind="varz")
+        fa = eng.set_reference(src_a)
+        eng.set_query(src_b)
+        out.append((fa, eng.evaluate(poses, histograms=True)))
+        eng.close()
+    (fa0, r0), (fa1, r1) = out
+    np.testing.assert_array_equal(fa0.keys, fa1.keys)
+    np.testing.assert_array_equal(fa0.values.view(np.int64), fa1.values.view(np.int64))
+    np.testing.assert_array_equal(fa0.bounds, fa1.bounds)
+    for x, y in zip(r0, r1):
+        np.testing.assert_array_equal(x, y)

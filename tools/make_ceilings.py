@@ -24,6 +24,9 @@ SOURCES = {
 }
 
 
+_BYTES = {"byte": 1.0, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9, "Tbyte": 1e12}
+
+
 def entry(path: str, poses: int) -> dict:
     d = json.load(open(os.path.join(ROOT, path)))
     ms = d["gpu__time_duration.sum"]
@@ -34,7 +37,8 @@ def entry(path: str, poses: int) -> dict:
         "kernel": d["Kernel Name"].split("(")[0],
         "poses_per_launch": poses,
         "ncu_kernel_ms": ms,
-        "dram_bytes_per_launch": int(round(d["dram_bytes_per_launch"] * 1e6)),
+        "dram_bytes_per_launch": int(round(sum(
+            d[k] * _BYTES[d["units"][k]] for k in ("dram__bytes_read.sum", "dram__bytes_write.sum")))),
         "warp_inst_per_pose": inst / poses,
         "fp64_pipe_active_frac": fp64,
         "issue_active_frac": d["smsp__issue_active.avg.pct_of_peak_sustained_active"] / 100.0,

@@ -28,6 +28,9 @@ def _raw(rep: str) -> dict:
     return {h: (v, u) for h, u, v in zip(hdr, units, vals)}
 
 
+_BYTES = {"byte": 1.0, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9, "Tbyte": 1e12}
+
+
 def _num(x):
     try:
         return float(str(x).replace(",", ""))
@@ -69,7 +72,10 @@ def full(rep: str, out: str) -> None:
                 stalls[k[len("smsp__average_warps_issue_stalled_"):-len("_per_issue_active.ratio")]] = x
     d["stall_cycles_per_issue"] = dict(sorted(stalls.items(), key=lambda t: -t[1]))
     if d.get("dram__bytes_read.sum") is not None:
-        d["dram_bytes_per_launch"] = (d.get("dram__bytes_read.sum") or 0) + (d.get("dram__bytes_write.sum") or 0)
+        # in bytes, whatever unit ncu chose for the raw fields (Mbyte, Gbyte, ...)
+        d["dram_bytes_per_launch"] = sum(
+            (d.get(k) or 0) * _BYTES.get(d["units"].get(k, "byte"), 1.0)
+            for k in ("dram__bytes_read.sum", "dram__bytes_write.sum"))
     src = subprocess.run([NCU, "-i", rep, "--page", "source", "--csv", "--print-source", "sass"],
                          capture_output=True, text=True).stdout
     rows = list(csv.reader(io.StringIO(src)))
