@@ -161,6 +161,27 @@ int vmi_argmax_device(vmi_ctx* ctx, const double* mi_dev, int64_t P, double* bes
 int vmi_topk_device(vmi_ctx* ctx, const double* mi_dev, int64_t P, int64_t K, double* top_mi,
                     int64_t* top_idx, void* stream);
 
+/* ---- Lockstep Nelder-Mead over many runs (nm_lockstep.cpp) -------------------
+   K independent nelder_mead_maximize runs (optim.py:62-175) advanced together:
+   each step hands ALL runs' pending probes to one evaluator call.  Decisions are
+   the reference's, in its order; a comparison between values closer than the
+   backend's error bound (and not from the same joint histogram) marks the run
+   `uncertain` -- the caller must redo it on exact values.  termination:
+   VMI_NM_CONVERGED_F / _X / VMI_NM_MAX_ITER.  trace: -values[0] after every sort
+   (OptimResult.trace), trace_cap doubles per run, trace_len = its length. */
+#define VMI_NM_CONVERGED_F 0
+#define VMI_NM_CONVERGED_X 1
+#define VMI_NM_MAX_ITER 2
+/* evaluator: n poses (n x 6) with their run index -> g[i] = -objective and an
+   identity h[i] of the value's source (equal identities must mean equal values) */
+typedef int (*vmi_nm_eval_fn)(void* user, const double* poses, const int32_t* run, int64_t n,
+                              double* g, uint64_t* h);
+int vmi_nm_run(int64_t K, const double* x0, const double steps[6], int max_iterations,
+               double f_tol, double x_tol, int restarts, vmi_nm_eval_fn fn, void* user,
+               double* best_x, double* best_value, int32_t* iterations, int32_t* termination,
+               int32_t* n_evaluations, int32_t* uncertain, double* trace, int32_t* trace_len,
+               int64_t trace_cap);
+
 /* Number of kernel launches issued by this context so far (bench accounting). */
 int64_t vmi_launch_count(const vmi_ctx* ctx);
 

@@ -29,7 +29,61 @@ EXPORTS = (
     "vmi_eval_poses", "vmi_eval_device", "vmi_eval_fixups", "vmi_eval_exact", "vmi_query_features",
     "vmi_fast_features",
     "vmi_argmax_device", "vmi_topk_device", "vmi_launch_count", "vmi_set_tuning", "vmi_set_passes",
+    "vmi_nm_run",
 )
+
+
+# vmi_nm_eval_fn: (user, poses, run, n, g, h) -> int
+NM_EVAL_FN = ctypes.CFUNCTYPE(ctypes.c_int, ctypes.c_void_p, ctypes.POINTER(ctypes.c_double),
+                              ctypes.POINTER(ctypes.c_int32), ctypes.c_int64,
+                              ctypes.POINTER(ctypes.c_double), ctypes.POINTER(ctypes.c_uint64))
+NM_TERMINATION = ("converged_f", "converged_x", "max_iter")
+
+
+def nm_outputs(K: int, trace_cap: int) -> dict:
+    """Host output arrays of the lockstep Nelder-Mead entry points."""
+    return {"best_x": np.zeros((K, 6)), "best_value": np.zeros(K),
+            "iterations": np.zeros(K, np.int32), "termination": np.zeros(K, np.int32),
+            "n_evaluations": np.zeros(K, np.int32), "uncertain": np.zeros(K, np.int32),
+            "trace": np.zeros((K, trace_cap)), "trace_len": np.zeros(K, np.int32)}
+
+
+def nm_out_args(o: dict) -> list:
+    return [ptr(o["best_x"], _d), ptr(o["best_value"], _d), ptr(o["iterations"], _i32),
+            ptr(o["termination"], _i32), ptr(o["n_evaluations"], _i32),
+            ptr(o["uncertain"], _i32), ptr(o["trace"], _d), ptr(o["trace_len"], _i32)]
+
+
+def nm_run(x0: np.ndarray, steps, max_iterations: int, f_tol: float, x_tol: float,
+           restarts: int, f_batch) -> dict:
+    """vmi_nm_run with a Python objective: ``f_batch(poses (n, 6), run (n,))`` ->
+    (values (n,), identities (n,) uint64).  Returns the output arrays."""
+    x0 = np.ascontiguousarray(x0, dtype=np.float64).reshape(-1, 6)
+    K = x0.shape[0]
+    st = np.ascontiguousarray(steps, dtype=np.float64).reshape(6)
+    cap = max_iterations + restarts + 2
+    o = nm_outputs(K, cap)
+    err = []
+
+    def cb(user, poses, run, n, g, h):
+        try:
+            P = np.ctypeslib.as_array(poses, shape=(n, 6)).copy()
+            R = np.ctypeslib.as_array(run, shape=(n,)).copy()
+            vals, ids = f_batch(P, R)
+            np.ctypeslib.as_array(g, shape=(n,))[:] = -np.asarray(vals, dtype=np.float64)
+            np.ctypeslib.as_array(h, shape=(n,))[:] = np.asarray(ids, dtype=np.uint64)
+            return 0
+        except Exception as e:  # noqa: BLE001 -- surfaced after the native call returns
+            err.append(e)
+            return -1
+    fn = NM_EVAL_FN(cb)
+    rc = load().vmi_nm_run(K, ptr(x0, _d), ptr(st, _d), int(max_iterations), float(f_tol),
+                           float(x_tol), int(restarts), fn, None, *nm_out_args(o), cap)
+    if err:
+        raise err[0]
+    if rc:
+        raise VmiError(f"vmi_nm_run failed ({rc})")
+    return o
 
 
 class VmiError(RuntimeError):
@@ -83,6 +137,9 @@ def load(path: str = LIB_PATH):
     L.vmi_launch_count.restype = ctypes.c_int64
     L.vmi_set_tuning.argtypes = [_ctx, ctypes.c_int, ctypes.c_int]
     L.vmi_set_passes.argtypes = [_ctx, ctypes.c_int]
+    L.vmi_nm_run.argtypes = [ctypes.c_int64, _d, _d, ctypes.c_int, ctypes.c_double,
+                             ctypes.c_double, ctypes.c_int, NM_EVAL_FN, _vp, _d, _d, _i32, _i32,
+                             _i32, _i32, _d, _i32, ctypes.c_int64]
     _lib = L
     return L
 

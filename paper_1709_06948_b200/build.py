@@ -19,8 +19,8 @@ BUILD_DIR = os.path.join(OUT_DIR, "obj")
 LIB = os.path.join(OUT_DIR, "libvmi.so")
 
 CU_SOURCES = ["k_fast.cu", "k_exact.cu", "vmi_api.cu"]
-CPP_SOURCES = ["pose_host.cpp"]
-HEADERS = ["vmi_device.cuh", "vmi_types.h", "vmi_kernels.h"]
+CPP_SOURCES = ["pose_host.cpp", "nm_lockstep.cpp"]
+HEADERS = ["vmi_device.cuh", "vmi_types.h", "vmi_kernels.h", "nm_lockstep.h"]
 
 NVCC_FLAGS = [
     "-gencode", "arch=compute_100a,code=sm_100a",
@@ -71,9 +71,9 @@ def build(verbose: bool = False, force: bool = False, out_dir: str | None = None
         s = os.path.join(CSRC, src)
         o = os.path.join(BUILD_DIR, src + ".o")
         objs.append(o)
-        if force or _stale(o, [s]):
+        if force or _stale(o, [s] + hdrs):
             cmd = ["g++", "-O2", "-fPIC", "-std=c++17", "-ffp-contract=off", "-fno-fast-math",
-                   "-c", s, "-o", o]
+                   "-Wall", "-Werror", "-c", s, "-o", o]
             subprocess.run(cmd, check=True)
     if force or _stale(LIB, objs):
         cmd = [nvcc, "-shared", "-gencode", "arch=compute_100a,code=sm_100a", "-o", LIB, *objs,

@@ -1,0 +1,42 @@
+// nm_lockstep.h -- lockstep Nelder-Mead over many scan pairs (nm_lockstep.cpp).
+#pragma once
+#include <cstdint>
+#include <functional>
+#include <vector>
+
+#include "../../include/vmi.h"
+
+namespace vmi {
+
+constexpr int kNmDim = 6;
+// OptimResult.termination (optim.py:49-59)
+constexpr int kNmConvergedF = VMI_NM_CONVERGED_F, kNmConvergedX = VMI_NM_CONVERGED_X,
+              kNmMaxIter = VMI_NM_MAX_ITER;
+
+struct NmConfig {  // SimplexConfig (optim.py:26-46)
+  double steps[kNmDim];
+  int max_iterations;
+  double f_tol, x_tol;
+  int restarts;
+};
+
+struct NmResult {
+  double best_x[kNmDim];
+  double best_value;  // MI (the maximised objective)
+  int iterations, termination, n_evaluations, n_batches, n_speculative, uncertain;
+  std::vector<double> trace, trace_spread;
+};
+
+// n poses (n x 6) with their run index -> g = -objective and a 64-bit identity
+// of the value's source (equal identities = equal values on every backend)
+using NmEvaluator =
+    std::function<int(const double* poses, const int32_t* run, int64_t n, double* g, uint64_t* h)>;
+
+int nm_lockstep(int64_t K, const double* x0, const NmConfig& cfg, const NmEvaluator& eval,
+                NmResult* out);
+
+int nm_write_results(const NmResult* res, int64_t K, double* best_x, double* best_value,
+                     int32_t* iterations, int32_t* termination, int32_t* n_evaluations,
+                     int32_t* uncertain, double* trace, int32_t* trace_len, int64_t trace_cap);
+
+}  // namespace vmi
