@@ -279,6 +279,11 @@ __device__ __forceinline__ uint32_t inside_lin(uint32_t rx, uint32_t ry, uint32_
 __device__ __forceinline__ double mkd(uint32_t lo, uint32_t hi) {
   return __hiloint2double((int)hi, (int)lo);
 }
+__device__ __forceinline__ uint32_t pin_u32(uint32_t v) {
+  uint32_t r;
+  asm volatile("mov.b32 %0, %1;" : "=r"(r) : "r"(v));
+  return r;
+}
 __device__ __forceinline__ double pin_reg(double v) {
   double r;
   asm volatile("mov.b64 %0, %1;" : "=d"(r) : "d"(v));
@@ -336,8 +341,10 @@ __global__ void __launch_bounds__(THREADS, 1)
   // Each warp's queue is aligned to its size QB, so a record address is
   // qbase | (byte offset mod QB): one LOP3 per push.
   constexpr uint32_t QB = (uint32_t)kQueue * kRec;
-  const uint32_t qbase =
-      (((uint32_t)__cvta_generic_to_shared(smem + L.queue) + QB - 1) & ~(QB - 1)) + wid * QB;
+  // (an opaque copy: otherwise it is rematerialised from the shared window
+  // base inside the point loop)
+  const uint32_t qbase = pin_u32(
+      (((uint32_t)__cvta_generic_to_shared(smem + L.queue) + QB - 1) & ~(QB - 1)) + wid * QB);
   if (KIND == 0) {
     VT.key = reinterpret_cast<VKey*>(smem + L.table);
     if (kGlobalCounts<MULTI>())  // counts next to the sums in L2 (native RED.ADD.U32)
@@ -401,10 +408,14 @@ __global__ void __launch_bounds__(THREADS, 1)
       const int amx = max(max(abs(A.amin[0]), abs(A.amin[1])), abs(A.amin[2]));
       const double lim = (MODE == kGridGeneral ? 2097152.0 - (double)amx : 1073741824.0) * g.res;
       const double mx = B.max_abs;
-      const bool unsafe =
-          fabs(t0 - g.origin[0]) + (fabs(m0) + fabs(m1) + fabs(m2)) * mx >= lim ||
-          fabs(t1 - g.origin[1]) + (fabs(m3) + fabs(m4) + fabs(m5)) * mx >= lim ||
-          fabs(t2 - g.origin[2]) + (fabs(m6) + fabs(m7) + fabs(m8)) * mx >= lim;
+      const double r0 = (fabs(m0) + fabs(m1) + fabs(m2)) * mx, r1 = (fabs(m3) + fabs(m4) + fabs(m5)) * mx,
+                   r2 = (fabs(m6) + fabs(m7) + fabs(m8)) * mx;
+      bool unsafe = fabs(t0 - g.origin[0]) + r0 >= lim || fabs(t1 - g.origin[1]) + r1 >= lim ||
+                    fabs(t2 - g.origin[2]) + r2 >= lim;
+      if (MODE == kGridGeneral) {  // the fast floor's |s + t| term (locate)
+        const double lim2 = 16777216.0 * g.res;
+        unsafe |= fabs(t0) + r0 >= lim2 || fabs(t1) + r1 >= lim2 || fabs(t2) + r2 >= lim2;
+      }
       if (unsafe) {
         if (tid == 0) {
           mi_out[p] = -1e300;
@@ -415,6 +426,17 @@ __global__ void __launch_bounds__(THREADS, 1)
         continue;
       }
     }
+
+    // general resolutions: u = RN(t - o) for the fast floor (locate), and the
+    // bound on its per-point error E in Z - o (locate: <= 2^-52 (|t| + |o| +
+    // |R p|)), which shifts each d by up to E: VARZ moves by <= 2 res E + E^2
+    const double u0 = __dsub_rn(t0, g.origin[0]), u1 = __dsub_rn(t1, g.origin[1]),
+                 u2 = __dsub_rn(t2, g.origin[2]);
+    const double var_shift =
+        MODE == kGridGeneral
+            ? 2.0 * g.res * 2.220446049250313e-16 *
+                  (fabs(t2) + fabs(g.origin[2]) + (fabs(m6) + fabs(m7) + fabs(m8)) * B.max_abs + g.res)
+            : 0.0;
 
     // ---- overlap region (voxel.py:298-318) -------------------------------
     int status = 0;
@@ -541,13 +563,25 @@ __global__ void __launch_bounds__(THREADS, 1)
       // inside A's AABB, and d = z - (the voxel's lower z face): pure per point
       auto locate = [&](double x, double y, double z, uint32_t& lin, double& d, int& ix, int& iy,
                         int& iz) {
-        const double X = xform_row(x, y, z, m0, m1, m2, t0);
-        const double Y = xform_row(x, y, z, m3, m4, m5, t1);
-        const double Z = xform_row(x, y, z, m6, m7, m8, t2);
         if constexpr (MODE == kGridGeneral) {
-          const double qx = __dmul_rn(__dsub_rn(X, g.origin[0]), g.inv_res);
-          const double qy = __dmul_rn(__dsub_rn(Y, g.origin[1]), g.inv_res);
-          const double qz = __dmul_rn(__dsub_rn(Z, g.origin[2]), g.inv_res);
+          // Fast floor of q = (X - o) / res: q' = RN(RN(s + u) * RN(1/res)) with
+          // s = the rows' FMA chains (xform_row before + t) and u = RN(t - o)
+          // per pose.  |q' - numpy's RN(RN(X - o) / res)| <= (|t - o| + |X - o|
+          // + |s + t|) / res * 2^-53 + |q| * 2^-52 < 2^-27.5 voxel under the
+          // pose bounds of `unsafe` (|t - o| + |R p| < 2^21 res, |t| + |R p| <
+          // 2^24 res).  q' is floored on a 2^-29 grid by DADD.RM against
+          // 1.5*2^23 - amin (mantissa >> 29 = 2^22 + floor(q') - amin, low 29
+          // bits = the fraction); only a fraction within 4 grid steps (2^-27) of
+          // an integer can floor differently from the reference, and such a
+          // point (about 1 in 10^8) takes the reference's own X = RN(s + t) and
+          // IEEE quotient.
+          const double sx = rot_row(x, y, z, m0, m1, m2);
+          const double sy = rot_row(x, y, z, m3, m4, m5);
+          const double sz = rot_row(x, y, z, m6, m7, m8);
+          const double Zp = __dadd_rn(sz, u2);  // ~ Z - o_z
+          const double qx = __dmul_rn(__dadd_rn(sx, u0), g.inv_res);
+          const double qy = __dmul_rn(__dadd_rn(sy, u1), g.inv_res);
+          const double qz = __dmul_rn(Zp, g.inv_res);
           const double rx = __dadd_rd(qx, kf0), ry = __dadd_rd(qy, kf1), rz = __dadd_rd(qz, kf2);
           const uint32_t lx = (uint32_t)__double2loint(rx), ly = (uint32_t)__double2loint(ry),
                          lz = (uint32_t)__double2loint(rz);
@@ -555,23 +589,29 @@ __global__ void __launch_bounds__(THREADS, 1)
           ix = (int)(__funnelshift_r(lx, (uint32_t)__double2hiint(rx), 29) - kFB);
           iy = (int)(__funnelshift_r(ly, (uint32_t)__double2hiint(ry), 29) - kFB);
           iz = (int)(__funnelshift_r(lz, (uint32_t)__double2hiint(rz), 29) - kFB);
-          const bool near = ((lx + 4u) & 0x1FFFFFFFu) < 8u || ((ly + 4u) & 0x1FFFFFFFu) < 8u ||
-                            ((lz + 4u) & 0x1FFFFFFFu) < 8u;
-          double qf = __dsub_rn(__dadd_rd(qz, 6755399441055744.0), 6755399441055744.0);
-          if (VMI_NEAR_FIX && __builtin_expect(near, 0)) {  // the reference's IEEE quotient
+          // fraction within 4 steps of an integer: ((l + 4) << 3) < 64, all three at once
+          const bool near = __vimin3_u32(lx * 8u + 32u, ly * 8u + 32u, lz * 8u + 32u) < 64u;
+          // floor(q_z) as a double: rz with its 29 fraction bits cleared, minus kf2
+          double qf = __dsub_rn(__hiloint2double(__double2hiint(rz), (int)(lz & 0xE0000000u)), kf2);
+          if (VMI_NEAR_FIX && __builtin_expect(near, 0)) {  // the reference's X and IEEE quotient
+            const double X = __dadd_rn(sx, t0), Y = __dadd_rn(sy, t1), Z = __dadd_rn(sz, t2);
             ix = __double2loint(__dadd_rd(grid_q<MODE>(X, g.origin[0], g.res, g.inv_res), kc0));
             iy = __double2loint(__dadd_rd(grid_q<MODE>(Y, g.origin[1], g.res, g.inv_res), kc1));
             const double fz = __dadd_rd(grid_q<MODE>(Z, g.origin[2], g.res, g.inv_res), kc2);
             iz = __double2loint(fz);
             qf = __dsub_rn(fz, kc2);
           }
-          d = __dsub_rn(Z, __fma_rn(qf, g.res, g.origin[2]));
+          // pivot: the voxel's lower face relative to o_z (a function of the voxel)
+          d = __fma_rn(-qf, g.res, Zp);
           lin = inside_lin((uint32_t)ix, (uint32_t)iy, (uint32_t)iz, ex0, ex1, ex2);
           if (MULTI && npass > 1 && lin != kNoVoxel &&
               __umulhi(lin * 0x85EBCA6Bu, (uint32_t)npass) != (uint32_t)pass)
             lin = kNoVoxel;  // another pass's partition
           return;
         }
+        const double X = xform_row(x, y, z, m0, m1, m2, t0);
+        const double Y = xform_row(x, y, z, m3, m4, m5, t1);
+        const double Z = xform_row(x, y, z, m6, m7, m8, t2);
         const double fx = __dadd_rd(grid_q<MODE>(X, g.origin[0], g.res, g.inv_res), kc0);
         const double fy = __dadd_rd(grid_q<MODE>(Y, g.origin[1], g.res, g.inv_res), kc1);
         const double fz = __dadd_rd(grid_q<MODE>(Z, g.origin[2], g.res, g.inv_res), kc2);
@@ -741,7 +781,7 @@ __global__ void __launch_bounds__(THREADS, 1)
           const double k = rint(x);
           if (k >= 1.0 && k <= bins_d - 1.0) {
             const double tol = ((nd + 8.0) * 4.440892098500626e-16 * (S2 + c1) * rn +
-                                feat * 9.094947017729282e-13) * bin_scale + 1e-300;
+                                feat * 9.094947017729282e-13 + var_shift) * bin_scale + 1e-300;
             if (fabs(x - k) <= tol) recheck = true;
           }
           const double f = floor(x);
@@ -836,6 +876,7 @@ __global__ void __launch_bounds__(THREADS, 1)
       } else {
         // COUNT / occupancy: four slots per thread per step, four A-grid loads
         // in flight (no L2 sums to fetch: compaction measured slower here)
+        uint32_t occ_miss = 0, occ_hit = 0;
         for (int s0 = tid; s0 < cap; s0 += 4 * THREADS) {
           uint32_t lin[4];
           int ba[4];
@@ -850,8 +891,26 @@ __global__ void __launch_bounds__(THREADS, 1)
             ba[u] = lin[u] != kNoVoxel ? (int)__ldg(&A.grid[lin[u]]) : 0;
           }
 #pragma unroll
-          for (int u = 0; u < 4; ++u)
-            if (lin[u] != kNoVoxel) finish_slot(s0 + u * THREADS, lin[u], ba[u], make_double2(0.0, 0.0), 0u);
+          for (int u = 0; u < 4; ++u) {
+            if (lin[u] == kNoVoxel) continue;
+            if (KIND == kKindOcc && !dump.keys && (ba[u] == 0 || ba[u] == g.occ_bin)) {
+              // occupancy: A's occupied voxels share the one bin too, so nearly
+              // every cell update lands on (0, occ) or (occ, occ): count them
+              // in registers (one atomic per warp below, not one per voxel)
+              ckey[s0 + u * THREADS] = kEmpty32;
+              if (ba[u] == 0) ++occ_miss; else ++occ_hit;
+            } else {
+              finish_slot(s0 + u * THREADS, lin[u], ba[u], make_double2(0.0, 0.0), 0u);
+            }
+          }
+        }
+        if (KIND == kKindOcc) {
+          occ_miss = __reduce_add_sync(0xffffffffu, occ_miss);
+          occ_hit = __reduce_add_sync(0xffffffffu, occ_hit);
+          if (lane == 0) {
+            if (occ_miss) atomicAdd(&hist[g.occ_bin], occ_miss);
+            if (occ_hit) atomicAdd(&hist[g.occ_bin * W + g.occ_bin], occ_hit);
+          }
         }
       }
       VMI_TR("walk done", 0)

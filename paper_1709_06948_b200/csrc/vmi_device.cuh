@@ -43,6 +43,11 @@ __device__ __forceinline__ void split_decode(uint4 v, double& x, double& y, doub
 
 // ---- geometry.py:162-166: numpy `points @ R.T + t` through OpenBLAS dgemm is,
 // bit for bit, fma(z, R[j][2], fma(y, R[j][1], x * R[j][0])) + t[j].
+// the same chain before + t[j] (R p alone)
+__device__ __forceinline__ double rot_row(double x, double y, double z, double r0, double r1,
+                                          double r2) {
+  return __fma_rn(z, r2, __fma_rn(y, r1, __dmul_rn(x, r0)));
+}
 __device__ __forceinline__ double xform_row(double x, double y, double z, double r0, double r1,
                                             double r2, double t) {
   return __dadd_rn(__fma_rn(z, r2, __fma_rn(y, r1, __dmul_rn(x, r0))), t);
