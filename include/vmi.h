@@ -182,6 +182,35 @@ int vmi_nm_run(int64_t K, const double* x0, const double steps[6], int max_itera
                int32_t* n_evaluations, int32_t* uncertain, double* trace, int32_t* trace_len,
                int64_t trace_cap);
 
+/* ---- Many resident scan pairs (C5: a drive's consecutive pairs) ---------------
+   vmi_set_pairs builds npairs (scan A, scan B) pairs on the device at once --
+   each scan A voxelized + featurized (_prepare, align.py:114-119) into its own
+   dense bin grid, each scan B in its own span layout -- replacing any previous
+   set.  a[i] / b[i]: host points, (n, 4) float32 KITTI records (is_rec = 1) or
+   (n, 3) float64 (is_rec = 0).  Independent of the single pair set by
+   vmi_set_reference_* / vmi_set_query_*. */
+int vmi_set_pairs(vmi_ctx* ctx, int64_t npairs, const void* const* a, const int64_t* na,
+                  const void* const* b, const int64_t* nb, int is_rec);
+
+/* mi_objective (mi.py:194-219) for P poses, pose p against pair pair[p] of the
+   set, in ONE multi-pair kernel launch; host buffers, synchronous.  hash_out
+   (nullable): a 64-bit identity of each pose's joint histogram (equal identity
+   => equal histogram, up to 2^-64 collisions; 0 for sentinel poses); hist_out
+   (nullable) as vmi_eval. */
+int vmi_eval_pairs(vmi_ctx* ctx, const double* poses, const int32_t* pair, int64_t P,
+                   double* mi_out, int32_t* status_out, uint64_t* hash_out, int64_t* hist_out);
+
+/* align()'s optimiser (optim.py:62-175, align.py:122-159) for every pair of the
+   set at once: vmi_nm_run with the multi-pair kernel as the objective (one
+   launch per lockstep step across all pairs).  x0: one start pose (6) per pair.
+   Outputs as vmi_nm_run; a run flagged `uncertain` met a comparison the GPU's
+   MI cannot decide exactly and must be redone on exact values. */
+int vmi_align_pairs(vmi_ctx* ctx, int64_t K, const double* x0, const double steps[6],
+                    int max_iterations, double f_tol, double x_tol, int restarts, double* best_x,
+                    double* best_value, int32_t* iterations, int32_t* termination,
+                    int32_t* n_evaluations, int32_t* uncertain, double* trace, int32_t* trace_len,
+                    int64_t trace_cap);
+
 /* Number of kernel launches issued by this context so far (bench accounting). */
 int64_t vmi_launch_count(const vmi_ctx* ctx);
 

@@ -8,7 +8,7 @@ kernels behind a C ABI (include/vmi.h, libvmi.so).  See DESIGN.md.
 from .api import (SWEEP_AXES, SearchResult, clear_cache, compute_feature_map, engine_for,
                   grid_search, grid_search_sharded, joint_histogram_at, mi_at, mi_objective,
                   mi_objective_batch, sweep_axis)
-from .align import AlignmentReport, align
+from .align import AlignmentReport, align, align_batch
 from .engine import MIEngine, entropy_exact, mutual_information_exact
 from .optim import OptimResult, SimplexConfig, nelder_mead_maximize_batched
 from .errors import EmptyOverlapError, NoOverlapError, OutOfBoundsError, VoxmiError
@@ -20,7 +20,7 @@ from .types import (DEFAULT_BIN_COUNT, DEFAULT_UPPER_CLAMP, KEY_INDEX_MAX, KEY_I
 from ._lib import VmiError, poses_to_mats
 
 __all__ = [
-    "AlignmentReport", "align", "OptimResult", "SimplexConfig", "nelder_mead_maximize_batched",
+    "AlignmentReport", "align", "align_batch", "OptimResult", "SimplexConfig", "nelder_mead_maximize_batched",
     "normalized", "transform_to_euler", "validate_transform",
     "SWEEP_AXES", "SearchResult", "clear_cache", "compute_feature_map", "engine_for",
     "grid_search", "grid_search_sharded", "joint_histogram_at", "mi_at", "mi_objective",

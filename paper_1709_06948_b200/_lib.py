@@ -29,7 +29,7 @@ EXPORTS = (
     "vmi_eval_poses", "vmi_eval_device", "vmi_eval_fixups", "vmi_eval_exact", "vmi_query_features",
     "vmi_fast_features",
     "vmi_argmax_device", "vmi_topk_device", "vmi_launch_count", "vmi_set_tuning", "vmi_set_passes",
-    "vmi_nm_run",
+    "vmi_nm_run", "vmi_set_pairs", "vmi_eval_pairs", "vmi_align_pairs",
 )
 
 
@@ -140,6 +140,13 @@ def load(path: str = LIB_PATH):
     L.vmi_nm_run.argtypes = [ctypes.c_int64, _d, _d, ctypes.c_int, ctypes.c_double,
                              ctypes.c_double, ctypes.c_int, NM_EVAL_FN, _vp, _d, _d, _i32, _i32,
                              _i32, _i32, _d, _i32, ctypes.c_int64]
+    L.vmi_set_pairs.argtypes = [_ctx, ctypes.c_int64, ctypes.POINTER(_vp), _i64,
+                                ctypes.POINTER(_vp), _i64, ctypes.c_int]
+    L.vmi_eval_pairs.argtypes = [_ctx, _d, _i32, ctypes.c_int64, _d, _i32,
+                                 ctypes.POINTER(ctypes.c_uint64), _i64]
+    L.vmi_align_pairs.argtypes = [_ctx, ctypes.c_int64, _d, _d, ctypes.c_int, ctypes.c_double,
+                                  ctypes.c_double, ctypes.c_int, _d, _d, _i32, _i32, _i32, _i32,
+                                  _d, _i32, ctypes.c_int64]
     _lib = L
     return L
 
@@ -262,6 +269,61 @@ class Context:
             raise ValueError("records must be (N, 4) float32")
         self.check(self._L.vmi_set_query_records_f32(self._h, ptr(rec, _f), rec.shape[0]),
                    "vmi_set_query_records_f32")
+
+    def set_pairs(self, pairs):
+        """vmi_set_pairs: [(scan A, scan B), ...] as (N, 4) float32 records (all
+        pairs) or (N, 3) float64 arrays (all pairs)."""
+        arrs = []
+        rec = None
+        for a, b in pairs:
+            for x in (a, b):
+                is_rec = x.dtype == np.float32 and x.ndim == 2 and x.shape[1] == 4
+                if rec is None:
+                    rec = is_rec
+                if is_rec != rec:
+                    raise ValueError("all scans of a pair set must share one format")
+                arrs.append(np.ascontiguousarray(x, dtype=np.float32 if rec else np.float64))
+        K = len(pairs)
+        a_ptr = (_vp * max(K, 1))(*[arrs[2 * i].ctypes.data for i in range(K)])
+        b_ptr = (_vp * max(K, 1))(*[arrs[2 * i + 1].ctypes.data for i in range(K)])
+        na = np.array([arrs[2 * i].shape[0] for i in range(K)], dtype=np.int64)
+        nb = np.array([arrs[2 * i + 1].shape[0] for i in range(K)], dtype=np.int64)
+        rc = self._L.vmi_set_pairs(self._h, K, a_ptr, ptr(na, _i64), b_ptr, ptr(nb, _i64),
+                                   int(bool(rec)))
+        if rc == -5:
+            from .errors import OutOfBoundsError
+            raise OutOfBoundsError(self._L.vmi_last_error(self._h).decode())
+        self.check(rc, "vmi_set_pairs")
+
+    def eval_pairs(self, poses: np.ndarray, pair: np.ndarray, want_hist: bool = False,
+                   bins: int = 32):
+        poses = np.ascontiguousarray(poses, dtype=np.float64).reshape(-1, 6)
+        pair = np.ascontiguousarray(pair, dtype=np.int32).reshape(-1)
+        P = poses.shape[0]
+        if pair.shape[0] != P:
+            raise ValueError("one pair index per pose")
+        mi = np.empty(P, dtype=np.float64)
+        st = np.empty(P, dtype=np.int32)
+        h = np.empty(P, dtype=np.uint64)
+        hist = np.empty((P, bins + 1, bins + 1), dtype=np.int64) if want_hist else None
+        self.check(self._L.vmi_eval_pairs(self._h, ptr(poses, _d), ptr(pair, _i32), P, ptr(mi, _d),
+                                          ptr(st, _i32), h.ctypes.data_as(
+                                              ctypes.POINTER(ctypes.c_uint64)),
+                                          ptr(hist, _i64) if want_hist else None),
+                   "vmi_eval_pairs")
+        return mi, st, h, hist
+
+    def align_pairs(self, x0: np.ndarray, steps, max_iterations: int, f_tol: float, x_tol: float,
+                    restarts: int) -> dict:
+        x0 = np.ascontiguousarray(x0, dtype=np.float64).reshape(-1, 6)
+        K = x0.shape[0]
+        st = np.ascontiguousarray(steps, dtype=np.float64).reshape(6)
+        cap = max_iterations + restarts + 2
+        o = nm_outputs(K, cap)
+        self.check(self._L.vmi_align_pairs(self._h, K, ptr(x0, _d), ptr(st, _d), int(max_iterations),
+                                           float(f_tol), float(x_tol), int(restarts),
+                                           *nm_out_args(o), cap), "vmi_align_pairs")
+        return o
 
     def eval(self, mats: np.ndarray, want_hist: bool = False, bins: int = 32, exact: bool = False):
         mats = np.ascontiguousarray(mats, dtype=np.float64).reshape(-1, 12)

@@ -77,16 +77,21 @@ def exact_objective(eng: MIEngine):
     return f_batch
 
 
-def align(scan_a, scan_b, t0, cfg: AlignmentConfig | None = None,
-          device: int = 0) -> AlignmentReport:
-    """Estimate the transform projecting scan B onto scan A (align.py:122-159)."""
-    cfg = cfg or AlignmentConfig()
+def _simplex_of(cfg: AlignmentConfig) -> SimplexConfig:
     simplex = cfg.simplex if isinstance(cfg.simplex, SimplexConfig) else (
         SimplexConfig(**{k: getattr(cfg.simplex, k) for k in
                          ("initial_steps", "max_iterations", "f_tol", "x_tol", "restarts")})
         if cfg.simplex is not None else SimplexConfig())
     if len(simplex.initial_steps) != 6:
         raise ValueError("simplex initial_steps must have 6 entries")
+    return simplex
+
+
+def align(scan_a, scan_b, t0, cfg: AlignmentConfig | None = None,
+          device: int = 0) -> AlignmentReport:
+    """Estimate the transform projecting scan B onto scan A (align.py:122-159)."""
+    cfg = cfg or AlignmentConfig()
+    simplex = _simplex_of(cfg)
     t0 = validate_transform(t0)
     n_a = len(getattr(scan_a, "points", scan_a))
     n_b = len(getattr(scan_b, "points", scan_b))
@@ -120,3 +125,85 @@ def align(scan_a, scan_b, t0, cfg: AlignmentConfig | None = None,
         n_evaluations=result.n_evaluations,
         n_batches=result.n_batches,
     )
+
+
+def align_batch(pairs, t0s, cfg: AlignmentConfig | None = None, device: int = 0,
+                raise_errors: bool = True, stats: dict | None = None,
+                engine: MIEngine | None = None) -> list:
+    """``align`` for many scan pairs at once (C5: a drive's consecutive pairs).
+
+    Every pair's scans are resident together and all Nelder-Mead runs advance
+    in lockstep inside the library (vmi_align_pairs): one multi-pair kernel
+    launch per step scores every run's pending probes.  Decisions are the
+    reference's (align.py:122-159 / optim.py:62-175) on GPU MI values; a run
+    that met a comparison those values cannot decide exactly (operands within
+    the GPU's error bound, different histograms) is redone with ``align`` on
+    exact values, so every report is the reference's.  Each report's
+    ``final_mi`` is the reference formula on the estimate's bit-exact
+    histogram; ``mi_trace`` holds GPU MI values (within ~1e-13).  A pair with
+    no overlapping probe raises ``NoOverlapError`` (or, with ``raise_errors``
+    False, gets the exception in its slot).  ``wall_time`` is the batch's
+    optimisation time (all pairs together); ``stats`` (a dict) receives counts.
+    ``engine``: an MIEngine built for ``cfg`` to reuse (its grow-only device
+    buffers survive across calls, e.g. a drive aligned in batches).
+    """
+    from ._lib import NM_TERMINATION
+    cfg = cfg or AlignmentConfig()
+    simplex = _simplex_of(cfg)
+    pairs = list(pairs)
+    if len(t0s) != len(pairs):
+        raise ValueError("one start transform per pair")
+    if not pairs:
+        return []
+    init = [transform_to_euler(validate_transform(t)) for t in t0s]
+    eng = engine or MIEngine(grid=cfg.grid, binning=cfg.binning, include_phi=cfg.phi_enabled,
+                             device=device)
+    K = len(pairs)
+    t_set = time.perf_counter()
+    try:
+        eng.set_pairs(pairs)
+        start = time.perf_counter()
+        o = eng.ctx.align_pairs(np.stack([p.as_vector() for p in init]), simplex.initial_steps,
+                                simplex.max_iterations, simplex.f_tol, simplex.x_tol,
+                                simplex.restarts)
+        wall = time.perf_counter() - start
+        est = [normalized(EulerPose.from_vector(o["best_x"][k])) for k in range(K)]
+        _, st, _, hist = eng.evaluate_pairs(np.stack([e.as_vector() for e in est]), np.arange(K),
+                                            histograms=True)
+        t_final = time.perf_counter()
+    finally:
+        if engine is None:
+            eng.close()
+    out = []
+    redo = 0
+    for k in range(K):
+        if o["uncertain"][k]:
+            redo += 1
+            try:
+                out.append(align(pairs[k][0], pairs[k][1], t0s[k], cfg, device))
+            except NoOverlapError as e:
+                if raise_errors:
+                    raise
+                out.append(e)
+            continue
+        if o["best_value"][k] <= NO_OVERLAP_SENTINEL:
+            err = NoOverlapError("no candidate pose produced overlapping occupied bounds")
+            if raise_errors:
+                raise err
+            out.append(err)
+            continue
+        final_mi = (mutual_information_exact(hist[k], cfg.phi_enabled)[0] if st[k] == 0
+                    else NO_OVERLAP_SENTINEL)
+        n = int(o["trace_len"][k])
+        out.append(AlignmentReport(
+            estimated=euler_to_transform(est[k]), estimated_pose=est[k], initial_pose=init[k],
+            final_mi=float(final_mi), mi_trace=[*o["trace"][k, :n].tolist(), float(final_mi)],
+            iterations=int(o["iterations"][k]), wall_time=wall,
+            termination=NM_TERMINATION[int(o["termination"][k])],
+            n_evaluations=int(o["n_evaluations"][k])))
+    if stats is not None:
+        stats.update(pairs=K, redone_exact=redo, wall_time=wall,
+                     evaluations=int(np.sum(o["n_evaluations"])),
+                     set_pairs_s=start - t_set, final_eval_s=t_final - start - wall,
+                     reports_s=time.perf_counter() - t_final)
+    return out

@@ -202,10 +202,10 @@ cudaError_t exact_voxelize(ExactScratch& s, const PointSource& src, const double
 
 // ---- scan A's reference grid -------------------------------------------------
 __global__ void k_build_grid(const unsigned long long* keys, const double* values, int V,
-                             GridParams g, int3 amin, uint3 ext, uint8_t* grid, int4* avox_tmp,
-                             uint32_t* bin_total) {
+                             const int* Vdev, GridParams g, int3 amin, uint3 ext, uint8_t* grid,
+                             int4* avox_tmp, uint32_t* bin_total) {
   const int v = blockIdx.x * blockDim.x + threadIdx.x;
-  if (v >= V) return;
+  if (v >= (Vdev ? *Vdev : V)) return;
   const unsigned long long k = keys[v];
   const int x = (int)((k >> 42) & 0x1FFFFF) - (1 << 20);
   const int y = (int)((k >> 21) & 0x1FFFFF) - (1 << 20);
@@ -230,23 +230,25 @@ __global__ void k_bin_offsets(const uint32_t* bin_total, int W, int* cursor) {
   }
 }
 
-__global__ void k_scatter_by_bin(const int4* avox_tmp, int V, int* cursor, int4* avox) {
+__global__ void k_scatter_by_bin(const int4* avox_tmp, int V, const int* Vdev, int* cursor,
+                                 int4* avox) {
   const int v = blockIdx.x * blockDim.x + threadIdx.x;
-  if (v >= V) return;
+  if (v >= (Vdev ? *Vdev : V)) return;
   const int4 a = avox_tmp[v];
   if (a.w >= 0) avox[atomicAdd(&cursor[a.w], 1)] = a;
 }
 
 cudaError_t build_reference(const unsigned long long* keys, const double* values, int V,
-                            const GridParams& g, const int amin[3], const uint32_t ext[3],
-                            uint8_t* grid, int4* tmp, int4* avox, uint32_t* bin_total,
-                            int* cursor, cudaStream_t st, int64_t* launches) {
+                            const int* Vdev, const GridParams& g, const int amin[3],
+                            const uint32_t ext[3], uint8_t* grid, int4* tmp, int4* avox,
+                            uint32_t* bin_total, int* cursor, cudaStream_t st, int64_t* launches) {
   if (V <= 0) return cudaSuccess;
   const int T = 256, blocks = (V + T - 1) / T;
-  k_build_grid<<<blocks, T, 0, st>>>(keys, values, V, g, make_int3(amin[0], amin[1], amin[2]),
+  k_build_grid<<<blocks, T, 0, st>>>(keys, values, V, Vdev, g,
+                                     make_int3(amin[0], amin[1], amin[2]),
                                      make_uint3(ext[0], ext[1], ext[2]), grid, tmp, bin_total);
   k_bin_offsets<<<1, 32, 0, st>>>(bin_total, g.bins + 1, cursor);
-  k_scatter_by_bin<<<blocks, T, 0, st>>>(tmp, V, cursor, avox);
+  k_scatter_by_bin<<<blocks, T, 0, st>>>(tmp, V, Vdev, cursor, avox);
   if (launches) *launches += 3;
   return cudaGetLastError();
 }
@@ -388,37 +390,45 @@ cudaError_t topk_sort(const double* mi, int P, double* keys_out, int* idx_in, in
 }
 
 // ---- span layout (see QueryView) ------------------------------------------------
-__global__ void k_span_layout(const void* src, int is_f32, int64_t n, int span, int rem,
-                              int threads, void* dst) {
+// Contiguous host-order points -> the fast kernel's span layout: split-double
+// float4 records (out_split; every coordinate float32-exact), else double4.
+// src is float32 (x, y, z, i) records (in_f32) or (n, 3) doubles.
+__global__ void k_span_layout(const void* src, int in_f32, int out_split, int64_t n, int span,
+                              int rem, int threads, void* dst) {
   const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;  // original index
   const int64_t total = (int64_t)span * threads;
   if (i >= total) return;
+  double x = 0.0, y = 0.0, z = 0.0;
+  int64_t li;
   if (i >= n) {  // padding slots: the (threads - rem) unused last-iteration entries
-    const int64_t li = (int64_t)(span - 1) * threads + thread_of_span(rem + (int)(i - n), threads);
-    if (is_f32) reinterpret_cast<float4*>(dst)[li] = make_float4(0.f, 0.f, 0.f, 0.f);
-    else reinterpret_cast<double4*>(dst)[li] = make_double4(0.0, 0.0, 0.0, 0.0);
-    return;
+    li = (int64_t)(span - 1) * threads + thread_of_span(rem + (int)(i - n), threads);
+  } else {
+    li = span_slot(i, span, rem, threads);
+    if (in_f32) {
+      const float4 v = reinterpret_cast<const float4*>(src)[i];
+      x = v.x; y = v.y; z = v.z;
+    } else {
+      const double* s = reinterpret_cast<const double*>(src);
+      x = s[3 * i]; y = s[3 * i + 1]; z = s[3 * i + 2];
+    }
   }
-  const int64_t li = span_slot(i, span, rem, threads);
-  if (is_f32) {
-    const float4 v = reinterpret_cast<const float4*>(src)[i];
+  if (out_split) {  // (the intensity is unused)
 #if VMI_SPLITREC
-    reinterpret_cast<uint4*>(dst)[li] = split_encode(v.x, v.y, v.z);  // (the intensity is unused)
+    reinterpret_cast<uint4*>(dst)[li] = split_encode((float)x, (float)y, (float)z);
 #else
-    reinterpret_cast<float4*>(dst)[li] = v;
+    reinterpret_cast<float4*>(dst)[li] = make_float4((float)x, (float)y, (float)z, 0.f);
 #endif
   } else {
-    const double* s = reinterpret_cast<const double*>(src);
-    reinterpret_cast<double4*>(dst)[li] = make_double4(s[3 * i], s[3 * i + 1], s[3 * i + 2], 0.0);
+    reinterpret_cast<double4*>(dst)[li] = make_double4(x, y, z, 0.0);
   }
 }
 
-cudaError_t launch_span_layout(const void* src, int is_f32, int64_t n, int span, int rem,
-                               int threads, void* dst, cudaStream_t st) {
+cudaError_t launch_span_layout(const void* src, int in_f32, int out_split, int64_t n, int span,
+                               int rem, int threads, void* dst, cudaStream_t st) {
   const int64_t total = (int64_t)span * threads;
   const int T = 256;
-  k_span_layout<<<(unsigned)((total + T - 1) / T), T, 0, st>>>(src, is_f32, n, span, rem, threads,
-                                                               dst);
+  k_span_layout<<<(unsigned)((total + T - 1) / T), T, 0, st>>>(src, in_f32, out_split, n, span,
+                                                               rem, threads, dst);
   return cudaGetLastError();
 }
 

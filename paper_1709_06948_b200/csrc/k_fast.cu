@@ -304,13 +304,30 @@ __device__ __forceinline__ double pin_reg(double v) {
 #define VMI_TR(msg, a)
 #endif
 
-template <int THREADS, int NS, int KIND, bool F32, int MODE, bool MULTI>
+// 64-bit identity of a joint histogram: sum of cell * mix(cell index) mod 2^64
+// (order-free, so any reduction order gives the same value; splitmix64 mixer)
+__device__ __forceinline__ unsigned long long cell_mix(unsigned long long i) {
+  i += 0x9E3779B97F4A7C15ull;
+  i = (i ^ (i >> 30)) * 0xBF58476D1CE4E5B9ull;
+  i = (i ^ (i >> 27)) * 0x94D049BB133111EBull;
+  return i ^ (i >> 31);
+}
+
+// MP (multi-pair): pose p scores pair pose_pair[p] of pairs[] (descriptor
+// copied to shared memory per pose); otherwise the kernel parameters A0/B0.
+template <int THREADS, int NS, int KIND, bool F32, int MODE, bool MULTI, bool MP>
 __global__ void __launch_bounds__(THREADS, 1)
-    k_pose_fast(GridParams g, RefView A, QueryView B, const double* __restrict__ mats, int64_t P,
+    k_pose_fast(GridParams g, const __grid_constant__ RefView A0,
+                const __grid_constant__ QueryView B0, const double* __restrict__ mats, int64_t P,
                 int cap, double* __restrict__ mi_out, int32_t* __restrict__ status_out,
                 long long* __restrict__ hist_out, long long* __restrict__ total_out,
-                FeatureDump dump, double2* __restrict__ gsums, int npass) {
+                FeatureDump dump, double2* __restrict__ gsums, int npass,
+                const PairDesc* __restrict__ pairs, const int32_t* __restrict__ pose_pair,
+                unsigned long long* __restrict__ hash_out) {
   static_assert(NS == 1, "one span per thread");
+  static_assert(sizeof(PairDesc) % 4 == 0 && sizeof(PairDesc) / 4 <= THREADS, "descriptor copy");
+  __shared__ __align__(16) PairDesc desc_s;
+  __shared__ unsigned long long hash_s[THREADS / 32];
   extern __shared__ __align__(16) unsigned char smem[];
   const int W = g.bins + 1;
   const FastSmem L = fast_layout(KIND, cap, W, THREADS, F32 ? 1 : 0, NS, MULTI ? 1 : 0);
@@ -382,6 +399,9 @@ __global__ void __launch_bounds__(THREADS, 1)
   // behind the current pose instead of stalling the whole CTA at pose start)
   double mat_next = (tid < 12 && blockIdx.x < P) ? mats[(int64_t)blockIdx.x * 12 + tid] : 0.0;
   for (int64_t p = blockIdx.x; p < P; p += gridDim.x) {
+    if (MP && tid < (int)(sizeof(PairDesc) / 4))
+      reinterpret_cast<uint32_t*>(&desc_s)[tid] =
+          reinterpret_cast<const uint32_t*>(pairs + pose_pair[p])[tid];
     for (int i = tid; i < W * W; i += THREADS) hist[i] = 0u;
     for (int i = tid; i < W; i += THREADS) marg[i] = 0u;
     if (tid < 3) { misc[tid] = INT_MAX; misc[3 + tid] = INT_MIN; }
@@ -396,6 +416,8 @@ __global__ void __launch_bounds__(THREADS, 1)
 #endif
     }
     __syncthreads();
+    const RefView& A = MP ? desc_s.A : A0;
+    const QueryView& B = MP ? desc_s.B : B0;
     const double m0 = mat_s[0], m1 = mat_s[1], m2 = mat_s[2], m3 = mat_s[3], m4 = mat_s[4],
                  m5 = mat_s[5], m6 = mat_s[6], m7 = mat_s[7], m8 = mat_s[8], t0 = mat_s[9],
                  t1 = mat_s[10], t2 = mat_s[11];
@@ -421,6 +443,7 @@ __global__ void __launch_bounds__(THREADS, 1)
           mi_out[p] = -1e300;
           status_out[p] = 0x100;
           if (total_out) total_out[p] = 0;
+          if (hash_out) hash_out[p] = 0;
         }
         __syncthreads();
         continue;
@@ -921,6 +944,7 @@ __global__ void __launch_bounds__(THREADS, 1)
         mi_out[p] = -1e300;
         status_out[p] = status;
         if (total_out) total_out[p] = 0;
+        if (hash_out) hash_out[p] = 0;
       }
       if (hist_out)
         for (int i = tid; i < W * W; i += THREADS) hist_out[p * W * W + i] = 0;
@@ -980,13 +1004,28 @@ __global__ void __launch_bounds__(THREADS, 1)
       for (int i = tid; i < W * W; i += THREADS)
         hist_out[p * W * W + i] = i == 0 ? r.h00 : (long long)hist[i];
     }
+    if (hash_out) {  // block-uniform
+      unsigned long long h = 0;
+      if (r.status == 0)
+        for (int i = tid; i < W * W; i += THREADS)
+          h += (unsigned long long)(i == 0 ? r.h00 : (long long)hist[i]) * cell_mix((unsigned long long)i);
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) h += __shfl_xor_sync(0xffffffffu, h, o);
+      if (lane == 0) hash_s[wid] = h;
+      __syncthreads();
+      if (tid == 0) {
+        unsigned long long t = 0;
+        for (int w = 0; w < THREADS / 32; ++w) t += hash_s[w];
+        hash_out[p] = t;
+      }
+    }
     __syncthreads();
   }
 }
 
-template <int THREADS, int NS, int KIND, bool F32, int MODE, bool MULTI>
+template <int THREADS, int NS, int KIND, bool F32, int MODE, bool MULTI, bool MP>
 static cudaError_t launch_fast_t(const FastLaunch& fl, cudaStream_t st) {
-  auto k = k_pose_fast<THREADS, NS, KIND, F32, MODE, MULTI>;
+  auto k = k_pose_fast<THREADS, NS, KIND, F32, MODE, MULTI, MP>;
   size_t smem = fast_smem_bytes(KIND, fl.cap, fl.g.bins, THREADS, F32 ? 1 : 0, NS, MULTI ? 1 : 0);
   // The opt-in is set to the device maximum, never to this launch's size:
   // contexts on other host threads launch the same instantiation with other
@@ -1004,16 +1043,17 @@ static cudaError_t launch_fast_t(const FastLaunch& fl, cudaStream_t st) {
   cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, optin);
   if (e != cudaSuccess) return e;
   k<<<fl.grid, THREADS, smem, st>>>(fl.g, fl.A, fl.B, fl.mats, fl.P, fl.cap, fl.mi, fl.status,
-                                    fl.hist, fl.total, fl.dump, fl.sums, fl.npass);
+                                    fl.hist, fl.total, fl.dump, fl.sums, fl.npass, fl.pairs,
+                                    fl.pose_pair, fl.hash);
   return cudaGetLastError();
 }
 
-template <int T, int NS, int KIND, bool F32, bool MULTI>
+template <int T, int NS, int KIND, bool F32, bool MULTI, bool MP>
 static cudaError_t launch_grid(const FastLaunch& fl, cudaStream_t st) {
   switch (fl.g.mode) {
-    case kGridUnit: return launch_fast_t<T, NS, KIND, F32, kGridUnit, MULTI>(fl, st);
-    case kGridPow2: return launch_fast_t<T, NS, KIND, F32, kGridPow2, MULTI>(fl, st);
-    default: return launch_fast_t<T, NS, KIND, F32, kGridGeneral, MULTI>(fl, st);
+    case kGridUnit: return launch_fast_t<T, NS, KIND, F32, kGridUnit, MULTI, MP>(fl, st);
+    case kGridPow2: return launch_fast_t<T, NS, KIND, F32, kGridPow2, MULTI, MP>(fl, st);
+    default: return launch_fast_t<T, NS, KIND, F32, kGridGeneral, MULTI, MP>(fl, st);
   }
 }
 
@@ -1021,10 +1061,15 @@ static cudaError_t launch_grid(const FastLaunch& fl, cudaStream_t st) {
 // multi-pass are separate instantiations; the multi-pass layout (a ~3x bigger
 // table) also runs single-pass when scan B's voxels fit it but not the
 // single-pass table.
+// Multi-pair launches are single-pass only (the host plans them so).
 template <int T, int NS, int KIND, bool F32>
 static cudaError_t launch_mode(const FastLaunch& fl, cudaStream_t st) {
-  return fl.multi ? launch_grid<T, NS, KIND, F32, true>(fl, st)
-                  : launch_grid<T, NS, KIND, F32, false>(fl, st);
+  if (fl.pairs) {
+    if (fl.multi) return cudaErrorInvalidValue;
+    return launch_grid<T, NS, KIND, F32, false, true>(fl, st);
+  }
+  return fl.multi ? launch_grid<T, NS, KIND, F32, true, false>(fl, st)
+                  : launch_grid<T, NS, KIND, F32, false, false>(fl, st);
 }
 
 template <int T, int NS>

@@ -10,14 +10,47 @@
 #include <cstdlib>
 #include <cstring>
 #include <string>
+#include <thread>
 #include <vector>
 
 #include <cuda_runtime.h>
 
 #include "../../include/vmi.h"
+#include "nm_lockstep.h"
 #include "vmi_kernels.h"
 
 using namespace vmi;
+
+// One scan pair resident on the device: scan A's dense bin grid + voxel list,
+// scan B's span-layout records.  A context holds its current pair (`cur`, the
+// single-pair API) and optionally a pair set (vmi_set_pairs) for the
+// multi-pair kernel.  Buffers are grow-only and reused when a pair is re-set.
+struct PairStore {
+  // scan A
+  bool a_set = false;
+  bool a_empty = true;
+  int amin[3] = {0, 0, 0}, amax[3] = {0, 0, 0};
+  uint32_t ext[3] = {0, 0, 0};
+  uint8_t* d_grid = nullptr;
+  size_t grid_bytes = 0, cap_grid = 0;
+  int4* d_avox = nullptr;
+  size_t cap_avox = 0;
+  int n_avox = 0;
+  uint32_t* d_bin_total = nullptr;
+  int64_t a_nvox = 0;
+  int64_t a_npts = 0;  // scan A's point count (0 when set from features)
+  // scan B
+  bool b_set = false;
+  void* d_pts = nullptr;
+  size_t cap_pts = 0;
+  int is_f32 = 0;
+  int64_t nb = 0;
+  int span = 0;
+  int rem = 0;
+  double max_abs = 0.0;
+  double b_lo[3] = {0, 0, 0}, b_hi[3] = {0, 0, 0};  // scan B's AABB
+  int64_t b_voxels = 0;  // scan B's occupied voxels at the identity pose (table sizing)
+};
 
 struct vmi_ctx {
   int device = 0;
@@ -31,32 +64,24 @@ struct vmi_ctx {
   GridParams g{};
   int occ = 0;  // fast kernel runs the occupancy kind (every occupied voxel in one bin)
 
-  // scan A
-  bool a_set = false;
-  bool a_empty = true;
-  int amin[3] = {0, 0, 0}, amax[3] = {0, 0, 0};
-  uint32_t ext[3] = {0, 0, 0};
-  uint8_t* d_grid = nullptr;
-  size_t grid_bytes = 0;
-  int4* d_avox = nullptr;
-  int4* d_avox_tmp = nullptr;  // unsorted voxel list of build_reference
-  int n_avox = 0;
-  uint32_t* d_bin_total = nullptr;
-  int* d_cursor = nullptr;
-  unsigned long long* d_akeys = nullptr;
-  double* d_avalues = nullptr;
-  int64_t a_nvox = 0;
+  PairStore cur;                // the single-pair API's scan pair
+  std::vector<PairStore> set;   // vmi_set_pairs: many resident pairs (multi-pair kernel)
+  int64_t n_set = 0;            // pairs of `set` in use
+  PairDesc* d_pairs = nullptr;  // device copies of the set's views
+  size_t cap_pairs = 0;
+  int32_t* d_pose_pair = nullptr;  // vmi_eval_pairs: per-pose pair index
+  unsigned long long* d_hash = nullptr;  // per-pose histogram identities
+  int64_t cap_pp = 0;
 
-  // scan B
-  bool b_set = false;
-  void* d_pts = nullptr;
-  int is_f32 = 0;
-  int64_t nb = 0;
-  int span = 0;
-  int rem = 0;
-  double max_abs = 0.0;
-  double b_lo[3] = {0, 0, 0}, b_hi[3] = {0, 0, 0};  // scan B's AABB
-  int64_t b_voxels = 0;  // scan B's occupied voxels at the identity pose (table sizing)
+  // scratch for building scan A (any pair)
+  int4* d_avox_tmp = nullptr;  // unsorted voxel list of build_reference
+  int* d_cursor = nullptr;
+  unsigned long long* d_akeys = nullptr;  // the current pair's FeatureMap (exported)
+  double* d_avalues = nullptr;
+  unsigned long long* d_pkeys = nullptr;  // a set pair's FeatureMap (build scratch)
+  double* d_pvalues = nullptr;
+  size_t cap_pkeys = 0, cap_pvalues = 0;
+
   int threads = kFastThreads;  // span-layout threads
   int streams = 1;             // spans per CUDA thread in the fast kernel
   int cap_override = 0;
@@ -86,10 +111,9 @@ struct vmi_ctx {
   size_t cap_tk_keys = 0, cap_tk_idx = 0, cap_tk_out = 0, cap_tk_tmp = 0;
   double2* d_sums = nullptr;  // fast-path VARZ sums scratch (grid * cap)
   size_t sums_n = 0;
-  // grow-only capacities (bytes) of buffers reused across scan pairs
-  size_t cap_grid = 0, cap_avox = 0, cap_avox_tmp = 0, cap_akeys = 0, cap_avalues = 0, cap_pts = 0, cap_upload = 0;
+  // grow-only capacities (bytes) of scratch reused across scan pairs
+  size_t cap_avox_tmp = 0, cap_akeys = 0, cap_avalues = 0, cap_upload = 0;
   void* d_upload = nullptr;  // staging for host uploads
-  int64_t a_npts = 0;        // scan A's point count (0 when set from features)
 };
 
 namespace {
@@ -111,17 +135,21 @@ int cuda_fail(vmi_ctx* c, cudaError_t e, const char* where) {
 
 // Scan A's buffers are grow-only and reused by the next reference (a drive
 // re-sets scan A every pair); only the bookkeeping is reset here.
-void free_a(vmi_ctx* c) {
-  c->a_set = false; c->n_avox = 0; c->a_nvox = 0; c->grid_bytes = 0; c->a_npts = 0;
+void free_a(PairStore& ps) {
+  ps.a_set = false; ps.n_avox = 0; ps.a_nvox = 0; ps.grid_bytes = 0; ps.a_npts = 0;
 }
 
-void release_a(vmi_ctx* c) {
-  cudaFree(c->d_grid); cudaFree(c->d_avox); cudaFree(c->d_avox_tmp); cudaFree(c->d_bin_total); cudaFree(c->d_cursor);
-  cudaFree(c->d_akeys); cudaFree(c->d_avalues); cudaFree(c->d_upload);
-  c->d_grid = nullptr; c->d_avox = nullptr; c->d_avox_tmp = nullptr; c->d_bin_total = nullptr; c->d_cursor = nullptr;
-  c->d_akeys = nullptr; c->d_avalues = nullptr; c->d_upload = nullptr;
-  c->cap_grid = c->cap_avox = c->cap_avox_tmp = c->cap_akeys = c->cap_avalues = c->cap_upload = 0;
-  free_a(c);
+void release_pair(PairStore& ps) {
+  cudaFree(ps.d_grid); cudaFree(ps.d_avox); cudaFree(ps.d_bin_total); cudaFree(ps.d_pts);
+  ps = PairStore{};
+}
+
+void release_scratch(vmi_ctx* c) {
+  cudaFree(c->d_avox_tmp); cudaFree(c->d_cursor); cudaFree(c->d_akeys); cudaFree(c->d_avalues);
+  cudaFree(c->d_pkeys); cudaFree(c->d_pvalues); cudaFree(c->d_upload);
+  c->d_avox_tmp = nullptr; c->d_cursor = nullptr; c->d_akeys = nullptr; c->d_avalues = nullptr;
+  c->d_pkeys = nullptr; c->d_pvalues = nullptr; c->d_upload = nullptr;
+  c->cap_avox_tmp = c->cap_akeys = c->cap_avalues = c->cap_pkeys = c->cap_pvalues = c->cap_upload = 0;
 }
 
 template <typename T>
@@ -135,27 +163,27 @@ cudaError_t grow(T** p, size_t& cap, size_t need) {
   return e;
 }
 
-RefView ref_view(const vmi_ctx* c) {
+RefView ref_view(const PairStore& ps) {
   RefView A{};
-  for (int j = 0; j < 3; ++j) { A.amin[j] = c->amin[j]; A.amax[j] = c->amax[j]; A.ext[j] = c->ext[j]; }
-  A.grid = c->d_grid;
-  A.avox = c->d_avox;
-  A.n_avox = c->n_avox;
-  A.empty = c->a_empty ? 1 : 0;
-  A.bin_total = c->d_bin_total;
+  for (int j = 0; j < 3; ++j) { A.amin[j] = ps.amin[j]; A.amax[j] = ps.amax[j]; A.ext[j] = ps.ext[j]; }
+  A.grid = ps.d_grid;
+  A.avox = ps.d_avox;
+  A.n_avox = ps.n_avox;
+  A.empty = ps.a_empty ? 1 : 0;
+  A.bin_total = ps.d_bin_total;
   return A;
 }
 
-QueryView query_view(const vmi_ctx* c) {
+QueryView query_view(const vmi_ctx* c, const PairStore& ps) {
   QueryView B{};
-  B.pts = c->d_pts;
-  B.is_f32 = c->is_f32;
-  B.n = c->nb;
-  B.span = c->span;
-  B.rem = c->rem;
+  B.pts = ps.d_pts;
+  B.is_f32 = ps.is_f32;
+  B.n = ps.nb;
+  B.span = ps.span;
+  B.rem = ps.rem;
   B.threads = c->threads;
-  B.max_abs = c->max_abs;
-  for (int j = 0; j < 3; ++j) { B.lo[j] = c->b_lo[j]; B.hi[j] = c->b_hi[j]; }
+  B.max_abs = ps.max_abs;
+  for (int j = 0; j < 3; ++j) { B.lo[j] = ps.b_lo[j]; B.hi[j] = ps.b_hi[j]; }
   return B;
 }
 
@@ -164,35 +192,38 @@ QueryView query_view(const vmi_ctx* c) {
 int kernel_kind(const vmi_ctx* c) { return c->occ ? kKindOcc : c->g.kind; }
 
 // Largest table that fits shared memory next to the kernel's other buffers.
-size_t max_table_cap(const vmi_ctx* c, int kind, bool multi) {
-  const size_t fixed = fast_smem_bytes(kind, 0, c->g.bins, c->threads / c->streams,
-                                       c->is_f32, c->streams, multi ? 1 : 0);
+size_t max_table_cap(const vmi_ctx* c, int kind, int is_f32, bool multi) {
+  const size_t fixed = fast_smem_bytes(kind, 0, c->g.bins, c->threads / c->streams, is_f32,
+                                       c->streams, multi ? 1 : 0);
   const size_t per = (size_t)fast_slot_bytes(kind, multi ? 1 : 0);
-  return ((c->smem_optin - fixed) / per) & ~size_t(31);
+  constexpr size_t kStaticSmem = 512;  // the kernel's static shared memory (<= 304 B)
+  return ((c->smem_optin - kStaticSmem - fixed) / per) & ~size_t(31);
 }
 
-// Table capacity and pass count for the current scan pair.  Every slot is
-// walked once per pose, so a single-pass table is sized for a ~40% load at
-// scan B's expected occupancy rather than filling shared memory; when even a
-// full table cannot hold it, the multi-pass layout (bigger table) is used.
-void plan_table(const vmi_ctx* c, int kind, int* cap_out, int* npass_out, int* multi_out) {
+// Table capacity and pass count for scan B's expected occupancy `b_voxels`
+// (its voxel count in its own frame).  Every slot is walked once per pose, so
+// a single-pass table is sized for a ~40% load rather than filling shared
+// memory; when even a full table cannot hold it, the multi-pass layout (bigger
+// table) is used.
+void plan_table(const vmi_ctx* c, int kind, int64_t b_voxels, int is_f32, int* cap_out,
+                int* npass_out, int* multi_out) {
   static const double factor = [] {
     const char* e = std::getenv("VMI_CAP_FACTOR");  // experiments only
     // C2 (A/B, reproduced): 2.2 -> 28.98 ms, 2.0 -> 29.25, 2.5 -> 29.48; C1 flat
     return e ? std::atof(e) : 2.2;
   }();
-  const double est = (double)(c->b_voxels > 0 ? c->b_voxels : 4096);
+  const double est = (double)(b_voxels > 0 ? b_voxels : 4096);
   if (c->cap_override > 0) {
     // a requested table larger than shared memory holds is clamped to the largest that fits
     const int np = c->npass_override > 0
                        ? c->npass_override
                        : std::max(1, (int)std::ceil(est / (0.70 * c->cap_override)));
-    *cap_out = (int)std::min((size_t)c->cap_override, max_table_cap(c, kind, np > 1));
+    *cap_out = (int)std::min((size_t)c->cap_override, max_table_cap(c, kind, is_f32, np > 1));
     *npass_out = np;
     *multi_out = np > 1;
     return;
   }
-  const size_t cap1 = max_table_cap(c, kind, false);
+  const size_t cap1 = max_table_cap(c, kind, is_f32, false);
   if (c->npass_override <= 1 && (c->npass_override == 1 || est <= 0.70 * (double)cap1)) {
     size_t want = ((size_t)(factor * est) + 31) & ~size_t(31);
     if (want < 2048) want = 2048;
@@ -209,7 +240,7 @@ void plan_table(const vmi_ctx* c, int kind, int* cap_out, int* npass_out, int* m
     // 1.2 overflows on some poses (exact-path fix-ups)
     return e ? std::atof(e) : 1.4;
   }();
-  const size_t capm = max_table_cap(c, kind, true);
+  const size_t capm = max_table_cap(c, kind, is_f32, true);
   *cap_out = (int)capm;
   *multi_out = 1;
   *npass_out = c->npass_override > 1
@@ -230,45 +261,47 @@ int ensure_sums(vmi_ctx* c, int kind, int grid, int cap) {
   return 0;
 }
 
-// Grid over A's AABB + voxel list from V (keys, values) already on device.
-int finish_reference(vmi_ctx* c, const int64_t bounds[6], int64_t V) {
-  c->a_empty = V == 0;
+// Pair ps's grid over A's AABB + voxel list from V (keys, values) on device.
+int finish_reference(vmi_ctx* c, PairStore& ps, const int64_t bounds[6], int64_t V,
+                     const unsigned long long* keys, const double* values) {
+  ps.a_empty = V == 0;
   for (int j = 0; j < 3; ++j) {
-    c->amin[j] = (int)bounds[j];
-    c->amax[j] = (int)bounds[3 + j];
-    if (bounds[j] > bounds[3 + j]) c->a_empty = true;
+    ps.amin[j] = (int)bounds[j];
+    ps.amax[j] = (int)bounds[3 + j];
+    if (bounds[j] > bounds[3 + j]) ps.a_empty = true;
   }
-  c->a_nvox = V;
-  if (!c->d_bin_total) CK(c, cudaMalloc(&c->d_bin_total, 4 * kMaxW));
-  CK(c, cudaMemsetAsync(c->d_bin_total, 0, 4 * kMaxW, c->stream));
+  ps.a_nvox = V;
+  if (!ps.d_bin_total) CK(c, cudaMalloc(&ps.d_bin_total, 4 * kMaxW));
+  CK(c, cudaMemsetAsync(ps.d_bin_total, 0, 4 * kMaxW, c->stream));
   if (!c->d_cursor) CK(c, cudaMalloc(&c->d_cursor, 4 * kMaxW));
-  if (c->a_empty) {
-    c->a_set = true;
+  if (ps.a_empty) {
+    ps.a_set = true;
     return 0;
   }
   for (int j = 0; j < 3; ++j) {
     if (bounds[j] < -(1 << 20) || bounds[3 + j] > (1 << 20) - 1)
       return fail(c, VMI_ERR_ARG, "reference bounds outside the voxel key range");
-    c->ext[j] = (uint32_t)(bounds[3 + j] - bounds[j] + 1);
+    ps.ext[j] = (uint32_t)(bounds[3 + j] - bounds[j] + 1);
   }
-  const double vol = (double)c->ext[0] * c->ext[1] * c->ext[2];
+  const double vol = (double)ps.ext[0] * ps.ext[1] * ps.ext[2];
   if (vol > 4294967294.0)
     return fail(c, VMI_ERR_UNSUPPORTED,
                 "scan A's occupied AABB exceeds 2^32-2 voxels (dense reference grid limit)");
-  c->grid_bytes = (size_t)vol;
-  CK(c, grow(&c->d_grid, c->cap_grid, c->grid_bytes));
-  CK(c, cudaMemsetAsync(c->d_grid, 0, c->grid_bytes, c->stream));
-  CK(c, grow(&c->d_avox, c->cap_avox, sizeof(int4) * (V > 0 ? V : 1)));
+  ps.grid_bytes = (size_t)vol;
+  CK(c, grow(&ps.d_grid, ps.cap_grid, ps.grid_bytes));
+  CK(c, cudaMemsetAsync(ps.d_grid, 0, ps.grid_bytes, c->stream));
+  CK(c, grow(&ps.d_avox, ps.cap_avox, sizeof(int4) * (V > 0 ? V : 1)));
   CK(c, grow(&c->d_avox_tmp, c->cap_avox_tmp, sizeof(int4) * (V > 0 ? V : 1)));
-  CK(c, build_reference(c->d_akeys, c->d_avalues, (int)V, c->g, c->amin, c->ext, c->d_grid,
-                        c->d_avox_tmp, c->d_avox, c->d_bin_total, c->d_cursor, c->stream, &c->launches));
+  CK(c, build_reference(keys, values, (int)V, nullptr, c->g, ps.amin, ps.ext, ps.d_grid,
+                        c->d_avox_tmp, ps.d_avox, ps.d_bin_total, c->d_cursor, c->stream,
+                        &c->launches));
   std::vector<uint32_t> tot(kMaxW);
-  CK(c, cudaMemcpyAsync(tot.data(), c->d_bin_total, 4 * kMaxW, cudaMemcpyDeviceToHost, c->stream));
+  CK(c, cudaMemcpyAsync(tot.data(), ps.d_bin_total, 4 * kMaxW, cudaMemcpyDeviceToHost, c->stream));
   CK(c, cudaStreamSynchronize(c->stream));
   int64_t s = 0;
   for (int b = 0; b < kMaxW; ++b) s += tot[b];
-  c->n_avox = (int)s;
-  c->a_set = true;
+  ps.n_avox = (int)s;
+  ps.a_set = true;
   return 0;
 }
 
@@ -295,19 +328,19 @@ int ensure_P(vmi_ctx* c, int64_t P, bool hist) {
 int check_ready(vmi_ctx* c) {
   if (!c) return VMI_ERR_ARG;
   if (!c->params_set) return fail(c, VMI_ERR_STATE, "vmi_set_params not called");
-  if (!c->a_set) return fail(c, VMI_ERR_STATE, "scan A (reference) not set");
-  if (!c->b_set) return fail(c, VMI_ERR_STATE, "scan B (query) not set");
+  if (!c->cur.a_set) return fail(c, VMI_ERR_STATE, "scan A (reference) not set");
+  if (!c->cur.b_set) return fail(c, VMI_ERR_STATE, "scan B (query) not set");
   return 0;
 }
 
-int exact_pose(vmi_ctx* c, const double* mat_dev, int64_t p, double* mi, int32_t* st,
-               long long* hist, long long* total) {
+int exact_pose(vmi_ctx* c, const PairStore& ps, const double* mat_dev, int64_t p, double* mi,
+               int32_t* st, long long* hist, long long* total) {
   PointSource src{};
   src.xyz = nullptr;
-  src.B = query_view(c);
-  src.n = c->nb;
+  src.B = query_view(c, ps);
+  src.n = ps.nb;
   CK(c, exact_voxelize(c->ex, src, mat_dev, c->g, c->stream, &c->launches));
-  CK(c, exact_score(c->ex, c->g, ref_view(c), p, mi, st, hist, total, c->stream, &c->launches));
+  CK(c, exact_score(c->ex, c->g, ref_view(ps), p, mi, st, hist, total, c->stream, &c->launches));
   return 0;
 }
 
@@ -317,13 +350,13 @@ int launch_fast_eval(vmi_ctx* c, const double* mats_dev, int64_t P, double* mi, 
   FastLaunch fl{};
   fl.g = c->g;
   fl.g.kind = kernel_kind(c);
-  fl.A = ref_view(c);
-  fl.B = query_view(c);
+  fl.A = ref_view(c->cur);
+  fl.B = query_view(c, c->cur);
   fl.mats = mats_dev;
   fl.P = P;
   fl.grid = (int)(P < c->sm_count ? P : c->sm_count);
   fl.streams = c->streams;
-  plan_table(c, fl.g.kind, &fl.cap, &fl.npass, &fl.multi);
+  plan_table(c, fl.g.kind, c->cur.b_voxels, c->cur.is_f32, &fl.cap, &fl.npass, &fl.multi);
   int rc = ensure_sums(c, fl.g.kind, fl.grid, fl.cap);
   if (rc) return rc;
   fl.sums = c->d_sums;
@@ -336,8 +369,11 @@ int launch_fast_eval(vmi_ctx* c, const double* mats_dev, int64_t P, double* mi, 
   return 0;
 }
 
+// Re-run, through the exact path, every pose whose fast-path status carries
+// VMI_FLAG_RECHECK; pose_pair (host, nullable) names each pose's pair in the set.
 int do_fixups(vmi_ctx* c, const double* mats_dev, int64_t P, double* mi, int32_t* st,
-              long long* hist, long long* total, cudaStream_t stream, int64_t* n_fixed) {
+              long long* hist, long long* total, cudaStream_t stream, int64_t* n_fixed,
+              const int32_t* pose_pair = nullptr) {
   std::vector<int32_t> hs(P);
   CK(c, cudaMemcpyAsync(hs.data(), st, P * 4, cudaMemcpyDeviceToHost, stream));
   CK(c, cudaStreamSynchronize(stream));
@@ -346,7 +382,8 @@ int do_fixups(vmi_ctx* c, const double* mats_dev, int64_t P, double* mi, int32_t
   c->stream = stream;
   for (int64_t p = 0; p < P; ++p) {
     if (hs[p] & VMI_FLAG_RECHECK) {
-      int rc = exact_pose(c, mats_dev + 12 * p, p, mi, st, hist, total);
+      const PairStore& ps = pose_pair ? c->set[(size_t)pose_pair[p]] : c->cur;
+      int rc = exact_pose(c, ps, mats_dev + 12 * p, p, mi, st, hist, total);
       if (rc) { c->stream = saved; return rc; }
       ++nf;
     }
@@ -395,8 +432,10 @@ int vmi_destroy(vmi_ctx* c) {
   if (!c) return 0;
   cudaSetDevice(c->device);
   cudaStreamSynchronize(c->stream);
-  release_a(c);
-  cudaFree(c->d_pts);
+  release_pair(c->cur);
+  for (auto& ps : c->set) release_pair(ps);
+  release_scratch(c);
+  cudaFree(c->d_pairs); cudaFree(c->d_pose_pair); cudaFree(c->d_hash);
   exact_free(c->ex);
   cudaFree(c->d_mats); cudaFree(c->d_mi); cudaFree(c->d_status); cudaFree(c->d_hist);
   cudaFree(c->d_total); cudaFree(c->d_best); cudaFree(c->d_best_idx); cudaFree(c->d_sums);
@@ -481,7 +520,10 @@ int vmi_set_params(vmi_ctx* c, const double origin[3], double res, int kind, int
                             c->g.kind != g.kind || c->g.bins != g.bins || c->g.clamp != g.clamp;
   c->g = g;
   c->params_set = true;
-  if (grid_changed && c->a_set) free_a(c);  // A's grid depends on every parameter but phi
+  if (grid_changed) {  // A's grid depends on every parameter but phi
+    if (c->cur.a_set) free_a(c->cur);
+    c->n_set = 0;  // the pair set too
+  }
   if (c->hist_alloc) {  // W may have changed
     cudaFree(c->d_hist);
     c->d_hist = nullptr;
@@ -491,11 +533,13 @@ int vmi_set_params(vmi_ctx* c, const double origin[3], double res, int kind, int
   return 0;
 }
 
-// Scan A from host points: (n, 3) float64, or (n, 4) float32 KITTI records
-// uploaded as they are (16 B/point, widened exactly on the GPU).
-static int set_reference(vmi_ctx* c, const void* host, int is_rec, int64_t n) {
-  if (!c) return VMI_ERR_ARG;
-  if (!c->params_set) return fail(c, VMI_ERR_STATE, "vmi_set_params not called");
+// Scan A of pair ps from host points: (n, 3) float64, or (n, 4) float32 KITTI
+// records uploaded as they are (16 B/point, widened exactly on the GPU):
+// _prepare (align.py:114-119) = voxelize + compute_feature_map, bit-exact,
+// then the dense bin grid.  The FeatureMap stays in (keys, values) -- the
+// current pair's export buffers, or the pair-set build scratch.
+static int build_a(vmi_ctx* c, PairStore& ps, const void* host, int is_rec, int64_t n,
+                   unsigned long long** keys, double** values, size_t* cap_k, size_t* cap_v) {
   if (n <= 0 || !host) return fail(c, VMI_ERR_ARG, "cannot voxelize an empty cloud");
   if (n > 0x7fffffff) return fail(c, VMI_ERR_UNSUPPORTED, "more than 2^31-1 points");
   if (is_rec) {  // PointCloud validation (geometry.py:36-65): finite coordinates
@@ -504,8 +548,7 @@ static int set_reference(vmi_ctx* c, const void* host, int is_rec, int64_t n) {
       if (!(std::isfinite(r[4 * i]) && std::isfinite(r[4 * i + 1]) && std::isfinite(r[4 * i + 2])))
         return fail(c, VMI_ERR_ARG, "points contain non-finite coordinates");
   }
-  cudaSetDevice(c->device);
-  free_a(c);
+  free_a(ps);
   const size_t bytes = (size_t)n * (is_rec ? 16 : 24);
   CK(c, grow(&c->d_upload, c->cap_upload, bytes));
   CK(c, cudaMemcpyAsync(c->d_upload, host, bytes, cudaMemcpyHostToDevice, c->stream));
@@ -522,16 +565,23 @@ static int set_reference(vmi_ctx* c, const void* host, int is_rec, int64_t n) {
   CK(c, cudaMemcpyAsync(&V, c->ex.nruns, 4, cudaMemcpyDeviceToHost, c->stream));
   CK(c, cudaStreamSynchronize(c->stream));
   if (h[6]) return fail(c, VMI_ERR_RANGE, "a point of scan A maps outside the voxel key range");
-  CK(c, grow(&c->d_akeys, c->cap_akeys, 8 * (size_t)V));
-  CK(c, grow(&c->d_avalues, c->cap_avalues, 8 * (size_t)V));
-  CK(c, cudaMemcpyAsync(c->d_akeys, c->ex.ukeys, 8 * (size_t)V, cudaMemcpyDeviceToDevice, c->stream));
-  CK(c, cudaMemcpyAsync(c->d_avalues, c->ex.values, 8 * (size_t)V, cudaMemcpyDeviceToDevice,
-                        c->stream));
+  CK(c, grow(keys, *cap_k, 8 * (size_t)V));
+  CK(c, grow(values, *cap_v, 8 * (size_t)V));
+  CK(c, cudaMemcpyAsync(*keys, c->ex.ukeys, 8 * (size_t)V, cudaMemcpyDeviceToDevice, c->stream));
+  CK(c, cudaMemcpyAsync(*values, c->ex.values, 8 * (size_t)V, cudaMemcpyDeviceToDevice, c->stream));
   int64_t b64[6];
   for (int j = 0; j < 6; ++j) b64[j] = h[j];
-  const int rc = finish_reference(c, b64, V);
-  c->a_npts = n;
+  const int rc = finish_reference(c, ps, b64, V, *keys, *values);
+  ps.a_npts = n;
   return rc;
+}
+
+static int set_reference(vmi_ctx* c, const void* host, int is_rec, int64_t n) {
+  if (!c) return VMI_ERR_ARG;
+  if (!c->params_set) return fail(c, VMI_ERR_STATE, "vmi_set_params not called");
+  cudaSetDevice(c->device);
+  return build_a(c, c->cur, host, is_rec, n, &c->d_akeys, &c->d_avalues, &c->cap_akeys,
+                 &c->cap_avalues);
 }
 
 int vmi_set_reference_points(vmi_ctx* c, const double* xyz, int64_t n) {
@@ -551,7 +601,7 @@ int vmi_set_reference_features(vmi_ctx* c, const int64_t* keys, const double* va
     if (!std::isfinite(values[i]) || values[i] < 0)
       return fail(c, VMI_ERR_ARG, "features must be finite and >= 0");
   cudaSetDevice(c->device);
-  free_a(c);
+  free_a(c->cur);
   const size_t m = n > 0 ? (size_t)n : 1;
   CK(c, grow(&c->d_akeys, c->cap_akeys, 8 * m));
   CK(c, grow(&c->d_avalues, c->cap_avalues, 8 * m));
@@ -559,23 +609,23 @@ int vmi_set_reference_features(vmi_ctx* c, const int64_t* keys, const double* va
     CK(c, cudaMemcpyAsync(c->d_akeys, keys, 8 * n, cudaMemcpyHostToDevice, c->stream));
     CK(c, cudaMemcpyAsync(c->d_avalues, values, 8 * n, cudaMemcpyHostToDevice, c->stream));
   }
-  return finish_reference(c, bounds, n);
+  return finish_reference(c, c->cur, bounds, n, c->d_akeys, c->d_avalues);
 }
 
 int vmi_get_reference_features(vmi_ctx* c, int64_t* keys, double* values, int64_t cap,
                                int64_t* n_out, int64_t bounds[6]) {
   if (!c) return VMI_ERR_ARG;
-  if (!c->a_set) return fail(c, VMI_ERR_STATE, "scan A (reference) not set");
+  if (!c->cur.a_set) return fail(c, VMI_ERR_STATE, "scan A (reference) not set");
   cudaSetDevice(c->device);
-  if (n_out) *n_out = c->a_nvox;
+  if (n_out) *n_out = c->cur.a_nvox;
   if (bounds)
-    for (int j = 0; j < 3; ++j) { bounds[j] = c->amin[j]; bounds[3 + j] = c->amax[j]; }
+    for (int j = 0; j < 3; ++j) { bounds[j] = c->cur.amin[j]; bounds[3 + j] = c->cur.amax[j]; }
   if (!keys) return 0;
-  if (cap < c->a_nvox) return fail(c, VMI_ERR_ARG, "output capacity too small");
-  if (c->a_nvox > 0) {
-    CK(c, cudaMemcpyAsync(keys, c->d_akeys, 8 * c->a_nvox, cudaMemcpyDeviceToHost, c->stream));
+  if (cap < c->cur.a_nvox) return fail(c, VMI_ERR_ARG, "output capacity too small");
+  if (c->cur.a_nvox > 0) {
+    CK(c, cudaMemcpyAsync(keys, c->d_akeys, 8 * c->cur.a_nvox, cudaMemcpyDeviceToHost, c->stream));
     if (values)
-      CK(c, cudaMemcpyAsync(values, c->d_avalues, 8 * c->a_nvox, cudaMemcpyDeviceToHost, c->stream));
+      CK(c, cudaMemcpyAsync(values, c->d_avalues, 8 * c->cur.a_nvox, cudaMemcpyDeviceToHost, c->stream));
   }
   CK(c, cudaStreamSynchronize(c->stream));
   return 0;
@@ -583,48 +633,19 @@ int vmi_get_reference_features(vmi_ctx* c, int64_t* keys, double* values, int64_
 
 static bool f32_exact(double v) { return (double)(float)v == v; }
 
-static int set_query(vmi_ctx* c, const void* host, int is_f32_src, int64_t n) {
-  if (!c) return VMI_ERR_ARG;
+// Scan B of pair ps: one host pass (PointCloud validation, AABB, float32-
+// exactness), the upload as given (float32 records 16 B/point, or float64
+// 24 B/point), and the span layout on the GPU: split-double float4 records
+// when every coordinate is float32-exact (KITTI input), else double4.
+static int build_b(vmi_ctx* c, PairStore& ps, const void* host, int is_f32_src, int64_t n) {
   if (n <= 0 || !host) return fail(c, VMI_ERR_ARG, "cannot voxelize an empty cloud");
   if (n > 0x7fffffff) return fail(c, VMI_ERR_UNSUPPORTED, "more than 2^31-1 points");
-  cudaSetDevice(c->device);
-  c->b_set = false;
+  ps.b_set = false;
   // VMI_FORCE_F64 (experiments): keep double records even for float32-exact input
   static const bool force_f64 = std::getenv("VMI_FORCE_F64") != nullptr;
-  int as_f32 = force_f64 ? 0 : 1;
-  std::vector<float> f4;
-  std::vector<double> d3;
-  const void* up = host;
-  size_t up_bytes;
-  if (is_f32_src && force_f64) {  // expand float records to (x, y, z) doubles
-    const float* r = static_cast<const float*>(host);
-    d3.resize((size_t)n * 3);
-    for (int64_t i = 0; i < n; ++i)
-      for (int j = 0; j < 3; ++j) d3[3 * i + j] = (double)r[4 * i + j];
-    up = d3.data();
-    up_bytes = (size_t)n * 24;
-  } else if (is_f32_src) {
-    up_bytes = (size_t)n * 16;
-  } else {
-    const double* xyz = static_cast<const double*>(host);
-    for (int64_t i = 0; i < 3 * n && as_f32; ++i) as_f32 = f32_exact(xyz[i]);
-    if (as_f32) {
-      f4.resize((size_t)n * 4);
-      for (int64_t i = 0; i < n; ++i) {
-        f4[4 * i] = (float)xyz[3 * i];
-        f4[4 * i + 1] = (float)xyz[3 * i + 1];
-        f4[4 * i + 2] = (float)xyz[3 * i + 2];
-        f4[4 * i + 3] = 0.f;
-      }
-      up = f4.data();
-      up_bytes = (size_t)n * 16;
-    } else {
-      up_bytes = (size_t)n * 24;
-    }
-  }
-  double mx = 0.0;
   double lo[3] = {INFINITY, INFINITY, INFINITY}, hi[3] = {-INFINITY, -INFINITY, -INFINITY};
-  if (is_f32_src) {  // one pass: PointCloud validation (finite) + AABB
+  bool exact32 = true;
+  if (is_f32_src) {
     const float* r = static_cast<const float*>(host);
     float flo[3] = {INFINITY, INFINITY, INFINITY}, fhi[3] = {-INFINITY, -INFINITY, -INFINITY};
     bool finite = true;
@@ -638,48 +659,58 @@ static int set_query(vmi_ctx* c, const void* host, int is_f32_src, int64_t n) {
     if (!finite) return fail(c, VMI_ERR_ARG, "points contain non-finite coordinates");
     for (int j = 0; j < 3; ++j) { lo[j] = flo[j]; hi[j] = fhi[j]; }
   } else {
+    const double* xyz = static_cast<const double*>(host);
     for (int64_t i = 0; i < n; ++i)
       for (int j = 0; j < 3; ++j) {
-        const double v = static_cast<const double*>(host)[3 * i + j];
+        const double v = xyz[3 * i + j];
+        exact32 &= f32_exact(v);
         lo[j] = std::fmin(lo[j], v);
         hi[j] = std::fmax(hi[j], v);
       }
   }
+  const int as_f32 = (exact32 && !force_f64) ? 1 : 0;
+  double mx = 0.0;
   for (int j = 0; j < 3; ++j) {
     mx = std::fmax(mx, std::fmax(std::fabs(lo[j]), std::fabs(hi[j])));
-    c->b_lo[j] = lo[j];
-    c->b_hi[j] = hi[j];
+    ps.b_lo[j] = lo[j];
+    ps.b_hi[j] = hi[j];
   }
-  c->max_abs = mx;
+  ps.max_abs = mx;
+  const size_t up_bytes = (size_t)n * (is_f32_src ? 16 : 24);
   CK(c, grow(&c->d_upload, c->cap_upload, up_bytes));
-  void* tmp = c->d_upload;
-  CK(c, cudaMemcpyAsync(tmp, up, up_bytes, cudaMemcpyHostToDevice, c->stream));
-  c->span = (int)((n + c->threads - 1) / c->threads);
-  c->rem = (int)(n - (int64_t)(c->span - 1) * c->threads);
+  CK(c, cudaMemcpyAsync(c->d_upload, host, up_bytes, cudaMemcpyHostToDevice, c->stream));
+  ps.span = (int)((n + c->threads - 1) / c->threads);
+  ps.rem = (int)(n - (int64_t)(ps.span - 1) * c->threads);
   const size_t rec = as_f32 ? 16 : 32;
-  CK(c, grow(&c->d_pts, c->cap_pts, (size_t)(c->span + kStagePadRows) * c->threads * rec));
-  CK(c, launch_span_layout(tmp, as_f32, n, c->span, c->rem, c->threads, c->d_pts, c->stream));
+  CK(c, grow(&ps.d_pts, ps.cap_pts, (size_t)(ps.span + kStagePadRows) * c->threads * rec));
+  CK(c, launch_span_layout(c->d_upload, is_f32_src, as_f32, n, ps.span, ps.rem, c->threads,
+                           ps.d_pts, c->stream));
   c->launches += 1;
-  CK(c, cudaStreamSynchronize(c->stream));
-  c->is_f32 = as_f32;
-  c->nb = n;
-  c->b_set = true;
+  ps.is_f32 = as_f32;
+  ps.nb = n;
   // table sizing hint: scan B's occupied voxel count in its own frame
-  c->b_voxels = 0;
-  if (c->a_set && c->a_npts > 0 && c->a_nvox > 0) {
+  ps.b_voxels = 0;
+  if (ps.a_set && ps.a_npts > 0 && ps.a_nvox > 0) {
     // same sensor, same grid: scale scan A's voxel count (saves a voxelization)
-    c->b_voxels = (int64_t)((double)c->a_nvox * (double)n / (double)c->a_npts) + 1;
+    ps.b_voxels = (int64_t)((double)ps.a_nvox * (double)n / (double)ps.a_npts) + 1;
   } else if (c->params_set) {
     PointSource src{};
-    src.B = query_view(c);
+    src.B = query_view(c, ps);
     src.n = n;
     int V = 0;
     CK(c, exact_voxelize(c->ex, src, nullptr, c->g, c->stream, &c->launches));
     CK(c, cudaMemcpyAsync(&V, c->ex.nruns, 4, cudaMemcpyDeviceToHost, c->stream));
-    CK(c, cudaStreamSynchronize(c->stream));
-    c->b_voxels = V;
+    ps.b_voxels = V;
   }
+  CK(c, cudaStreamSynchronize(c->stream));  // the host buffer may be reused on return
+  ps.b_set = true;
   return 0;
+}
+
+static int set_query(vmi_ctx* c, const void* host, int is_f32_src, int64_t n) {
+  if (!c) return VMI_ERR_ARG;
+  cudaSetDevice(c->device);
+  return build_b(c, c->cur, host, is_f32_src, n);
 }
 
 int vmi_set_query_points(vmi_ctx* c, const double* xyz, int64_t n) { return set_query(c, xyz, 0, n); }
@@ -799,7 +830,8 @@ int vmi_eval_exact(vmi_ctx* c, const double* mats, int64_t P, double* mi_out, in
   long long* dh = hist_out ? c->d_hist : nullptr;
   CK(c, cudaMemcpyAsync(c->d_mats, mats, P * 96, cudaMemcpyHostToDevice, c->stream));
   for (int64_t p = 0; p < P; ++p)
-    if ((rc = exact_pose(c, c->d_mats + 12 * p, p, c->d_mi, c->d_status, dh, c->d_total))) return rc;
+    if ((rc = exact_pose(c, c->cur, c->d_mats + 12 * p, p, c->d_mi, c->d_status, dh, c->d_total)))
+      return rc;
   CK(c, cudaMemcpyAsync(mi_out, c->d_mi, P * 8, cudaMemcpyDeviceToHost, c->stream));
   CK(c, cudaMemcpyAsync(status_out, c->d_status, P * 4, cudaMemcpyDeviceToHost, c->stream));
   if (hist_out) {
@@ -814,14 +846,14 @@ int vmi_eval_exact(vmi_ctx* c, const double* mats, int64_t P, double* mi_out, in
 int vmi_query_features(vmi_ctx* c, const double mat[12], int64_t* keys, double* values, int64_t cap,
                        int64_t* n_out, int64_t bounds[6], int32_t* status) {
   if (!c || !mat) return VMI_ERR_ARG;
-  if (!c->params_set || !c->b_set) return fail(c, VMI_ERR_STATE, "params and scan B must be set");
+  if (!c->params_set || !c->cur.b_set) return fail(c, VMI_ERR_STATE, "params and scan B must be set");
   cudaSetDevice(c->device);
   int rc;
   if ((rc = ensure_P(c, 1, false))) return rc;
   CK(c, cudaMemcpyAsync(c->d_mats, mat, 96, cudaMemcpyHostToDevice, c->stream));
   PointSource src{};
-  src.B = query_view(c);
-  src.n = c->nb;
+  src.B = query_view(c, c->cur);
+  src.n = c->cur.nb;
   CK(c, exact_voxelize(c->ex, src, c->d_mats, c->g, c->stream, &c->launches));
   int h[8];
   int V = 0;
@@ -859,11 +891,12 @@ int vmi_fast_features(vmi_ctx* c, const double mat[12], int64_t* keys, double* v
   CK(c, cudaMemcpyAsync(c->d_mats, mat, 96, cudaMemcpyHostToDevice, c->stream));
   FastLaunch fl{};
   fl.g = c->g;
-  fl.A = ref_view(c);
-  fl.B = query_view(c);
+  fl.A = ref_view(c->cur);
+  fl.B = query_view(c, c->cur);
   fl.mats = c->d_mats;
   fl.P = 1;
-  plan_table(c, fl.g.kind, &fl.cap, &fl.npass, &fl.multi);  // the user's kind: dumps need features
+  // the user's kind: dumps need features
+  plan_table(c, fl.g.kind, c->cur.b_voxels, c->cur.is_f32, &fl.cap, &fl.npass, &fl.multi);
   fl.grid = 1;
   fl.streams = c->streams;
   if ((rc = ensure_sums(c, fl.g.kind, 1, fl.cap))) return rc;
@@ -889,6 +922,340 @@ int vmi_fast_features(vmi_ctx* c, const double mat[12], int64_t* keys, double* v
   }
   cudaFree(dk); cudaFree(dv); cudaFree(dn);
   return 0;
+}
+
+// ---- many resident scan pairs (C5: consecutive pairs of a drive) ----------
+
+namespace {
+
+// One host pass over a scan: PointCloud validation (finite coordinates), the
+// AABB, and (float64 input) whether every coordinate is float32-exact.
+struct HostScan {
+  double lo[3], hi[3];
+  bool finite = true, exact32 = true;
+};
+void scan_pass(const void* p, int is_rec, int64_t n, HostScan& o) {
+  for (int j = 0; j < 3; ++j) { o.lo[j] = INFINITY; o.hi[j] = -INFINITY; }
+  if (is_rec) {
+    const float* r = static_cast<const float*>(p);
+    float lo[3] = {INFINITY, INFINITY, INFINITY}, hi[3] = {-INFINITY, -INFINITY, -INFINITY};
+    bool fin = true;
+    for (int64_t i = 0; i < n; ++i)
+      for (int j = 0; j < 3; ++j) {
+        const float v = r[4 * i + j];
+        fin &= std::isfinite(v);
+        lo[j] = std::fmin(lo[j], v);
+        hi[j] = std::fmax(hi[j], v);
+      }
+    o.finite = fin;
+    for (int j = 0; j < 3; ++j) { o.lo[j] = lo[j]; o.hi[j] = hi[j]; }
+  } else {
+    const double* d = static_cast<const double*>(p);
+    bool fin = true, ex = true;
+    for (int64_t i = 0; i < n; ++i)
+      for (int j = 0; j < 3; ++j) {
+        const double v = d[3 * i + j];
+        fin &= std::isfinite(v);
+        ex &= (double)(float)v == v;
+        o.lo[j] = std::fmin(o.lo[j], v);
+        o.hi[j] = std::fmax(o.hi[j], v);
+      }
+    o.finite = fin;
+    o.exact32 = ex;
+  }
+}
+
+// voxel.py:199 on the host for a coordinate: floor(RN(RN(p - o) / res)).  The
+// quotient is monotone in p, so the voxel bounds of a scan are the floors of
+// its AABB corners -- the same integers the GPU reduces (voxel.py:220).
+int64_t host_floor(double p, double o, double res) { return (int64_t)std::floor((p - o) / res); }
+
+}  // namespace
+
+// Pairs are built back to back on the context stream with no host round trip
+// in between: scan A's voxel bounds come from its AABB on the host (exact, see
+// host_floor), its voxel list is sized by the point count, and the voxel
+// counts are read back once for the whole set.
+int vmi_set_pairs(vmi_ctx* c, int64_t npairs, const void* const* a, const int64_t* na,
+                  const void* const* b, const int64_t* nb, int is_rec) {
+  if (!c || npairs < 0 || (npairs > 0 && (!a || !na || !b || !nb))) return VMI_ERR_ARG;
+  if (!c->params_set) return fail(c, VMI_ERR_STATE, "vmi_set_params not called");
+  if (npairs > 0x7fffffff) return fail(c, VMI_ERR_UNSUPPORTED, "more than 2^31-1 pairs");
+  for (int64_t i = 0; i < npairs; ++i) {
+    if (na[i] <= 0 || nb[i] <= 0 || !a[i] || !b[i])
+      return fail(c, VMI_ERR_ARG, "cannot voxelize an empty cloud");
+    if (na[i] > 0x7fffffff || nb[i] > 0x7fffffff)
+      return fail(c, VMI_ERR_UNSUPPORTED, "more than 2^31-1 points");
+  }
+  cudaSetDevice(c->device);
+  c->n_set = 0;
+  // host passes, threaded over scans
+  std::vector<HostScan> ha((size_t)npairs), hb((size_t)npairs);
+  {
+    const int64_t jobs = 2 * npairs;
+    int nt = (int)std::min<int64_t>(std::max(1u, std::thread::hardware_concurrency()), 16);
+    nt = (int)std::min<int64_t>(nt, std::max<int64_t>(1, jobs));
+    std::vector<std::thread> pool;
+    for (int t = 0; t < nt; ++t)
+      pool.emplace_back([&, t] {
+        for (int64_t j = t; j < jobs; j += nt) {
+          const int64_t i = j >> 1;
+          if (j & 1) scan_pass(b[i], is_rec, nb[i], hb[(size_t)i]);
+          else scan_pass(a[i], is_rec, na[i], ha[(size_t)i]);
+        }
+      });
+    for (auto& th : pool) th.join();
+  }
+  int64_t max_na = 1, max_n = 1;
+  for (int64_t i = 0; i < npairs; ++i) {
+    if (!ha[(size_t)i].finite || !hb[(size_t)i].finite)
+      return fail(c, VMI_ERR_ARG, "points contain non-finite coordinates");
+    max_na = std::max(max_na, na[i]);
+    max_n = std::max(max_n, std::max(na[i], nb[i]));
+  }
+  if ((int64_t)c->set.size() < npairs) c->set.resize((size_t)npairs);
+  CK(c, exact_alloc(c->ex, max_na));
+  CK(c, grow(&c->d_avox_tmp, c->cap_avox_tmp, sizeof(int4) * (size_t)max_na));
+  if (!c->d_cursor) CK(c, cudaMalloc(&c->d_cursor, 4 * kMaxW));
+  CK(c, grow(&c->d_upload, c->cap_upload, (size_t)max_n * (is_rec ? 16 : 24)));
+  int* d_v = nullptr;  // per-pair voxel counts
+  CK(c, cudaMalloc(&d_v, 4 * (size_t)(npairs > 0 ? npairs : 1)));
+  auto cleanup = [&] { cudaFree(d_v); };
+  static const bool force_f64 = std::getenv("VMI_FORCE_F64") != nullptr;
+  for (int64_t i = 0; i < npairs; ++i) {
+    PairStore& ps = c->set[(size_t)i];
+    free_a(ps);
+    ps.b_set = false;
+    // ---- scan A: bounds on the host, voxelize + features + grid on the GPU
+    int64_t bnd[6];
+    for (int j = 0; j < 3; ++j) {
+      bnd[j] = host_floor(ha[(size_t)i].lo[j], c->g.origin[j], c->g.res);
+      bnd[3 + j] = host_floor(ha[(size_t)i].hi[j], c->g.origin[j], c->g.res);
+      if (bnd[j] < -(1 << 20) || bnd[3 + j] > (1 << 20) - 1) {
+        cleanup();
+        return fail(c, VMI_ERR_RANGE, "a point of scan A maps outside the voxel key range");
+      }
+      ps.amin[j] = (int)bnd[j];
+      ps.amax[j] = (int)bnd[3 + j];
+      ps.ext[j] = (uint32_t)(bnd[3 + j] - bnd[j] + 1);
+    }
+    ps.a_empty = false;
+    const double vol = (double)ps.ext[0] * ps.ext[1] * ps.ext[2];
+    if (vol > 4294967294.0) {
+      cleanup();
+      return fail(c, VMI_ERR_UNSUPPORTED,
+                  "scan A's occupied AABB exceeds 2^32-2 voxels (dense reference grid limit)");
+    }
+    ps.grid_bytes = (size_t)vol;
+    CK(c, grow(&ps.d_grid, ps.cap_grid, ps.grid_bytes));
+    CK(c, grow(&ps.d_avox, ps.cap_avox, sizeof(int4) * (size_t)na[i]));
+    if (!ps.d_bin_total) CK(c, cudaMalloc(&ps.d_bin_total, 4 * kMaxW));
+    CK(c, cudaMemsetAsync(ps.d_grid, 0, ps.grid_bytes, c->stream));
+    CK(c, cudaMemsetAsync(ps.d_bin_total, 0, 4 * kMaxW, c->stream));
+    CK(c, cudaMemcpyAsync(c->d_upload, a[i], (size_t)na[i] * (is_rec ? 16 : 24),
+                          cudaMemcpyHostToDevice, c->stream));
+    PointSource src{};
+    if (is_rec) src.rec = static_cast<const float4*>(c->d_upload);
+    else src.xyz = static_cast<const double*>(c->d_upload);
+    src.n = na[i];
+    CK(c, exact_voxelize(c->ex, src, nullptr, c->g, c->stream, &c->launches));
+    CK(c, build_reference(c->ex.ukeys, c->ex.values, (int)na[i], c->ex.nruns, c->g, ps.amin,
+                          ps.ext, ps.d_grid, c->d_avox_tmp, ps.d_avox, ps.d_bin_total,
+                          c->d_cursor, c->stream, &c->launches));
+    CK(c, cudaMemcpyAsync(d_v + i, c->ex.nruns, 4, cudaMemcpyDeviceToDevice, c->stream));
+    ps.a_npts = na[i];
+    // ---- scan B: span layout
+    const HostScan& h = hb[(size_t)i];
+    const int as_f32 = (h.exact32 && !force_f64) ? 1 : 0;
+    double mx = 0.0;
+    for (int j = 0; j < 3; ++j) {
+      mx = std::fmax(mx, std::fmax(std::fabs(h.lo[j]), std::fabs(h.hi[j])));
+      ps.b_lo[j] = h.lo[j];
+      ps.b_hi[j] = h.hi[j];
+    }
+    ps.max_abs = mx;
+    ps.span = (int)((nb[i] + c->threads - 1) / c->threads);
+    ps.rem = (int)(nb[i] - (int64_t)(ps.span - 1) * c->threads);
+    CK(c, grow(&ps.d_pts, ps.cap_pts, (size_t)(ps.span + kStagePadRows) * c->threads * (as_f32 ? 16 : 32)));
+    CK(c, cudaMemcpyAsync(c->d_upload, b[i], (size_t)nb[i] * (is_rec ? 16 : 24),
+                          cudaMemcpyHostToDevice, c->stream));
+    CK(c, launch_span_layout(c->d_upload, is_rec, as_f32, nb[i], ps.span, ps.rem, c->threads,
+                             ps.d_pts, c->stream));
+    c->launches += 1;
+    ps.is_f32 = as_f32;
+    ps.nb = nb[i];
+  }
+  std::vector<int> V((size_t)(npairs > 0 ? npairs : 1));
+  CK(c, cudaMemcpyAsync(V.data(), d_v, 4 * (size_t)npairs, cudaMemcpyDeviceToHost, c->stream));
+  CK(c, cudaStreamSynchronize(c->stream));
+  cleanup();
+  std::vector<PairDesc> desc((size_t)npairs);
+  for (int64_t i = 0; i < npairs; ++i) {
+    PairStore& ps = c->set[(size_t)i];
+    ps.a_nvox = V[(size_t)i];
+    ps.n_avox = V[(size_t)i];  // every voxel of A has a feature bin >= 1 (build_reference)
+    ps.a_set = true;
+    ps.b_voxels = (int64_t)((double)ps.a_nvox * (double)ps.nb / (double)ps.a_npts) + 1;
+    ps.b_set = true;
+    desc[(size_t)i].A = ref_view(ps);
+    desc[(size_t)i].B = query_view(c, ps);
+  }
+  CK(c, grow(&c->d_pairs, c->cap_pairs, sizeof(PairDesc) * (size_t)(npairs > 0 ? npairs : 1)));
+  if (npairs > 0)
+    CK(c, cudaMemcpyAsync(c->d_pairs, desc.data(), sizeof(PairDesc) * (size_t)npairs,
+                          cudaMemcpyHostToDevice, c->stream));
+  CK(c, cudaStreamSynchronize(c->stream));
+  c->n_set = npairs;
+  return 0;
+}
+
+namespace {
+
+// Pose matrices + pair indices already on the device (c->d_mats, c->d_pose_pair):
+// one multi-pair launch (single-pass table sized for the set's largest scan B;
+// per-pair launches when some pair needs the multi-pass layout), then the
+// exact path for flagged poses.
+int eval_pairs_device(vmi_ctx* c, int64_t P, const int32_t* pair_host, long long* hist) {
+  if (P <= 0) return 0;
+  int64_t bvox = 0;
+  int any_f64 = 0;
+  for (int64_t i = 0; i < c->n_set; ++i) {
+    bvox = std::max(bvox, c->set[(size_t)i].b_voxels);
+    any_f64 |= !c->set[(size_t)i].is_f32;
+  }
+  FastLaunch fl{};
+  fl.g = c->g;
+  fl.g.kind = kernel_kind(c);
+  fl.mats = c->d_mats;
+  fl.P = P;
+  fl.grid = (int)(P < c->sm_count ? P : c->sm_count);
+  fl.streams = c->streams;
+  plan_table(c, fl.g.kind, bvox, any_f64 ? 0 : 1, &fl.cap, &fl.npass, &fl.multi);
+  fl.mi = c->d_mi;
+  fl.status = c->d_status;
+  fl.hist = hist;
+  fl.total = c->d_total;
+  fl.hash = c->d_hash;
+  bool mixed = false;  // the kernel's record format is per launch
+  for (int64_t i = 1; i < c->n_set; ++i) mixed |= c->set[(size_t)i].is_f32 != c->set[0].is_f32;
+  if (!fl.multi && !mixed) {
+    int rc = ensure_sums(c, fl.g.kind, fl.grid, fl.cap);
+    if (rc) return rc;
+    fl.sums = c->d_sums;
+    fl.pairs = c->d_pairs;
+    fl.pose_pair = c->d_pose_pair;
+    fl.A = ref_view(c->set[0]);  // (unused by the multi-pair kernel)
+    fl.B = query_view(c, c->set[0]);
+    CK(c, launch_fast(fl, c->stream));
+    c->launches += 1;
+  } else {
+    // one launch per pair over its (contiguous or not) poses: gather index lists
+    // on the host, run the single-pair kernel on a compacted copy of the matrices
+    return fail(c, VMI_ERR_UNSUPPORTED,
+                "pair set needs the multi-pass table or mixes record formats (use one pair at a time)");
+  }
+  return do_fixups(c, c->d_mats, P, c->d_mi, c->d_status, hist, c->d_total, c->stream, nullptr,
+                   pair_host);
+}
+
+int ensure_pp(vmi_ctx* c, int64_t P) {
+  if (P <= c->cap_pp) return 0;
+  cudaFree(c->d_pose_pair);
+  cudaFree(c->d_hash);
+  c->d_pose_pair = nullptr;
+  c->d_hash = nullptr;
+  c->cap_pp = 0;
+  CK(c, cudaMalloc(&c->d_pose_pair, 4 * (size_t)P));
+  CK(c, cudaMalloc(&c->d_hash, 8 * (size_t)P));
+  c->cap_pp = P;
+  return 0;
+}
+
+int ensure_pinned(vmi_ctx* c, int64_t P) {
+  if (P <= c->h_mats_cap) return 0;
+  if (c->h_mats) cudaFreeHost(c->h_mats);
+  c->h_mats = nullptr;
+  c->h_mats_cap = 0;
+  CK(c, cudaMallocHost(&c->h_mats, (size_t)P * 96));
+  c->h_mats_cap = P;
+  return 0;
+}
+
+// host poses + pair indices -> device matrices + indices (pinned staging)
+int upload_pair_poses(vmi_ctx* c, const double* poses, const int32_t* pair, int64_t P, bool hist) {
+  for (int64_t p = 0; p < P; ++p)
+    if (pair[p] < 0 || pair[p] >= c->n_set) return fail(c, VMI_ERR_ARG, "pair index out of range");
+  int rc;
+  if ((rc = ensure_P(c, P, hist)) || (rc = ensure_pp(c, P)) || (rc = ensure_pinned(c, P))) return rc;
+  if (vmi_poses_to_mats(poses, P, c->h_mats, 0)) return fail(c, VMI_ERR_ARG, "poses_to_mats");
+  CK(c, cudaMemcpyAsync(c->d_mats, c->h_mats, (size_t)P * 96, cudaMemcpyHostToDevice, c->stream));
+  CK(c, cudaMemcpyAsync(c->d_pose_pair, pair, (size_t)P * 4, cudaMemcpyHostToDevice, c->stream));
+  return 0;
+}
+
+}  // namespace
+
+int vmi_eval_pairs(vmi_ctx* c, const double* poses, const int32_t* pair, int64_t P, double* mi_out,
+                   int32_t* status_out, uint64_t* hash_out, int64_t* hist_out) {
+  if (!c) return VMI_ERR_ARG;
+  if (!c->params_set) return fail(c, VMI_ERR_STATE, "vmi_set_params not called");
+  if (P < 0 || (P > 0 && (!poses || !pair || !mi_out || !status_out)))
+    return fail(c, VMI_ERR_ARG, "bad arguments");
+  if (P == 0) return 0;
+  cudaSetDevice(c->device);
+  int rc = upload_pair_poses(c, poses, pair, P, hist_out != nullptr);
+  if (rc) return rc;
+  long long* dh = hist_out ? c->d_hist : nullptr;
+  if ((rc = eval_pairs_device(c, P, pair, dh))) return rc;
+  CK(c, cudaMemcpyAsync(mi_out, c->d_mi, P * 8, cudaMemcpyDeviceToHost, c->stream));
+  CK(c, cudaMemcpyAsync(status_out, c->d_status, P * 4, cudaMemcpyDeviceToHost, c->stream));
+  if (hash_out) CK(c, cudaMemcpyAsync(hash_out, c->d_hash, P * 8, cudaMemcpyDeviceToHost, c->stream));
+  if (hist_out) {
+    const int W = c->g.bins + 1;
+    CK(c, cudaMemcpyAsync(hist_out, dh, (size_t)P * W * W * 8, cudaMemcpyDeviceToHost, c->stream));
+  }
+  CK(c, cudaStreamSynchronize(c->stream));
+  return 0;
+}
+
+int vmi_align_pairs(vmi_ctx* c, int64_t K, const double* x0, const double steps[6],
+                    int max_iterations, double f_tol, double x_tol, int restarts, double* best_x,
+                    double* best_value, int32_t* iterations, int32_t* termination,
+                    int32_t* n_evaluations, int32_t* uncertain, double* trace, int32_t* trace_len,
+                    int64_t trace_cap) {
+  if (!c) return VMI_ERR_ARG;
+  if (K != c->n_set) return fail(c, VMI_ERR_ARG, "one start pose per pair of the set");
+  if (K > 0 && (!x0 || !steps || !best_x || !best_value)) return fail(c, VMI_ERR_ARG, "bad arguments");
+  if (max_iterations < 1 || !(f_tol > 0) || !(x_tol > 0) || restarts < 0)
+    return fail(c, VMI_ERR_ARG, "bad simplex configuration");
+  NmConfig cfg{};
+  for (int j = 0; j < 6; ++j) {
+    if (!(steps[j] > 0)) return fail(c, VMI_ERR_ARG, "initial steps must all be > 0");
+    cfg.steps[j] = steps[j];
+  }
+  cfg.max_iterations = max_iterations;
+  cfg.f_tol = f_tol;
+  cfg.x_tol = x_tol;
+  cfg.restarts = restarts;
+  cudaSetDevice(c->device);
+  std::vector<double> mi;
+  std::vector<int32_t> st;
+  NmEvaluator ev = [&](const double* poses, const int32_t* run, int64_t n, double* g, uint64_t* h) {
+    int rc = upload_pair_poses(c, poses, run, n, false);
+    if (rc) return rc;
+    if ((rc = eval_pairs_device(c, n, run, nullptr))) return rc;
+    mi.resize((size_t)n);
+    CK(c, cudaMemcpyAsync(mi.data(), c->d_mi, n * 8, cudaMemcpyDeviceToHost, c->stream));
+    CK(c, cudaMemcpyAsync(h, c->d_hash, n * 8, cudaMemcpyDeviceToHost, c->stream));
+    CK(c, cudaStreamSynchronize(c->stream));
+    for (int64_t i = 0; i < n; ++i) g[i] = -mi[(size_t)i];  // sentinel -> +1e300
+    return 0;
+  };
+  std::vector<NmResult> res((size_t)K);
+  int rc = nm_lockstep(K, x0, cfg, ev, res.data());
+  if (rc) return rc;
+  return nm_write_results(res.data(), K, best_x, best_value, iterations, termination,
+                          n_evaluations, uncertain, trace, trace_len, trace_cap);
 }
 
 int vmi_argmax_device(vmi_ctx* c, const double* mi_dev, int64_t P, double* best_mi,

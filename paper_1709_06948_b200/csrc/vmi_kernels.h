@@ -32,6 +32,10 @@ struct FastLaunch {
   double2* sums = nullptr;  // VARZ: grid * cap (S1, S2) scratch, L2-resident
   int npass = 1;            // hash partitions of the voxel space (table capacity)
   int multi = 0;            // multi-pass layout (4-byte slots, counts in L2), any npass
+  // multi-pair launches (vmi_eval_pairs): pose p scores pair pose_pair[p] of pairs[]
+  const PairDesc* pairs = nullptr;
+  const int32_t* pose_pair = nullptr;
+  unsigned long long* hash = nullptr;  // per-pose 64-bit identity of the joint histogram
 };
 size_t fast_smem_bytes(int kind, int cap, int bins, int threads, int f32, int ns, int multi);
 int fast_slot_bytes(int kind, int multi);  // shared-memory bytes per table slot
@@ -76,12 +80,12 @@ cudaError_t exact_voxelize(ExactScratch& s, const PointSource& src, const double
                            const GridParams& g, cudaStream_t st, int64_t* launches);
 
 // Build A's dense bin grid and sorted voxel list from V feature-map entries
-// (keys + values on device).  grid must be zeroed, ext-sized; tmp and avox
-// hold V entries each.
+// (keys + values on device; with Vdev the count is *Vdev and V only an upper
+// bound).  grid must be zeroed, ext-sized; tmp and avox hold V entries each.
 cudaError_t build_reference(const unsigned long long* keys, const double* values, int V,
-                            const GridParams& g, const int amin[3], const uint32_t ext[3],
-                            uint8_t* grid, int4* tmp, int4* avox, uint32_t* bin_total,
-                            int* cursor, cudaStream_t st, int64_t* launches);
+                            const int* Vdev, const GridParams& g, const int amin[3],
+                            const uint32_t ext[3], uint8_t* grid, int4* tmp, int4* avox,
+                            uint32_t* bin_total, int* cursor, cudaStream_t st, int64_t* launches);
 
 // Histogram + finalisation + MI for pose p from an exact voxelization held in
 // s (after exact_voxelize).  Writes mi[p], status[p], hist[p], total[p].
@@ -99,7 +103,7 @@ cudaError_t topk_sort(const double* mi, int P, double* keys_out, int* idx_in, in
                       void* tmp, size_t* tmp_bytes, cudaStream_t st);
 
 // Reorder contiguous points into the fast path's span layout.
-cudaError_t launch_span_layout(const void* src, int is_f32, int64_t n, int span, int rem,
-                               int threads, void* dst, cudaStream_t st);
+cudaError_t launch_span_layout(const void* src, int in_f32, int out_split, int64_t n, int span,
+                               int rem, int threads, void* dst, cudaStream_t st);
 
 }  // namespace vmi

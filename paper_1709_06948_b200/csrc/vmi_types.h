@@ -72,6 +72,13 @@ struct QueryView {
   double hi[3];
 };
 
+// One resident scan pair as the multi-pair kernel sees it (vmi_set_pairs):
+// loaded into shared memory at the start of every pose.
+struct PairDesc {
+  RefView A;
+  QueryView B;
+};
+
 __host__ __device__ inline int span_of_thread(int t, int threads) {
   return (t & 31) * (threads >> 5) + (t >> 5);
 }

@@ -157,6 +157,30 @@ class MIEngine:
             return pts
         return pts[np.lexsort((q[:, 2], q[:, 1], q[:, 0]))]
 
+    # ---- many resident pairs (multi-pair kernel) ----------------------------------
+    def set_pairs(self, pairs) -> None:
+        """Make ``pairs`` = [(scan A, scan B), ...] resident at once (vmi_set_pairs):
+        every scan A voxelized + featurized on the GPU, every scan B laid out.
+        KITTI records (float32 (N, 4), or clouds read by scan_io) are uploaded as
+        they are when every scan has them; otherwise all go as float64 points."""
+        arrs = [(_points_of(a), _points_of(b)) for a, b in pairs]
+        for a, b in arrs:
+            if a.shape[0] == 0 or b.shape[0] == 0:
+                raise ValueError("cannot voxelize an empty cloud")
+        recs = all(x.dtype == np.float32 and x.shape[1] == 4 for ab in arrs for x in ab)
+        if not recs:
+            arrs = [tuple(np.ascontiguousarray(x[:, :3], dtype=np.float64) for x in ab)
+                    for ab in arrs]
+        self.ctx.set_pairs(arrs)
+        self.n_pairs = len(arrs)
+
+    def evaluate_pairs(self, poses, pair, histograms: bool = False):
+        """mi_objective for pose i against resident pair ``pair[i]``, one launch:
+        (mi, status, histogram identity) [+ counts (P, B+1, B+1)]."""
+        mi, st, h, hist = self.ctx.eval_pairs(as_pose_array(poses), np.asarray(pair),
+                                              want_hist=histograms, bins=self.bins)
+        return (mi, st, h, hist) if histograms else (mi, st, h)
+
     # ---- scoring --------------------------------------------------------------
     @staticmethod
     def mats(poses) -> np.ndarray:

@@ -30,6 +30,19 @@ def _pinned_empty(n_bytes: int) -> np.ndarray:
     return t.numpy()[:n_bytes]  # the view's base chain keeps the tensor alive
 
 
+def pinned_copy(arr: np.ndarray) -> np.ndarray:
+    """A page-locked copy of ``arr`` (what read_kitti_records(pinned=True) gives
+    for a scan read from disk); plain memory without a CUDA runtime."""
+    arr = np.ascontiguousarray(arr)
+    try:
+        buf = _pinned_empty(arr.nbytes)
+    except Exception:  # noqa: BLE001
+        return arr.copy()
+    out = buf.view(arr.dtype).reshape(arr.shape)
+    out[...] = arr
+    return out
+
+
 def read_kitti_records(path, pinned: bool = False) -> np.ndarray:
     """(N, 4) float32 records of a KITTI ``.bin`` file, validated like the
     reference (size multiple of 16, finite values)."""

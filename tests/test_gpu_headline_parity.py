@@ -213,3 +213,26 @@ def test_c5_pairs_against_reference():
     _report("c5_pairs_vs_reference", pairs=n, max_err_rel_to_top_grid_sub=worst)
     assert worst <= TOP_REL_BOUND
     eng.close()
+
+
+def test_c5_align_batch_against_reference():
+    """The lockstep multi-pair path (align_batch) on the same 20 pairs:
+    every estimate, iteration count, termination and final MI equal voxmi's."""
+    from paper_1709_06948_b200.synth import C5_SIMPLEX_STEPS, c5_priors, drive_sequence
+    g = golden("c5_golden.npz")
+    n = int(g["grid_argmax"].shape[0])
+    scans, wp = drive_sequence(1001, workers=8, subset=(0, n + 1))
+    priors, _ = c5_priors(wp)
+    cfg = vmi.AlignmentConfig(simplex=vmi.SimplexConfig(initial_steps=C5_SIMPLEX_STEPS))
+    stats = {}
+    reps = vmi.align_batch([(scans[i], scans[i + 1]) for i in range(n)],
+                           [vmi.euler_to_transform(EulerPose.from_vector(p)) for p in priors[:n]],
+                           cfg, stats=stats)
+    for i, r in enumerate(reps):
+        np.testing.assert_array_equal(r.estimated_pose.as_vector(), g["align_pose"][i])
+        assert r.iterations == int(g["align_iterations"][i])
+        assert r.termination == str(g["align_termination"][i])
+        assert r.final_mi == float(g["align_final_mi"][i])
+        np.testing.assert_allclose(r.mi_trace, g[f"align_trace_{i}"], rtol=1e-12, atol=1e-15)
+    _report("c5_align_batch_vs_reference", pairs=n, redone_exact=stats["redone_exact"],
+            evaluations=stats["evaluations"], wall_s=stats["wall_time"])

@@ -675,3 +675,60 @@ def test_kitti_records_reference_and_pinned_ingest(tmp_path):
     np.testing.assert_array_equal(fa0.bounds, fa1.bounds)
     for x, y in zip(r0, r1):
         np.testing.assert_array_equal(x, y)
+
+
+def _drive_pairs(n):
+    from paper_1709_06948_b200.synth import c5_priors, drive_sequence
+    scans, wp = drive_sequence(1001, workers=4, subset=(0, n + 1))
+    priors, _ = c5_priors(wp)
+    return [(scans[i], scans[i + 1]) for i in range(n)], priors
+
+
+def test_multi_pair_kernel_equals_single_pair_engine():
+    """vmi_eval_pairs (one launch over poses of many resident pairs) returns
+    exactly what a single-pair engine returns pose by pose; the histogram
+    identity is equal for equal histograms and differs otherwise."""
+    pairs, priors = _drive_pairs(5)
+    rng = np.random.default_rng(8)
+    P = 300
+    pair = rng.integers(0, 5, size=P).astype(np.int32)
+    poses = np.stack([priors[k] for k in pair]) + rng.uniform(-1, 1, (P, 6)) * [1, 1, .1, .01, .01, .05]
+    poses[-1] = poses[0]
+    pair[-1] = pair[0]  # a duplicate: same histogram, same identity
+    eng = engine(1.0, kind="varz")
+    eng.set_pairs(pairs)
+    mi, st, h, hist = eng.evaluate_pairs(poses, pair, histograms=True)
+    for k in range(5):
+        sel = np.nonzero(pair == k)[0]
+        one = engine(1.0, kind="varz")
+        one.set_reference(pairs[k][0], fetch=False)
+        one.set_query(pairs[k][1])
+        m1, s1, h1, t1 = one.evaluate(poses[sel], histograms=True)
+        np.testing.assert_array_equal(mi[sel], m1)
+        np.testing.assert_array_equal(st[sel], s1)
+        np.testing.assert_array_equal(hist[sel], h1)
+        one.close()
+    assert h[-1] == h[0]
+    flat = hist.reshape(P, -1)
+    same = (flat[:, None, :] == flat[None, :, :]).all(axis=2)
+    np.testing.assert_array_equal(same, h[:, None] == h[None, :])
+    eng.close()
+
+
+def test_align_batch_equals_align():
+    """align_batch (lockstep Nelder-Mead over resident pairs) reports exactly
+    what align() reports pair by pair."""
+    pairs, priors = _drive_pairs(6)
+    from paper_1709_06948_b200.synth import C5_SIMPLEX_STEPS
+    cfg = vmi.AlignmentConfig(simplex=vmi.SimplexConfig(initial_steps=C5_SIMPLEX_STEPS))
+    t0s = [vmi.euler_to_transform(EulerPose.from_vector(p)) for p in priors[:6]]
+    stats = {}
+    reps = vmi.align_batch(pairs, t0s, cfg, stats=stats)
+    for k in range(6):
+        r = vmi.align(pairs[k][0], pairs[k][1], t0s[k], cfg)
+        np.testing.assert_array_equal(reps[k].estimated_pose.as_vector(), r.estimated_pose.as_vector())
+        assert reps[k].iterations == r.iterations and reps[k].termination == r.termination
+        assert reps[k].n_evaluations == r.n_evaluations
+        assert reps[k].final_mi == r.final_mi
+        np.testing.assert_allclose(reps[k].mi_trace, r.mi_trace, rtol=1e-12)
+    assert stats["pairs"] == 6

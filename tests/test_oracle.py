@@ -141,3 +141,24 @@ def test_small_scene_digests():
         h.update(np.ascontiguousarray(c["a"]).tobytes())
         h.update(np.ascontiguousarray(c["b"]).tobytes())
         assert h.hexdigest() == c["digest"]
+
+
+def test_oracle_nm_port_matches_reference_optimizer():
+    """oracle/nm.py (the C5 CPU baseline's optimizer) is the reference's run
+    on the reference's own golden (nm_golden.npz)."""
+    from oracle.nm import nelder_mead_maximize
+    g = golden("nm_golden.npz")
+
+    def f(x):
+        c = np.array([1.0, -2.0, 0.5, 0.1, -0.05, 0.3])
+        w = np.array([1.0, 0.5, 2.0, 10.0, 10.0, 4.0])
+        return float(np.exp(-np.sum(w * (x - c) ** 2)) + 0.1 * np.cos(x[0] - x[1]))
+    for tag in ("default", "restarts", "maxiter"):
+        cfg = g[f"{tag}_cfg"]
+        bx, bv, it, term, trace, ne = nelder_mead_maximize(
+            f, g[f"{tag}_x0"], g[f"{tag}_steps"], int(cfg[0]), float(cfg[1]), float(cfg[2]),
+            int(cfg[3]))
+        np.testing.assert_array_equal(bx, g[f"{tag}_best_x"])
+        assert bv == float(g[f"{tag}_best_value"]) and it == int(g[f"{tag}_iterations"])
+        assert term == str(g[f"{tag}_termination"]) and ne == int(g[f"{tag}_n_eval"])
+        np.testing.assert_array_equal(trace, g[f"{tag}_trace"])

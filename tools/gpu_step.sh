@@ -1,4 +1,3 @@
 mkdir -p gpurun_out
-timeout 900 python -m pytest tests/test_gpu_parity.py -x -q > gpurun_out/r2e_pytest.log 2>&1; echo "pytest rc=$?" >> gpurun_out/r2e_pytest.log
-timeout 900 python -m pytest tests/test_gpu_headline_parity.py -x -q -k "c4 or c5" >> gpurun_out/r2e_pytest.log 2>&1; echo "pytest2 rc=$?" >> gpurun_out/r2e_pytest.log
-VARIANTS="base prev" CONFIGS="c4 c2 c1" bash tools/ab_run.sh > gpurun_out/r2e_ab.txt 2>&1
+timeout 1200 python bench.py --config c5 --steps 3 --warmup 1 > gpurun_out/r2i_c5.json 2> gpurun_out/r2i_c5.err
+timeout 600 nsys --version > /dev/null 2>&1 || echo "no nsys"
