@@ -626,16 +626,19 @@ def run_c5(args, world, rank, local):
         pin = {i: pinned_copy(scans[i]) for i in range(lo, hi + 1)}
         my_pairs = [(pin[i], pin[i + 1]) for i in mine]
         t0s = [vmi.euler_to_transform(vmi.EulerPose.from_vector(priors[i])) for i in mine]
-        for _ in range(max(1, args.warmup)):
-            vmi.align_batch(my_pairs[:64], t0s[:64], cfg, engine=eng)
+        for _ in range(max(1, args.warmup)):  # (sizes the engine's grow-only buffers)
+            vmi.align_batch(my_pairs, t0s, cfg, engine=eng)
         torch.cuda.synchronize()
         if dist:
             dist.barrier()
         stats = {}
+        acc = {}
         launches0 = eng.ctx.launches
         t0 = time.perf_counter()
         for _ in range(args.steps):
             reps = vmi.align_batch(my_pairs, t0s, cfg, engine=eng, stats=stats)
+            for k in ("set_pairs_s", "wall_time", "final_eval_s", "reports_s"):
+                acc[k] = acc.get(k, 0.0) + stats[k] / args.steps
         torch.cuda.synchronize()
         dt = time.perf_counter() - t0
         launches = eng.ctx.launches - launches0
@@ -644,8 +647,7 @@ def run_c5(args, world, rank, local):
         extra = {"redone_exact": int(sum_over_ranks(dist, cdev, float(stats["redone_exact"]))),
                  "gpu_launches_per_step": launches / args.steps,
                  "nm_wall_s_per_step": stats["wall_time"],
-                 "breakdown_s_per_step": {k: round(stats[k], 4) for k in
-                                          ("set_pairs_s", "wall_time", "final_eval_s", "reports_s")},
+                 "breakdown_s_per_step": {k: round(v, 4) for k, v in acc.items()},
                  "input": "float32 KITTI records in pinned host memory, uploaded every step"}
         eng.close()
     else:

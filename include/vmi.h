@@ -176,8 +176,12 @@ int vmi_topk_device(vmi_ctx* ctx, const double* mi_dev, int64_t P, int64_t K, do
    identity h[i] of the value's source (equal identities must mean equal values) */
 typedef int (*vmi_nm_eval_fn)(void* user, const double* poses, const int32_t* run, int64_t n,
                               double* g, uint64_t* h);
+/* spec_budget: probes per step up to which an iteration evaluates its four
+   candidates at once (< 0: always); above it, the reflection first and then the
+   one follow-up the reference needs (same decisions, fewer probes). */
 int vmi_nm_run(int64_t K, const double* x0, const double steps[6], int max_iterations,
-               double f_tol, double x_tol, int restarts, vmi_nm_eval_fn fn, void* user,
+               double f_tol, double x_tol, int restarts, int64_t spec_budget, vmi_nm_eval_fn fn,
+               void* user,
                double* best_x, double* best_value, int32_t* iterations, int32_t* termination,
                int32_t* n_evaluations, int32_t* uncertain, double* trace, int32_t* trace_len,
                int64_t trace_cap);

@@ -55,7 +55,7 @@ def nm_out_args(o: dict) -> list:
 
 
 def nm_run(x0: np.ndarray, steps, max_iterations: int, f_tol: float, x_tol: float,
-           restarts: int, f_batch) -> dict:
+           restarts: int, f_batch, spec_budget: int = -1) -> dict:
     """vmi_nm_run with a Python objective: ``f_batch(poses (n, 6), run (n,))`` ->
     (values (n,), identities (n,) uint64).  Returns the output arrays."""
     x0 = np.ascontiguousarray(x0, dtype=np.float64).reshape(-1, 6)
@@ -78,7 +78,8 @@ def nm_run(x0: np.ndarray, steps, max_iterations: int, f_tol: float, x_tol: floa
             return -1
     fn = NM_EVAL_FN(cb)
     rc = load().vmi_nm_run(K, ptr(x0, _d), ptr(st, _d), int(max_iterations), float(f_tol),
-                           float(x_tol), int(restarts), fn, None, *nm_out_args(o), cap)
+                           float(x_tol), int(restarts), int(spec_budget), fn, None,
+                           *nm_out_args(o), cap)
     if err:
         raise err[0]
     if rc:
@@ -138,8 +139,8 @@ def load(path: str = LIB_PATH):
     L.vmi_set_tuning.argtypes = [_ctx, ctypes.c_int, ctypes.c_int]
     L.vmi_set_passes.argtypes = [_ctx, ctypes.c_int]
     L.vmi_nm_run.argtypes = [ctypes.c_int64, _d, _d, ctypes.c_int, ctypes.c_double,
-                             ctypes.c_double, ctypes.c_int, NM_EVAL_FN, _vp, _d, _d, _i32, _i32,
-                             _i32, _i32, _d, _i32, ctypes.c_int64]
+                             ctypes.c_double, ctypes.c_int, ctypes.c_int64, NM_EVAL_FN, _vp, _d,
+                             _d, _i32, _i32, _i32, _i32, _d, _i32, ctypes.c_int64]
     L.vmi_set_pairs.argtypes = [_ctx, ctypes.c_int64, ctypes.POINTER(_vp), _i64,
                                 ctypes.POINTER(_vp), _i64, ctypes.c_int]
     L.vmi_eval_pairs.argtypes = [_ctx, _d, _i32, ctypes.c_int64, _d, _i32,

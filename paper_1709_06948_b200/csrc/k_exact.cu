@@ -163,6 +163,18 @@ cudaError_t exact_alloc(ExactScratch& s, int64_t n) {
   VMI_TRY(cub::DeviceScan::ExclusiveSum(nullptr, b3, s.counts, s.offsets, (int)m));
   s.cub_bytes = b1 > b2 ? b1 : b2;
   if (b3 > s.cub_bytes) s.cub_bytes = b3;
+  {  // the box path (box_voxelize) sorts / encodes 32-bit keys in the same buffers
+    uint32_t* k32 = reinterpret_cast<uint32_t*>(s.keys);
+    uint32_t* k32s = reinterpret_cast<uint32_t*>(s.keys_sorted);
+    size_t c1 = 0, c2 = 0;
+    VMI_TRY(cub::DeviceRadixSort::SortPairs(nullptr, c1, k32, k32s, s.idx, s.idx_sorted, (int)m, 0,
+                                            32));
+    VMI_TRY(cub::DeviceRunLengthEncode::Encode(nullptr, c2, k32s,
+                                               reinterpret_cast<uint32_t*>(s.ukeys), s.counts,
+                                               s.nruns, (int)m));
+    if (c1 > s.cub_bytes) s.cub_bytes = c1;
+    if (c2 > s.cub_bytes) s.cub_bytes = c2;
+  }
   VMI_TRY(cudaMalloc(&s.cub_tmp, s.cub_bytes));
   s.cap_n = m;
   return cudaSuccess;
@@ -198,6 +210,78 @@ cudaError_t exact_voxelize(ExactScratch& s, const PointSource& src, const double
   k_features<<<blocks, T, 0, st>>>(s.counts, s.offsets, s.nruns, s.zs, g.kind, s.values);
   if (launches) *launches += 5;  // own kernels (CUB launches not counted)
   return cudaGetLastError();
+}
+
+// ---- scan A inside a known box (pair sets: bounds from the host AABB) --------
+// The packed key's x-major lexicographic order (voxel.py:65-73) is the order of
+// the linear index inside scan A's voxel box, so a stable sort of 32-bit box
+// indices over ceil(log2(volume)) bits gives voxelize's exact order (stable
+// within a voxel: numpy's reduceat order for VARZ) in a few radix passes
+// instead of eight 64-bit ones.
+__global__ void k_box_keys(PointSource src, GridParams g, int3 amin, uint3 ext, uint32_t* keys,
+                           int* idx, double* zout, int* bad) {
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= src.n) return;
+  double x, y, z;
+  point_at(src, i, x, y, z);
+  int a, b, c;
+  bool ok = voxel_coord(x, g.origin[0], g.res, g.inv_res, g.mode, a);
+  ok &= voxel_coord(y, g.origin[1], g.res, g.inv_res, g.mode, b);
+  ok &= voxel_coord(z, g.origin[2], g.res, g.inv_res, g.mode, c);
+  const uint32_t rx = (uint32_t)(a - amin.x), ry = (uint32_t)(b - amin.y), rz = (uint32_t)(c - amin.z);
+  if (!ok || rx >= ext.x || ry >= ext.y || rz >= ext.z) {  // cannot happen: the box is exact
+    *bad = 1;
+    keys[i] = 0;
+  } else {
+    keys[i] = (rx * ext.y + ry) * ext.z + rz;
+  }
+  idx[i] = (int)i;
+  zout[i] = z;
+}
+
+cudaError_t box_voxelize(ExactScratch& s, const PointSource& src, const GridParams& g,
+                         const int amin[3], const uint32_t ext[3], cudaStream_t st,
+                         int64_t* launches) {
+  const int64_t n = src.n;
+  VMI_TRY(exact_alloc(s, n));
+  const uint64_t vol = (uint64_t)ext[0] * ext[1] * ext[2];
+  int nbits = 1;
+  while (nbits < 32 && (1ull << nbits) < vol) ++nbits;
+  const int T = 256;
+  const int blocks = (int)((n + T - 1) / T);
+  uint32_t* k32 = reinterpret_cast<uint32_t*>(s.keys);
+  uint32_t* k32s = reinterpret_cast<uint32_t*>(s.keys_sorted);
+  uint32_t* u32 = reinterpret_cast<uint32_t*>(s.ukeys);
+  VMI_TRY(cudaMemsetAsync(s.bounds + 6, 0, 4, st));
+  k_box_keys<<<blocks, T, 0, st>>>(src, g, make_int3(amin[0], amin[1], amin[2]),
+                                   make_uint3(ext[0], ext[1], ext[2]), k32, s.idx, s.z,
+                                   s.bounds + 6);
+  size_t bytes = s.cub_bytes;
+  VMI_TRY(cub::DeviceRadixSort::SortPairs(s.cub_tmp, bytes, k32, k32s, s.idx, s.idx_sorted, (int)n,
+                                          0, nbits, st));
+  bytes = s.cub_bytes;
+  VMI_TRY(cub::DeviceRunLengthEncode::Encode(s.cub_tmp, bytes, k32s, u32, s.counts, s.nruns,
+                                             (int)n, st));
+  bytes = s.cub_bytes;
+  VMI_TRY(cub::DeviceScan::ExclusiveSum(s.cub_tmp, bytes, s.counts, s.offsets, (int)n, st));
+  k_gather<<<blocks, T, 0, st>>>(s.z, s.idx_sorted, n, s.zs);
+  k_features<<<blocks, T, 0, st>>>(s.counts, s.offsets, s.nruns, s.zs, g.kind, s.values);
+  if (launches) *launches += 3;
+  return cudaGetLastError();
+}
+
+__global__ void k_build_grid_box(const uint32_t* lin, const double* values, const int* Vdev,
+                                 GridParams g, uint3 ext, uint8_t* grid, int4* avox_tmp,
+                                 uint32_t* bin_total) {
+  const int v = blockIdx.x * blockDim.x + threadIdx.x;
+  if (v >= *Vdev) return;
+  const uint32_t l = lin[v];
+  const uint32_t rz = l % ext.z, rxy = l / ext.z;
+  const uint32_t ry = rxy % ext.y, rx = rxy / ext.y;
+  const int bin = feature_bin(values[v], g.clamp, g.bins);
+  grid[l] = (uint8_t)bin;
+  avox_tmp[v] = make_int4((int)rx, (int)ry, (int)rz, bin);
+  atomicAdd(&bin_total[bin], 1u);
 }
 
 // ---- scan A's reference grid -------------------------------------------------
@@ -238,6 +322,21 @@ __global__ void k_scatter_by_bin(const int4* avox_tmp, int V, const int* Vdev, i
   if (a.w >= 0) avox[atomicAdd(&cursor[a.w], 1)] = a;
 }
 
+cudaError_t build_reference_box(const ExactScratch& s, int Vmax, const GridParams& g,
+                                const uint32_t ext[3], uint8_t* grid, int4* tmp, int4* avox,
+                                uint32_t* bin_total, int* cursor, cudaStream_t st,
+                                int64_t* launches) {
+  if (Vmax <= 0) return cudaSuccess;
+  const int T = 256, blocks = (Vmax + T - 1) / T;
+  k_build_grid_box<<<blocks, T, 0, st>>>(reinterpret_cast<const uint32_t*>(s.ukeys), s.values,
+                                         s.nruns, g, make_uint3(ext[0], ext[1], ext[2]), grid, tmp,
+                                         bin_total);
+  k_bin_offsets<<<1, 32, 0, st>>>(bin_total, g.bins + 1, cursor);
+  k_scatter_by_bin<<<blocks, T, 0, st>>>(tmp, Vmax, s.nruns, cursor, avox);
+  if (launches) *launches += 3;
+  return cudaGetLastError();
+}
+
 cudaError_t build_reference(const unsigned long long* keys, const double* values, int V,
                             const int* Vdev, const GridParams& g, const int amin[3],
                             const uint32_t ext[3], uint8_t* grid, int4* tmp, int4* avox,
@@ -275,7 +374,7 @@ constexpr int kScoreThreads = 512;
 __global__ void __launch_bounds__(kScoreThreads)
     k_exact_finalize(const int* bounds, const unsigned int* ghist, GridParams g, RefView A,
                      int64_t p, double* mi_out, int32_t* status_out, long long* hist_out,
-                     long long* total_out) {
+                     long long* total_out, unsigned long long* hash_out) {
   __shared__ uint32_t hist[kMaxW * kMaxW];
   __shared__ uint32_t marg[kMaxW];
   __shared__ double red[3 * kScoreThreads / 32];
@@ -301,6 +400,7 @@ __global__ void __launch_bounds__(kScoreThreads)
       mi_out[p] = -1e300;
       status_out[p] = status;
       if (total_out) total_out[p] = 0;
+      if (hash_out) hash_out[p] = 0;
     }
     if (hist_out)
       for (int i = tid; i < W * W; i += kScoreThreads) hist_out[p * W * W + i] = 0;
@@ -325,17 +425,23 @@ __global__ void __launch_bounds__(kScoreThreads)
   if (hist_out)
     for (int i = tid; i < W * W; i += kScoreThreads)
       hist_out[p * W * W + i] = i == 0 ? r.h00 : (long long)hist[i];
+  if (hash_out) {  // the fast kernel's histogram identity (vmi_device.cuh)
+    __shared__ unsigned long long hred[kScoreThreads / 32];
+    const unsigned long long h = block_hist_hash<kScoreThreads>(hist, r.h00, W, hred);
+    if (tid == 0) hash_out[p] = r.status == 0 ? h : 0ull;
+  }
 }
 
 cudaError_t exact_score(ExactScratch& s, const GridParams& g, const RefView& A, int64_t p,
                         double* mi, int32_t* status, long long* hist, long long* total,
-                        cudaStream_t st, int64_t* launches) {
+                        cudaStream_t st, int64_t* launches, unsigned long long* hash) {
   const int W = g.bins + 1;
   VMI_TRY(cudaMemsetAsync(s.ghist, 0, (size_t)W * W * 4, st));
   const int T = 256;
   const int blocks = (int)((s.cap_n + T - 1) / T);
   k_exact_hist<<<blocks, T, 0, st>>>(s.ukeys, s.values, s.nruns, g, A, s.ghist);
-  k_exact_finalize<<<1, kScoreThreads, 0, st>>>(s.bounds, s.ghist, g, A, p, mi, status, hist, total);
+  k_exact_finalize<<<1, kScoreThreads, 0, st>>>(s.bounds, s.ghist, g, A, p, mi, status, hist, total,
+                                                hash);
   if (launches) *launches += 2;
   return cudaGetLastError();
 }

@@ -304,15 +304,6 @@ __device__ __forceinline__ double pin_reg(double v) {
 #define VMI_TR(msg, a)
 #endif
 
-// 64-bit identity of a joint histogram: sum of cell * mix(cell index) mod 2^64
-// (order-free, so any reduction order gives the same value; splitmix64 mixer)
-__device__ __forceinline__ unsigned long long cell_mix(unsigned long long i) {
-  i += 0x9E3779B97F4A7C15ull;
-  i = (i ^ (i >> 30)) * 0xBF58476D1CE4E5B9ull;
-  i = (i ^ (i >> 27)) * 0x94D049BB133111EBull;
-  return i ^ (i >> 31);
-}
-
 // MP (multi-pair): pose p scores pair pose_pair[p] of pairs[] (descriptor
 // copied to shared memory per pose); otherwise the kernel parameters A0/B0.
 template <int THREADS, int NS, int KIND, bool F32, int MODE, bool MULTI, bool MP>
@@ -1005,19 +996,8 @@ __global__ void __launch_bounds__(THREADS, 1)
         hist_out[p * W * W + i] = i == 0 ? r.h00 : (long long)hist[i];
     }
     if (hash_out) {  // block-uniform
-      unsigned long long h = 0;
-      if (r.status == 0)
-        for (int i = tid; i < W * W; i += THREADS)
-          h += (unsigned long long)(i == 0 ? r.h00 : (long long)hist[i]) * cell_mix((unsigned long long)i);
-#pragma unroll
-      for (int o = 16; o > 0; o >>= 1) h += __shfl_xor_sync(0xffffffffu, h, o);
-      if (lane == 0) hash_s[wid] = h;
-      __syncthreads();
-      if (tid == 0) {
-        unsigned long long t = 0;
-        for (int w = 0; w < THREADS / 32; ++w) t += hash_s[w];
-        hash_out[p] = t;
-      }
+      const unsigned long long h = block_hist_hash<THREADS>(hist, r.h00, W, hash_s);
+      if (tid == 0) hash_out[p] = r.status == 0 ? h : 0ull;
     }
     __syncthreads();
   }

@@ -42,7 +42,9 @@ constexpr int V = kNmDim + 1;  // simplex vertices
 constexpr double kRefl = 1.0, kExp = 2.0, kContr = 0.5, kShrink = 0.5;  // optim.py:19-22
 constexpr double kRel = 1e-11, kAbs = 1e-13;  // "cannot be told apart" bound on -MI values
 
-enum Phase { kInit, kIter, kShrinkPh, kRestart, kDone };
+// kIter: the four speculative candidates pending; kIterR: the reflection
+// alone; kIterE / kIterCO / kIterCI: the one follow-up it asked for
+enum Phase { kInit, kIter, kIterR, kIterE, kIterCO, kIterCI, kShrinkPh, kRestart, kDone };
 
 struct Run {
   double simplex[V][N];
@@ -61,6 +63,8 @@ struct Run {
   std::vector<double> trace, spread;
   int termination = kNmMaxIter;
   bool uncertain = false;
+  double g_r = 0.0;  // two-phase iterations: the reflection's value
+  uint64_t h_r = 0;
 };
 
 // Could a and b (each within the backend's error of the reference's value)
@@ -100,7 +104,7 @@ void commit(Run& r, const double x[N], double g, uint64_t h) {
 
 // the sort / convergence / next-probe block at the top of the reference loop
 // (optim.py:110-160); leaves the run with its next pending batch, or done
-void check(Run& r, const NmConfig& cfg) {
+void check(Run& r, const NmConfig& cfg, bool speculate) {
   {
     int order[V];
     for (int v = 0; v < V; ++v) order[v] = v;
@@ -179,6 +183,11 @@ void check(Run& r, const NmConfig& cfg) {
       r.cin_[j] = c[j] - kContr * (c[j] - w[j]);
     }
     std::memcpy(r.pend[0], r.refl, sizeof(r.refl));
+    if (!speculate) {
+      r.npend = 1;
+      r.phase = kIterR;
+      return;
+    }
     std::memcpy(r.pend[1], r.expd, sizeof(r.expd));
     std::memcpy(r.pend[2], r.cout_, sizeof(r.cout_));
     std::memcpy(r.pend[3], r.cin_, sizeof(r.cin_));
@@ -203,8 +212,14 @@ void replace_worst(Run& r, const double x[N], double g, uint64_t h) {
   r.hashes[V - 1] = h;
 }
 
+void pend_one(Run& r, const double x[N], Phase ph) {
+  std::memcpy(r.pend[0], x, sizeof(double) * N);
+  r.npend = 1;
+  r.phase = ph;
+}
+
 // the run's pending probes came back: apply the reference's rules (optim.py:135-175)
-void apply(Run& r, const NmConfig& cfg, const double* g, const uint64_t* h) {
+void apply(Run& r, const NmConfig& cfg, const double* g, const uint64_t* h, bool speculate) {
   r.n_batches += 1;
   r.n_spec += r.npend;
   switch (r.phase) {
@@ -253,10 +268,47 @@ void apply(Run& r, const NmConfig& cfg, const double* g, const uint64_t* h) {
       shrink(r);
       return;  // wait for the shrunk vertices
     }
+    case kIterR: {  // the same rules, one probe at a time (the reference's order)
+      r.g_r = g[0];
+      r.h_r = h[0];
+      commit(r, r.refl, r.g_r, r.h_r);
+      if (lt(r, r.g_r, r.h_r, r.values[0], r.hashes[0])) {
+        pend_one(r, r.expd, kIterE);
+        return;
+      }
+      if (lt(r, r.g_r, r.h_r, r.values[V - 2], r.hashes[V - 2])) {
+        replace_worst(r, r.refl, r.g_r, r.h_r);
+        break;
+      }
+      if (lt(r, r.g_r, r.h_r, r.values[V - 1], r.hashes[V - 1])) pend_one(r, r.cout_, kIterCO);
+      else pend_one(r, r.cin_, kIterCI);
+      return;
+    }
+    case kIterE:
+      commit(r, r.expd, g[0], h[0]);
+      if (lt(r, g[0], h[0], r.g_r, r.h_r)) replace_worst(r, r.expd, g[0], h[0]);
+      else replace_worst(r, r.refl, r.g_r, r.h_r);
+      break;
+    case kIterCO:
+      commit(r, r.cout_, g[0], h[0]);
+      if (le(r, g[0], h[0], r.g_r, r.h_r)) {
+        replace_worst(r, r.cout_, g[0], h[0]);
+        break;
+      }
+      shrink(r);
+      return;
+    case kIterCI:
+      commit(r, r.cin_, g[0], h[0]);
+      if (lt(r, g[0], h[0], r.values[V - 1], r.hashes[V - 1])) {
+        replace_worst(r, r.cin_, g[0], h[0]);
+        break;
+      }
+      shrink(r);
+      return;
     default:
       return;
   }
-  check(r, cfg);
+  check(r, cfg, speculate);
 }
 
 }  // namespace
@@ -295,6 +347,9 @@ int nm_lockstep(int64_t K, const double* x0, const NmConfig& cfg, const NmEvalua
     }
     const int64_t P = (int64_t)pair.size();
     if (P == 0) break;
+    int64_t active = 0;
+    for (int64_t k = 0; k < K; ++k) active += runs[(size_t)k].phase != kDone;
+    const bool speculate = 4 * active <= cfg.spec_budget;
     g.assign((size_t)P, 0.0);
     h.assign((size_t)P, 0);
     const int rc = eval(poses.data(), pair.data(), P, g.data(), h.data());
@@ -304,7 +359,7 @@ int nm_lockstep(int64_t K, const double* x0, const NmConfig& cfg, const NmEvalua
       Run& r = runs[(size_t)k];
       if (r.phase == kDone) continue;
       const size_t f = (size_t)first[(size_t)k];
-      apply(r, cfg, g.data() + f, h.data() + f);
+      apply(r, cfg, g.data() + f, h.data() + f, speculate);
     }
   }
   for (int64_t k = 0; k < K; ++k) {
@@ -329,7 +384,8 @@ int nm_lockstep(int64_t K, const double* x0, const NmConfig& cfg, const NmEvalua
 
 // ---- C ABI: the driver with a caller-supplied objective (tests, other backends)
 extern "C" int vmi_nm_run(int64_t K, const double* x0, const double steps[6], int max_iterations,
-                          double f_tol, double x_tol, int restarts, vmi_nm_eval_fn fn, void* user,
+                          double f_tol, double x_tol, int restarts, int64_t spec_budget,
+                          vmi_nm_eval_fn fn, void* user,
                           double* best_x, double* best_value, int32_t* iterations,
                           int32_t* termination, int32_t* n_evaluations, int32_t* uncertain,
                           double* trace, int32_t* trace_len, int64_t trace_cap) {
@@ -343,6 +399,7 @@ extern "C" int vmi_nm_run(int64_t K, const double* x0, const double steps[6], in
   cfg.f_tol = f_tol;
   cfg.x_tol = x_tol;
   cfg.restarts = restarts;
+  cfg.spec_budget = spec_budget < 0 ? INT64_MAX : spec_budget;
   std::vector<vmi::NmResult> res((size_t)K);
   vmi::NmEvaluator ev = [&](const double* p, const int32_t* pr, int64_t n, double* g, uint64_t* h) {
     return fn(user, p, pr, n, g, h);

@@ -1,6 +1,7 @@
 // nm_lockstep.h -- lockstep Nelder-Mead over many scan pairs (nm_lockstep.cpp).
 #pragma once
 #include <cstdint>
+#include <climits>
 #include <functional>
 #include <vector>
 
@@ -18,6 +19,11 @@ struct NmConfig {  // SimplexConfig (optim.py:26-46)
   int max_iterations;
   double f_tol, x_tol;
   int restarts;
+  // Probes per step up to which an iteration evaluates all four candidates
+  // (reflection, expansion, both contractions) at once; above it, the
+  // reflection first and then only the one follow-up the reference needs (two
+  // steps, ~2.5x fewer probes: the evaluator is throughput-bound there).
+  int64_t spec_budget = INT64_MAX;
 };
 
 struct NmResult {

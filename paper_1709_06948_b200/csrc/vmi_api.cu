@@ -9,8 +9,10 @@
 #include <algorithm>
 #include <cstdlib>
 #include <cstring>
+#include <chrono>
 #include <string>
 #include <thread>
+#include <unordered_map>
 #include <vector>
 
 #include <cuda_runtime.h>
@@ -52,6 +54,18 @@ struct PairStore {
   int64_t b_voxels = 0;  // scan B's occupied voxels at the identity pose (table sizing)
 };
 
+// A CUDA stream with its own scratch: pair-set builds run kBuildLanes pairs at
+// a time (small per-pair kernels and uploads overlap across lanes).
+struct BuildLane {
+  cudaStream_t st = nullptr;
+  cudaEvent_t done = nullptr;
+  ExactScratch ex;
+  int4* d_avox_tmp = nullptr;
+  size_t cap_avox_tmp = 0;
+  int* d_cursor = nullptr;
+};
+constexpr int kBuildLanes = 4;
+
 struct vmi_ctx {
   int device = 0;
   int sm_count = 0;
@@ -69,6 +83,13 @@ struct vmi_ctx {
   int64_t n_set = 0;            // pairs of `set` in use
   PairDesc* d_pairs = nullptr;  // device copies of the set's views
   size_t cap_pairs = 0;
+  BuildLane lanes[kBuildLanes];
+  void* d_raw = nullptr;  // vmi_set_pairs: the distinct scans as uploaded
+  size_t cap_raw = 0;
+  std::vector<cudaEvent_t> chunk_ev;  // vmi_set_pairs: raw-upload chunk done
+  cudaEvent_t set_start = nullptr;
+  int* d_setv = nullptr;  // per-pair voxel counts + "left the box" flags (vmi_set_pairs)
+  size_t cap_setv = 0;
   int32_t* d_pose_pair = nullptr;  // vmi_eval_pairs: per-pose pair index
   unsigned long long* d_hash = nullptr;  // per-pose histogram identities
   int64_t cap_pp = 0;
@@ -334,13 +355,15 @@ int check_ready(vmi_ctx* c) {
 }
 
 int exact_pose(vmi_ctx* c, const PairStore& ps, const double* mat_dev, int64_t p, double* mi,
-               int32_t* st, long long* hist, long long* total) {
+               int32_t* st, long long* hist, long long* total,
+               unsigned long long* hash = nullptr) {
   PointSource src{};
   src.xyz = nullptr;
   src.B = query_view(c, ps);
   src.n = ps.nb;
   CK(c, exact_voxelize(c->ex, src, mat_dev, c->g, c->stream, &c->launches));
-  CK(c, exact_score(c->ex, c->g, ref_view(ps), p, mi, st, hist, total, c->stream, &c->launches));
+  CK(c, exact_score(c->ex, c->g, ref_view(ps), p, mi, st, hist, total, c->stream, &c->launches,
+                    hash));
   return 0;
 }
 
@@ -371,19 +394,27 @@ int launch_fast_eval(vmi_ctx* c, const double* mats_dev, int64_t P, double* mi, 
 
 // Re-run, through the exact path, every pose whose fast-path status carries
 // VMI_FLAG_RECHECK; pose_pair (host, nullable) names each pose's pair in the set.
+// hs_in: the statuses already on the host (nullable: read them here); hash:
+// the per-pose histogram identities to keep in step (nullable).
 int do_fixups(vmi_ctx* c, const double* mats_dev, int64_t P, double* mi, int32_t* st,
               long long* hist, long long* total, cudaStream_t stream, int64_t* n_fixed,
-              const int32_t* pose_pair = nullptr) {
-  std::vector<int32_t> hs(P);
-  CK(c, cudaMemcpyAsync(hs.data(), st, P * 4, cudaMemcpyDeviceToHost, stream));
-  CK(c, cudaStreamSynchronize(stream));
+              const int32_t* pose_pair = nullptr, const int32_t* hs_in = nullptr,
+              unsigned long long* hash = nullptr) {
+  std::vector<int32_t> own;
+  const int32_t* hs = hs_in;
+  if (!hs) {
+    own.resize((size_t)P);
+    CK(c, cudaMemcpyAsync(own.data(), st, P * 4, cudaMemcpyDeviceToHost, stream));
+    CK(c, cudaStreamSynchronize(stream));
+    hs = own.data();
+  }
   int64_t nf = 0;
   cudaStream_t saved = c->stream;
   c->stream = stream;
   for (int64_t p = 0; p < P; ++p) {
     if (hs[p] & VMI_FLAG_RECHECK) {
       const PairStore& ps = pose_pair ? c->set[(size_t)pose_pair[p]] : c->cur;
-      int rc = exact_pose(c, ps, mats_dev + 12 * p, p, mi, st, hist, total);
+      int rc = exact_pose(c, ps, mats_dev + 12 * p, p, mi, st, hist, total, hash);
       if (rc) { c->stream = saved; return rc; }
       ++nf;
     }
@@ -435,7 +466,17 @@ int vmi_destroy(vmi_ctx* c) {
   release_pair(c->cur);
   for (auto& ps : c->set) release_pair(ps);
   release_scratch(c);
-  cudaFree(c->d_pairs); cudaFree(c->d_pose_pair); cudaFree(c->d_hash);
+  cudaFree(c->d_pairs); cudaFree(c->d_pose_pair); cudaFree(c->d_hash); cudaFree(c->d_setv);
+  for (auto& l : c->lanes) {
+    if (l.st) cudaStreamSynchronize(l.st);
+    exact_free(l.ex);
+    cudaFree(l.d_avox_tmp); cudaFree(l.d_cursor);
+    if (l.done) cudaEventDestroy(l.done);
+    if (l.st) cudaStreamDestroy(l.st);
+  }
+  if (c->set_start) cudaEventDestroy(c->set_start);
+  for (auto e : c->chunk_ev) cudaEventDestroy(e);
+  cudaFree(c->d_raw);
   exact_free(c->ex);
   cudaFree(c->d_mats); cudaFree(c->d_mi); cudaFree(c->d_status); cudaFree(c->d_hist);
   cudaFree(c->d_total); cudaFree(c->d_best); cudaFree(c->d_best_idx); cudaFree(c->d_sums);
@@ -935,33 +976,37 @@ struct HostScan {
   bool finite = true, exact32 = true;
 };
 void scan_pass(const void* p, int is_rec, int64_t n, HostScan& o) {
-  for (int j = 0; j < 3; ++j) { o.lo[j] = INFINITY; o.hi[j] = -INFINITY; }
+  // branch-free min / max / finiteness (vectorisable; a NaN or inf anywhere
+  // sets `bad` -- |v| <= FLT_MAX / DBL_MAX is false for both)
   if (is_rec) {
     const float* r = static_cast<const float*>(p);
-    float lo[3] = {INFINITY, INFINITY, INFINITY}, hi[3] = {-INFINITY, -INFINITY, -INFINITY};
-    bool fin = true;
+    float lo[4] = {INFINITY, INFINITY, INFINITY, INFINITY};
+    float hi[4] = {-INFINITY, -INFINITY, -INFINITY, -INFINITY};
+    int bad[4] = {0, 0, 0, 0};
     for (int64_t i = 0; i < n; ++i)
-      for (int j = 0; j < 3; ++j) {
+      for (int j = 0; j < 4; ++j) {  // all four fields: the intensity's are ignored below
         const float v = r[4 * i + j];
-        fin &= std::isfinite(v);
-        lo[j] = std::fmin(lo[j], v);
-        hi[j] = std::fmax(hi[j], v);
+        lo[j] = v < lo[j] ? v : lo[j];
+        hi[j] = v > hi[j] ? v : hi[j];
+        bad[j] |= !(std::fabs(v) <= 3.4028234663852886e+38f);
       }
-    o.finite = fin;
+    o.finite = !(bad[0] | bad[1] | bad[2]);
     for (int j = 0; j < 3; ++j) { o.lo[j] = lo[j]; o.hi[j] = hi[j]; }
   } else {
     const double* d = static_cast<const double*>(p);
-    bool fin = true, ex = true;
+    double lo[3] = {INFINITY, INFINITY, INFINITY}, hi[3] = {-INFINITY, -INFINITY, -INFINITY};
+    int bad = 0, inexact = 0;
     for (int64_t i = 0; i < n; ++i)
       for (int j = 0; j < 3; ++j) {
         const double v = d[3 * i + j];
-        fin &= std::isfinite(v);
-        ex &= (double)(float)v == v;
-        o.lo[j] = std::fmin(o.lo[j], v);
-        o.hi[j] = std::fmax(o.hi[j], v);
+        lo[j] = v < lo[j] ? v : lo[j];
+        hi[j] = v > hi[j] ? v : hi[j];
+        bad |= !(std::fabs(v) <= 1.7976931348623157e+308);
+        inexact |= (double)(float)v != v;
       }
-    o.finite = fin;
-    o.exact32 = ex;
+    o.finite = !bad;
+    o.exact32 = !inexact;
+    for (int j = 0; j < 3; ++j) { o.lo[j] = lo[j]; o.hi[j] = hi[j]; }
   }
 }
 
@@ -972,10 +1017,13 @@ int64_t host_floor(double p, double o, double res) { return (int64_t)std::floor(
 
 }  // namespace
 
-// Pairs are built back to back on the context stream with no host round trip
-// in between: scan A's voxel bounds come from its AABB on the host (exact, see
-// host_floor), its voxel list is sized by the point count, and the voxel
-// counts are read back once for the whole set.
+// Pairs are built without a host round trip per pair.  Distinct scans (a drive
+// shares one scan between consecutive pairs) are validated once on the host
+// (threaded) and uploaded once into a raw device pool, in chunks on a copy
+// stream; kBuildLanes streams then build pairs side by side: scan A's voxel
+// bounds come from its AABB on the host (exact, see host_floor), its voxel
+// list is sized by the point count, and the voxel counts of the whole set are
+// read back once at the end.
 int vmi_set_pairs(vmi_ctx* c, int64_t npairs, const void* const* a, const int64_t* na,
                   const void* const* b, const int64_t* nb, int is_rec) {
   if (!c || npairs < 0 || (npairs > 0 && (!a || !na || !b || !nb))) return VMI_ERR_ARG;
@@ -989,106 +1037,196 @@ int vmi_set_pairs(vmi_ctx* c, int64_t npairs, const void* const* a, const int64_
   }
   cudaSetDevice(c->device);
   c->n_set = 0;
-  // host passes, threaded over scans
-  std::vector<HostScan> ha((size_t)npairs), hb((size_t)npairs);
+  static const bool trace = std::getenv("VMI_TRACE") != nullptr;  // phase timings to stderr
+  auto now = [] { return std::chrono::steady_clock::now(); };
+  auto ms = [](auto x, auto y) { return std::chrono::duration<double, std::milli>(y - x).count(); };
+  const auto t_begin = now();
+  const size_t rb = is_rec ? 16 : 24;  // host bytes per point
+  // ---- distinct scans (by buffer), their pool offsets
+  std::unordered_map<const void*, int64_t> id;
+  std::vector<const void*> scan;
+  std::vector<int64_t> scan_n;
+  std::vector<int64_t> ia((size_t)npairs), ib((size_t)npairs);
+  auto intern = [&](const void* p, int64_t n) -> int64_t {
+    auto it = id.find(p);
+    if (it != id.end()) return scan_n[(size_t)it->second] == n ? it->second : -1;
+    id.emplace(p, (int64_t)scan.size());
+    scan.push_back(p);
+    scan_n.push_back(n);
+    return (int64_t)scan.size() - 1;
+  };
+  for (int64_t i = 0; i < npairs; ++i) {
+    ia[(size_t)i] = intern(a[i], na[i]);
+    ib[(size_t)i] = intern(b[i], nb[i]);
+    if (ia[(size_t)i] < 0 || ib[(size_t)i] < 0)
+      return fail(c, VMI_ERR_ARG, "one buffer passed with two point counts");
+  }
+  const int64_t ns = (int64_t)scan.size();
+  std::vector<size_t> off((size_t)ns + 1, 0);
+  for (int64_t k = 0; k < ns; ++k) off[(size_t)k + 1] = off[(size_t)k] + (size_t)scan_n[(size_t)k] * rb;
+  // ---- host passes, threaded over distinct scans
+  std::vector<HostScan> hs((size_t)ns);
   {
-    const int64_t jobs = 2 * npairs;
     int nt = (int)std::min<int64_t>(std::max(1u, std::thread::hardware_concurrency()), 16);
-    nt = (int)std::min<int64_t>(nt, std::max<int64_t>(1, jobs));
+    nt = (int)std::min<int64_t>(nt, std::max<int64_t>(1, ns));
     std::vector<std::thread> pool;
     for (int t = 0; t < nt; ++t)
       pool.emplace_back([&, t] {
-        for (int64_t j = t; j < jobs; j += nt) {
-          const int64_t i = j >> 1;
-          if (j & 1) scan_pass(b[i], is_rec, nb[i], hb[(size_t)i]);
-          else scan_pass(a[i], is_rec, na[i], ha[(size_t)i]);
-        }
+        for (int64_t k = t; k < ns; k += nt) scan_pass(scan[(size_t)k], is_rec, scan_n[(size_t)k], hs[(size_t)k]);
       });
     for (auto& th : pool) th.join();
   }
-  int64_t max_na = 1, max_n = 1;
-  for (int64_t i = 0; i < npairs; ++i) {
-    if (!ha[(size_t)i].finite || !hb[(size_t)i].finite)
-      return fail(c, VMI_ERR_ARG, "points contain non-finite coordinates");
-    max_na = std::max(max_na, na[i]);
-    max_n = std::max(max_n, std::max(na[i], nb[i]));
-  }
+  int64_t max_na = 1;
+  for (int64_t k = 0; k < ns; ++k)
+    if (!hs[(size_t)k].finite) return fail(c, VMI_ERR_ARG, "points contain non-finite coordinates");
+  for (int64_t i = 0; i < npairs; ++i) max_na = std::max(max_na, na[i]);
+  const auto t_host = now();
   if ((int64_t)c->set.size() < npairs) c->set.resize((size_t)npairs);
-  CK(c, exact_alloc(c->ex, max_na));
-  CK(c, grow(&c->d_avox_tmp, c->cap_avox_tmp, sizeof(int4) * (size_t)max_na));
-  if (!c->d_cursor) CK(c, cudaMalloc(&c->d_cursor, 4 * kMaxW));
-  CK(c, grow(&c->d_upload, c->cap_upload, (size_t)max_n * (is_rec ? 16 : 24)));
-  int* d_v = nullptr;  // per-pair voxel counts
-  CK(c, cudaMalloc(&d_v, 4 * (size_t)(npairs > 0 ? npairs : 1)));
-  auto cleanup = [&] { cudaFree(d_v); };
-  static const bool force_f64 = std::getenv("VMI_FORCE_F64") != nullptr;
-  for (int64_t i = 0; i < npairs; ++i) {
-    PairStore& ps = c->set[(size_t)i];
-    free_a(ps);
-    ps.b_set = false;
-    // ---- scan A: bounds on the host, voxelize + features + grid on the GPU
-    int64_t bnd[6];
-    for (int j = 0; j < 3; ++j) {
-      bnd[j] = host_floor(ha[(size_t)i].lo[j], c->g.origin[j], c->g.res);
-      bnd[3 + j] = host_floor(ha[(size_t)i].hi[j], c->g.origin[j], c->g.res);
-      if (bnd[j] < -(1 << 20) || bnd[3 + j] > (1 << 20) - 1) {
-        cleanup();
-        return fail(c, VMI_ERR_RANGE, "a point of scan A maps outside the voxel key range");
-      }
-      ps.amin[j] = (int)bnd[j];
-      ps.amax[j] = (int)bnd[3 + j];
-      ps.ext[j] = (uint32_t)(bnd[3 + j] - bnd[j] + 1);
-    }
-    ps.a_empty = false;
-    const double vol = (double)ps.ext[0] * ps.ext[1] * ps.ext[2];
-    if (vol > 4294967294.0) {
-      cleanup();
-      return fail(c, VMI_ERR_UNSUPPORTED,
-                  "scan A's occupied AABB exceeds 2^32-2 voxels (dense reference grid limit)");
-    }
-    ps.grid_bytes = (size_t)vol;
-    CK(c, grow(&ps.d_grid, ps.cap_grid, ps.grid_bytes));
-    CK(c, grow(&ps.d_avox, ps.cap_avox, sizeof(int4) * (size_t)na[i]));
-    if (!ps.d_bin_total) CK(c, cudaMalloc(&ps.d_bin_total, 4 * kMaxW));
-    CK(c, cudaMemsetAsync(ps.d_grid, 0, ps.grid_bytes, c->stream));
-    CK(c, cudaMemsetAsync(ps.d_bin_total, 0, 4 * kMaxW, c->stream));
-    CK(c, cudaMemcpyAsync(c->d_upload, a[i], (size_t)na[i] * (is_rec ? 16 : 24),
-                          cudaMemcpyHostToDevice, c->stream));
-    PointSource src{};
-    if (is_rec) src.rec = static_cast<const float4*>(c->d_upload);
-    else src.xyz = static_cast<const double*>(c->d_upload);
-    src.n = na[i];
-    CK(c, exact_voxelize(c->ex, src, nullptr, c->g, c->stream, &c->launches));
-    CK(c, build_reference(c->ex.ukeys, c->ex.values, (int)na[i], c->ex.nruns, c->g, ps.amin,
-                          ps.ext, ps.d_grid, c->d_avox_tmp, ps.d_avox, ps.d_bin_total,
-                          c->d_cursor, c->stream, &c->launches));
-    CK(c, cudaMemcpyAsync(d_v + i, c->ex.nruns, 4, cudaMemcpyDeviceToDevice, c->stream));
-    ps.a_npts = na[i];
-    // ---- scan B: span layout
-    const HostScan& h = hb[(size_t)i];
-    const int as_f32 = (h.exact32 && !force_f64) ? 1 : 0;
-    double mx = 0.0;
-    for (int j = 0; j < 3; ++j) {
-      mx = std::fmax(mx, std::fmax(std::fabs(h.lo[j]), std::fabs(h.hi[j])));
-      ps.b_lo[j] = h.lo[j];
-      ps.b_hi[j] = h.hi[j];
-    }
-    ps.max_abs = mx;
-    ps.span = (int)((nb[i] + c->threads - 1) / c->threads);
-    ps.rem = (int)(nb[i] - (int64_t)(ps.span - 1) * c->threads);
-    CK(c, grow(&ps.d_pts, ps.cap_pts, (size_t)(ps.span + kStagePadRows) * c->threads * (as_f32 ? 16 : 32)));
-    CK(c, cudaMemcpyAsync(c->d_upload, b[i], (size_t)nb[i] * (is_rec ? 16 : 24),
-                          cudaMemcpyHostToDevice, c->stream));
-    CK(c, launch_span_layout(c->d_upload, is_rec, as_f32, nb[i], ps.span, ps.rem, c->threads,
-                             ps.d_pts, c->stream));
-    c->launches += 1;
-    ps.is_f32 = as_f32;
-    ps.nb = nb[i];
+  const size_t np1 = (size_t)(npairs > 0 ? npairs : 1);
+  CK(c, grow(&c->d_setv, c->cap_setv, 8 * np1));
+  int* d_v = c->d_setv;  // per-pair voxel counts, then "left the box" flags
+  int* d_bad = d_v + np1;
+  CK(c, grow(&c->d_raw, c->cap_raw, off[(size_t)ns] > 0 ? off[(size_t)ns] : 16));
+  char* raw = static_cast<char*>(c->d_raw);
+  // everything starts after the work already queued on the context stream (an
+  // earlier evaluation may still read the buffers being rebuilt)
+  if (!c->set_start) CK(c, cudaEventCreateWithFlags(&c->set_start, cudaEventDisableTiming));
+  CK(c, cudaEventRecord(c->set_start, c->stream));
+  if (!c->copy_stream) CK(c, cudaStreamCreateWithFlags(&c->copy_stream, cudaStreamNonBlocking));
+  CK(c, cudaStreamWaitEvent(c->copy_stream, c->set_start, 0));
+  // ---- raw uploads in chunks of kChunk scans, one event each
+  constexpr int64_t kChunk = 32;
+  const int64_t nchunk = (ns + kChunk - 1) / kChunk;
+  while ((int64_t)c->chunk_ev.size() < nchunk) {
+    cudaEvent_t e;
+    CK(c, cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+    c->chunk_ev.push_back(e);
   }
-  std::vector<int> V((size_t)(npairs > 0 ? npairs : 1));
-  CK(c, cudaMemcpyAsync(V.data(), d_v, 4 * (size_t)npairs, cudaMemcpyDeviceToHost, c->stream));
+  for (int64_t ch = 0; ch < nchunk; ++ch) {
+    for (int64_t k = ch * kChunk; k < std::min(ns, (ch + 1) * kChunk); ++k)
+      CK(c, cudaMemcpyAsync(raw + off[(size_t)k], scan[(size_t)k], off[(size_t)k + 1] - off[(size_t)k],
+                            cudaMemcpyHostToDevice, c->copy_stream));
+    CK(c, cudaEventRecord(c->chunk_ev[(size_t)ch], c->copy_stream));
+  }
+  for (auto& l : c->lanes) {
+    if (!l.st) {
+      CK(c, cudaStreamCreateWithFlags(&l.st, cudaStreamNonBlocking));
+      CK(c, cudaEventCreateWithFlags(&l.done, cudaEventDisableTiming));
+      CK(c, cudaMalloc(&l.d_cursor, 4 * kMaxW));
+    }
+    CK(c, exact_alloc(l.ex, max_na));
+    CK(c, grow(&l.d_avox_tmp, l.cap_avox_tmp, sizeof(int4) * (size_t)max_na));
+    CK(c, cudaStreamWaitEvent(l.st, c->set_start, 0));
+  }
+  // one host thread per lane enqueues its pairs (launch-bound otherwise)
+  static const bool force_f64 = std::getenv("VMI_FORCE_F64") != nullptr;
+  std::vector<int> lane_rc(kBuildLanes, 0);
+  std::vector<int64_t> lane_launches(kBuildLanes, 0);
+  std::vector<std::string> lane_err(kBuildLanes);
+  auto lane_work = [&](int li) -> int {
+    BuildLane& ln = c->lanes[li];
+    cudaStream_t st = ln.st;
+    cudaSetDevice(c->device);
+    int64_t waited = -1;  // the last raw-upload chunk this lane waited for
+    auto lfail = [&](int code, const std::string& m) { lane_err[(size_t)li] = m; return code; };
+#define LCK(x)                                                                       \
+  do {                                                                               \
+    cudaError_t e_ = (x);                                                            \
+    if (e_ != cudaSuccess) return lfail(VMI_ERR_CUDA, std::string(#x) + ": " + cudaGetErrorString(e_)); \
+  } while (0)
+    for (int64_t i = li; i < npairs; i += kBuildLanes) {
+      PairStore& ps = c->set[(size_t)i];
+      const int64_t need = std::max(ia[(size_t)i], ib[(size_t)i]) / kChunk;
+      if (need > waited) {  // chunks upload in order: the latest one suffices
+        LCK(cudaStreamWaitEvent(st, c->chunk_ev[(size_t)need], 0));
+        waited = need;
+      }
+      free_a(ps);
+      ps.b_set = false;
+      const HostScan& h_a = hs[(size_t)ia[(size_t)i]];
+      const HostScan& h_b = hs[(size_t)ib[(size_t)i]];
+      // ---- scan A: bounds on the host, voxelize + features + grid on the GPU
+      for (int j = 0; j < 3; ++j) {
+        const int64_t lo = host_floor(h_a.lo[j], c->g.origin[j], c->g.res);
+        const int64_t hi = host_floor(h_a.hi[j], c->g.origin[j], c->g.res);
+        if (lo < -(1 << 20) || hi > (1 << 20) - 1)
+          return lfail(VMI_ERR_RANGE, "a point of scan A maps outside the voxel key range");
+        ps.amin[j] = (int)lo;
+        ps.amax[j] = (int)hi;
+        ps.ext[j] = (uint32_t)(hi - lo + 1);
+      }
+      ps.a_empty = false;
+      const double vol = (double)ps.ext[0] * ps.ext[1] * ps.ext[2];
+      if (vol > 4294967294.0)
+        return lfail(VMI_ERR_UNSUPPORTED,
+                     "scan A's occupied AABB exceeds 2^32-2 voxels (dense reference grid limit)");
+      ps.grid_bytes = (size_t)vol;
+      LCK(grow(&ps.d_grid, ps.cap_grid, ps.grid_bytes));
+      LCK(grow(&ps.d_avox, ps.cap_avox, sizeof(int4) * (size_t)na[i]));
+      if (!ps.d_bin_total) LCK(cudaMalloc(&ps.d_bin_total, 4 * kMaxW));
+      LCK(cudaMemsetAsync(ps.d_grid, 0, ps.grid_bytes, st));
+      LCK(cudaMemsetAsync(ps.d_bin_total, 0, 4 * kMaxW, st));
+      PointSource src{};
+      const char* ra = raw + off[(size_t)ia[(size_t)i]];
+      if (is_rec) src.rec = reinterpret_cast<const float4*>(ra);
+      else src.xyz = reinterpret_cast<const double*>(ra);
+      src.n = na[i];
+      LCK(box_voxelize(ln.ex, src, c->g, ps.amin, ps.ext, st, &lane_launches[(size_t)li]));
+      LCK(build_reference_box(ln.ex, (int)na[i], c->g, ps.ext, ps.d_grid, ln.d_avox_tmp,
+                              ps.d_avox, ps.d_bin_total, ln.d_cursor, st,
+                              &lane_launches[(size_t)li]));
+      LCK(cudaMemcpyAsync(d_v + i, ln.ex.nruns, 4, cudaMemcpyDeviceToDevice, st));
+      LCK(cudaMemcpyAsync(d_bad + i, ln.ex.bounds + 6, 4, cudaMemcpyDeviceToDevice, st));
+      ps.a_npts = na[i];
+      // ---- scan B: span layout
+      const int as_f32 = (h_b.exact32 && !force_f64) ? 1 : 0;
+      double mx = 0.0;
+      for (int j = 0; j < 3; ++j) {
+        mx = std::fmax(mx, std::fmax(std::fabs(h_b.lo[j]), std::fabs(h_b.hi[j])));
+        ps.b_lo[j] = h_b.lo[j];
+        ps.b_hi[j] = h_b.hi[j];
+      }
+      ps.max_abs = mx;
+      ps.span = (int)((nb[i] + c->threads - 1) / c->threads);
+      ps.rem = (int)(nb[i] - (int64_t)(ps.span - 1) * c->threads);
+      LCK(grow(&ps.d_pts, ps.cap_pts,
+               (size_t)(ps.span + kStagePadRows) * c->threads * (as_f32 ? 16 : 32)));
+      LCK(launch_span_layout(raw + off[(size_t)ib[(size_t)i]], is_rec, as_f32, nb[i], ps.span,
+                             ps.rem, c->threads, ps.d_pts, st));
+      lane_launches[(size_t)li] += 1;
+      ps.is_f32 = as_f32;
+      ps.nb = nb[i];
+    }
+#undef LCK
+    return 0;
+  };
+  {
+    std::vector<std::thread> th;
+    for (int li = 0; li < kBuildLanes; ++li)
+      th.emplace_back([&, li] { lane_rc[(size_t)li] = lane_work(li); });
+    for (auto& t : th) t.join();
+  }
+  for (int li = 0; li < kBuildLanes; ++li) {
+    c->launches += lane_launches[(size_t)li];
+    if (lane_rc[(size_t)li]) {
+      cudaDeviceSynchronize();
+      return fail(c, lane_rc[(size_t)li], lane_err[(size_t)li]);
+    }
+  }
+  const auto t_enq = now();
+  for (auto& l : c->lanes) {  // the context stream continues after every lane
+    CK(c, cudaEventRecord(l.done, l.st));
+    CK(c, cudaStreamWaitEvent(c->stream, l.done, 0));
+  }
+  std::vector<int> V(2 * np1);
+  CK(c, cudaMemcpyAsync(V.data(), d_v, 8 * np1, cudaMemcpyDeviceToHost, c->stream));
   CK(c, cudaStreamSynchronize(c->stream));
-  cleanup();
+  if (trace)
+    std::fprintf(stderr, "vmi_set_pairs %lld pairs (%lld scans): host pass %.1f ms, enqueue %.1f ms, drain %.1f ms\n",
+                 (long long)npairs, (long long)ns, ms(t_begin, t_host), ms(t_host, t_enq), ms(t_enq, now()));
+  for (int64_t i = 0; i < npairs; ++i)
+    if (V[np1 + (size_t)i])  // the host box and the GPU's voxel coordinates disagree
+      return fail(c, VMI_ERR_CUDA, "internal: scan A left its host-computed voxel box");
   std::vector<PairDesc> desc((size_t)npairs);
   for (int64_t i = 0; i < npairs; ++i) {
     PairStore& ps = c->set[(size_t)i];
@@ -1100,7 +1238,7 @@ int vmi_set_pairs(vmi_ctx* c, int64_t npairs, const void* const* a, const int64_
     desc[(size_t)i].A = ref_view(ps);
     desc[(size_t)i].B = query_view(c, ps);
   }
-  CK(c, grow(&c->d_pairs, c->cap_pairs, sizeof(PairDesc) * (size_t)(npairs > 0 ? npairs : 1)));
+  CK(c, grow(&c->d_pairs, c->cap_pairs, sizeof(PairDesc) * np1));
   if (npairs > 0)
     CK(c, cudaMemcpyAsync(c->d_pairs, desc.data(), sizeof(PairDesc) * (size_t)npairs,
                           cudaMemcpyHostToDevice, c->stream));
@@ -1154,8 +1292,14 @@ int eval_pairs_device(vmi_ctx* c, int64_t P, const int32_t* pair_host, long long
     return fail(c, VMI_ERR_UNSUPPORTED,
                 "pair set needs the multi-pass table or mixes record formats (use one pair at a time)");
   }
-  return do_fixups(c, c->d_mats, P, c->d_mi, c->d_status, hist, c->d_total, c->stream, nullptr,
-                   pair_host);
+  return 0;
+}
+
+// after eval_pairs_device: re-run flagged poses exactly (identities kept in step)
+int fix_pairs(vmi_ctx* c, int64_t P, const int32_t* pair_host, long long* hist,
+              const int32_t* status_host, int64_t* n_fixed) {
+  return do_fixups(c, c->d_mats, P, c->d_mi, c->d_status, hist, c->d_total, c->stream, n_fixed,
+                   pair_host, status_host, c->d_hash);
 }
 
 int ensure_pp(vmi_ctx* c, int64_t P) {
@@ -1207,6 +1351,7 @@ int vmi_eval_pairs(vmi_ctx* c, const double* poses, const int32_t* pair, int64_t
   if (rc) return rc;
   long long* dh = hist_out ? c->d_hist : nullptr;
   if ((rc = eval_pairs_device(c, P, pair, dh))) return rc;
+  if ((rc = fix_pairs(c, P, pair, dh, nullptr, nullptr))) return rc;
   CK(c, cudaMemcpyAsync(mi_out, c->d_mi, P * 8, cudaMemcpyDeviceToHost, c->stream));
   CK(c, cudaMemcpyAsync(status_out, c->d_status, P * 4, cudaMemcpyDeviceToHost, c->stream));
   if (hash_out) CK(c, cudaMemcpyAsync(hash_out, c->d_hash, P * 8, cudaMemcpyDeviceToHost, c->stream));
@@ -1237,6 +1382,8 @@ int vmi_align_pairs(vmi_ctx* c, int64_t K, const double* x0, const double steps[
   cfg.f_tol = f_tol;
   cfg.x_tol = x_tol;
   cfg.restarts = restarts;
+  // below ~two poses per SM a launch costs the same for 1 or 4 probes per run
+  cfg.spec_budget = 2 * (int64_t)c->sm_count;
   cudaSetDevice(c->device);
   std::vector<double> mi;
   std::vector<int32_t> st;
@@ -1245,9 +1392,21 @@ int vmi_align_pairs(vmi_ctx* c, int64_t K, const double* x0, const double steps[
     if (rc) return rc;
     if ((rc = eval_pairs_device(c, n, run, nullptr))) return rc;
     mi.resize((size_t)n);
+    st.resize((size_t)n);
+    // one round trip: values, statuses and identities together; the rare
+    // flagged pose is re-run exactly and read again
     CK(c, cudaMemcpyAsync(mi.data(), c->d_mi, n * 8, cudaMemcpyDeviceToHost, c->stream));
+    CK(c, cudaMemcpyAsync(st.data(), c->d_status, n * 4, cudaMemcpyDeviceToHost, c->stream));
     CK(c, cudaMemcpyAsync(h, c->d_hash, n * 8, cudaMemcpyDeviceToHost, c->stream));
     CK(c, cudaStreamSynchronize(c->stream));
+    int64_t nf = 0;
+    for (int64_t i = 0; i < n; ++i) nf += (st[(size_t)i] & VMI_FLAG_RECHECK) != 0;
+    if (nf) {
+      if ((rc = fix_pairs(c, n, run, nullptr, st.data(), nullptr))) return rc;
+      CK(c, cudaMemcpyAsync(mi.data(), c->d_mi, n * 8, cudaMemcpyDeviceToHost, c->stream));
+      CK(c, cudaMemcpyAsync(h, c->d_hash, n * 8, cudaMemcpyDeviceToHost, c->stream));
+      CK(c, cudaStreamSynchronize(c->stream));
+    }
     for (int64_t i = 0; i < n; ++i) g[i] = -mi[(size_t)i];  // sentinel -> +1e300
     return 0;
   };

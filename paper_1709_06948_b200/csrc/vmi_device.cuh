@@ -164,6 +164,33 @@ __device__ __forceinline__ double warp_sum(double v) {
   return v;
 }
 
+// ---- 64-bit identity of a joint histogram: sum of cell * mix(cell index)
+// mod 2^64 (order-free, so any reduction order gives the same value; the
+// splitmix64 mixer).  Equal identities <=> equal histograms up to 2^-64.
+__device__ __forceinline__ unsigned long long cell_mix(unsigned long long i) {
+  i += 0x9E3779B97F4A7C15ull;
+  i = (i ^ (i >> 30)) * 0xBF58476D1CE4E5B9ull;
+  i = (i ^ (i >> 27)) * 0x94D049BB133111EBull;
+  return i ^ (i >> 31);
+}
+// block-wide: hist (W x W, cell (0,0) = h00) -> identity; red >= THREADS/32
+// entries of shared memory; result valid in thread 0; all threads must call
+template <int THREADS>
+__device__ unsigned long long block_hist_hash(const uint32_t* hist, long long h00, int W,
+                                              unsigned long long* red) {
+  unsigned long long h = 0;
+  for (int i = threadIdx.x; i < W * W; i += THREADS)
+    h += (unsigned long long)(i == 0 ? h00 : (long long)hist[i]) * cell_mix((unsigned long long)i);
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) h += __shfl_xor_sync(0xffffffffu, h, o);
+  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = h;
+  __syncthreads();
+  unsigned long long t = 0;
+  if (threadIdx.x == 0)
+    for (int w = 0; w < THREADS / 32; ++w) t += red[w];
+  return t;
+}
+
 // ---- Histogram finalisation + MI (mi.py:124-160 analytic cells, :163-191).
 // hist: (W x W) u32 in shared memory holding the enumerated cells (every B
 // voxel inside the region, binned against A's grid); marg: per-A-bin count of

@@ -79,6 +79,19 @@ struct PointSource {
 cudaError_t exact_voxelize(ExactScratch& s, const PointSource& src, const double* mat,
                            const GridParams& g, cudaStream_t st, int64_t* launches);
 
+// Scan A of a pair set whose voxel box [amin, amin + ext) is known exactly
+// (host AABB): voxelize + compute_feature_map with 32-bit box indices as keys
+// (same order, fewer radix passes).  Leaves box indices in s.ukeys (as u32),
+// features in s.values, *s.nruns = V, s.bounds[6] = 1 if a point left the box.
+cudaError_t box_voxelize(ExactScratch& s, const PointSource& src, const GridParams& g,
+                         const int amin[3], const uint32_t ext[3], cudaStream_t st,
+                         int64_t* launches);
+// A's grid + voxel list from box_voxelize's output (V = *s.nruns <= Vmax)
+cudaError_t build_reference_box(const ExactScratch& s, int Vmax, const GridParams& g,
+                                const uint32_t ext[3], uint8_t* grid, int4* tmp, int4* avox,
+                                uint32_t* bin_total, int* cursor, cudaStream_t st,
+                                int64_t* launches);
+
 // Build A's dense bin grid and sorted voxel list from V feature-map entries
 // (keys + values on device; with Vdev the count is *Vdev and V only an upper
 // bound).  grid must be zeroed, ext-sized; tmp and avox hold V entries each.
@@ -91,7 +104,7 @@ cudaError_t build_reference(const unsigned long long* keys, const double* values
 // s (after exact_voxelize).  Writes mi[p], status[p], hist[p], total[p].
 cudaError_t exact_score(ExactScratch& s, const GridParams& g, const RefView& A, int64_t p,
                         double* mi, int32_t* status, long long* hist, long long* total,
-                        cudaStream_t st, int64_t* launches);
+                        cudaStream_t st, int64_t* launches, unsigned long long* hash = nullptr);
 
 // First-max argmax (np.argmax) over P doubles -> out[0] = value, out_idx[0] = index.
 cudaError_t launch_argmax(const double* v, int64_t P, double* out_val, long long* out_idx,

@@ -32,11 +32,14 @@ def _case(g, tag):
     return g[f"{tag}_x0"], g[f"{tag}_steps"], int(cfg[0]), float(cfg[1]), float(cfg[2]), int(cfg[3])
 
 
+@pytest.mark.parametrize("spec", [-1, 0])
 @pytest.mark.parametrize("tag", ["default", "restarts", "maxiter"])
-def test_lockstep_matches_reference_optimizer(tag):
+def test_lockstep_matches_reference_optimizer(tag, spec):
+    """spec -1: every iteration scores its four candidates at once; 0: the
+    reflection first, then only the follow-up the reference needs."""
     g = golden("nm_golden.npz")
     x0, steps, it, ft, xt, rs = _case(g, tag)
-    o = _lib.nm_run(x0[None, :], steps, it, ft, xt, rs, _f_batch)
+    o = _lib.nm_run(x0[None, :], steps, it, ft, xt, rs, _f_batch, spec_budget=spec)
     np.testing.assert_array_equal(o["best_x"][0], g[f"{tag}_best_x"])
     assert o["best_value"][0] == float(g[f"{tag}_best_value"])
     assert o["iterations"][0] == int(g[f"{tag}_iterations"])
@@ -46,15 +49,17 @@ def test_lockstep_matches_reference_optimizer(tag):
     np.testing.assert_array_equal(o["trace"][0, :n], g[f"{tag}_trace"])
 
 
-def test_many_runs_in_lockstep_equal_single_runs():
+@pytest.mark.parametrize("spec", [-1, 0, 12])
+def test_many_runs_in_lockstep_equal_single_runs(spec):
     """K runs from different starts advance together (different iteration
-    counts, restarts): each equals the one-run optimizer (optim.py) exactly."""
+    counts, restarts; spec 12 switches between one-probe and four-probe
+    iterations as runs finish): each equals the one-run optimizer exactly."""
     rng = np.random.default_rng(4)
     x0 = rng.normal(size=(9, 6)) * np.array([2, 2, 0.5, 0.1, 0.1, 0.3])
     cfg = SimplexConfig(initial_steps=(1.0, 1.0, 0.5, 0.05, 0.05, 0.2), max_iterations=120,
                         restarts=1, f_tol=1e-9, x_tol=1e-6)
     o = _lib.nm_run(x0, cfg.initial_steps, cfg.max_iterations, cfg.f_tol, cfg.x_tol, cfg.restarts,
-                    _f_batch)
+                    _f_batch, spec_budget=spec)
     for k in range(x0.shape[0]):
         r = nelder_mead_maximize_batched(lambda P: np.array([nm_test_function(p) for p in P]),
                                          x0[k], cfg)

@@ -1,3 +1,4 @@
 mkdir -p gpurun_out
-timeout 1200 python bench.py --config c5 --steps 3 --warmup 1 > gpurun_out/r2i_c5.json 2> gpurun_out/r2i_c5.err
-timeout 600 nsys --version > /dev/null 2>&1 || echo "no nsys"
+timeout 900 python -m pytest tests/test_gpu_parity.py -x -q -k "multi_pair or align_batch" > gpurun_out/r2o_pytest.log 2>&1; echo "pytest rc=$?" >> gpurun_out/r2o_pytest.log
+timeout 900 python -m pytest tests/test_gpu_headline_parity.py -x -q -k "c5" >> gpurun_out/r2o_pytest.log 2>&1; echo "pytest rc=$?" >> gpurun_out/r2o_pytest.log
+VMI_TRACE=1 timeout 1200 python bench.py --config c5 --steps 3 --warmup 1 > gpurun_out/r2o_c5.json 2> gpurun_out/r2o_c5.err
