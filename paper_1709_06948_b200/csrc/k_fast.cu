@@ -222,6 +222,15 @@ __device__ __forceinline__ uint4 ld_shared_v4(uint32_t a) {
                : "memory");
   return v;
 }
+__device__ __forceinline__ uint32_t atom_cas_shared(uint32_t a, uint32_t cmp, uint32_t v) {
+  uint32_t old;
+  asm volatile("atom.shared.cas.b32 %0, [%1], %2, %3;" : "=r"(old) : "r"(a), "r"(cmp), "r"(v)
+               : "memory");
+  return old;
+}
+__device__ __forceinline__ void red_add_shared(uint32_t a, uint32_t v) {
+  asm volatile("red.shared.add.u32 [%0], %1;" ::"r"(a), "r"(v) : "memory");
+}
 __device__ __forceinline__ uint32_t ld_shared_u32(uint32_t a) {
   uint32_t v;
   asm volatile("ld.shared.u32 %0, [%1];" : "=r"(v) : "r"(a) : "memory");
@@ -365,6 +374,9 @@ __global__ void __launch_bounds__(THREADS, 1)
     if (KIND == kKindCount) ccnt = reinterpret_cast<uint32_t*>(smem + L.table + (size_t)cap * 4);
   }
 
+  // shared-window addresses of the table's keys / counts (pinned: see my_stage)
+  const uint32_t key_sa = pin_u32((uint32_t)__cvta_generic_to_shared(smem + L.table));
+  const uint32_t cnt_sa = pin_u32(key_sa + (uint32_t)cap * 4u);  // counts follow the keys
   // The table is cleared once here; afterwards the per-pose table walk resets
   // every slot it reads, so each pose starts from an empty table.
   auto clear_table = [&]() {
@@ -483,19 +495,21 @@ __global__ void __launch_bounds__(THREADS, 1)
         } else if (has) {
           r0 = ld_shared_v2(a);
         }
-        uint32_t* keys = KIND == 0 ? reinterpret_cast<uint32_t*>(VT.key) : ckey;
         uint32_t sl = slot_of(r0.x, ucap);
-        // first probe = one CAS (hit or insert), no branch before the atomics
-        const uint32_t old0 = has ? atomicCAS(&keys[sl], kEmpty32, r0.x) : 0u;
+        // first probe = one CAS (hit or insert), no branch before the atomics;
+        // shared-window addresses (key_sa / cnt_sa) avoid generic -> shared
+        // conversions in this loop
+        const uint32_t old0 = has ? atom_cas_shared(key_sa + 4u * sl, kEmpty32, r0.x) : 0u;
         const bool done = has && (old0 == kEmpty32 || old0 == r0.x);
         auto add = [&](uint32_t slot) {
           if (KIND == 0) {
             const uint4 r1 = ld_shared_v4(a + 16);
-            atomicAdd(&VT.cnt[slot], r0.y);
+            if (kGlobalCounts<MULTI>()) atomicAdd(&VT.cnt[slot], r0.y);
+            else red_add_shared(cnt_sa + 4u * slot, r0.y);
             atomicAdd(&VT.sums[slot].x, mkd(r1.x, r1.y));
             atomicAdd(&VT.sums[slot].y, mkd(r1.z, r1.w));
           } else if (KIND == kKindCount) {
-            atomicAdd(&ccnt[slot], r0.y);
+            red_add_shared(cnt_sa + 4u * slot, r0.y);
           }  // occupancy: the key is all there is
         };
         if (done) {
@@ -505,10 +519,10 @@ __global__ void __launch_bounds__(THREADS, 1)
           while (true) {
             if (++sl == ucap) sl = 0;
             if (probes++ >= ucap) { misc[7] = 1; break; }  // table full -> exact path
-            const uint32_t w = ((volatile uint32_t*)keys)[sl];
+            const uint32_t w = ld_shared_u32(key_sa + 4u * sl);
             if (w == r0.x) { add(sl); break; }
             if (w == kEmpty32) {
-              const uint32_t old = atomicCAS(&keys[sl], kEmpty32, r0.x);
+              const uint32_t old = atom_cas_shared(key_sa + 4u * sl, kEmpty32, r0.x);
               if (old == kEmpty32 || old == r0.x) { add(sl); break; }
             }
           }
@@ -652,7 +666,9 @@ __global__ void __launch_bounds__(THREADS, 1)
       // kStagePadRows rows, so rows past the span are issued unconditionally
       // (and never read back).
       constexpr int S = kStages<F32, MULTI>();
-      const uint32_t my_stage = stage_base + (uint32_t)tid * (uint32_t)sizeof(Rec);
+      // (opaque: otherwise rebuilt from the CTA's shared window base, an
+      // S2UR SR_CgaCtaId round trip, before every group)
+      const uint32_t my_stage = pin_u32(stage_base + (uint32_t)tid * (uint32_t)sizeof(Rec));
       constexpr uint32_t kStageStride = (uint32_t)(THREADS * sizeof(Rec));
       static_assert(S % kPG == 0, "ring holds whole groups");
       static_assert(S <= kStagePadRows, "span layout padding covers the ring");
