@@ -98,6 +98,14 @@ int vmi_set_query_points(vmi_ctx* ctx, const double* xyz, int64_t n);
 /* Scan B as KITTI .bin records (x, y, z, intensity float32; scan_io.py:57-75). */
 int vmi_set_query_records_f32(vmi_ctx* ctx, const float* xyzi, int64_t n);
 
+/* Optional, after vmi_set_query_*: a superset of scan B's convex-hull vertices
+   ((n, 3) float64, the scan's own coordinates; qhull's vertices qualify).  The
+   fast kernel then takes each pose's voxel bounds (voxel.py:220) from these
+   instead of from every point; a pose whose extreme lies within 1e-6 voxel of
+   an integer is re-run on the exact path.  n = 0 removes it.  Passing points
+   that do NOT cover the hull gives wrong bounds. */
+int vmi_set_query_hull(vmi_ctx* ctx, const double* xyz, int64_t n);
+
 /* euler_to_transform (geometry.py:126-138) for P poses (tx,ty,tz,rx,ry,rz):
    12 float64 per pose, R row-major then t, bit-identical to the reference
    (glibc sin/cos, no FP contraction).  Host only; threads <= 0 = all cores. */

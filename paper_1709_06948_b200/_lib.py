@@ -25,7 +25,8 @@ SENTINEL = -1e300
 EXPORTS = (
     "vmi_create", "vmi_destroy", "vmi_last_error", "vmi_version", "vmi_set_params",
     "vmi_set_reference_points", "vmi_set_reference_records_f32", "vmi_set_reference_features", "vmi_get_reference_features",
-    "vmi_set_query_points", "vmi_set_query_records_f32", "vmi_poses_to_mats", "vmi_eval",
+    "vmi_set_query_points", "vmi_set_query_records_f32", "vmi_set_query_hull",
+    "vmi_poses_to_mats", "vmi_eval",
     "vmi_eval_poses", "vmi_eval_device", "vmi_eval_fixups", "vmi_eval_exact", "vmi_query_features",
     "vmi_fast_features",
     "vmi_argmax_device", "vmi_topk_device", "vmi_launch_count", "vmi_set_tuning", "vmi_set_passes",
@@ -124,6 +125,7 @@ def load(path: str = LIB_PATH):
     L.vmi_get_reference_features.argtypes = [_ctx, _i64, _d, ctypes.c_int64, _i64, _i64]
     L.vmi_set_query_points.argtypes = [_ctx, _d, ctypes.c_int64]
     L.vmi_set_query_records_f32.argtypes = [_ctx, _f, ctypes.c_int64]
+    L.vmi_set_query_hull.argtypes = [_ctx, _d, ctypes.c_int64]
     L.vmi_poses_to_mats.argtypes = [_d, ctypes.c_int64, _d, ctypes.c_int]
     L.vmi_eval.argtypes = [_ctx, _d, ctypes.c_int64, _d, _i32, _i64, _i64]
     L.vmi_eval_poses.argtypes = [_ctx, _d, ctypes.c_int64, _d, _i32, _i64, _i64]
@@ -263,6 +265,11 @@ class Context:
         xyz = np.ascontiguousarray(xyz, dtype=np.float64)
         self.check(self._L.vmi_set_query_points(self._h, ptr(xyz, _d), xyz.shape[0]),
                    "vmi_set_query_points")
+
+    def set_query_hull(self, xyz: np.ndarray):
+        xyz = np.ascontiguousarray(xyz, dtype=np.float64).reshape(-1, 3)
+        self.check(self._L.vmi_set_query_hull(self._h, ptr(xyz, _d), xyz.shape[0]),
+                   "vmi_set_query_hull")
 
     def set_query_records(self, rec: np.ndarray):
         rec = np.ascontiguousarray(rec, dtype=np.float32)

@@ -327,6 +327,7 @@ __global__ void __launch_bounds__(THREADS, 1)
   static_assert(NS == 1, "one span per thread");
   static_assert(sizeof(PairDesc) % 4 == 0 && sizeof(PairDesc) / 4 <= THREADS, "descriptor copy");
   __shared__ __align__(16) PairDesc desc_s;
+  __shared__ double hull_s[6][THREADS / 32];
   __shared__ unsigned long long hash_s[THREADS / 32];
   extern __shared__ __align__(16) unsigned char smem[];
   const int W = g.bins + 1;
@@ -463,6 +464,51 @@ __global__ void __launch_bounds__(THREADS, 1)
             ? 2.0 * g.res * 2.220446049250313e-16 *
                   (fabs(t2) + fabs(g.origin[2]) + (fabs(m6) + fabs(m7) + fabs(m8)) * B.max_abs + g.res)
             : 0.0;
+
+    // ---- scan B's voxel bounds (voxel.py:220) from its convex hull ----------
+    // For every direction the extreme of a point set is attained at a hull
+    // vertex, so min/max of each transformed coordinate over ALL points equal
+    // those over the hull -- up to rounding (~1e-13) and qhull's precision
+    // (~1e-11 m) for points on or next to a face.  The floors are therefore
+    // exact unless an extreme q lies within kHullEps of an integer; such a
+    // pose (a few in 10^6) is re-run on the exact path.  The point loop then
+    // skips its per-point min/max.
+    const bool hull_bounds = B.hull_n > 0;
+    if (hull_bounds) {
+      double lo[3] = {INFINITY, INFINITY, INFINITY}, hi[3] = {-INFINITY, -INFINITY, -INFINITY};
+      for (int i = tid; i < B.hull_n; i += THREADS) {
+        const double x = B.hull[3 * i], y = B.hull[3 * i + 1], z = B.hull[3 * i + 2];
+        const double q[3] = {grid_q<MODE>(xform_row(x, y, z, m0, m1, m2, t0), g.origin[0], g.res, g.inv_res),
+                             grid_q<MODE>(xform_row(x, y, z, m3, m4, m5, t1), g.origin[1], g.res, g.inv_res),
+                             grid_q<MODE>(xform_row(x, y, z, m6, m7, m8, t2), g.origin[2], g.res, g.inv_res)};
+#pragma unroll
+        for (int j = 0; j < 3; ++j) { lo[j] = fmin(lo[j], q[j]); hi[j] = fmax(hi[j], q[j]); }
+      }
+#pragma unroll
+      for (int j = 0; j < 3; ++j) {
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) {
+          lo[j] = fmin(lo[j], __shfl_xor_sync(0xffffffffu, lo[j], o));
+          hi[j] = fmax(hi[j], __shfl_xor_sync(0xffffffffu, hi[j], o));
+        }
+        if (lane == 0) { hull_s[j][wid] = lo[j]; hull_s[3 + j][wid] = hi[j]; }
+      }
+      __syncthreads();
+      if (tid == 0) {
+        bool amb = false;
+        for (int j = 0; j < 3; ++j) {
+          double a = INFINITY, b = -INFINITY;
+          for (int w = 0; w < THREADS / 32; ++w) { a = fmin(a, hull_s[j][w]); b = fmax(b, hull_s[3 + j][w]); }
+          const double fa = floor(a), fb = floor(b);
+          constexpr double kHullEps = 1e-6;  // voxel units
+          amb |= a - fa <= kHullEps + fabs(a) * 1e-12;           // the true min may be below fa
+          amb |= fb + 1.0 - b <= kHullEps + fabs(b) * 1e-12;     // the true max may reach fb + 1
+          misc[j] = (int)fa;
+          misc[3 + j] = (int)fb;
+        }
+        if (amb) misc[8] = 1;  // exact path
+      }
+    }
 
     // ---- overlap region (voxel.py:298-318) -------------------------------
     int status = 0;
@@ -697,15 +743,16 @@ __global__ void __launch_bounds__(THREADS, 1)
           locate(x, y, z, l[u], D[u], ix[u], iy[u], iz[u]);
         }
         issue_group(slot0);  // refill the slots just consumed with rows r+S ..
-        // bounds: one min/max tree per group (3-input VIMNMX3)
-        int n0 = ix[0], n1 = iy[0], n2 = iz[0], x0 = ix[0], x1 = iy[0], x2 = iz[0];
+        if (!hull_bounds) {  // bounds: one min/max tree per group (3-input VIMNMX3)
+          int n0 = ix[0], n1 = iy[0], n2 = iz[0], x0 = ix[0], x1 = iy[0], x2 = iz[0];
 #pragma unroll
-        for (int u = 1; u < kPG; ++u) {
-          n0 = min(n0, ix[u]); n1 = min(n1, iy[u]); n2 = min(n2, iz[u]);
-          x0 = max(x0, ix[u]); x1 = max(x1, iy[u]); x2 = max(x2, iz[u]);
+          for (int u = 1; u < kPG; ++u) {
+            n0 = min(n0, ix[u]); n1 = min(n1, iy[u]); n2 = min(n2, iz[u]);
+            x0 = max(x0, ix[u]); x1 = max(x1, iy[u]); x2 = max(x2, iz[u]);
+          }
+          bmin0 = min(bmin0, n0); bmin1 = min(bmin1, n1); bmin2 = min(bmin2, n2);
+          bmax0 = max(bmax0, x0); bmax1 = max(bmax1, x1); bmax2 = max(bmax2, x2);
         }
-        bmin0 = min(bmin0, n0); bmin1 = min(bmin1, n1); bmin2 = min(bmin2, n2);
-        bmax0 = max(bmax0, x0); bmax1 = max(bmax1, x1); bmax2 = max(bmax2, x2);
         // a group adds <= 32*kPG records to < 32 unflushed ones
 #pragma unroll
         for (int u = 0; u < kPG; ++u) run_step(l[u], D[u]);
@@ -760,7 +807,7 @@ __global__ void __launch_bounds__(THREADS, 1)
         bmax0 = __reduce_max_sync(0xffffffffu, bmax0);
         bmax1 = __reduce_max_sync(0xffffffffu, bmax1);
         bmax2 = __reduce_max_sync(0xffffffffu, bmax2);
-        if (lane == 0 && bmin0 != INT_MAX) {  // relative to amin (locate); a warp may have no points
+        if (!hull_bounds && lane == 0 && bmin0 != INT_MAX) {  // relative to amin (locate); a warp may have no points
           atomicMin(&misc[0], bmin0 + am0); atomicMin(&misc[1], bmin1 + am1);
           atomicMin(&misc[2], bmin2 + am2);
           atomicMax(&misc[3], bmax0 + am0); atomicMax(&misc[4], bmax1 + am1);

@@ -52,6 +52,9 @@ struct PairStore {
   double max_abs = 0.0;
   double b_lo[3] = {0, 0, 0}, b_hi[3] = {0, 0, 0};  // scan B's AABB
   int64_t b_voxels = 0;  // scan B's occupied voxels at the identity pose (table sizing)
+  double* d_hull = nullptr;  // scan B's convex-hull vertices (vmi_set_query_hull), or none
+  size_t cap_hull = 0;
+  int hull_n = 0;
 };
 
 // A CUDA stream with its own scratch: pair-set builds run kBuildLanes pairs at
@@ -162,6 +165,7 @@ void free_a(PairStore& ps) {
 
 void release_pair(PairStore& ps) {
   cudaFree(ps.d_grid); cudaFree(ps.d_avox); cudaFree(ps.d_bin_total); cudaFree(ps.d_pts);
+  cudaFree(ps.d_hull);
   ps = PairStore{};
 }
 
@@ -204,6 +208,8 @@ QueryView query_view(const vmi_ctx* c, const PairStore& ps) {
   B.rem = ps.rem;
   B.threads = c->threads;
   B.max_abs = ps.max_abs;
+  B.hull = ps.hull_n > 0 ? ps.d_hull : nullptr;
+  B.hull_n = ps.hull_n;
   for (int j = 0; j < 3; ++j) { B.lo[j] = ps.b_lo[j]; B.hi[j] = ps.b_hi[j]; }
   return B;
 }
@@ -217,7 +223,7 @@ size_t max_table_cap(const vmi_ctx* c, int kind, int is_f32, bool multi) {
   const size_t fixed = fast_smem_bytes(kind, 0, c->g.bins, c->threads / c->streams, is_f32,
                                        c->streams, multi ? 1 : 0);
   const size_t per = (size_t)fast_slot_bytes(kind, multi ? 1 : 0);
-  constexpr size_t kStaticSmem = 512;  // the kernel's static shared memory (<= 304 B)
+  constexpr size_t kStaticSmem = 2048;  // the kernel's static shared memory (~1.1 KB)
   return ((c->smem_optin - kStaticSmem - fixed) / per) & ~size_t(31);
 }
 
@@ -682,6 +688,7 @@ static int build_b(vmi_ctx* c, PairStore& ps, const void* host, int is_f32_src, 
   if (n <= 0 || !host) return fail(c, VMI_ERR_ARG, "cannot voxelize an empty cloud");
   if (n > 0x7fffffff) return fail(c, VMI_ERR_UNSUPPORTED, "more than 2^31-1 points");
   ps.b_set = false;
+  ps.hull_n = 0;
   // VMI_FORCE_F64 (experiments): keep double records even for float32-exact input
   static const bool force_f64 = std::getenv("VMI_FORCE_F64") != nullptr;
   double lo[3] = {INFINITY, INFINITY, INFINITY}, hi[3] = {-INFINITY, -INFINITY, -INFINITY};
@@ -755,6 +762,23 @@ static int set_query(vmi_ctx* c, const void* host, int is_f32_src, int64_t n) {
 }
 
 int vmi_set_query_points(vmi_ctx* c, const double* xyz, int64_t n) { return set_query(c, xyz, 0, n); }
+
+int vmi_set_query_hull(vmi_ctx* c, const double* xyz, int64_t n) {
+  if (!c || n < 0 || (n > 0 && !xyz)) return VMI_ERR_ARG;
+  if (!c->cur.b_set) return fail(c, VMI_ERR_STATE, "scan B (query) not set");
+  if (n > (1 << 24)) return fail(c, VMI_ERR_UNSUPPORTED, "hull of more than 2^24 points");
+  for (int64_t i = 0; i < 3 * n; ++i)
+    if (!std::isfinite(xyz[i])) return fail(c, VMI_ERR_ARG, "hull points must be finite");
+  cudaSetDevice(c->device);
+  PairStore& ps = c->cur;
+  ps.hull_n = 0;
+  if (n == 0) return 0;
+  CK(c, grow(&ps.d_hull, ps.cap_hull, 24 * (size_t)n));
+  CK(c, cudaMemcpyAsync(ps.d_hull, xyz, 24 * (size_t)n, cudaMemcpyHostToDevice, c->stream));
+  CK(c, cudaStreamSynchronize(c->stream));
+  ps.hull_n = (int)n;
+  return 0;
+}
 
 int vmi_set_query_records_f32(vmi_ctx* c, const float* xyzi, int64_t n) {
   return set_query(c, xyzi, 1, n);

@@ -68,6 +68,8 @@ struct QueryView {
   int rem;
   int threads;
   double max_abs;  // max |coordinate| of scan B (pose safety bound)
+  const double* hull;  // (hull_n, 3): a superset of scan B's convex-hull vertices, or none
+  int hull_n;          // > 0: per-pose voxel bounds from the hull instead of every point
   double lo[3];    // scan B's AABB in its own frame (per-pose key box, k_fast.cu)
   double hi[3];
 };

@@ -524,7 +524,10 @@ def test_general_resolution_near_integer_quotients(res, kind):
     if kind == "count":  # voxel ids and counts of the fused kernel itself
         for i in range(len(poses)):
             keys, vals, fst = eng.ctx.fast_features(mats[i], 200000)
-            assert fst == 0
+            # (VMI_FLAG_RECHECK may be set: these dyadic scans put the hull's
+            # extremes exactly on voxel faces, so the pose's bounds are taken
+            # on the exact path -- the dumped voxels are the fast kernel's own)
+            assert (fst & 0xFF) == 0
             fb = oracle.feature_map(oracle.transform(pts_b, mats[i]), (0, 0, 0), res, kind)
             ijk = unpack(fb.keys)
             lo, hi = fa.bounds
@@ -732,3 +735,57 @@ def test_align_batch_equals_align():
         assert reps[k].final_mi == r.final_mi
         np.testing.assert_allclose(reps[k].mi_trace, r.mi_trace, rtol=1e-12)
     assert stats["pairs"] == 6
+
+
+@pytest.mark.parametrize("res,kind", [(1.0, "varz"), (0.5, "count"), (0.7, "varz"), (0.2, "varz")])
+def test_hull_bounds_equal_per_point_bounds(monkeypatch, res, kind):
+    """Per-pose voxel bounds from scan B's convex hull (vmi_set_query_hull) give
+    exactly the per-point kernel's results (VMI_NO_HULL=1) and the oracle's."""
+    a, b = hdl_pair()
+    from paper_1709_06948_b200.synth import candidate_batch
+    poses = candidate_batch(EulerPose(1.5, 0.3, 0, 0, 0, 0.05), 64, seed=31,
+                            half_width=(8.0, 8.0, 1.0, 0.05, 0.05, 0.6))
+    import paper_1709_06948_b200.engine as engmod
+    monkeypatch.setattr(engmod, "HULL_MIN_POINTS", 8)
+    out = []
+    for flag in ("0", "1"):
+        monkeypatch.setenv("VMI_NO_HULL", flag)
+        eng = engine(res, kind=kind)
+        eng.set_reference(a[:, :3].astype(np.float64), fetch=False)
+        eng.set_query(b)
+        out.append(eng.evaluate(poses, histograms=True))
+        eng.close()
+    for x, y in zip(*out):
+        np.testing.assert_array_equal(x, y)
+    fa = oracle.feature_map(a[:, :3].astype(np.float64), (0, 0, 0), res, kind)
+    mats = oracle.poses_to_mats(poses[:4])
+    for k in range(4):
+        _, ost, oc, otot = oracle.mi_objective_full(fa, b[:, :3].astype(np.float64), mats[k], res=res)
+        assert ost == out[0][1][k]
+        np.testing.assert_array_equal(out[0][2][k], oc)
+
+
+def test_hull_bounds_on_voxel_faces_take_the_exact_path(monkeypatch):
+    """Scan B's extremes exactly on voxel faces (integer coordinates, integer
+    translations): every hull bound is ambiguous within 1e-6 voxel, so the
+    poses are re-run on the exact path -- results still equal the oracle's."""
+    import paper_1709_06948_b200.engine as engmod
+    monkeypatch.setattr(engmod, "HULL_MIN_POINTS", 8)
+    rng = np.random.default_rng(12)
+    a = rng.integers(-20, 20, size=(3000, 3)).astype(np.float64) + rng.uniform(0, 1, (3000, 3))
+    b = a.copy()
+    b[:8] = [[-25, -25, -3], [25, 25, 4], [-25, 25, -3], [25, -25, 4],
+             [-25, -25, 4], [25, 25, -3], [-25, 25, 4], [25, -25, -3]]  # integer corners
+    poses = np.array([[0, 0, 0, 0, 0, 0], [1, 2, 0, 0, 0, 0], [-3, 1, 1, 0, 0, 0]], dtype=np.float64)
+    eng = engine(1.0, kind="varz")
+    eng.set_reference(a, fetch=False)
+    eng.set_query(b)
+    mi, st, hist, total = eng.evaluate(poses, histograms=True)
+    fa = oracle.feature_map(a, (0, 0, 0), 1.0, "varz")
+    mats = oracle.poses_to_mats(poses)
+    for k in range(3):
+        omi, ost, oc, otot = oracle.mi_objective_full(fa, b, mats[k])
+        assert ost == st[k]
+        np.testing.assert_array_equal(hist[k], oc)
+        assert otot == total[k]
+    eng.close()
