@@ -52,8 +52,9 @@ def parse():
     ap.add_argument("--threads", type=int, default=0, help="CTA size (0 = library default)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--e2e-steps", type=int, default=3)
-    ap.add_argument("--config", default="c2", choices=["c1", "c2", "c3", "c4", "c5"],
-                    help="SURVEY.md 8(d) workload (c2 = the headline)")
+    ap.add_argument("--config", default="c2", choices=["c1", "c1v", "c2", "c3", "c4", "c5"],
+                    help="SURVEY.md 8(d) workload (c2 = the headline; c1v = C1's unordered "
+                         "scans with the VARZ feature)")
     ap.add_argument("--frames", type=int, default=1001,
                     help="c5: frames in the synthetic drive (1001 frames = the 1000-pair sequence)")
     ap.add_argument("--c5-mode", default="nm", choices=["grid", "nm"],
@@ -198,14 +199,16 @@ def workload(cfg: str, world: int, per_gpu: int) -> Workload:
     from paper_1709_06948_b200.geometry import EulerPose
     from paper_1709_06948_b200.synth import (LidarSceneSpec, candidate_batch, grid_poses,
                                              hdl64_pair)
-    if cfg == "c1":
+    if cfg in ("c1", "c1v"):
         s = np.load(os.path.join(ROOT, "tests", "golden", "c1_scans.npz"))
         t = np.array([1.0, 0.5, 0.0, 0.0, 0.0, 0.1])
         poses = grid_poses(t, {"tx": t[0] + np.arange(-8, 9) * 0.25,
                                "ty": t[1] + np.arange(-8, 9) * 0.25,
                                "rz": t[5] + np.radians(np.arange(-10, 11) * 0.5)})
-        return Workload("c1", s["a"], s["b"], poses, 0.5, "count", "strong",
-                        "C1: reference synth_scene_pair(seed=0, 20k points), 0.5 m COUNT, "
+        kind = "count" if cfg == "c1" else "varz"
+        return Workload(cfg, s["a"], s["b"], poses, 0.5, kind, "strong",
+                        f"C1{'' if cfg == 'c1' else ' (VARZ variant)'}: reference "
+                        f"synth_scene_pair(seed=0, 20k points, unordered), 0.5 m {kind.upper()}, "
                         "17x17x21 = 6069-pose (tx, ty, yaw) grid around the truth")
     if cfg == "c4":
         spec = LidarSceneSpec(extent=100.0, n_boxes=120, box_height=(1.0, 10.0))

@@ -496,6 +496,40 @@ cudaError_t topk_sort(const double* mi, int P, double* keys_out, int* idx_in, in
 }
 
 // ---- span layout (see QueryView) ------------------------------------------------
+// ---- scan B's voxel-grouped order (unordered scans) ---------------------------
+// Keys are exact_voxelize's packed voxel keys in ORIGINAL point order (s.keys):
+// count the places where consecutive points change voxel (runs - 1).
+__global__ void k_count_changes(const unsigned long long* keys, int64_t n, int* out) {
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  const bool ch = i >= 1 && i < n && keys[i] != keys[i - 1];
+  const unsigned m = __ballot_sync(0xffffffffu, ch);
+  if ((threadIdx.x & 31) == 0 && m) atomicAdd(out, __popc(m));
+}
+
+// dst[i] = src[perm[i]] for 16- or 24-byte point records
+__global__ void k_gather_points(const void* src, int rec, const int* perm, int64_t n, void* dst) {
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  const int64_t j = perm[i];
+  if (rec == 16) {
+    reinterpret_cast<float4*>(dst)[i] = reinterpret_cast<const float4*>(src)[j];
+  } else {
+    const double* s = reinterpret_cast<const double*>(src) + 3 * j;
+    double* d = reinterpret_cast<double*>(dst) + 3 * i;
+    d[0] = s[0]; d[1] = s[1]; d[2] = s[2];
+  }
+}
+
+cudaError_t voxel_order(const ExactScratch& s, const void* src, int rec, int64_t n, int* changes,
+                        void* dst, cudaStream_t st) {
+  const int T = 256;
+  const int blocks = (int)((n + T - 1) / T);
+  VMI_TRY(cudaMemsetAsync(changes, 0, 4, st));
+  k_count_changes<<<blocks, T, 0, st>>>(s.keys, n, changes);
+  if (dst) k_gather_points<<<blocks, T, 0, st>>>(src, rec, s.idx_sorted, n, dst);
+  return cudaGetLastError();
+}
+
 // Contiguous host-order points -> the fast kernel's span layout: split-double
 // float4 records (out_split; every coordinate float32-exact), else double4.
 // src is float32 (x, y, z, i) records (in_f32) or (n, 3) doubles.

@@ -55,6 +55,9 @@ struct PairStore {
   double* d_hull = nullptr;  // scan B's convex-hull vertices (vmi_set_query_hull), or none
   size_t cap_hull = 0;
   int hull_n = 0;
+  bool regrouped = false;        // d_pts in voxel-grouped order, d_pts_exact in input order
+  void* d_pts_exact = nullptr;
+  size_t cap_pts_exact = 0;
 };
 
 // A CUDA stream with its own scratch: pair-set builds run kBuildLanes pairs at
@@ -138,6 +141,7 @@ struct vmi_ctx {
   // grow-only capacities (bytes) of scratch reused across scan pairs
   size_t cap_avox_tmp = 0, cap_akeys = 0, cap_avalues = 0, cap_upload = 0;
   void* d_upload = nullptr;  // staging for host uploads
+  int* d_counter = nullptr;  // device scalar scratch
 };
 
 namespace {
@@ -165,7 +169,7 @@ void free_a(PairStore& ps) {
 
 void release_pair(PairStore& ps) {
   cudaFree(ps.d_grid); cudaFree(ps.d_avox); cudaFree(ps.d_bin_total); cudaFree(ps.d_pts);
-  cudaFree(ps.d_hull);
+  cudaFree(ps.d_hull); cudaFree(ps.d_pts_exact);
   ps = PairStore{};
 }
 
@@ -199,9 +203,11 @@ RefView ref_view(const PairStore& ps) {
   return A;
 }
 
-QueryView query_view(const vmi_ctx* c, const PairStore& ps) {
+// exact = true: the layout in the caller's point order (the exact path's
+// VARZ sums depend on it); the fast kernel's may be voxel-grouped (build_b)
+QueryView query_view(const vmi_ctx* c, const PairStore& ps, bool exact = false) {
   QueryView B{};
-  B.pts = ps.d_pts;
+  B.pts = exact && ps.regrouped ? ps.d_pts_exact : ps.d_pts;
   B.is_f32 = ps.is_f32;
   B.n = ps.nb;
   B.span = ps.span;
@@ -365,7 +371,7 @@ int exact_pose(vmi_ctx* c, const PairStore& ps, const double* mat_dev, int64_t p
                unsigned long long* hash = nullptr) {
   PointSource src{};
   src.xyz = nullptr;
-  src.B = query_view(c, ps);
+  src.B = query_view(c, ps, true);
   src.n = ps.nb;
   CK(c, exact_voxelize(c->ex, src, mat_dev, c->g, c->stream, &c->launches));
   CK(c, exact_score(c->ex, c->g, ref_view(ps), p, mi, st, hist, total, c->stream, &c->launches,
@@ -472,6 +478,7 @@ int vmi_destroy(vmi_ctx* c) {
   release_pair(c->cur);
   for (auto& ps : c->set) release_pair(ps);
   release_scratch(c);
+  cudaFree(c->d_counter);
   cudaFree(c->d_pairs); cudaFree(c->d_pose_pair); cudaFree(c->d_hash); cudaFree(c->d_setv);
   for (auto& l : c->lanes) {
     if (l.st) cudaStreamSynchronize(l.st);
@@ -724,32 +731,60 @@ static int build_b(vmi_ctx* c, PairStore& ps, const void* host, int is_f32_src, 
     ps.b_hi[j] = hi[j];
   }
   ps.max_abs = mx;
-  const size_t up_bytes = (size_t)n * (is_f32_src ? 16 : 24);
-  CK(c, grow(&c->d_upload, c->cap_upload, up_bytes));
+  const int rb = is_f32_src ? 16 : 24;
+  const size_t up_bytes = (size_t)n * rb;
+  CK(c, grow(&c->d_upload, c->cap_upload, 2 * up_bytes));  // + a voxel-grouped copy
   CK(c, cudaMemcpyAsync(c->d_upload, host, up_bytes, cudaMemcpyHostToDevice, c->stream));
   ps.span = (int)((n + c->threads - 1) / c->threads);
   ps.rem = (int)(n - (int64_t)(ps.span - 1) * c->threads);
   const size_t rec = as_f32 ? 16 : 32;
-  CK(c, grow(&ps.d_pts, ps.cap_pts, (size_t)(ps.span + kStagePadRows) * c->threads * rec));
-  CK(c, launch_span_layout(c->d_upload, is_f32_src, as_f32, n, ps.span, ps.rem, c->threads,
+  const size_t layout_bytes = (size_t)(ps.span + kStagePadRows) * c->threads * rec;
+  // scan B voxelized at the identity pose: its voxel count sizes the fast
+  // kernel's table, and its point order decides the layout.  The fused kernel
+  // aggregates runs of consecutive points in one voxel: a ring-ordered LiDAR
+  // scan runs ~12 points per voxel run, an unordered one (e.g. the reference's
+  // synth_scene_pair) ~1.  Unordered scans (mean run < 1.25 points) get the
+  // fast layout in voxel-grouped order (the stable sort's), while the exact
+  // path keeps the original order (its VARZ sums follow numpy's order over it,
+  // voxel.py:225-229); every result is order-free otherwise (counts, bounds;
+  // the fast VARZ is checked against bin edges), hence identical.
+  const char* rg = std::getenv("VMI_REGROUP");  // "0": keep the input order (A/B, tests)
+  const bool no_regroup = rg && std::strcmp(rg, "0") == 0;
+  bool regroup = false;
+  ps.b_voxels = 0;
+  if (c->params_set) {
+    PointSource src{};
+    if (is_f32_src) src.rec = static_cast<const float4*>(c->d_upload);
+    else src.xyz = static_cast<const double*>(c->d_upload);
+    src.n = n;
+    CK(c, exact_voxelize(c->ex, src, nullptr, c->g, c->stream, &c->launches));
+    if (!c->d_counter) CK(c, cudaMalloc(&c->d_counter, 16));
+    CK(c, voxel_order(c->ex, c->d_upload, rb, n, c->d_counter, nullptr, c->stream));
+    int h[2] = {0, 0};
+    CK(c, cudaMemcpyAsync(&h[0], c->ex.nruns, 4, cudaMemcpyDeviceToHost, c->stream));
+    CK(c, cudaMemcpyAsync(&h[1], c->d_counter, 4, cudaMemcpyDeviceToHost, c->stream));
+    CK(c, cudaStreamSynchronize(c->stream));
+    ps.b_voxels = h[0];
+    regroup = !no_regroup && (double)(h[1] + 1) * 1.25 >= (double)n && n > 1;
+  }
+  char* ordered = static_cast<char*>(c->d_upload);
+  if (regroup) {  // fast layout from the voxel-grouped copy, exact layout from the original
+    ordered += up_bytes;
+    CK(c, voxel_order(c->ex, c->d_upload, rb, n, c->d_counter, ordered, c->stream));
+    CK(c, grow(&ps.d_pts_exact, ps.cap_pts_exact, layout_bytes));
+    CK(c, launch_span_layout(c->d_upload, is_f32_src, as_f32, n, ps.span, ps.rem, c->threads,
+                             ps.d_pts_exact, c->stream));
+    c->launches += 3;
+  }
+  ps.regrouped = regroup;
+  CK(c, grow(&ps.d_pts, ps.cap_pts, layout_bytes));
+  CK(c, launch_span_layout(ordered, is_f32_src, as_f32, n, ps.span, ps.rem, c->threads,
                            ps.d_pts, c->stream));
   c->launches += 1;
   ps.is_f32 = as_f32;
   ps.nb = n;
-  // table sizing hint: scan B's occupied voxel count in its own frame
-  ps.b_voxels = 0;
-  if (ps.a_set && ps.a_npts > 0 && ps.a_nvox > 0) {
-    // same sensor, same grid: scale scan A's voxel count (saves a voxelization)
+  if (ps.b_voxels <= 0 && ps.a_set && ps.a_npts > 0 && ps.a_nvox > 0)  // (params unset: unreachable)
     ps.b_voxels = (int64_t)((double)ps.a_nvox * (double)n / (double)ps.a_npts) + 1;
-  } else if (c->params_set) {
-    PointSource src{};
-    src.B = query_view(c, ps);
-    src.n = n;
-    int V = 0;
-    CK(c, exact_voxelize(c->ex, src, nullptr, c->g, c->stream, &c->launches));
-    CK(c, cudaMemcpyAsync(&V, c->ex.nruns, 4, cudaMemcpyDeviceToHost, c->stream));
-    ps.b_voxels = V;
-  }
   CK(c, cudaStreamSynchronize(c->stream));  // the host buffer may be reused on return
   ps.b_set = true;
   return 0;
@@ -917,7 +952,7 @@ int vmi_query_features(vmi_ctx* c, const double mat[12], int64_t* keys, double* 
   if ((rc = ensure_P(c, 1, false))) return rc;
   CK(c, cudaMemcpyAsync(c->d_mats, mat, 96, cudaMemcpyHostToDevice, c->stream));
   PointSource src{};
-  src.B = query_view(c, c->cur);
+  src.B = query_view(c, c->cur, true);
   src.n = c->cur.nb;
   CK(c, exact_voxelize(c->ex, src, c->d_mats, c->g, c->stream, &c->launches));
   int h[8];
@@ -1167,6 +1202,8 @@ int vmi_set_pairs(vmi_ctx* c, int64_t npairs, const void* const* a, const int64_
       }
       free_a(ps);
       ps.b_set = false;
+      ps.regrouped = false;  // (a drive's scans are ring-ordered)
+      ps.hull_n = 0;
       const HostScan& h_a = hs[(size_t)ia[(size_t)i]];
       const HostScan& h_b = hs[(size_t)ib[(size_t)i]];
       // ---- scan A: bounds on the host, voxelize + features + grid on the GPU

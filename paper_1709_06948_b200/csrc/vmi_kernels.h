@@ -115,6 +115,13 @@ cudaError_t launch_argmax(const double* v, int64_t P, double* out_val, long long
 cudaError_t topk_sort(const double* mi, int P, double* keys_out, int* idx_in, int* idx_out,
                       void* tmp, size_t* tmp_bytes, cudaStream_t st);
 
+// After exact_voxelize of n contiguous points (identity pose): *changes =
+// number of voxel changes between consecutive points (runs - 1), and, with
+// dst, the points (rec = 16: float4 records, 24: float64 xyz) in the sort's
+// voxel-grouped order (dst[i] = src[s.idx_sorted[i]]).
+cudaError_t voxel_order(const ExactScratch& s, const void* src, int rec, int64_t n, int* changes,
+                        void* dst, cudaStream_t st);
+
 // Reorder contiguous points into the fast path's span layout.
 cudaError_t launch_span_layout(const void* src, int in_f32, int out_split, int64_t n, int span,
                                int rem, int threads, void* dst, cudaStream_t st);

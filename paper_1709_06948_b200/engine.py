@@ -150,8 +150,6 @@ class MIEngine:
         pts = _points_of(scan_b)
         if pts.shape[0] == 0:
             raise ValueError("cannot voxelize an empty cloud")
-        if self.kind is FeatureKind.COUNT and os.environ.get("VMI_COUNT_ORDER", "1") != "0":
-            pts = self._voxel_order(pts)
         if pts.dtype == np.float32 and pts.shape[1] == 4:
             self.ctx.set_query_records(pts)  # KITTI .bin records, float4 as is
         else:
@@ -159,26 +157,6 @@ class MIEngine:
         hull = hull_vertices(pts)
         if hull is not None:
             self.ctx.set_query_hull(hull)
-
-    def _voxel_order(self, pts: np.ndarray) -> np.ndarray:
-        """COUNT only: scan B's points grouped by their voxel at the identity
-        pose (x, y, z lexicographic, the kernel's x-major order).  The fused
-        kernel aggregates runs of consecutive points that land in one voxel, so
-        an unordered scan (e.g. the reference's synthetic scenes) turns into a
-        table update per point; grouped, a small pose keeps most of a voxel's
-        points in one run (C1: K1 2.00 -> 1.85 ms).  COUNT features, bounds and histograms are integer
-        and order-free, so every result is unchanged.  (VARZ keeps the input
-        order: the exact path's z sums follow numpy's order over it.)"""
-        q = np.floor((np.asarray(pts[:, :3], dtype=np.float64) - self.origin) / self.resolution)
-        if not np.isfinite(q).all() or q.shape[0] < 2:
-            return pts
-        # only an unordered scan (mean run < 1.25 points at the identity pose):
-        # ring-ordered HDL-64 scans already run ~12 points per voxel run, and
-        # voxel order measured slower there (C2-shaped VARZ: 31.2 vs 28.9 ms)
-        runs = 1 + np.count_nonzero(np.any(q[1:] != q[:-1], axis=1))
-        if runs * 1.25 < q.shape[0]:
-            return pts
-        return pts[np.lexsort((q[:, 2], q[:, 1], q[:, 0]))]
 
     # ---- many resident pairs (multi-pair kernel) ----------------------------------
     def set_pairs(self, pairs) -> None:

@@ -592,21 +592,48 @@ def test_ragged_query_sizes_match_oracle(nb, kind):
         assert_mi_close([mi[i]], [omi])
 
 
-def test_count_voxel_order_changes_nothing(monkeypatch):
-    """COUNT scans that arrive unordered are regrouped by voxel before upload
-    (engine.MIEngine._voxel_order); every output must be bit-identical to the
-    input-order upload."""
-    c = small_case("s1")  # COUNT, 0.5 m, unordered synthetic scene
+@pytest.mark.parametrize("tag", ["s0", "s1", "s3"])
+def test_voxel_regroup_changes_nothing(monkeypatch, tag):
+    """Unordered scans (mean voxel run < 1.25 points) get the fast kernel's
+    layout in voxel-grouped order while the exact path keeps the input order
+    (its VARZ sums follow numpy's order): every output -- fast and exact --
+    must be bit-identical to the input-order upload (VMI_REGROUP=0) and match
+    the reference golden."""
+    c = small_case(tag)
     out = []
     for flag in ("0", "1"):
-        monkeypatch.setenv("VMI_COUNT_ORDER", flag)
+        monkeypatch.setenv("VMI_REGROUP", flag)
         eng = engine(c["res"], c["origin"], c["kind"], c["phi"])
         eng.set_reference(c["a"])
         eng.set_query(c["b"])
-        out.append(eng.evaluate(c["poses"], histograms=True))
+        out.append(eng.evaluate(c["poses"], histograms=True)
+                   + eng.evaluate(c["poses"], histograms=True, exact=True))
+        eng.close()
     for x, y in zip(*out):
         np.testing.assert_array_equal(x, y)
     assert_mi_close(out[1][0], c["mi"])
+    np.testing.assert_array_equal(out[1][2][(c["status"] == 0)], c["hist"][c["status"] == 0])
+
+
+def test_c1_scans_varz_regrouped_against_oracle():
+    """The reference's own unordered C1 scans (synth_scene_pair) with VARZ at
+    0.5 m: voxel-grouped fast layout, histograms equal the oracle's."""
+    s = golden("c1_scans.npz")
+    eng = engine(0.5, kind="varz")
+    eng.set_reference(s["a"], fetch=False)
+    eng.set_query(s["b"])
+    g = golden("c1_golden.npz")
+    poses = g["poses"][::97]
+    mi, st, hist, total = eng.evaluate(poses, histograms=True)
+    fa = oracle.feature_map(s["a"], (0, 0, 0), 0.5, "varz")
+    mats = oracle.poses_to_mats(poses)
+    for k in range(poses.shape[0]):
+        omi, ost, oc, otot = oracle.mi_objective_full(fa, s["b"], mats[k], res=0.5)
+        assert ost == st[k]
+        np.testing.assert_array_equal(hist[k], oc)
+        assert otot == total[k]
+        assert_mi_close([mi[k]], [omi])
+    eng.close()
 
 
 @pytest.mark.parametrize("res,kind,clamp", [(0.2, "varz", None), (0.3, "varz", None),
