@@ -225,6 +225,10 @@ int vmi_align_pairs(vmi_ctx* ctx, int64_t K, const double* x0, const double step
 
 /* Number of kernel launches issued by this context so far (bench accounting). */
 int64_t vmi_launch_count(const vmi_ctx* ctx);
+/* Counters: [0] kernel launches, [1] table re-plans (an under-estimated scan-B
+   occupancy grown after > 1% of a launch overflowed), [2] poses re-run on the
+   exact path, [3] the current pair's scan-B occupancy estimate. */
+int vmi_get_counters(const vmi_ctx* ctx, int64_t out[4]);
 
 /* Fast-path configuration knobs (tests/bench): table capacity (0 = sized from
    scan B's occupancy; larger than fits shared memory = clamped) and CUDA threads per CTA (0 = default = 512, one scan-B span per

@@ -30,7 +30,7 @@ EXPORTS = (
     "vmi_eval_poses", "vmi_eval_device", "vmi_eval_fixups", "vmi_eval_exact", "vmi_query_features",
     "vmi_fast_features",
     "vmi_argmax_device", "vmi_topk_device", "vmi_launch_count", "vmi_set_tuning", "vmi_set_passes",
-    "vmi_nm_run", "vmi_set_pairs", "vmi_eval_pairs", "vmi_align_pairs",
+    "vmi_nm_run", "vmi_set_pairs", "vmi_eval_pairs", "vmi_align_pairs", "vmi_get_counters",
 )
 
 
@@ -139,6 +139,7 @@ def load(path: str = LIB_PATH):
     L.vmi_launch_count.argtypes = [_ctx]
     L.vmi_launch_count.restype = ctypes.c_int64
     L.vmi_set_tuning.argtypes = [_ctx, ctypes.c_int, ctypes.c_int]
+    L.vmi_get_counters.argtypes = [_ctx, _i64]
     L.vmi_set_passes.argtypes = [_ctx, ctypes.c_int]
     L.vmi_nm_run.argtypes = [ctypes.c_int64, _d, _d, ctypes.c_int, ctypes.c_double,
                              ctypes.c_double, ctypes.c_int, ctypes.c_int64, NM_EVAL_FN, _vp, _d,
@@ -212,6 +213,13 @@ class Context:
     @property
     def launches(self) -> int:
         return int(self._L.vmi_launch_count(self._h))
+
+    def counters(self) -> dict:
+        """launches, table re-plans, exact-path poses, scan-B occupancy estimate"""
+        out = np.zeros(4, dtype=np.int64)
+        self.check(self._L.vmi_get_counters(self._h, ptr(out, _i64)), "vmi_get_counters")
+        return dict(zip(("launches", "replans", "exact_poses", "b_voxels_estimate"),
+                        (int(x) for x in out)))
 
     def set_params(self, origin, res, kind: int, bins: int, clamp: float, include_phi: bool):
         o = np.ascontiguousarray(origin, dtype=np.float64)

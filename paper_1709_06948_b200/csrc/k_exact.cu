@@ -530,6 +530,38 @@ cudaError_t voxel_order(const ExactScratch& s, const void* src, int rec, int64_t
   return cudaGetLastError();
 }
 
+// ---- re-planned re-runs of flagged poses (vmi_api.cu do_fixups) ----------------
+template <typename T>
+__global__ void k_gather_rows(const T* src, const int64_t* idx, int64_t n, int w, T* dst) {
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n * w) return;
+  const int64_t r = i / w, k = i - r * w;
+  dst[i] = src[idx[r] * w + k];
+}
+template <typename T>
+__global__ void k_scatter_rows(const T* src, const int64_t* idx, int64_t n, int w, T* dst) {
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n * w) return;
+  const int64_t r = i / w, k = i - r * w;
+  dst[idx[r] * w + k] = src[i];
+}
+template <typename T>
+cudaError_t gather_rows(const T* src, const int64_t* idx, int64_t n, int w, T* dst, bool scatter,
+                        cudaStream_t st) {
+  if (n <= 0) return cudaSuccess;
+  const int T_ = 256;
+  const unsigned blocks = (unsigned)((n * w + T_ - 1) / T_);
+  if (scatter) k_scatter_rows<T><<<blocks, T_, 0, st>>>(src, idx, n, w, dst);
+  else k_gather_rows<T><<<blocks, T_, 0, st>>>(src, idx, n, w, dst);
+  return cudaGetLastError();
+}
+template cudaError_t gather_rows<double>(const double*, const int64_t*, int64_t, int, double*, bool,
+                                         cudaStream_t);
+template cudaError_t gather_rows<int32_t>(const int32_t*, const int64_t*, int64_t, int, int32_t*,
+                                          bool, cudaStream_t);
+template cudaError_t gather_rows<long long>(const long long*, const int64_t*, int64_t, int,
+                                            long long*, bool, cudaStream_t);
+
 // Contiguous host-order points -> the fast kernel's span layout: split-double
 // float4 records (out_split; every coordinate float32-exact), else double4.
 // src is float32 (x, y, z, i) records (in_f32) or (n, 3) doubles.

@@ -142,6 +142,12 @@ struct vmi_ctx {
   size_t cap_avox_tmp = 0, cap_akeys = 0, cap_avalues = 0, cap_upload = 0;
   void* d_upload = nullptr;  // staging for host uploads
   int* d_counter = nullptr;  // device scalar scratch
+  void* d_fix = nullptr;     // re-planned re-runs: indices, matrices, outputs
+  int64_t cap_fix = 0;
+  long long* d_fix_hist = nullptr;
+  size_t cap_fix_hist = 0;
+  int64_t replans = 0;       // times an under-estimated table plan was grown
+  int64_t exact_poses = 0;   // poses re-run on the exact path
 };
 
 namespace {
@@ -406,6 +412,63 @@ int launch_fast_eval(vmi_ctx* c, const double* mats_dev, int64_t P, double* mi, 
 
 // Re-run, through the exact path, every pose whose fast-path status carries
 // VMI_FLAG_RECHECK; pose_pair (host, nullable) names each pose's pair in the set.
+// More than ~1% of a launch flagged means the table plan under-estimated scan
+// B's occupancy (table overflow), not the rare VARZ bin-edge re-check: grow
+// the estimate 4x (sticky for later launches: a bigger single-pass table, or
+// the multi-pass layout) and re-run just the flagged poses through the fast
+// kernel, gathered into one launch -- up to three times -- before the exact
+// path takes what is still flagged.  `hs` is updated in place (own holds it).
+int replan_flagged(vmi_ctx* c, const double* mats_dev, int64_t P, double* mi, int32_t* st,
+                   long long* hist, long long* total, cudaStream_t stream,
+                   std::vector<int32_t>& own, const int32_t*& hs) {
+  const int W = c->g.bins + 1;
+  for (int attempt = 0; attempt < 3; ++attempt) {
+    std::vector<int64_t> idx;
+    for (int64_t p = 0; p < P; ++p)
+      if (hs[p] & VMI_FLAG_RECHECK) idx.push_back(p);
+    const int64_t n = (int64_t)idx.size();
+    if (n <= std::max<int64_t>(16, P / 100)) return 0;
+    c->cur.b_voxels = std::max<int64_t>(4 * std::max<int64_t>(c->cur.b_voxels, 1024), 4096);
+    c->replans += 1;
+    if (n > c->cap_fix) {
+      cudaFree(c->d_fix);
+      c->d_fix = nullptr;
+      c->cap_fix = 0;
+      CK(c, cudaMalloc(&c->d_fix, (size_t)n * (8 + 96 + 8 + 4 + 8) + 64));
+      c->cap_fix = n;
+    }
+    int64_t* d_idx = static_cast<int64_t*>(c->d_fix);
+    double* d_m = reinterpret_cast<double*>(d_idx + c->cap_fix);
+    double* d_mi = d_m + 12 * c->cap_fix;
+    long long* d_tot = reinterpret_cast<long long*>(d_mi + c->cap_fix);
+    int32_t* d_st = reinterpret_cast<int32_t*>(d_tot + c->cap_fix);
+    long long* d_h = nullptr;
+    if (hist) {
+      if ((size_t)n * W * W > c->cap_fix_hist) {
+        cudaFree(c->d_fix_hist);
+        c->d_fix_hist = nullptr;
+        CK(c, cudaMalloc(&c->d_fix_hist, (size_t)n * W * W * 8));
+        c->cap_fix_hist = (size_t)n * W * W;
+      }
+      d_h = c->d_fix_hist;
+    }
+    CK(c, cudaMemcpyAsync(d_idx, idx.data(), 8 * (size_t)n, cudaMemcpyHostToDevice, stream));
+    CK(c, gather_rows<double>(mats_dev, d_idx, n, 12, d_m, false, stream));
+    int rc = launch_fast_eval(c, d_m, n, d_mi, d_st, d_h, d_tot, stream);
+    if (rc) return rc;
+    CK(c, gather_rows<double>(d_mi, d_idx, n, 1, mi, true, stream));
+    CK(c, gather_rows<int32_t>(d_st, d_idx, n, 1, st, true, stream));
+    if (total) CK(c, gather_rows<long long>(d_tot, d_idx, n, 1, total, true, stream));
+    if (hist) CK(c, gather_rows<long long>(d_h, d_idx, n, W * W, hist, true, stream));
+    c->launches += 6;
+    own.resize((size_t)P);
+    CK(c, cudaMemcpyAsync(own.data(), st, P * 4, cudaMemcpyDeviceToHost, stream));
+    CK(c, cudaStreamSynchronize(stream));
+    hs = own.data();
+  }
+  return 0;
+}
+
 // hs_in: the statuses already on the host (nullable: read them here); hash:
 // the per-pose histogram identities to keep in step (nullable).
 int do_fixups(vmi_ctx* c, const double* mats_dev, int64_t P, double* mi, int32_t* st,
@@ -421,6 +484,10 @@ int do_fixups(vmi_ctx* c, const double* mats_dev, int64_t P, double* mi, int32_t
     hs = own.data();
   }
   int64_t nf = 0;
+  if (!pose_pair) {
+    int rc = replan_flagged(c, mats_dev, P, mi, st, hist, total, stream, own, hs);
+    if (rc) return rc;
+  }
   cudaStream_t saved = c->stream;
   c->stream = stream;
   for (int64_t p = 0; p < P; ++p) {
@@ -429,6 +496,7 @@ int do_fixups(vmi_ctx* c, const double* mats_dev, int64_t P, double* mi, int32_t
       int rc = exact_pose(c, ps, mats_dev + 12 * p, p, mi, st, hist, total, hash);
       if (rc) { c->stream = saved; return rc; }
       ++nf;
+      c->exact_poses += 1;
     }
   }
   c->stream = saved;
@@ -478,7 +546,7 @@ int vmi_destroy(vmi_ctx* c) {
   release_pair(c->cur);
   for (auto& ps : c->set) release_pair(ps);
   release_scratch(c);
-  cudaFree(c->d_counter);
+  cudaFree(c->d_counter); cudaFree(c->d_fix); cudaFree(c->d_fix_hist);
   cudaFree(c->d_pairs); cudaFree(c->d_pose_pair); cudaFree(c->d_hash); cudaFree(c->d_setv);
   for (auto& l : c->lanes) {
     if (l.st) cudaStreamSynchronize(l.st);
@@ -505,6 +573,15 @@ int vmi_destroy(vmi_ctx* c) {
 const char* vmi_last_error(const vmi_ctx* c) { return c ? c->err.c_str() : "null context"; }
 
 int64_t vmi_launch_count(const vmi_ctx* c) { return c ? c->launches : 0; }
+
+int vmi_get_counters(const vmi_ctx* c, int64_t out[4]) {
+  if (!c || !out) return VMI_ERR_ARG;
+  out[0] = c->launches;
+  out[1] = c->replans;
+  out[2] = c->exact_poses;
+  out[3] = c->cur.b_voxels;
+  return 0;
+}
 
 int vmi_set_tuning(vmi_ctx* c, int table_cap_, int threads) {
   if (!c) return VMI_ERR_ARG;
@@ -765,6 +842,8 @@ static int build_b(vmi_ctx* c, PairStore& ps, const void* host, int is_f32_src, 
     CK(c, cudaMemcpyAsync(&h[1], c->d_counter, 4, cudaMemcpyDeviceToHost, c->stream));
     CK(c, cudaStreamSynchronize(c->stream));
     ps.b_voxels = h[0];
+    if (const char* e = std::getenv("VMI_EST_SCALE"))  // tests: mis-estimate the occupancy
+      ps.b_voxels = std::max<int64_t>(1, (int64_t)(ps.b_voxels * std::atof(e)));
     regroup = !no_regroup && (double)(h[1] + 1) * 1.25 >= (double)n && n > 1;
   }
   char* ordered = static_cast<char*>(c->d_upload);

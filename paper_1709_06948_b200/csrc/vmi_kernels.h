@@ -122,6 +122,11 @@ cudaError_t topk_sort(const double* mi, int P, double* keys_out, int* idx_in, in
 cudaError_t voxel_order(const ExactScratch& s, const void* src, int rec, int64_t n, int* changes,
                         void* dst, cudaStream_t st);
 
+// dst[r] = src[idx[r]] (rows of w elements), or the reverse with scatter.
+template <typename T>
+cudaError_t gather_rows(const T* src, const int64_t* idx, int64_t n, int w, T* dst, bool scatter,
+                        cudaStream_t st);
+
 // Reorder contiguous points into the fast path's span layout.
 cudaError_t launch_span_layout(const void* src, int in_f32, int out_split, int64_t n, int span,
                                int rem, int threads, void* dst, cudaStream_t st);

@@ -816,3 +816,30 @@ def test_hull_bounds_on_voxel_faces_take_the_exact_path(monkeypatch):
         np.testing.assert_array_equal(hist[k], oc)
         assert otot == total[k]
     eng.close()
+
+
+@pytest.mark.parametrize("kind,res", [("varz", 1.0), ("count", 0.5), ("varz", 0.2)])
+def test_underestimated_table_is_replanned(monkeypatch, kind, res):
+    """A table planned for 1/30 of scan B's occupancy overflows on every pose:
+    the library grows the estimate and re-runs the flagged poses through the
+    fast kernel (re-plan) instead of sending them all to the exact path --
+    results equal the well-planned run bit for bit."""
+    a, b = hdl_pair()
+    from paper_1709_06948_b200.synth import candidate_batch
+    poses = candidate_batch(EulerPose(1.5, 0.3, 0, 0, 0, 0.05), 512, seed=41)
+    out = []
+    for scale in (None, "0.033"):
+        if scale:
+            monkeypatch.setenv("VMI_EST_SCALE", scale)
+        else:
+            monkeypatch.delenv("VMI_EST_SCALE", raising=False)
+        eng = engine(res, kind=kind)
+        eng.set_reference(a[:, :3].astype(np.float64), fetch=False)
+        eng.set_query(b)
+        out.append(eng.evaluate(poses, histograms=True))
+        cnt = eng.ctx.counters()
+        eng.close()
+    for x, y in zip(*out):
+        np.testing.assert_array_equal(x, y)
+    assert cnt["replans"] >= 1
+    assert cnt["exact_poses"] <= 16  # the re-plan took (nearly) all of them
