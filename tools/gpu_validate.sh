@@ -5,7 +5,7 @@ timeout 1500 python -m pytest tests -m gpu -x -q > gpurun_out/pytest_gpu_$V.log 
 timeout 300 python -c "import __graft_entry__ as g; g.smoke()" > gpurun_out/smoke_$V.log 2>&1; echo "smoke rc=$?" >> gpurun_out/smoke_$V.log
 timeout 900 python bench.py > gpurun_out/bench_c2_$V.json 2> gpurun_out/bench_c2_$V.err
 timeout 900 python bench.py --impl reference --steps 3 --warmup 3 > gpurun_out/bench_ref_$V.json 2> gpurun_out/bench_ref_$V.err
-for c in c1 c3 c4; do timeout 900 python bench.py --config $c --no-cpu-baseline > gpurun_out/bench_${c}_$V.json 2> gpurun_out/bench_${c}_$V.err; done
+for c in c1 c1v c3 c4; do timeout 900 python bench.py --config $c --no-cpu-baseline > gpurun_out/bench_${c}_$V.json 2> gpurun_out/bench_${c}_$V.err; done
 timeout 1200 python bench.py --config c5 --steps 3 --warmup 1 > gpurun_out/bench_c5_$V.json 2> gpurun_out/bench_c5_$V.err
 timeout 900 python bench.py --config c5 --impl reference --steps 1 --warmup 0 > gpurun_out/bench_c5ref_$V.json 2> gpurun_out/bench_c5ref_$V.err
 timeout 600 python bench.py --steps 2 --warmup 3 --no-cpu-baseline --parity-sample 0 --e2e-steps 1 > gpurun_out/ncu_plain_$V.log 2>&1 && \
