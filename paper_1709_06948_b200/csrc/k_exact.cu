@@ -11,6 +11,7 @@
 // It builds scan A's reference grid once per scan pair (_prepare,
 // align.py:114-119) and re-evaluates, exactly, the rare poses the fast path
 // flags (VMI_FLAG_RECHECK).  Sorting uses CUB (CUDA toolkit library code).
+#include <algorithm>
 #include <cstdint>
 #include <climits>
 #include <cub/cub.cuh>
@@ -565,11 +566,9 @@ template cudaError_t gather_rows<long long>(const long long*, const int64_t*, in
 // Contiguous host-order points -> the fast kernel's span layout: split-double
 // float4 records (out_split; every coordinate float32-exact), else double4.
 // src is float32 (x, y, z, i) records (in_f32) or (n, 3) doubles.
-__global__ void k_span_layout(const void* src, int in_f32, int out_split, int64_t n, int span,
-                              int rem, int threads, void* dst) {
-  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;  // original index
-  const int64_t total = (int64_t)span * threads;
-  if (i >= total) return;
+__device__ __forceinline__ void span_layout_one(const void* src, int in_f32, int out_split,
+                                                int64_t n, int span, int rem, int threads,
+                                                void* dst, int64_t i) {
   double x = 0.0, y = 0.0, z = 0.0;
   int64_t li;
   if (i >= n) {  // padding slots: the (threads - rem) unused last-iteration entries
@@ -593,6 +592,134 @@ __global__ void k_span_layout(const void* src, int in_f32, int out_split, int64_
   } else {
     reinterpret_cast<double4*>(dst)[li] = make_double4(x, y, z, 0.0);
   }
+}
+
+__global__ void k_span_layout(const void* src, int in_f32, int out_split, int64_t n, int span,
+                              int rem, int threads, void* dst) {
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;  // original index
+  if (i >= (int64_t)span * threads) return;
+  span_layout_one(src, in_f32, out_split, n, span, rem, threads, dst, i);
+}
+
+// ---- a group of pair-set pairs built together (vmi_set_pairs) -----------------
+// One launch per stage for G pairs: scan A's 32-bit keys are (pair << nbits) |
+// box index, so ONE stable radix sort over the group orders every pair's
+// points exactly as its own voxelize would (pair-major, then x-major, then
+// input order), and run-length encoding, the features and the grids follow in
+// single launches too.
+__global__ void k_group_zero(const GroupPair* gp, int* vcount) {
+  const GroupPair& q = gp[blockIdx.y];
+  for (size_t i = (size_t)blockIdx.x * blockDim.x + threadIdx.x; i < q.grid_bytes;
+       i += (size_t)gridDim.x * blockDim.x)
+    q.grid[i] = 0;
+  if (blockIdx.x == 0 && threadIdx.x < kMaxW) q.bin_total[threadIdx.x] = 0u;
+  if (blockIdx.x == 0 && threadIdx.x == 0) vcount[blockIdx.y] = 0;
+}
+
+__global__ void k_group_keys(const GroupPair* gp, GridParams g, int in_f32, int nbits,
+                             uint32_t* keys, int* idx, double* zout, int* bad) {
+  const GroupPair& q = gp[blockIdx.y];
+  const int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (j >= q.n) return;
+  PointSource src{};
+  if (in_f32) src.rec = static_cast<const float4*>(q.raw_a);
+  else src.xyz = static_cast<const double*>(q.raw_a);
+  src.n = q.n;
+  double x, y, z;
+  point_at(src, j, x, y, z);
+  int a, b, c;
+  bool ok = voxel_coord(x, g.origin[0], g.res, g.inv_res, g.mode, a);
+  ok &= voxel_coord(y, g.origin[1], g.res, g.inv_res, g.mode, b);
+  ok &= voxel_coord(z, g.origin[2], g.res, g.inv_res, g.mode, c);
+  const uint32_t rx = (uint32_t)(a - q.amin.x), ry = (uint32_t)(b - q.amin.y),
+                 rz = (uint32_t)(c - q.amin.z);
+  const int64_t o = q.off + j;
+  if (!ok || rx >= q.ext.x || ry >= q.ext.y || rz >= q.ext.z) {  // cannot happen: exact box
+    bad[blockIdx.y] = 1;
+    keys[o] = (uint32_t)blockIdx.y << nbits;
+  } else {
+    keys[o] = ((uint32_t)blockIdx.y << nbits) | ((rx * q.ext.y + ry) * q.ext.z + rz);
+  }
+  idx[o] = (int)o;
+  zout[o] = z;
+}
+
+__global__ void k_group_grid(const GroupPair* gp, const uint32_t* ukeys, const double* values,
+                             const int* nruns, GridParams g, int nbits, int4* avox_tmp,
+                             int* vcount) {
+  const int v = blockIdx.x * blockDim.x + threadIdx.x;
+  if (v >= *nruns) return;
+  const uint32_t k = ukeys[v];
+  const int pr = (int)(k >> nbits);
+  const uint32_t l = k & ((1u << nbits) - 1u);
+  const GroupPair& q = gp[pr];
+  const uint32_t rz = l % q.ext.z, rxy = l / q.ext.z;
+  const uint32_t ry = rxy % q.ext.y, rx = rxy / q.ext.y;
+  const int bin = feature_bin(values[v], g.clamp, g.bins);
+  q.grid[l] = (uint8_t)bin;
+  avox_tmp[v] = make_int4((int)rx, (int)ry, (int)rz, bin | (pr << 16));
+  atomicAdd(&q.bin_total[bin], 1u);
+  atomicAdd(&vcount[pr], 1);
+}
+
+__global__ void k_group_cursors(const GroupPair* gp, int W, int* cursor) {
+  if (threadIdx.x == 0) {
+    const GroupPair& q = gp[blockIdx.x];
+    int s = 0;
+    for (int b = 0; b < W; ++b) { cursor[blockIdx.x * kMaxW + b] = s; s += (int)q.bin_total[b]; }
+  }
+}
+
+__global__ void k_group_scatter(const GroupPair* gp, const int4* avox_tmp, const int* nruns,
+                                int* cursor) {
+  const int v = blockIdx.x * blockDim.x + threadIdx.x;
+  if (v >= *nruns) return;
+  int4 a = avox_tmp[v];
+  const int pr = a.w >> 16;
+  a.w &= 0xFFFF;
+  gp[pr].avox[atomicAdd(&cursor[pr * kMaxW + a.w], 1)] = a;
+}
+
+__global__ void k_group_layout(const GroupPair* gp, int in_f32, int threads) {
+  const GroupPair& q = gp[blockIdx.y];
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= (int64_t)q.span * threads) return;
+  span_layout_one(q.raw_b, in_f32, q.b_split, q.nb, q.span, q.rem, threads, q.pts, i);
+}
+
+cudaError_t build_pair_group(ExactScratch& s, const GroupPair* gp_dev, int G, int64_t n_total,
+                             int max_na, int max_nb_rows, size_t max_grid, int nbits,
+                             const GridParams& g, int in_f32, int threads, int4* avox_tmp,
+                             int* cursor, int* vcount, int* bad, cudaStream_t st,
+                             int64_t* launches) {
+  VMI_TRY(exact_alloc(s, n_total));
+  const int T = 256;
+  const int zb = (int)std::min<size_t>(1024, (max_grid + T * 4 - 1) / (T * 4));
+  k_group_zero<<<dim3(zb > 0 ? zb : 1, G), T, 0, st>>>(gp_dev, vcount);
+  uint32_t* k32 = reinterpret_cast<uint32_t*>(s.keys);
+  uint32_t* k32s = reinterpret_cast<uint32_t*>(s.keys_sorted);
+  uint32_t* u32 = reinterpret_cast<uint32_t*>(s.ukeys);
+  k_group_keys<<<dim3((max_na + T - 1) / T, G), T, 0, st>>>(gp_dev, g, in_f32, nbits, k32, s.idx,
+                                                            s.z, bad);
+  int gbits = 0;
+  while ((1 << gbits) < G) ++gbits;
+  size_t bytes = s.cub_bytes;
+  VMI_TRY(cub::DeviceRadixSort::SortPairs(s.cub_tmp, bytes, k32, k32s, s.idx, s.idx_sorted,
+                                          (int)n_total, 0, nbits + gbits, st));
+  bytes = s.cub_bytes;
+  VMI_TRY(cub::DeviceRunLengthEncode::Encode(s.cub_tmp, bytes, k32s, u32, s.counts, s.nruns,
+                                             (int)n_total, st));
+  bytes = s.cub_bytes;
+  VMI_TRY(cub::DeviceScan::ExclusiveSum(s.cub_tmp, bytes, s.counts, s.offsets, (int)n_total, st));
+  const int blocks = (int)((n_total + T - 1) / T);
+  k_gather<<<blocks, T, 0, st>>>(s.z, s.idx_sorted, n_total, s.zs);
+  k_features<<<blocks, T, 0, st>>>(s.counts, s.offsets, s.nruns, s.zs, g.kind, s.values);
+  k_group_grid<<<blocks, T, 0, st>>>(gp_dev, u32, s.values, s.nruns, g, nbits, avox_tmp, vcount);
+  k_group_cursors<<<G, 32, 0, st>>>(gp_dev, g.bins + 1, cursor);
+  k_group_scatter<<<blocks, T, 0, st>>>(gp_dev, avox_tmp, s.nruns, cursor);
+  k_group_layout<<<dim3((max_nb_rows + T - 1) / T, G), T, 0, st>>>(gp_dev, in_f32, threads);
+  if (launches) *launches += 9;
+  return cudaGetLastError();
 }
 
 cudaError_t launch_span_layout(const void* src, int in_f32, int out_split, int64_t n, int span,

@@ -7,6 +7,7 @@
 #include <cmath>
 #include <cstdio>
 #include <algorithm>
+#include <array>
 #include <cstdlib>
 #include <cstring>
 #include <chrono>
@@ -93,6 +94,12 @@ struct vmi_ctx {
   void* d_raw = nullptr;  // vmi_set_pairs: the distinct scans as uploaded
   size_t cap_raw = 0;
   std::vector<cudaEvent_t> chunk_ev;  // vmi_set_pairs: raw-upload chunk done
+  void* d_group = nullptr;    // vmi_set_pairs: GroupPair descriptors
+  size_t cap_group = 0;
+  void* d_gavox = nullptr;    // grouped build: unsorted voxel lists
+  size_t cap_gavox = 0;
+  void* d_gcursor = nullptr;  // grouped build: per-pair bin cursors
+  size_t cap_gcursor = 0;
   cudaEvent_t set_start = nullptr;
   int* d_setv = nullptr;  // per-pair voxel counts + "left the box" flags (vmi_set_pairs)
   size_t cap_setv = 0;
@@ -557,7 +564,7 @@ int vmi_destroy(vmi_ctx* c) {
   }
   if (c->set_start) cudaEventDestroy(c->set_start);
   for (auto e : c->chunk_ev) cudaEventDestroy(e);
-  cudaFree(c->d_raw);
+  cudaFree(c->d_raw); cudaFree(c->d_group); cudaFree(c->d_gavox); cudaFree(c->d_gcursor);
   exact_free(c->ex);
   cudaFree(c->d_mats); cudaFree(c->d_mi); cudaFree(c->d_status); cudaFree(c->d_hist);
   cudaFree(c->d_total); cudaFree(c->d_best); cudaFree(c->d_best_idx); cudaFree(c->d_sums);
@@ -1256,7 +1263,127 @@ int vmi_set_pairs(vmi_ctx* c, int64_t npairs, const void* const* a, const int64_
     CK(c, grow(&l.d_avox_tmp, l.cap_avox_tmp, sizeof(int4) * (size_t)max_na));
     CK(c, cudaStreamWaitEvent(l.st, c->set_start, 0));
   }
-  // one host thread per lane enqueues its pairs (launch-bound otherwise)
+  // ---- grouped builds: up to kGroup pairs per launch sequence (the common
+  // case); pairs whose voxel box needs more than 27 bits use the lanes below
+  std::vector<char> grouped((size_t)npairs, 0);
+  if (!std::getenv("VMI_NO_GROUP")) {  // (VMI_NO_GROUP=1: lanes only, A/B and tests)
+    constexpr int kGroup = 32;
+    auto nbits_of = [&](int64_t i, uint32_t ext[3], int amin[3]) -> int {
+      const HostScan& h = hs[(size_t)ia[(size_t)i]];
+      double vol = 1.0;
+      for (int j = 0; j < 3; ++j) {
+        const int64_t lo = host_floor(h.lo[j], c->g.origin[j], c->g.res);
+        const int64_t hi = host_floor(h.hi[j], c->g.origin[j], c->g.res);
+        if (lo < -(1 << 20) || hi > (1 << 20) - 1) return -1;  // -> lanes path (reports the error)
+        amin[j] = (int)lo;
+        ext[j] = (uint32_t)(hi - lo + 1);
+        vol *= (double)ext[j];
+      }
+      int nb = 1;
+      while (nb < 40 && (double)(1ull << nb) < vol) ++nb;
+      return nb;
+    };
+    std::vector<GroupPair> gph;
+    cudaStream_t st = c->lanes[0].st;
+    for (int64_t g0 = 0; g0 < npairs;) {
+      // the next run of pairs that fit one 32-bit key space together
+      int nbits = 0;
+      int64_t g1 = g0;
+      std::vector<std::array<int, 3>> amins;
+      std::vector<std::array<uint32_t, 3>> exts;
+      while (g1 < npairs && g1 - g0 < kGroup) {
+        uint32_t e[3];
+        int am[3];
+        const int nb = nbits_of(g1, e, am);
+        if (nb < 0 || nb > 27) break;
+        const int nbn = std::max(nbits, nb);
+        int gb = 0;
+        while ((1 << gb) < (int)(g1 - g0 + 1)) ++gb;
+        if (nbn + gb > 32) break;
+        nbits = nbn;
+        amins.push_back({am[0], am[1], am[2]});
+        exts.push_back({e[0], e[1], e[2]});
+        ++g1;
+      }
+      if (g1 == g0) { ++g0; continue; }  // this pair goes the lane path
+      const int G = (int)(g1 - g0);
+      gph.assign((size_t)G, GroupPair{});
+      int64_t n_total = 0, max_na_g = 1, max_rows = 1;
+      size_t max_grid = 1;
+      for (int k = 0; k < G; ++k) {
+        const int64_t i = g0 + k;
+        PairStore& ps = c->set[(size_t)i];
+        free_a(ps);
+        ps.b_set = false;
+        ps.regrouped = false;
+        ps.hull_n = 0;
+        for (int j = 0; j < 3; ++j) {
+          ps.amin[j] = amins[(size_t)k][j];
+          ps.ext[j] = exts[(size_t)k][j];
+          ps.amax[j] = ps.amin[j] + (int)ps.ext[j] - 1;
+        }
+        ps.a_empty = false;
+        ps.grid_bytes = (size_t)ps.ext[0] * ps.ext[1] * ps.ext[2];
+        CK(c, grow(&ps.d_grid, ps.cap_grid, ps.grid_bytes));
+        CK(c, grow(&ps.d_avox, ps.cap_avox, sizeof(int4) * (size_t)na[i]));
+        if (!ps.d_bin_total) CK(c, cudaMalloc(&ps.d_bin_total, 4 * kMaxW));
+        const HostScan& h_b = hs[(size_t)ib[(size_t)i]];
+        const int as_f32 = (h_b.exact32 && !std::getenv("VMI_FORCE_F64")) ? 1 : 0;
+        double mx = 0.0;
+        for (int j = 0; j < 3; ++j) {
+          mx = std::fmax(mx, std::fmax(std::fabs(h_b.lo[j]), std::fabs(h_b.hi[j])));
+          ps.b_lo[j] = h_b.lo[j];
+          ps.b_hi[j] = h_b.hi[j];
+        }
+        ps.max_abs = mx;
+        ps.span = (int)((nb[i] + c->threads - 1) / c->threads);
+        ps.rem = (int)(nb[i] - (int64_t)(ps.span - 1) * c->threads);
+        CK(c, grow(&ps.d_pts, ps.cap_pts,
+                   (size_t)(ps.span + kStagePadRows) * c->threads * (as_f32 ? 16 : 32)));
+        ps.is_f32 = as_f32;
+        ps.nb = nb[i];
+        ps.a_npts = na[i];
+        GroupPair& q = gph[(size_t)k];
+        q.raw_a = raw + off[(size_t)ia[(size_t)i]];
+        q.raw_b = raw + off[(size_t)ib[(size_t)i]];
+        q.n = na[i];
+        q.off = n_total;
+        q.nb = nb[i];
+        q.amin = make_int3(ps.amin[0], ps.amin[1], ps.amin[2]);
+        q.ext = make_uint3(ps.ext[0], ps.ext[1], ps.ext[2]);
+        q.grid = ps.d_grid;
+        q.grid_bytes = ps.grid_bytes;
+        q.avox = ps.d_avox;
+        q.bin_total = ps.d_bin_total;
+        q.pts = ps.d_pts;
+        q.span = ps.span;
+        q.rem = ps.rem;
+        q.b_split = as_f32;
+        n_total += na[i];
+        max_na_g = std::max(max_na_g, na[i]);
+        max_rows = std::max<int64_t>(max_rows, (int64_t)ps.span * c->threads);
+        max_grid = std::max(max_grid, ps.grid_bytes);
+        grouped[(size_t)i] = 1;
+      }
+      // raw uploads this group reads
+      int64_t need = 0;
+      for (int64_t i = g0; i < g1; ++i) need = std::max(need, std::max(ia[(size_t)i], ib[(size_t)i]));
+      CK(c, cudaStreamWaitEvent(st, c->chunk_ev[(size_t)(need / kChunk)], 0));
+      CK(c, grow(&c->d_group, c->cap_group, sizeof(GroupPair) * kGroup));
+      CK(c, grow(&c->d_gavox, c->cap_gavox, sizeof(int4) * (size_t)n_total));
+      CK(c, grow(&c->d_gcursor, c->cap_gcursor, 4 * (size_t)kGroup * kMaxW));
+      CK(c, cudaMemcpyAsync(c->d_group, gph.data(), sizeof(GroupPair) * (size_t)G,
+                            cudaMemcpyHostToDevice, st));
+      CK(c, cudaMemsetAsync(d_bad + g0, 0, 4 * (size_t)G, st));
+      CK(c, build_pair_group(c->lanes[0].ex, static_cast<const GroupPair*>(c->d_group), G, n_total,
+                             (int)max_na_g, (int)max_rows, max_grid, nbits, c->g, is_rec,
+                             c->threads, static_cast<int4*>(c->d_gavox),
+                             static_cast<int*>(c->d_gcursor), d_v + g0, d_bad + g0, st,
+                             &c->launches));
+      g0 = g1;
+    }
+  }
+  // one host thread per lane enqueues its (remaining) pairs (launch-bound otherwise)
   static const bool force_f64 = std::getenv("VMI_FORCE_F64") != nullptr;
   std::vector<int> lane_rc(kBuildLanes, 0);
   std::vector<int64_t> lane_launches(kBuildLanes, 0);
@@ -1273,6 +1400,7 @@ int vmi_set_pairs(vmi_ctx* c, int64_t npairs, const void* const* a, const int64_
     if (e_ != cudaSuccess) return lfail(VMI_ERR_CUDA, std::string(#x) + ": " + cudaGetErrorString(e_)); \
   } while (0)
     for (int64_t i = li; i < npairs; i += kBuildLanes) {
+      if (grouped[(size_t)i]) continue;
       PairStore& ps = c->set[(size_t)i];
       const int64_t need = std::max(ia[(size_t)i], ib[(size_t)i]) / kChunk;
       if (need > waited) {  // chunks upload in order: the latest one suffices

@@ -122,6 +122,33 @@ cudaError_t topk_sort(const double* mi, int P, double* keys_out, int* idx_in, in
 cudaError_t voxel_order(const ExactScratch& s, const void* src, int rec, int64_t n, int* changes,
                         void* dst, cudaStream_t st);
 
+// One pair of a pair-set group (vmi_set_pairs): inputs (raw uploaded scans)
+// and outputs (A's grid / voxel list / bin totals, B's span layout).
+struct GroupPair {
+  const void* raw_a;
+  const void* raw_b;
+  int64_t n;    // scan A's points
+  int64_t off;  // their offset in the group's key array
+  int64_t nb;   // scan B's points
+  int3 amin;
+  uint3 ext;
+  uint8_t* grid;
+  size_t grid_bytes;
+  int4* avox;
+  uint32_t* bin_total;
+  void* pts;    // scan B's span layout
+  int span, rem, b_split;
+};
+// Build G pairs at once (scan A: keys (pair << nbits) | box index, one sort /
+// encode / scan / features / grid / scatter launch each; scan B: one layout
+// launch).  vcount[g] = pair g's voxel count; bad[g] set if a point left its
+// host-computed box (cannot happen).  G <= 2^(32 - nbits).
+cudaError_t build_pair_group(ExactScratch& s, const GroupPair* gp_dev, int G, int64_t n_total,
+                             int max_na, int max_nb_rows, size_t max_grid, int nbits,
+                             const GridParams& g, int in_f32, int threads, int4* avox_tmp,
+                             int* cursor, int* vcount, int* bad, cudaStream_t st,
+                             int64_t* launches);
+
 // dst[r] = src[idx[r]] (rows of w elements), or the reverse with scatter.
 template <typename T>
 cudaError_t gather_rows(const T* src, const int64_t* idx, int64_t n, int w, T* dst, bool scatter,
