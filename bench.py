@@ -645,12 +645,15 @@ def run_c5(args, world, rank, local):
         torch.cuda.synchronize()
         dt = time.perf_counter() - t0
         launches = eng.ctx.launches - launches0
+        cnt = eng.ctx.counters()
         errs = [terr(i, r.estimated_pose.as_vector()) for i, r in zip(mine, reps)]
         n_evals = sum_over_ranks(dist, cdev, float(stats["evaluations"]) * args.steps)
         extra = {"redone_exact": int(sum_over_ranks(dist, cdev, float(stats["redone_exact"]))),
                  "gpu_launches_per_step": launches / args.steps,
                  "nm_wall_s_per_step": stats["wall_time"],
                  "breakdown_s_per_step": {k: round(v, 4) for k, v in acc.items()},
+                 "nm_steps_per_step": cnt["nm_steps"] / (args.steps + max(1, args.warmup)),
+                 "nm_probes_per_step": cnt["nm_probes"] / (args.steps + max(1, args.warmup)),
                  "input": "float32 KITTI records in pinned host memory, uploaded every step"}
         eng.close()
     else:

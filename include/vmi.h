@@ -227,8 +227,9 @@ int vmi_align_pairs(vmi_ctx* ctx, int64_t K, const double* x0, const double step
 int64_t vmi_launch_count(const vmi_ctx* ctx);
 /* Counters: [0] kernel launches, [1] table re-plans (an under-estimated scan-B
    occupancy grown after > 1% of a launch overflowed), [2] poses re-run on the
-   exact path, [3] the current pair's scan-B occupancy estimate. */
-int vmi_get_counters(const vmi_ctx* ctx, int64_t out[4]);
+   exact path, [3] the current pair's scan-B occupancy estimate, [4] lockstep
+   Nelder-Mead steps, [5] poses they scored (vmi_align_pairs, cumulative). */
+int vmi_get_counters(const vmi_ctx* ctx, int64_t out[6]);
 
 /* Fast-path configuration knobs (tests/bench): table capacity (0 = sized from
    scan B's occupancy; larger than fits shared memory = clamped) and CUDA threads per CTA (0 = default = 512, one scan-B span per

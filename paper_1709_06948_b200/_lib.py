@@ -216,10 +216,10 @@ class Context:
 
     def counters(self) -> dict:
         """launches, table re-plans, exact-path poses, scan-B occupancy estimate"""
-        out = np.zeros(4, dtype=np.int64)
+        out = np.zeros(6, dtype=np.int64)
         self.check(self._L.vmi_get_counters(self._h, ptr(out, _i64)), "vmi_get_counters")
-        return dict(zip(("launches", "replans", "exact_poses", "b_voxels_estimate"),
-                        (int(x) for x in out)))
+        return dict(zip(("launches", "replans", "exact_poses", "b_voxels_estimate", "nm_steps",
+                         "nm_probes"), (int(x) for x in out)))
 
     def set_params(self, origin, res, kind: int, bins: int, clamp: float, include_phi: bool):
         o = np.ascontiguousarray(origin, dtype=np.float64)

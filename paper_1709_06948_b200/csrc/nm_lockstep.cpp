@@ -27,6 +27,7 @@
 #include <algorithm>
 #include <cmath>
 #include <cstdint>
+#include <cstdlib>
 #include <cstring>
 #include <functional>
 #include <vector>
@@ -313,8 +314,9 @@ void apply(Run& r, const NmConfig& cfg, const double* g, const uint64_t* h, bool
 
 }  // namespace
 
-int nm_lockstep(int64_t K, const double* x0, const NmConfig& cfg, const NmEvaluator& eval,
-                NmResult* out) {
+int nm_lockstep_async(int64_t K, const double* x0, const NmConfig& cfg,
+                      const NmAsyncEvaluator& ev, NmResult* out, int64_t* steps_out,
+                      int64_t* probes_out) {
   std::vector<Run> runs((size_t)K);
   for (int64_t k = 0; k < K; ++k) {
     Run& r = runs[(size_t)k];
@@ -327,39 +329,66 @@ int nm_lockstep(int64_t K, const double* x0, const NmConfig& cfg, const NmEvalua
     r.npend = V;
     r.phase = kInit;
   }
-  std::vector<double> poses;
-  std::vector<int32_t> pair;
-  std::vector<int64_t> first((size_t)K);
-  std::vector<double> g;
-  std::vector<uint64_t> h;
-  int64_t steps = 0;
-  while (true) {
-    poses.clear();
-    pair.clear();
-    for (int64_t k = 0; k < K; ++k) {
+  // runs k with k % L == l form lane l; a lane's batch is in flight while the
+  // host applies the other lanes' results (the evaluator overlaps them)
+  const int L = std::max(1, ev.lanes);
+  struct Lane {
+    std::vector<double> poses;
+    std::vector<int32_t> pair;
+    std::vector<int64_t> run, first;
+    std::vector<double> g;
+    std::vector<uint64_t> h;
+    bool pending = false;
+    bool speculate = true;
+  };
+  std::vector<Lane> lane((size_t)L);
+  int64_t active = K, steps = 0;
+  auto submit = [&](int l) -> int {
+    Lane& ln = lane[(size_t)l];
+    ln.poses.clear();
+    ln.pair.clear();
+    ln.run.clear();
+    ln.first.clear();
+    ln.speculate = 4 * active <= cfg.spec_budget;
+    for (int64_t k = l; k < K; k += L) {
       Run& r = runs[(size_t)k];
-      first[(size_t)k] = (int64_t)pair.size();
       if (r.phase == kDone) continue;
+      ln.run.push_back(k);
+      ln.first.push_back((int64_t)ln.pair.size());
       for (int i = 0; i < r.npend; ++i) {
-        poses.insert(poses.end(), r.pend[i], r.pend[i] + N);
-        pair.push_back((int32_t)k);
+        ln.poses.insert(ln.poses.end(), r.pend[i], r.pend[i] + N);
+        ln.pair.push_back((int32_t)k);
       }
     }
-    const int64_t P = (int64_t)pair.size();
-    if (P == 0) break;
-    int64_t active = 0;
-    for (int64_t k = 0; k < K; ++k) active += runs[(size_t)k].phase != kDone;
-    const bool speculate = 4 * active <= cfg.spec_budget;
-    g.assign((size_t)P, 0.0);
-    h.assign((size_t)P, 0);
-    const int rc = eval(poses.data(), pair.data(), P, g.data(), h.data());
-    if (rc) return rc;
+    const int64_t P = (int64_t)ln.pair.size();
+    ln.pending = P > 0;
+    if (!ln.pending) return 0;
     ++steps;
-    for (int64_t k = 0; k < K; ++k) {
-      Run& r = runs[(size_t)k];
-      if (r.phase == kDone) continue;
-      const size_t f = (size_t)first[(size_t)k];
-      apply(r, cfg, g.data() + f, h.data() + f, speculate);
+    if (probes_out) *probes_out += P;
+    ln.g.assign((size_t)P, 0.0);
+    ln.h.assign((size_t)P, 0);
+    return ev.submit(l, ln.poses.data(), ln.pair.data(), P);
+  };
+  for (int l = 0; l < L; ++l) {
+    const int rc = submit(l);
+    if (rc) return rc;
+  }
+  bool any = true;
+  while (any) {
+    any = false;
+    for (int l = 0; l < L; ++l) {
+      Lane& ln = lane[(size_t)l];
+      if (!ln.pending) continue;
+      int rc = ev.wait(l, ln.g.data(), ln.h.data());
+      if (rc) return rc;
+      for (size_t q = 0; q < ln.run.size(); ++q) {
+        Run& r = runs[(size_t)ln.run[q]];
+        const size_t f = (size_t)ln.first[q];
+        apply(r, cfg, ln.g.data() + f, ln.h.data() + f, ln.speculate);
+        if (r.phase == kDone) --active;
+      }
+      if ((rc = submit(l))) return rc;
+      any |= ln.pending;
     }
   }
   for (int64_t k = 0; k < K; ++k) {
@@ -376,8 +405,26 @@ int nm_lockstep(int64_t K, const double* x0, const NmConfig& cfg, const NmEvalua
     o.trace = r.trace;
     o.trace_spread = r.spread;
   }
-  (void)steps;
+  if (steps_out) *steps_out += steps;
   return 0;
+}
+
+int nm_lockstep(int64_t K, const double* x0, const NmConfig& cfg, const NmEvaluator& eval,
+                NmResult* out, int64_t* steps_out, int64_t* probes_out) {
+  // one lane, evaluated on wait()
+  const double* sp = nullptr;
+  const int32_t* sr = nullptr;
+  int64_t sn = 0;
+  NmAsyncEvaluator ev;
+  ev.lanes = 1;
+  ev.submit = [&](int, const double* p, const int32_t* r, int64_t n) {
+    sp = p;
+    sr = r;
+    sn = n;
+    return 0;
+  };
+  ev.wait = [&](int, double* g, uint64_t* h) { return eval(sp, sr, sn, g, h); };
+  return nm_lockstep_async(K, x0, cfg, ev, out, steps_out, probes_out);
 }
 
 }  // namespace vmi
@@ -401,10 +448,27 @@ extern "C" int vmi_nm_run(int64_t K, const double* x0, const double steps[6], in
   cfg.restarts = restarts;
   cfg.spec_budget = spec_budget < 0 ? INT64_MAX : spec_budget;
   std::vector<vmi::NmResult> res((size_t)K);
-  vmi::NmEvaluator ev = [&](const double* p, const int32_t* pr, int64_t n, double* g, uint64_t* h) {
-    return fn(user, p, pr, n, g, h);
+  // VMI_NM_LANES (tests): deal the runs to that many lanes, as the GPU driver
+  // does (vmi_align_pairs); the callback runs when a lane is waited for
+  const char* le = std::getenv("VMI_NM_LANES");
+  const int lanes = le ? std::max(1, std::atoi(le)) : 1;
+  struct Pend {
+    const double* p = nullptr;
+    const int32_t* r = nullptr;
+    int64_t n = 0;
   };
-  int rc = vmi::nm_lockstep(K, x0, cfg, ev, res.data());
+  std::vector<Pend> pend((size_t)lanes);
+  vmi::NmAsyncEvaluator ev;
+  ev.lanes = lanes;
+  ev.submit = [&](int l, const double* p, const int32_t* r, int64_t n) {
+    pend[(size_t)l] = {p, r, n};
+    return 0;
+  };
+  ev.wait = [&](int l, double* g, uint64_t* h) {
+    const Pend& q = pend[(size_t)l];
+    return fn(user, q.p, q.r, q.n, g, h);
+  };
+  int rc = vmi::nm_lockstep_async(K, x0, cfg, ev, res.data());
   if (rc) return rc;
   return vmi::nm_write_results(res.data(), K, best_x, best_value, iterations, termination,
                                n_evaluations, uncertain, trace, trace_len, trace_cap);

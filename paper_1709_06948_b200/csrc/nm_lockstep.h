@@ -38,8 +38,22 @@ struct NmResult {
 using NmEvaluator =
     std::function<int(const double* poses, const int32_t* run, int64_t n, double* g, uint64_t* h)>;
 
+// The same evaluator split in two so batches can be in flight while the host
+// works: runs are dealt to `lanes` lanes (run k -> lane k % lanes); submit(l,
+// ...) starts lane l's batch, wait(l, g, h) finishes it (g, h sized as that
+// batch).  Decisions are unchanged: every run only ever sees its own values.
+struct NmAsyncEvaluator {
+  int lanes = 1;
+  std::function<int(int lane, const double* poses, const int32_t* run, int64_t n)> submit;
+  std::function<int(int lane, double* g, uint64_t* h)> wait;
+};
+int nm_lockstep_async(int64_t K, const double* x0, const NmConfig& cfg,
+                      const NmAsyncEvaluator& ev, NmResult* out, int64_t* steps = nullptr,
+                      int64_t* probes = nullptr);
+
+// steps / probes (nullable): evaluator calls and poses evaluated
 int nm_lockstep(int64_t K, const double* x0, const NmConfig& cfg, const NmEvaluator& eval,
-                NmResult* out);
+                NmResult* out, int64_t* steps = nullptr, int64_t* probes = nullptr);
 
 int nm_write_results(const NmResult* res, int64_t K, double* best_x, double* best_value,
                      int32_t* iterations, int32_t* termination, int32_t* n_evaluations,

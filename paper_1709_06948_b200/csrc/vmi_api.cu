@@ -73,6 +73,29 @@ struct BuildLane {
 };
 constexpr int kBuildLanes = 4;
 
+// Device buffers of one multi-pair evaluation (matrices + pair index in,
+// MI / status / histogram identity / total out).
+struct PairBufs {
+  const double* mats;
+  const int32_t* pose_pair;
+  double* mi;
+  int32_t* status;
+  unsigned long long* hash;
+  long long* total;
+};
+
+// One lane of the lockstep optimiser's evaluations (vmi_align_pairs): device
+// buffers (matrices, MI, identities, totals, statuses, pair indices) and
+// pinned host buffers (matrices, then MI / identities / statuses read back).
+struct NmSlot {
+  void* d_buf = nullptr;
+  void* h_buf = nullptr;
+  int64_t cap = 0, n = 0;
+  cudaEvent_t ev = nullptr;
+  const int32_t* run = nullptr;  // the lane's pair indices (host), valid until wait
+  PairBufs bufs{};
+};
+
 struct vmi_ctx {
   int device = 0;
   int sm_count = 0;
@@ -155,6 +178,8 @@ struct vmi_ctx {
   size_t cap_fix_hist = 0;
   int64_t replans = 0;       // times an under-estimated table plan was grown
   int64_t exact_poses = 0;   // poses re-run on the exact path
+  int64_t nm_steps = 0, nm_probes = 0;  // vmi_align_pairs: lockstep steps, poses scored
+  NmSlot nm_slot[2];
 };
 
 namespace {
@@ -563,6 +588,11 @@ int vmi_destroy(vmi_ctx* c) {
     if (l.st) cudaStreamDestroy(l.st);
   }
   if (c->set_start) cudaEventDestroy(c->set_start);
+  for (auto& sl : c->nm_slot) {
+    cudaFree(sl.d_buf);
+    if (sl.h_buf) cudaFreeHost(sl.h_buf);
+    if (sl.ev) cudaEventDestroy(sl.ev);
+  }
   for (auto e : c->chunk_ev) cudaEventDestroy(e);
   cudaFree(c->d_raw); cudaFree(c->d_group); cudaFree(c->d_gavox); cudaFree(c->d_gcursor);
   exact_free(c->ex);
@@ -581,12 +611,14 @@ const char* vmi_last_error(const vmi_ctx* c) { return c ? c->err.c_str() : "null
 
 int64_t vmi_launch_count(const vmi_ctx* c) { return c ? c->launches : 0; }
 
-int vmi_get_counters(const vmi_ctx* c, int64_t out[4]) {
+int vmi_get_counters(const vmi_ctx* c, int64_t out[6]) {
   if (!c || !out) return VMI_ERR_ARG;
   out[0] = c->launches;
   out[1] = c->replans;
   out[2] = c->exact_poses;
   out[3] = c->cur.b_voxels;
+  out[4] = c->nm_steps;
+  out[5] = c->nm_probes;
   return 0;
 }
 
@@ -1521,8 +1553,11 @@ namespace {
 // one multi-pair launch (single-pass table sized for the set's largest scan B;
 // per-pair launches when some pair needs the multi-pass layout), then the
 // exact path for flagged poses.
-int eval_pairs_device(vmi_ctx* c, int64_t P, const int32_t* pair_host, long long* hist) {
+int eval_pairs_device(vmi_ctx* c, int64_t P, const int32_t* pair_host, long long* hist,
+                      const PairBufs* bufs = nullptr) {
   if (P <= 0) return 0;
+  const PairBufs def{c->d_mats, c->d_pose_pair, c->d_mi, c->d_status, c->d_hash, c->d_total};
+  const PairBufs& bf = bufs ? *bufs : def;
   int64_t bvox = 0;
   int any_f64 = 0;
   for (int64_t i = 0; i < c->n_set; ++i) {
@@ -1532,16 +1567,16 @@ int eval_pairs_device(vmi_ctx* c, int64_t P, const int32_t* pair_host, long long
   FastLaunch fl{};
   fl.g = c->g;
   fl.g.kind = kernel_kind(c);
-  fl.mats = c->d_mats;
+  fl.mats = bf.mats;
   fl.P = P;
   fl.grid = (int)(P < c->sm_count ? P : c->sm_count);
   fl.streams = c->streams;
   plan_table(c, fl.g.kind, bvox, any_f64 ? 0 : 1, &fl.cap, &fl.npass, &fl.multi);
-  fl.mi = c->d_mi;
-  fl.status = c->d_status;
+  fl.mi = bf.mi;
+  fl.status = bf.status;
   fl.hist = hist;
-  fl.total = c->d_total;
-  fl.hash = c->d_hash;
+  fl.total = bf.total;
+  fl.hash = bf.hash;
   bool mixed = false;  // the kernel's record format is per launch
   for (int64_t i = 1; i < c->n_set; ++i) mixed |= c->set[(size_t)i].is_f32 != c->set[0].is_f32;
   if (!fl.multi && !mixed) {
@@ -1549,7 +1584,7 @@ int eval_pairs_device(vmi_ctx* c, int64_t P, const int32_t* pair_host, long long
     if (rc) return rc;
     fl.sums = c->d_sums;
     fl.pairs = c->d_pairs;
-    fl.pose_pair = c->d_pose_pair;
+    fl.pose_pair = bf.pose_pair;
     fl.A = ref_view(c->set[0]);  // (unused by the multi-pair kernel)
     fl.B = query_view(c, c->set[0]);
     CK(c, launch_fast(fl, c->stream));
@@ -1653,33 +1688,84 @@ int vmi_align_pairs(vmi_ctx* c, int64_t K, const double* x0, const double steps[
   // below ~two poses per SM a launch costs the same for 1 or 4 probes per run
   cfg.spec_budget = 2 * (int64_t)c->sm_count;
   cudaSetDevice(c->device);
-  std::vector<double> mi;
-  std::vector<int32_t> st;
-  NmEvaluator ev = [&](const double* poses, const int32_t* run, int64_t n, double* g, uint64_t* h) {
-    int rc = upload_pair_poses(c, poses, run, n, false);
+  // Two lanes of runs alternate on the context stream: lane l's batch
+  // (matrices built on the host into pinned memory, upload, one multi-pair
+  // launch, read-back of values / statuses / identities) is queued while the
+  // host applies the other lane's results, so the GPU rarely waits for the
+  // host.  Flagged poses (table overflow, VARZ bin edges) are re-run exactly
+  // and read again before the lane's results are used.
+  NmAsyncEvaluator ev;
+  ev.lanes = 2;
+  ev.submit = [&](int l, const double* poses, const int32_t* run, int64_t n) -> int {
+    NmSlot& sl = c->nm_slot[l];
+    if (n > sl.cap) {
+      cudaFree(sl.d_buf);
+      if (sl.h_buf) cudaFreeHost(sl.h_buf);
+      sl.d_buf = nullptr;
+      sl.h_buf = nullptr;
+      sl.cap = 0;
+      CK(c, cudaMalloc(&sl.d_buf, (size_t)n * 128));
+      CK(c, cudaMallocHost(&sl.h_buf, (size_t)n * 116));
+      if (!sl.ev) CK(c, cudaEventCreateWithFlags(&sl.ev, cudaEventDisableTiming));
+      sl.cap = n;
+    }
+    char* d = static_cast<char*>(sl.d_buf);
+    char* hb = static_cast<char*>(sl.h_buf);
+    const size_t cp = (size_t)sl.cap;
+    PairBufs bf{reinterpret_cast<double*>(d), reinterpret_cast<int32_t*>(d + cp * 124),
+                reinterpret_cast<double*>(d + cp * 96),
+                reinterpret_cast<int32_t*>(d + cp * 120),
+                reinterpret_cast<unsigned long long*>(d + cp * 104),
+                reinterpret_cast<long long*>(d + cp * 112)};
+    double* h_mats = reinterpret_cast<double*>(hb);
+    for (int64_t p = 0; p < n; ++p)
+      if (run[p] < 0 || run[p] >= c->n_set) return fail(c, VMI_ERR_ARG, "pair index out of range");
+    if (vmi_poses_to_mats(poses, n, h_mats, 1)) return fail(c, VMI_ERR_ARG, "poses_to_mats");
+    CK(c, cudaMemcpyAsync(const_cast<double*>(bf.mats), h_mats, (size_t)n * 96,
+                          cudaMemcpyHostToDevice, c->stream));
+    CK(c, cudaMemcpyAsync(const_cast<int32_t*>(bf.pose_pair), run, (size_t)n * 4,
+                          cudaMemcpyHostToDevice, c->stream));
+    int rc = eval_pairs_device(c, n, run, nullptr, &bf);
     if (rc) return rc;
-    if ((rc = eval_pairs_device(c, n, run, nullptr))) return rc;
-    mi.resize((size_t)n);
-    st.resize((size_t)n);
-    // one round trip: values, statuses and identities together; the rare
-    // flagged pose is re-run exactly and read again
-    CK(c, cudaMemcpyAsync(mi.data(), c->d_mi, n * 8, cudaMemcpyDeviceToHost, c->stream));
-    CK(c, cudaMemcpyAsync(st.data(), c->d_status, n * 4, cudaMemcpyDeviceToHost, c->stream));
-    CK(c, cudaMemcpyAsync(h, c->d_hash, n * 8, cudaMemcpyDeviceToHost, c->stream));
-    CK(c, cudaStreamSynchronize(c->stream));
+    CK(c, cudaMemcpyAsync(hb + cp * 96, bf.mi, (size_t)n * 8, cudaMemcpyDeviceToHost, c->stream));
+    CK(c, cudaMemcpyAsync(hb + cp * 104, bf.hash, (size_t)n * 8, cudaMemcpyDeviceToHost,
+                          c->stream));
+    CK(c, cudaMemcpyAsync(hb + cp * 112, bf.status, (size_t)n * 4, cudaMemcpyDeviceToHost,
+                          c->stream));
+    CK(c, cudaEventRecord(sl.ev, c->stream));
+    sl.n = n;
+    sl.run = run;
+    sl.bufs = bf;
+    return 0;
+  };
+  ev.wait = [&](int l, double* g, uint64_t* h) -> int {
+    NmSlot& sl = c->nm_slot[l];
+    CK(c, cudaEventSynchronize(sl.ev));
+    char* hb = static_cast<char*>(sl.h_buf);
+    const size_t cp = (size_t)sl.cap;
+    const double* mi = reinterpret_cast<const double*>(hb + cp * 96);
+    const uint64_t* hh = reinterpret_cast<const uint64_t*>(hb + cp * 104);
+    const int32_t* st = reinterpret_cast<const int32_t*>(hb + cp * 112);
     int64_t nf = 0;
-    for (int64_t i = 0; i < n; ++i) nf += (st[(size_t)i] & VMI_FLAG_RECHECK) != 0;
-    if (nf) {
-      if ((rc = fix_pairs(c, n, run, nullptr, st.data(), nullptr))) return rc;
-      CK(c, cudaMemcpyAsync(mi.data(), c->d_mi, n * 8, cudaMemcpyDeviceToHost, c->stream));
-      CK(c, cudaMemcpyAsync(h, c->d_hash, n * 8, cudaMemcpyDeviceToHost, c->stream));
+    for (int64_t i = 0; i < sl.n; ++i) nf += (st[i] & VMI_FLAG_RECHECK) != 0;
+    if (nf) {  // rare: exact path on the same stream, then read this lane again
+      int rc = do_fixups(c, sl.bufs.mats, sl.n, sl.bufs.mi, sl.bufs.status, nullptr, nullptr,
+                         c->stream, nullptr, sl.run, st, sl.bufs.hash);
+      if (rc) return rc;
+      CK(c, cudaMemcpyAsync(hb + cp * 96, sl.bufs.mi, (size_t)sl.n * 8, cudaMemcpyDeviceToHost,
+                            c->stream));
+      CK(c, cudaMemcpyAsync(hb + cp * 104, sl.bufs.hash, (size_t)sl.n * 8,
+                            cudaMemcpyDeviceToHost, c->stream));
       CK(c, cudaStreamSynchronize(c->stream));
     }
-    for (int64_t i = 0; i < n; ++i) g[i] = -mi[(size_t)i];  // sentinel -> +1e300
+    for (int64_t i = 0; i < sl.n; ++i) {
+      g[i] = -mi[i];  // sentinel -> +1e300
+      h[i] = hh[i];
+    }
     return 0;
   };
   std::vector<NmResult> res((size_t)K);
-  int rc = nm_lockstep(K, x0, cfg, ev, res.data());
+  int rc = nm_lockstep_async(K, x0, cfg, ev, res.data(), &c->nm_steps, &c->nm_probes);
   if (rc) return rc;
   return nm_write_results(res.data(), K, best_x, best_value, iterations, termination,
                           n_evaluations, uncertain, trace, trace_len, trace_cap);

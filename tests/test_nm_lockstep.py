@@ -49,11 +49,14 @@ def test_lockstep_matches_reference_optimizer(tag, spec):
     np.testing.assert_array_equal(o["trace"][0, :n], g[f"{tag}_trace"])
 
 
+@pytest.mark.parametrize("lanes", ["1", "3"])
 @pytest.mark.parametrize("spec", [-1, 0, 12])
-def test_many_runs_in_lockstep_equal_single_runs(spec):
+def test_many_runs_in_lockstep_equal_single_runs(spec, lanes, monkeypatch):
     """K runs from different starts advance together (different iteration
     counts, restarts; spec 12 switches between one-probe and four-probe
-    iterations as runs finish): each equals the one-run optimizer exactly."""
+    iterations as runs finish; 3 lanes deal the runs to interleaved batches as
+    the GPU driver does): each equals the one-run optimizer exactly."""
+    monkeypatch.setenv("VMI_NM_LANES", lanes)
     rng = np.random.default_rng(4)
     x0 = rng.normal(size=(9, 6)) * np.array([2, 2, 0.5, 0.1, 0.1, 0.3])
     cfg = SimplexConfig(initial_steps=(1.0, 1.0, 0.5, 0.05, 0.05, 0.2), max_iterations=120,
