@@ -527,6 +527,10 @@ __global__ void __launch_bounds__(THREADS, 1)
       uint32_t cur = kNoVoxel, cn = 0u;
       double cs1 = 0.0, cs2 = 0.0;
       uint32_t qh = 0, qt = 0;  // warp-uniform queue head / tail, in bytes
+      // occupancy kind: cells counted at insert time (no table walk) unless a
+      // feature dump wants the walk
+      const bool occ_insert = KIND == kKindOcc && !dump.keys;
+      uint32_t occ_miss = 0, occ_hit = 0;
 
       // one queued record per lane -> table.  The first probe (a hit, or the
       // insert into an empty home slot: most records) is one straight-line CAS,
@@ -542,11 +546,22 @@ __global__ void __launch_bounds__(THREADS, 1)
           r0 = ld_shared_v2(a);
         }
         uint32_t sl = slot_of(r0.x, ucap);
+        // occupancy: A's bin at this voxel, loaded ahead (its latency overlaps
+        // the CAS); a voxel's cell is counted when its key is first inserted
+        const int ba_occ = (KIND == kKindOcc && occ_insert && has) ? (int)__ldg(&A.grid[r0.x]) : 0;
+        auto count_new = [&]() {
+          if (KIND == kKindOcc && occ_insert) {
+            if (ba_occ == 0) ++occ_miss;
+            else if (ba_occ == g.occ_bin) ++occ_hit;
+            else atomicAdd(&hist[ba_occ * W + g.occ_bin], 1u);  // (injected A features)
+          }
+        };
         // first probe = one CAS (hit or insert), no branch before the atomics;
         // shared-window addresses (key_sa / cnt_sa) avoid generic -> shared
         // conversions in this loop
         const uint32_t old0 = has ? atom_cas_shared(key_sa + 4u * sl, kEmpty32, r0.x) : 0u;
         const bool done = has && (old0 == kEmpty32 || old0 == r0.x);
+        if (KIND == kKindOcc && has && old0 == kEmpty32) count_new();
         auto add = [&](uint32_t slot) {
           if (KIND == 0) {
             const uint4 r1 = ld_shared_v4(a + 16);
@@ -569,6 +584,7 @@ __global__ void __launch_bounds__(THREADS, 1)
             if (w == r0.x) { add(sl); break; }
             if (w == kEmpty32) {
               const uint32_t old = atom_cas_shared(key_sa + 4u * sl, kEmpty32, r0.x);
+              if (old == kEmpty32) count_new();
               if (old == kEmpty32 || old == r0.x) { add(sl); break; }
             }
           }
@@ -889,7 +905,18 @@ __global__ void __launch_bounds__(THREADS, 1)
         }
       };
       VMI_TR("walk start", status)
-      if constexpr (KIND == 0) {
+      if (KIND == kKindOcc && occ_insert) {
+        // the cells were counted at insert time: add them up and reset the keys
+        occ_miss = __reduce_add_sync(0xffffffffu, occ_miss);
+        occ_hit = __reduce_add_sync(0xffffffffu, occ_hit);
+        if (lane == 0) {
+          if (occ_miss) atomicAdd(&hist[g.occ_bin], occ_miss);
+          if (occ_hit) atomicAdd(&hist[g.occ_bin * W + g.occ_bin], occ_hit);
+        }
+        uint4* t4 = reinterpret_cast<uint4*>(smem + L.table);
+        const uint4 ones = make_uint4(~0u, ~0u, ~0u, ~0u);
+        for (int i = tid; i < cap / 4; i += THREADS) t4[i] = ones;
+      } else if constexpr (KIND == 0) {
         // VARZ: each warp owns a contiguous slice of the table; it compacts the
         // occupied slots (ballot) into a ring in its share of the (idle)
         // staging buffer, then takes them four per lane, so a lane's A-grid and
@@ -953,7 +980,6 @@ __global__ void __launch_bounds__(THREADS, 1)
       } else {
         // COUNT / occupancy: four slots per thread per step, four A-grid loads
         // in flight (no L2 sums to fetch: compaction measured slower here)
-        uint32_t occ_miss = 0, occ_hit = 0;
         for (int s0 = tid; s0 < cap; s0 += 4 * THREADS) {
           uint32_t lin[4];
           int ba[4];
