@@ -49,10 +49,10 @@ __device__ __forceinline__ uint32_t slot_of(uint32_t lin, uint32_t cap) {
 // (large grids): shared memory goes to the table instead (more capacity =
 // fewer passes), so one point per push and a 4-record ring.
 // VARZ walk: compaction ring entries (loads in flight per lane = ring / 64).
-// A/B: single-pass C2 512 -> 28.87 ms, 256 -> 28.97, 128 -> 29.34; multi-layout
+// A/B (round 1): single-pass C2 512 -> 28.87 ms, 256 -> 28.97, 128 -> 29.34; multi-layout
 // C4 128 -> 87.3 ms, 256 -> 91.9, 512 -> 97.2.
 #ifndef VMI_WALK_RING
-#define VMI_WALK_RING 512
+#define VMI_WALK_RING 256  // round 2 A/B (C2): 256 -> 27.80 ms, 512 -> 28.56 (was best in round 1)
 #endif
 #ifndef VMI_WALK_RING_M
 #define VMI_WALK_RING_M 128
@@ -78,9 +78,15 @@ __device__ __forceinline__ uint32_t slot_of(uint32_t lin, uint32_t cap) {
 #ifndef VMI_STAGES64
 #define VMI_STAGES64 2  // double records: a small ring leaves room for the table (A/B: C1)
 #endif
-template <bool F32, bool MULTI = false>
+// occupancy kind (4-byte keys, no counts / sums): a 3-deep ring (one push group
+// in flight) -- the shared memory goes to a bigger key table (fewer probes).
+// A/B (C4): 3 stages 45.8 ms, 6 stages 49.3; C2 (VARZ) keeps 6: 27.8 vs 28.2.
+#ifndef VMI_STAGES_OCC
+#define VMI_STAGES_OCC 3
+#endif
+template <bool F32, bool MULTI = false, int KIND = 0>
 __host__ __device__ constexpr int kStages() {
-  return MULTI ? VMI_STAGESM : (F32 ? VMI_STAGES : VMI_STAGES64);
+  return MULTI ? VMI_STAGESM : (F32 ? (KIND == 2 ? VMI_STAGES_OCC : VMI_STAGES) : VMI_STAGES64);
 }
 template <typename Rec>
 __device__ __forceinline__ void cp_async_rec(uint32_t dst, const Rec* src) {
@@ -186,7 +192,9 @@ __host__ __device__ inline FastSmem fast_layout(int kind, int cap, int W, int th
   FastSmem L;
   size_t off = 0;
   L.stage = off;
-  const int stages = multi ? kStages<true, true>() : (f32 ? kStages<true>() : kStages<false>());
+  const int stages = multi ? kStages<true, true>()
+                           : (f32 ? (kind == 2 ? kStages<true, false, 2>() : kStages<true>())
+                                  : kStages<false>());
   off += (size_t)threads * ns * (f32 ? 16 : 32) * stages;
   L.table = off;
   off += (size_t)cap * slot_bytes(kind, multi);
@@ -727,7 +735,7 @@ __global__ void __launch_bounds__(THREADS, 1)
       // commit group from a running pointer; the span layout is padded with
       // kStagePadRows rows, so rows past the span are issued unconditionally
       // (and never read back).
-      constexpr int S = kStages<F32, MULTI>();
+      constexpr int S = kStages<F32, MULTI, KIND>();
       // (opaque: otherwise rebuilt from the CTA's shared window base, an
       // S2UR SR_CgaCtaId round trip, before every group)
       const uint32_t my_stage = pin_u32(stage_base + (uint32_t)tid * (uint32_t)sizeof(Rec));
@@ -926,10 +934,10 @@ __global__ void __launch_bounds__(THREADS, 1)
         constexpr int NW = THREADS / 32;
         constexpr int kWR = MULTI ? VMI_WALK_RING_M : VMI_WALK_RING;  // ring entries; kWU ballots per scan step / entries per lane
         constexpr int kWU = kWR / 64;
-        static_assert(kStages<F32, MULTI>() * NS * (F32 ? 16 : 32) * 32 >= kWR * 4,
+        static_assert(kStages<F32, MULTI, KIND>() * NS * (F32 ? 16 : 32) * 32 >= kWR * 4,
                       "walk ring fits the warp's staging slice");
         uint32_t* wl = reinterpret_cast<uint32_t*>(
-            smem + L.stage + (size_t)wid * 32 * NS * (F32 ? 16 : 32) * kStages<F32, MULTI>());
+            smem + L.stage + (size_t)wid * 32 * NS * (F32 ? 16 : 32) * kStages<F32, MULTI, KIND>());
         const int per = ((cap + NW - 1) / NW + 31) & ~31;
         const int se = min(cap, wid * per + per);
         int scan = wid * per;
