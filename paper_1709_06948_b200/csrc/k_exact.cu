@@ -531,6 +531,52 @@ cudaError_t voxel_order(const ExactScratch& s, const void* src, int rec, int64_t
   return cudaGetLastError();
 }
 
+// ---- summed-volume tables of scan A per present bin (RefView.sat) -------------
+__global__ void k_sat_fill(const int4* avox, int n, const int* bin_slot, uint3 ext, uint32_t* sat) {
+  const int v = blockIdx.x * blockDim.x + threadIdx.x;
+  if (v >= n) return;
+  const int4 a = avox[v];
+  const int k = bin_slot[a.w];
+  if (k < 0) return;
+  const size_t sy = ext.z + 1, sx = (size_t)(ext.y + 1) * sy, vol = sx * (ext.x + 1);
+  sat[(size_t)k * vol + (a.x + 1) * sx + (a.y + 1) * sy + (a.z + 1)] = 1u;
+}
+// inclusive prefix along one axis: lines = every (k, other two coordinates)
+__global__ void k_sat_scan(uint32_t* sat, int nb, uint3 ext, int axis) {
+  const size_t sy = ext.z + 1, sx = (size_t)(ext.y + 1) * sy, vol = sx * (ext.x + 1);
+  const size_t n1 = ext.x + 1, n2 = ext.y + 1, n3 = ext.z + 1;
+  const size_t len = axis == 0 ? n1 : axis == 1 ? n2 : n3;
+  const size_t stride = axis == 0 ? sx : axis == 1 ? sy : 1;
+  const size_t lines_per = vol / len;
+  const size_t line = (size_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (line >= lines_per * (size_t)nb) return;
+  const size_t k = line / lines_per, r = line - k * lines_per;
+  size_t base;
+  if (axis == 2) base = r * n3;                           // r = x * n2 + y
+  else if (axis == 1) base = (r / n3) * sx + (r % n3);    // r = x * n3 + z
+  else base = r;                                          // r = y * n3 + z
+  uint32_t* t = sat + k * vol + base;
+  uint32_t acc = 0;
+  for (size_t i = 0; i < len; ++i) {
+    acc += t[i * stride];
+    t[i * stride] = acc;
+  }
+}
+cudaError_t build_sat(const int4* avox, int n, const int* bin_slot_dev, int nb, const uint32_t ext[3],
+                      uint32_t* sat, cudaStream_t st) {
+  const uint3 e = make_uint3(ext[0], ext[1], ext[2]);
+  const size_t vol = (size_t)(e.x + 1) * (e.y + 1) * (e.z + 1);
+  VMI_TRY(cudaMemsetAsync(sat, 0, vol * nb * 4, st));
+  const int T = 256;
+  if (n > 0) k_sat_fill<<<(n + T - 1) / T, T, 0, st>>>(avox, n, bin_slot_dev, e, sat);
+  const size_t lens[3] = {e.x + 1, e.y + 1, e.z + 1};
+  for (int axis = 2; axis >= 0; --axis) {
+    const size_t lines = vol / lens[axis] * nb;
+    k_sat_scan<<<(unsigned)((lines + T - 1) / T), T, 0, st>>>(sat, nb, e, axis);
+  }
+  return cudaGetLastError();
+}
+
 // ---- re-planned re-runs of flagged poses (vmi_api.cu do_fixups) ----------------
 template <typename T>
 __global__ void k_gather_rows(const T* src, const int64_t* idx, int64_t n, int w, T* dst) {

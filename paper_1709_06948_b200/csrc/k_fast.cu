@@ -1051,6 +1051,20 @@ __global__ void __launch_bounds__(THREADS, 1)
 #endif
     if (cover_all) {
       for (int i = tid; i < W; i += THREADS) marg[i] = A.bin_total[i];
+    } else if (A.sat) {
+      // inclusion-exclusion on the summed-volume table of each present bin
+      const uint32_t x0 = rlo[0] - A.amin[0], y0 = rlo[1] - A.amin[1], z0 = rlo[2] - A.amin[2];
+      const uint32_t x1 = rhi[0] - A.amin[0] + 1, y1 = rhi[1] - A.amin[1] + 1,
+                     z1 = rhi[2] - A.amin[2] + 1;
+      const size_t sy = A.ext[2] + 1, sx = (size_t)(A.ext[1] + 1) * sy;
+      const size_t vol = sx * (A.ext[0] + 1);
+      for (int k = tid; k < A.sat_nb; k += THREADS) {
+        const uint32_t* t = A.sat + (size_t)k * vol;
+        auto at = [&](uint32_t x, uint32_t y, uint32_t z) { return __ldg(&t[x * sx + y * sy + z]); };
+        const uint32_t c = at(x1, y1, z1) - at(x0, y1, z1) - at(x1, y0, z1) - at(x1, y1, z0) +
+                           at(x0, y0, z1) + at(x0, y1, z0) + at(x1, y0, z0) - at(x0, y0, z0);
+        marg[A.sat_bin[k]] = c;
+      }
     } else {
       const int lo0 = rlo[0] - A.amin[0], lo1 = rlo[1] - A.amin[1], lo2 = rlo[2] - A.amin[2];
       const int hi0 = rhi[0] - A.amin[0], hi1 = rhi[1] - A.amin[1], hi2 = rhi[2] - A.amin[2];

@@ -56,6 +56,10 @@ struct PairStore {
   double* d_hull = nullptr;  // scan B's convex-hull vertices (vmi_set_query_hull), or none
   size_t cap_hull = 0;
   int hull_n = 0;
+  uint32_t* d_sat = nullptr;     // summed-volume tables of A per present bin, or none
+  size_t cap_sat = 0;
+  int* d_sat_bin = nullptr;      // [kMaxW] present bins, then [kMaxW] bin -> table
+  int sat_nb = 0;
   bool regrouped = false;        // d_pts in voxel-grouped order, d_pts_exact in input order
   void* d_pts_exact = nullptr;
   size_t cap_pts_exact = 0;
@@ -203,11 +207,12 @@ int cuda_fail(vmi_ctx* c, cudaError_t e, const char* where) {
 // re-sets scan A every pair); only the bookkeeping is reset here.
 void free_a(PairStore& ps) {
   ps.a_set = false; ps.n_avox = 0; ps.a_nvox = 0; ps.grid_bytes = 0; ps.a_npts = 0;
+  ps.sat_nb = 0;
 }
 
 void release_pair(PairStore& ps) {
   cudaFree(ps.d_grid); cudaFree(ps.d_avox); cudaFree(ps.d_bin_total); cudaFree(ps.d_pts);
-  cudaFree(ps.d_hull); cudaFree(ps.d_pts_exact);
+  cudaFree(ps.d_hull); cudaFree(ps.d_pts_exact); cudaFree(ps.d_sat); cudaFree(ps.d_sat_bin);
   ps = PairStore{};
 }
 
@@ -238,6 +243,9 @@ RefView ref_view(const PairStore& ps) {
   A.n_avox = ps.n_avox;
   A.empty = ps.a_empty ? 1 : 0;
   A.bin_total = ps.d_bin_total;
+  A.sat = ps.sat_nb > 0 ? ps.d_sat : nullptr;
+  A.sat_bin = ps.d_sat_bin;
+  A.sat_nb = ps.sat_nb;
   return A;
 }
 
@@ -372,6 +380,27 @@ int finish_reference(vmi_ctx* c, PairStore& ps, const int64_t bounds[6], int64_t
   int64_t s = 0;
   for (int b = 0; b < kMaxW; ++b) s += tot[b];
   ps.n_avox = (int)s;
+  // summed-volume tables for the per-pose A marginal (when they fit a budget)
+  ps.sat_nb = 0;
+  int slot[2 * kMaxW];
+  int nbp = 0;
+  for (int b = 0; b < kMaxW; ++b) {
+    slot[kMaxW + b] = tot[b] ? nbp : -1;
+    if (tot[b]) slot[nbp++] = b;
+  }
+  const double cells = (double)(ps.ext[0] + 1) * (ps.ext[1] + 1) * (ps.ext[2] + 1);
+  const char* sat_env = std::getenv("VMI_SAT_MB");  // table budget per pair; 0 disables
+  const double budget = (sat_env ? std::atof(sat_env) : 512.0) * 1048576.0;
+  if (nbp > 0 && cells * nbp * 4.0 <= budget && cells < 2147483647.0) {
+    CK(c, grow(&ps.d_sat, ps.cap_sat, (size_t)(cells * nbp * 4.0)));
+    if (!ps.d_sat_bin) CK(c, cudaMalloc(&ps.d_sat_bin, sizeof(int) * 2 * kMaxW));
+    CK(c, cudaMemcpyAsync(ps.d_sat_bin, slot, sizeof(int) * 2 * kMaxW, cudaMemcpyHostToDevice,
+                          c->stream));
+    CK(c, build_sat(ps.d_avox, ps.n_avox, ps.d_sat_bin + kMaxW, nbp, ps.ext, ps.d_sat, c->stream));
+    CK(c, cudaStreamSynchronize(c->stream));
+    ps.sat_nb = nbp;
+    c->launches += 4;
+  }
   ps.a_set = true;
   return 0;
 }

@@ -149,6 +149,11 @@ cudaError_t build_pair_group(ExactScratch& s, const GroupPair* gp_dev, int G, in
                              int* cursor, int* vcount, int* bad, cudaStream_t st,
                              int64_t* launches);
 
+// Summed-volume tables of A's n voxels (avox) for nb bins: bin_slot_dev[bin]
+// = table index or -1; sat holds nb * (ext+1)^3-shaped u32 tables.
+cudaError_t build_sat(const int4* avox, int n, const int* bin_slot_dev, int nb,
+                      const uint32_t ext[3], uint32_t* sat, cudaStream_t st);
+
 // dst[r] = src[idx[r]] (rows of w elements), or the reverse with scatter.
 template <typename T>
 cudaError_t gather_rows(const T* src, const int64_t* idx, int64_t n, int w, T* dst, bool scatter,

@@ -42,6 +42,12 @@ struct RefView {
   int n_avox;
   int empty;                  // FeatureMap with no voxels / empty bounds
   const uint32_t* bin_total;  // per-bin count of all A voxels (full-cover shortcut)
+  // Summed-volume tables of A's voxels, one per bin present in A (or none):
+  // sat[k][x][y][z] = # voxels with bin sat_bin[k] in [0,x)x[0,y)x[0,z) of the
+  // box, (ext+1)-strided -- a region's marginal is 8 lookups per bin.
+  const uint32_t* sat;
+  const int* sat_bin;
+  int sat_nb;
 };
 
 // Scan B in the fast path's "span layout".  The ring-ordered scan is cut into

@@ -843,3 +843,28 @@ def test_underestimated_table_is_replanned(monkeypatch, kind, res):
         np.testing.assert_array_equal(x, y)
     assert cnt["replans"] >= 1
     assert cnt["exact_poses"] <= 16  # the re-plan took (nearly) all of them
+
+
+@pytest.mark.parametrize("tag,res,kind", [("c2", 1.0, "varz"), ("c1", 0.5, "count"),
+                                          ("c4", 0.2, "varz")])
+def test_sat_marginals_equal_voxel_list_marginals(monkeypatch, tag, res, kind):
+    """The per-pose A marginal from summed-volume tables (8 lookups per bin)
+    equals the scan over A's voxel list (VMI_SAT_MB=0) bit for bit, on poses
+    whose region cuts A's box on every side."""
+    a, b = hdl_pair()
+    if tag == "c1":
+        s = golden("c1_scans.npz")
+        a, b = s["a"], s["b"]
+    from paper_1709_06948_b200.synth import candidate_batch
+    poses = candidate_batch(EulerPose(1.5, 0.3, 0, 0, 0, 0.05), 96, seed=51,
+                            half_width=(20.0, 20.0, 2.0, 0.05, 0.05, 0.8))
+    out = []
+    for mb in ("512", "0"):
+        monkeypatch.setenv("VMI_SAT_MB", mb)
+        eng = engine(res, kind=kind)
+        eng.set_reference(np.asarray(a)[:, :3].astype(np.float64), fetch=False)
+        eng.set_query(b)
+        out.append(eng.evaluate(poses, histograms=True))
+        eng.close()
+    for x, y in zip(*out):
+        np.testing.assert_array_equal(x, y)
