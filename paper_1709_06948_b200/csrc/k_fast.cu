@@ -467,6 +467,8 @@ __global__ void __launch_bounds__(THREADS, 1)
     // |R p|)), which shifts each d by up to E: VARZ moves by <= 2 res E + E^2
     const double u0 = __dsub_rn(t0, g.origin[0]), u1 = __dsub_rn(t1, g.origin[1]),
                  u2 = __dsub_rn(t2, g.origin[2]);
+    const double cq0 = __dmul_rn(u0, g.inv_res), cq1 = __dmul_rn(u1, g.inv_res),
+                 cq2 = __dmul_rn(u2, g.inv_res);
     const double var_shift =
         MODE == kGridGeneral
             ? 2.0 * g.res * 2.220446049250313e-16 *
@@ -676,10 +678,14 @@ __global__ void __launch_bounds__(THREADS, 1)
           const double sx = rot_row(x, y, z, m0, m1, m2);
           const double sy = rot_row(x, y, z, m3, m4, m5);
           const double sz = rot_row(x, y, z, m6, m7, m8);
+          // q' = RN(s * RN(1/res) + RN(u * RN(1/res))) in one FMA: besides the
+          // rounding of c = u * RN(1/res) (|u / res| 2^-53 < 2^-32), the same
+          // bound as RN(RN(s + u) * RN(1/res)).  VARZ keeps Zp = RN(s + u) for
+          // its pivot-relative z.
           const double Zp = __dadd_rn(sz, u2);  // ~ Z - o_z
-          const double qx = __dmul_rn(__dadd_rn(sx, u0), g.inv_res);
-          const double qy = __dmul_rn(__dadd_rn(sy, u1), g.inv_res);
-          const double qz = __dmul_rn(Zp, g.inv_res);
+          const double qx = __fma_rn(sx, g.inv_res, cq0);
+          const double qy = __fma_rn(sy, g.inv_res, cq1);
+          const double qz = KIND == kKindOcc ? __fma_rn(sz, g.inv_res, cq2) : __dmul_rn(Zp, g.inv_res);
           const double rx = __dadd_rd(qx, kf0), ry = __dadd_rd(qy, kf1), rz = __dadd_rd(qz, kf2);
           const uint32_t lx = (uint32_t)__double2loint(rx), ly = (uint32_t)__double2loint(ry),
                          lz = (uint32_t)__double2loint(rz);
