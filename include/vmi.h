@@ -47,7 +47,7 @@ enum vmi_error {
   VMI_ERR_ALLOC = -3,
   VMI_ERR_STATE = -4,
   VMI_ERR_RANGE = -5,       /* scan A leaves the voxel key range (voxel.py:200-206) */
-  VMI_ERR_UNSUPPORTED = -6  /* e.g. bins > 64, reference AABB too large for the dense grid */
+  VMI_ERR_UNSUPPORTED = -6  /* e.g. bins > 64, a pair set whose scan A needs the sparse reference */
 };
 
 /* Context lifetime.  device = CUDA ordinal.  Replaces nothing in the reference

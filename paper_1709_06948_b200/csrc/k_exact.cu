@@ -288,7 +288,7 @@ __global__ void k_build_grid_box(const uint32_t* lin, const double* values, cons
 // ---- scan A's reference grid -------------------------------------------------
 __global__ void k_build_grid(const unsigned long long* keys, const double* values, int V,
                              const int* Vdev, GridParams g, int3 amin, uint3 ext, uint8_t* grid,
-                             int4* avox_tmp, uint32_t* bin_total) {
+                             int4* avox_tmp, uint32_t* bin_total, SparseRef sp) {
   const int v = blockIdx.x * blockDim.x + threadIdx.x;
   if (v >= (Vdev ? *Vdev : V)) return;
   const unsigned long long k = keys[v];
@@ -303,7 +303,14 @@ __global__ void k_build_grid(const unsigned long long* keys, const double* value
     avox_tmp[v] = make_int4(0, 0, 0, -1);
     return;
   }
-  grid[((size_t)rx * ext.y + ry) * ext.z + rz] = (uint8_t)bin;
+  if (grid) {
+    grid[((size_t)rx * ext.y + ry) * ext.z + rz] = (uint8_t)bin;
+  } else {  // sparse reference: insert k (a repeated key keeps one slot, last bin wins)
+    for (uint32_t h = ref_slot(k, sp.mask);; h = (h + 1) & sp.mask) {
+      const unsigned long long prev = atomicCAS(&sp.keys[h], ~0ull, k);
+      if (prev == ~0ull || prev == k) { sp.bins[h] = (uint8_t)bin; break; }
+    }
+  }
   avox_tmp[v] = make_int4((int)rx, (int)ry, (int)rz, bin);
   atomicAdd(&bin_total[bin], 1u);
 }
@@ -341,12 +348,13 @@ cudaError_t build_reference_box(const ExactScratch& s, int Vmax, const GridParam
 cudaError_t build_reference(const unsigned long long* keys, const double* values, int V,
                             const int* Vdev, const GridParams& g, const int amin[3],
                             const uint32_t ext[3], uint8_t* grid, int4* tmp, int4* avox,
-                            uint32_t* bin_total, int* cursor, cudaStream_t st, int64_t* launches) {
+                            uint32_t* bin_total, int* cursor, cudaStream_t st, int64_t* launches,
+                            SparseRef sp) {
   if (V <= 0) return cudaSuccess;
   const int T = 256, blocks = (V + T - 1) / T;
   k_build_grid<<<blocks, T, 0, st>>>(keys, values, V, Vdev, g,
                                      make_int3(amin[0], amin[1], amin[2]),
-                                     make_uint3(ext[0], ext[1], ext[2]), grid, tmp, bin_total);
+                                     make_uint3(ext[0], ext[1], ext[2]), grid, tmp, bin_total, sp);
   k_bin_offsets<<<1, 32, 0, st>>>(bin_total, g.bins + 1, cursor);
   k_scatter_by_bin<<<blocks, T, 0, st>>>(tmp, V, Vdev, cursor, avox);
   if (launches) *launches += 3;
@@ -365,7 +373,7 @@ __global__ void k_exact_hist(const unsigned long long* keys, const double* value
   const uint32_t rx = x - A.amin[0], ry = y - A.amin[1], rz = z - A.amin[2];
   if (A.empty || !(rx < A.ext[0] && ry < A.ext[1] && rz < A.ext[2])) return;
   const int W = g.bins + 1;
-  const int ba = A.grid[((size_t)rx * A.ext[1] + ry) * A.ext[2] + rz];
+  const int ba = A.sparse ? ref_sparse_bin(A, k) : A.grid[((size_t)rx * A.ext[1] + ry) * A.ext[2] + rz];
   const int bb = feature_bin(values[v], g.clamp, g.bins);
   atomicAdd(&ghist[ba * W + bb], 1u);
 }

@@ -450,6 +450,7 @@ __global__ void __launch_bounds__(THREADS, 1)
         const double lim2 = 16777216.0 * g.res;
         unsafe |= fabs(t0) + r0 >= lim2 || fabs(t1) + r1 >= lim2 || fabs(t2) + r2 >= lim2;
       }
+      unsafe |= A.sparse != 0;  // no dense grid: the exact path looks A up (RefView.sparse)
       if (unsafe) {
         if (tid == 0) {
           mi_out[p] = -1e300;

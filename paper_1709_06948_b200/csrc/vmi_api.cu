@@ -40,6 +40,11 @@ struct PairStore {
   size_t cap_avox = 0;
   int n_avox = 0;
   uint32_t* d_bin_total = nullptr;
+  bool sparse = false;                // A's AABB too large for the dense grid
+  unsigned long long* d_hkeys = nullptr;  // sparse A: packed keys (RefView.hkeys)
+  uint8_t* d_hbins = nullptr;
+  size_t cap_hkeys = 0, cap_hbins = 0;
+  uint32_t hmask = 0;
   int64_t a_nvox = 0;
   int64_t a_npts = 0;  // scan A's point count (0 when set from features)
   // scan B
@@ -207,12 +212,13 @@ int cuda_fail(vmi_ctx* c, cudaError_t e, const char* where) {
 // re-sets scan A every pair); only the bookkeeping is reset here.
 void free_a(PairStore& ps) {
   ps.a_set = false; ps.n_avox = 0; ps.a_nvox = 0; ps.grid_bytes = 0; ps.a_npts = 0;
-  ps.sat_nb = 0;
+  ps.sat_nb = 0; ps.sparse = false;
 }
 
 void release_pair(PairStore& ps) {
   cudaFree(ps.d_grid); cudaFree(ps.d_avox); cudaFree(ps.d_bin_total); cudaFree(ps.d_pts);
   cudaFree(ps.d_hull); cudaFree(ps.d_pts_exact); cudaFree(ps.d_sat); cudaFree(ps.d_sat_bin);
+  cudaFree(ps.d_hkeys); cudaFree(ps.d_hbins);
   ps = PairStore{};
 }
 
@@ -238,7 +244,11 @@ cudaError_t grow(T** p, size_t& cap, size_t need) {
 RefView ref_view(const PairStore& ps) {
   RefView A{};
   for (int j = 0; j < 3; ++j) { A.amin[j] = ps.amin[j]; A.amax[j] = ps.amax[j]; A.ext[j] = ps.ext[j]; }
-  A.grid = ps.d_grid;
+  A.grid = ps.sparse ? nullptr : ps.d_grid;
+  A.sparse = ps.sparse ? 1 : 0;
+  A.hkeys = ps.sparse ? ps.d_hkeys : nullptr;
+  A.hbins = ps.sparse ? ps.d_hbins : nullptr;
+  A.hmask = ps.hmask;
   A.avox = ps.d_avox;
   A.n_avox = ps.n_avox;
   A.empty = ps.a_empty ? 1 : 0;
@@ -363,17 +373,31 @@ int finish_reference(vmi_ctx* c, PairStore& ps, const int64_t bounds[6], int64_t
     ps.ext[j] = (uint32_t)(bounds[3 + j] - bounds[j] + 1);
   }
   const double vol = (double)ps.ext[0] * ps.ext[1] * ps.ext[2];
-  if (vol > 4294967294.0)
-    return fail(c, VMI_ERR_UNSUPPORTED,
-                "scan A's occupied AABB exceeds 2^32-2 voxels (dense reference grid limit)");
-  ps.grid_bytes = (size_t)vol;
-  CK(c, grow(&ps.d_grid, ps.cap_grid, ps.grid_bytes));
-  CK(c, cudaMemsetAsync(ps.d_grid, 0, ps.grid_bytes, c->stream));
+  // Over the dense grid's 32-bit index (or VMI_SPARSE_REF=1, tests): A as a
+  // sparse key table; the fast kernel then flags every pose for the exact path.
+  const char* sp_env = std::getenv("VMI_SPARSE_REF");
+  ps.sparse = vol > 4294967294.0 || (sp_env && std::atoi(sp_env) != 0);
+  SparseRef sp{};
+  if (ps.sparse) {
+    if (V > (1 << 30)) return fail(c, VMI_ERR_UNSUPPORTED, "sparse reference over 2^30 voxels");
+    size_t cap = 1024;
+    while (cap < 2 * (size_t)V) cap <<= 1;
+    CK(c, grow(&ps.d_hkeys, ps.cap_hkeys, 8 * cap));
+    CK(c, grow(&ps.d_hbins, ps.cap_hbins, cap));
+    CK(c, cudaMemsetAsync(ps.d_hkeys, 0xFF, 8 * cap, c->stream));
+    ps.hmask = (uint32_t)(cap - 1);
+    sp = SparseRef{ps.d_hkeys, ps.d_hbins, ps.hmask};
+    ps.grid_bytes = 0;
+  } else {
+    ps.grid_bytes = (size_t)vol;
+    CK(c, grow(&ps.d_grid, ps.cap_grid, ps.grid_bytes));
+    CK(c, cudaMemsetAsync(ps.d_grid, 0, ps.grid_bytes, c->stream));
+  }
   CK(c, grow(&ps.d_avox, ps.cap_avox, sizeof(int4) * (V > 0 ? V : 1)));
   CK(c, grow(&c->d_avox_tmp, c->cap_avox_tmp, sizeof(int4) * (V > 0 ? V : 1)));
-  CK(c, build_reference(keys, values, (int)V, nullptr, c->g, ps.amin, ps.ext, ps.d_grid,
-                        c->d_avox_tmp, ps.d_avox, ps.d_bin_total, c->d_cursor, c->stream,
-                        &c->launches));
+  CK(c, build_reference(keys, values, (int)V, nullptr, c->g, ps.amin, ps.ext,
+                        ps.sparse ? nullptr : ps.d_grid, c->d_avox_tmp, ps.d_avox, ps.d_bin_total,
+                        c->d_cursor, c->stream, &c->launches, sp));
   std::vector<uint32_t> tot(kMaxW);
   CK(c, cudaMemcpyAsync(tot.data(), ps.d_bin_total, 4 * kMaxW, cudaMemcpyDeviceToHost, c->stream));
   CK(c, cudaStreamSynchronize(c->stream));
@@ -391,7 +415,7 @@ int finish_reference(vmi_ctx* c, PairStore& ps, const int64_t bounds[6], int64_t
   const double cells = (double)(ps.ext[0] + 1) * (ps.ext[1] + 1) * (ps.ext[2] + 1);
   const char* sat_env = std::getenv("VMI_SAT_MB");  // table budget per pair; 0 disables
   const double budget = (sat_env ? std::atof(sat_env) : 512.0) * 1048576.0;
-  if (nbp > 0 && cells * nbp * 4.0 <= budget && cells < 2147483647.0) {
+  if (!ps.sparse && nbp > 0 && cells * nbp * 4.0 <= budget && cells < 2147483647.0) {
     CK(c, grow(&ps.d_sat, ps.cap_sat, (size_t)(cells * nbp * 4.0)));
     if (!ps.d_sat_bin) CK(c, cudaMalloc(&ps.d_sat_bin, sizeof(int) * 2 * kMaxW));
     CK(c, cudaMemcpyAsync(ps.d_sat_bin, slot, sizeof(int) * 2 * kMaxW, cudaMemcpyHostToDevice,
@@ -483,6 +507,7 @@ int replan_flagged(vmi_ctx* c, const double* mats_dev, int64_t P, double* mi, in
                    long long* hist, long long* total, cudaStream_t stream,
                    std::vector<int32_t>& own, const int32_t*& hs) {
   const int W = c->g.bins + 1;
+  if (c->cur.sparse) return 0;  // flagged by design (sparse reference), not by the table plan
   for (int attempt = 0; attempt < 3; ++attempt) {
     std::vector<int64_t> idx;
     for (int64_t p = 0; p < P; ++p)
@@ -1488,7 +1513,8 @@ int vmi_set_pairs(vmi_ctx* c, int64_t npairs, const void* const* a, const int64_
       const double vol = (double)ps.ext[0] * ps.ext[1] * ps.ext[2];
       if (vol > 4294967294.0)
         return lfail(VMI_ERR_UNSUPPORTED,
-                     "scan A's occupied AABB exceeds 2^32-2 voxels (dense reference grid limit)");
+                     "scan A's occupied AABB exceeds 2^32-2 voxels: pair sets need the dense "
+                     "reference grid (the single-pair API takes a sparse reference)");
       ps.grid_bytes = (size_t)vol;
       LCK(grow(&ps.d_grid, ps.cap_grid, ps.grid_bytes));
       LCK(grow(&ps.d_avox, ps.cap_avox, sizeof(int4) * (size_t)na[i]));

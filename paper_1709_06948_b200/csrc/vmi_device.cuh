@@ -95,6 +95,21 @@ __device__ __forceinline__ int feature_bin(double v, double clamp, int bins) {
   return 1 + raw;
 }
 
+// ---- sparse reference table (RefView.sparse) ----------------------------------
+// Slot of packed key k: multiplicative hash, linear probing, ~0 = empty.
+__device__ __forceinline__ uint32_t ref_slot(unsigned long long k, uint32_t mask) {
+  return (uint32_t)((k * 0x9E3779B97F4A7C15ull) >> 32) & mask;
+}
+
+// Scan A's bin of packed key k (0 = not occupied).
+__device__ __forceinline__ int ref_sparse_bin(const RefView& A, unsigned long long k) {
+  for (uint32_t h = ref_slot(k, A.hmask);; h = (h + 1) & A.hmask) {
+    const unsigned long long s = __ldg(&A.hkeys[h]);
+    if (s == k) return __ldg(&A.hbins[h]);
+    if (s == ~0ull) return 0;
+  }
+}
+
 // numpy pairwise_sum (loops_utils.h.src) over f(lo .. lo+n-1); F(i) -> double.
 template <typename F>
 __device__ double pairwise_sum(const F& f, int64_t lo, int64_t n) {

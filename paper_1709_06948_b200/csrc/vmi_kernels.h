@@ -92,13 +92,23 @@ cudaError_t build_reference_box(const ExactScratch& s, int Vmax, const GridParam
                                 uint32_t* bin_total, int* cursor, cudaStream_t st,
                                 int64_t* launches);
 
-// Build A's dense bin grid and sorted voxel list from V feature-map entries
-// (keys + values on device; with Vdev the count is *Vdev and V only an upper
-// bound).  grid must be zeroed, ext-sized; tmp and avox hold V entries each.
+// Sparse reference table being built (RefView.hkeys/hbins/hmask): keys
+// pre-filled with ~0, mask + 1 a power of two >= 2x the voxel count.
+struct SparseRef {
+  unsigned long long* keys;
+  uint8_t* bins;
+  uint32_t mask;
+};
+
+// Build A's bin grid and sorted voxel list from V feature-map entries (keys +
+// values on device; with Vdev the count is *Vdev and V only an upper bound).
+// grid (zeroed, ext-sized) or, with grid null, the sparse table sp; tmp and
+// avox hold V entries each.
 cudaError_t build_reference(const unsigned long long* keys, const double* values, int V,
                             const int* Vdev, const GridParams& g, const int amin[3],
                             const uint32_t ext[3], uint8_t* grid, int4* tmp, int4* avox,
-                            uint32_t* bin_total, int* cursor, cudaStream_t st, int64_t* launches);
+                            uint32_t* bin_total, int* cursor, cudaStream_t st, int64_t* launches,
+                            SparseRef sp = SparseRef{});
 
 // Histogram + finalisation + MI for pose p from an exact voxelization held in
 // s (after exact_voxelize).  Writes mi[p], status[p], hist[p], total[p].

@@ -48,6 +48,16 @@ struct RefView {
   const uint32_t* sat;
   const int* sat_bin;
   int sat_nb;
+  // Sparse reference: when A's AABB exceeds the dense grid's 32-bit index
+  // (> 2^32-2 voxels, e.g. a map-scale scan A at fine resolution) `grid` is
+  // null and A is an open-addressing table of its packed voxel keys
+  // (voxel.py:65-73's int64 packing; empty slot = ~0) with a parallel bin
+  // array -- the reference's own sparse representation.  The fast kernel
+  // flags such poses; the exact path looks bins up here.
+  const unsigned long long* hkeys;
+  const uint8_t* hbins;
+  uint32_t hmask;
+  int sparse;
 };
 
 // Scan B in the fast path's "span layout".  The ring-ordered scan is cut into

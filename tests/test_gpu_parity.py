@@ -868,3 +868,61 @@ def test_sat_marginals_equal_voxel_list_marginals(monkeypatch, tag, res, kind):
         eng.close()
     for x, y in zip(*out):
         np.testing.assert_array_equal(x, y)
+
+
+@pytest.mark.parametrize("tag,res,kind", [("c1", 0.5, "count"), ("hdl", 1.0, "varz"),
+                                          ("hdl", 0.2, "varz")])
+def test_sparse_reference_equals_dense_grid(monkeypatch, tag, res, kind):
+    """Scan A as the sparse key table (VMI_SPARSE_REF=1: every pose through the
+    exact path's table lookups) gives the dense grid's results bit for bit."""
+    a, b = hdl_pair()
+    if tag == "c1":
+        s = golden("c1_scans.npz")
+        a, b = s["a"], s["b"]
+    from paper_1709_06948_b200.synth import candidate_batch
+    poses = candidate_batch(EulerPose(1.5, 0.3, 0, 0, 0, 0.05), 24, seed=53,
+                            half_width=(10.0, 10.0, 1.0, 0.05, 0.05, 0.5))
+    out = []
+    for sp in ("0", "1"):
+        monkeypatch.setenv("VMI_SPARSE_REF", sp)
+        eng = engine(res, kind=kind)
+        eng.set_reference(np.asarray(a)[:, :3].astype(np.float64), fetch=False)
+        eng.set_query(b)
+        out.append(eng.evaluate(poses, histograms=True))
+        if sp == "1":
+            assert eng.ctx.counters()["exact_poses"] >= len(poses)
+        eng.close()
+    for x, y in zip(*out):
+        np.testing.assert_array_equal(x, y)
+
+
+@pytest.mark.parametrize("kind", ["varz", "count"])
+def test_reference_aabb_over_2_32_voxels_matches_oracle(kind):
+    """A map-scale scan A: a local scan plus landmarks ~3 km away, at 0.1 m an
+    AABB of ~1e12 voxels (the dense grid's 32-bit index cannot hold it).  The
+    reference stores packed keys (voxel.py:65-73) and has no such limit; the
+    sparse reference table matches the oracle pose for pose."""
+    s = golden("c1_scans.npz")
+    a, b = np.asarray(s["a"])[:, :3], np.asarray(s["b"])[:, :3]
+    rng = np.random.default_rng(7)
+    far = np.array([3000.0, -2500.0, 40.0]) + rng.normal(0, 0.3, size=(500, 3))
+    a_map = np.vstack([a, far])
+    res = 0.1
+    eng = engine(res, kind=kind)
+    eng.set_reference(a_map)
+    eng.set_query(b)
+    poses = np.array([[0.0, 0.0, 0.0, 0.0, 0.0, 0.0], [0.4, -0.3, 0.05, 0.01, -0.02, 0.1],
+                      [-1.5, 2.0, 0.0, 0.0, 0.0, -0.3], [3000.0, -2500.0, 40.0, 0.0, 0.0, 0.0],
+                      [1e4, 0.0, 0.0, 0.0, 0.0, 0.0]])
+    mats = oracle.poses_to_mats(poses)
+    mi, st, hist, total = eng.evaluate(poses, histograms=True)
+    fa = oracle.feature_map(a_map, (0, 0, 0), res, kind)
+    for i in range(len(poses)):
+        omi, ost, ohist, ototal = oracle.mi_objective_full(fa, b, mats[i], res=res)
+        assert st[i] == ost
+        if ost in (0, 3):
+            np.testing.assert_array_equal(hist[i], ohist)
+            assert total[i] == ototal
+        assert_mi_close([mi[i]], [omi])
+    assert eng.ctx.counters()["exact_poses"] >= len(poses)
+    eng.close()
