@@ -60,6 +60,17 @@ __device__ __forceinline__ uint32_t slot_of(uint32_t lin, uint32_t cap) {
 #ifndef VMI_MAT_PREFETCH  // A/B switch: pose matrices loaded one pose ahead
 #define VMI_MAT_PREFETCH 1
 #endif
+// VARZ sums are taken of s_z = the z row's FMA chain before + t_z (= Z - t_z
+// up to one rounding of Z), not of z relative to the voxel's lower face: no
+// per-point pivot arithmetic.  The per-point offset r (|r| <= 2^-53 |Z|) moves
+// a voxel's variance by at most res |r|max + r^2 (var_shift), and the sums'
+// own rounding is bounded through S2 + S1^2/n whatever the pivot.
+#ifndef VMI_REC_V2  // the run record's two sums in one 16-byte store
+#define VMI_REC_V2 1
+#endif
+#ifndef VMI_PIVOT_SZ
+#define VMI_PIVOT_SZ 1
+#endif
 #ifndef VMI_NEAR_FIX  // 0: teeth check of the near-integer test only (wrong floors)
 #define VMI_NEAR_FIX 1
 #endif
@@ -257,8 +268,12 @@ __device__ __forceinline__ void st_rec32_if(bool p, uint32_t a, uint32_t l, uint
   asm volatile(
       "{\n .reg .pred q;\n setp.ne.b32 q, %0, 0;\n"
       " @q st.shared.v2.u32 [%1], {%2, %3};\n"
+#if VMI_REC_V2
+      " @q st.shared.v2.f64 [%1+16], {%4, %5};\n}" ::"r"((int)p),
+#else
       " @q st.shared.f64 [%1+16], %4;\n"
       " @q st.shared.f64 [%1+24], %5;\n}" ::"r"((int)p),
+#endif
       "r"(a), "r"(l), "r"(n), "d"(s1), "d"(s2)
       : "memory");
 }
@@ -463,15 +478,17 @@ __global__ void __launch_bounds__(THREADS, 1)
       }
     }
 
-    // general resolutions: u = RN(t - o) for the fast floor (locate), and the
-    // bound on its per-point error E in Z - o (locate: <= 2^-52 (|t| + |o| +
-    // |R p|)), which shifts each d by up to E: VARZ moves by <= 2 res E + E^2
+    // general resolutions: u = RN(t - o) for the fast floor (locate).  The
+    // per-point error E of d against the reference's Z up to a per-pose
+    // constant (d = s_z: one rounding of Z, <= 2^-53 |Z|; general mode's
+    // pivot-relative d: <= 2^-52 (|t| + |o| + |R p|)) moves a voxel's VARZ by
+    // <= res E + E^2 (its z spread is below res): var_shift covers both.
     const double u0 = __dsub_rn(t0, g.origin[0]), u1 = __dsub_rn(t1, g.origin[1]),
                  u2 = __dsub_rn(t2, g.origin[2]);
     const double cq0 = __dmul_rn(u0, g.inv_res), cq1 = __dmul_rn(u1, g.inv_res),
                  cq2 = __dmul_rn(u2, g.inv_res);
     const double var_shift =
-        MODE == kGridGeneral
+        (MODE == kGridGeneral || VMI_PIVOT_SZ)
             ? 2.0 * g.res * 2.220446049250313e-16 *
                   (fabs(t2) + fabs(g.origin[2]) + (fabs(m6) + fabs(m7) + fabs(m8)) * B.max_abs + g.res)
             : 0.0;
@@ -707,7 +724,7 @@ __global__ void __launch_bounds__(THREADS, 1)
             qf = __dsub_rn(fz, kc2);
           }
           // pivot: the voxel's lower face relative to o_z (a function of the voxel)
-          d = __fma_rn(-qf, g.res, Zp);
+          d = VMI_PIVOT_SZ ? sz : __fma_rn(-qf, g.res, Zp);
           lin = inside_lin((uint32_t)ix, (uint32_t)iy, (uint32_t)iz, ex0, ex1, ex2);
           if (MULTI && npass > 1 && lin != kNoVoxel &&
               __umulhi(lin * 0x85EBCA6Bu, (uint32_t)npass) != (uint32_t)pass)
@@ -716,7 +733,8 @@ __global__ void __launch_bounds__(THREADS, 1)
         }
         const double X = xform_row(x, y, z, m0, m1, m2, t0);
         const double Y = xform_row(x, y, z, m3, m4, m5, t1);
-        const double Z = xform_row(x, y, z, m6, m7, m8, t2);
+        const double sz = rot_row(x, y, z, m6, m7, m8);
+        const double Z = __dadd_rn(sz, t2);  // = xform_row
         const double fx = __dadd_rd(grid_q<MODE>(X, g.origin[0], g.res, g.inv_res), kc0);
         const double fy = __dadd_rd(grid_q<MODE>(Y, g.origin[1], g.res, g.inv_res), kc1);
         const double fz = __dadd_rd(grid_q<MODE>(Z, g.origin[2], g.res, g.inv_res), kc2);
@@ -724,8 +742,12 @@ __global__ void __launch_bounds__(THREADS, 1)
         iy = __double2loint(fy);
         iz = __double2loint(fz);
         // fz - kc2 == floor(q_z) exactly (both integers below 2^53)
-        const double qf = __dsub_rn(fz, kc2);
-        d = __dsub_rn(Z, MODE == kGridUnit ? qf : __fma_rn(qf, g.res, g.origin[2]));
+        if (VMI_PIVOT_SZ) {
+          d = sz;
+        } else {
+          const double qf = __dsub_rn(fz, kc2);
+          d = __dsub_rn(Z, MODE == kGridUnit ? qf : __fma_rn(qf, g.res, g.origin[2]));
+        }
         lin = inside_lin((uint32_t)ix, (uint32_t)iy, (uint32_t)iz, ex0, ex1, ex2);
         if (MULTI && npass > 1 && lin != kNoVoxel &&
             __umulhi(lin * 0x85EBCA6Bu, (uint32_t)npass) != (uint32_t)pass)

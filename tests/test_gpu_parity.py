@@ -357,22 +357,34 @@ def test_fast_path_features_match_reference(tag, res, kind):
     if kind == "count":
         np.testing.assert_array_equal(vals, bv[inside])
     else:
-        # The kernel sums (z - K) and (z - K)^2 around K = the voxel's lower z
-        # face, so its VARZ error is bounded by the summation error of those
-        # sums: |err| <= (n + 8) * 2^-51 * (S2 + S1^2/n) / n <= (n + 8) * 2^-50 * res^2
-        # -- the same bound the kernel's bin-edge guard uses (any voxel that
-        # close to a bin edge sends the pose to the exact path, so histograms
-        # stay bit-exact).  Relative 1e-6 holds wherever that bound is below it.
+        # The kernel sums d and d^2 with d = s_z, the z row's FMA chain before
+        # + t_z (k_fast.cu VMI_PIVOT_SZ; = Z - t_z up to one rounding of Z), so
+        # its VARZ error is bounded by those sums' rounding, |err| <= (n + 8) *
+        # 2^-50 * max d^2, plus the offset term res * 2^-51 * |Z|max -- the
+        # bounds the kernel's bin-edge guard uses (any voxel that close to a bin
+        # edge sends the pose to the exact path, so histograms stay bit-exact).
+        # Relative 1e-6 holds wherever that bound is below it.
         want = bv[inside]
         ck = g["c1_b_keys"]  # COUNT at the same resolution: per-voxel n
         n = g["c1_b_values"][np.searchsorted(ck, keys)]
         assert np.array_equal(ck[np.searchsorted(ck, keys)], keys)
-        bound = (n + 8) * 2.0 ** -50 * res * res
+        m = oracle.poses_to_mats(g["poses"][:1])[0]
+        Z = oracle.transform(b[:, :3].astype(np.float64), m)
+        ijk, _ = oracle.voxel_indices(Z, (0, 0, 0), res)
+        off = 1 << 20
+        pk = ((ijk[:, 0] + off) << 42) | ((ijk[:, 1] + off) << 21) | (ijk[:, 2] + off)
+        d2 = (Z[:, 2] - m[11]) ** 2
+        order = np.argsort(pk, kind="stable")
+        uk, first = np.unique(pk[order], return_index=True)
+        maxd2 = np.maximum.reduceat(d2[order], first)[np.searchsorted(uk, keys)]
+        assert np.array_equal(uk[np.searchsorted(uk, keys)], keys)
+        bound = ((n + 8) * 2.0 ** -50 * np.maximum(maxd2, res * res)
+                 + res * 2.0 ** -51 * (np.abs(Z[:, 2]).max() + res))
         err = np.abs(vals - want)
         assert np.all(err <= bound), np.max(err / bound)
         big = want > 1e4 * bound
         np.testing.assert_allclose(vals[big], want[big], rtol=1e-6)
-        assert big.mean() > 0.9  # measured 0.93 (the rest: near-flat voxels, var < 1e4 * bound)
+        assert big.mean() > 0.8  # (the rest: near-flat voxels, var < 1e4 * bound)
 
 
 @pytest.mark.parametrize("tag", ["varz1", "count05"])
