@@ -360,10 +360,12 @@ class Context:
         P = poses.shape[0]
         mi = np.empty(P, dtype=np.float64)
         st = np.empty(P, dtype=np.int32)
-        total = np.empty(P, dtype=np.int64)
+        # region totals only travel with histograms (evaluate() returns them then)
+        total = np.empty(P, dtype=np.int64) if want_hist else None
         hist = np.empty((P, bins + 1, bins + 1), dtype=np.int64) if want_hist else None
         self.check(self._L.vmi_eval_poses(self._h, ptr(poses, _d), P, ptr(mi, _d), ptr(st, _i32),
-                                          ptr(hist, _i64) if want_hist else None, ptr(total, _i64)),
+                                          ptr(hist, _i64) if want_hist else None,
+                                          ptr(total, _i64) if want_hist else None),
                    "vmi_eval_poses")
         return mi, st, hist, total
 

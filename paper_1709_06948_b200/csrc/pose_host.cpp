@@ -6,12 +6,89 @@
 // -ffp-contract=off (see build.py) and calls glibc's sin/cos, so every entry
 // is bit-identical; CUDA's device sin/cos carry no such guarantee, which is
 // why this O(P) step stays on the host.
+#include <unistd.h>
+
 #include <algorithm>
+#include <atomic>
 #include <cmath>
-#include <cstdlib>
+#include <condition_variable>
 #include <cstdint>
+#include <cstdlib>
+#include <functional>
+#include <mutex>
 #include <thread>
 #include <vector>
+
+namespace {
+
+// Persistent workers: a conversion on the critical path of vmi_eval_poses
+// (the first chunk, before its kernel can start) must not pay ~20 us per
+// thread creation.  Chunks are claimed from an atomic counter; the calling
+// thread works too.
+class Pool {
+ public:
+  void run(int workers, int64_t nchunks, const std::function<void(int64_t)>& fn) {
+    std::lock_guard<std::mutex> one(run_m_);  // one job at a time (calls from several host threads)
+    std::unique_lock<std::mutex> lk(m_);
+    ensure(workers);
+    fn_ = &fn;
+    nchunks_ = nchunks;
+    next_.store(0);
+    active_ = (int)th_;
+    ++gen_;
+    cv_.notify_all();
+    lk.unlock();
+    drain();
+    lk.lock();
+    done_cv_.wait(lk, [&] { return active_ == 0; });
+    fn_ = nullptr;
+  }
+
+ private:
+  void ensure(int workers) {  // (m_ held)
+    while ((int)th_ < workers) {  // a new worker joins the job about to be posted
+      const uint64_t seen = gen_;
+      std::thread([this, seen] { loop(seen); }).detach();
+      ++th_;
+    }
+  }
+  void drain() {
+    for (int64_t k; (k = next_.fetch_add(1)) < nchunks_;) (*fn_)(k);
+  }
+  void loop(uint64_t seen) {
+    for (;;) {
+      std::unique_lock<std::mutex> lk(m_);
+      cv_.wait(lk, [&] { return gen_ != seen; });
+      seen = gen_;
+      lk.unlock();
+      drain();
+      lk.lock();
+      if (--active_ == 0) done_cv_.notify_all();
+    }
+  }
+  std::mutex run_m_, m_;
+  std::condition_variable cv_, done_cv_;
+  const std::function<void(int64_t)>* fn_ = nullptr;
+  std::atomic<int64_t> next_{0};
+  int64_t nchunks_ = 0;
+  int active_ = 0;
+  uint64_t gen_ = 0;
+  size_t th_ = 0;
+};
+
+Pool& pool() {
+  // never destroyed: detached workers may still wait on it at exit.  A forked
+  // child gets a fresh pool (its copy's workers and lock state are not usable).
+  static Pool* p = nullptr;
+  static pid_t owner = 0;
+  if (!p || owner != getpid()) {
+    p = new Pool;
+    owner = getpid();
+  }
+  return *p;
+}
+
+}  // namespace
 
 extern "C" int vmi_poses_to_mats(const double* poses, int64_t n, double* mats, int threads) {
   if (n < 0 || (n > 0 && (!poses || !mats))) return -1;
@@ -43,18 +120,16 @@ extern "C" int vmi_poses_to_mats(const double* poses, int64_t n, double* mats, i
     const int ranks = lws ? std::max(1, std::atoi(lws)) : 1;
     threads = hw > 0 ? std::max(1, hw / ranks) : 1;
   }
-  if (n < 4096 || threads == 1) {
+  if (n < 512 || threads == 1) {
     work(0, n);
     return 0;
   }
   if (threads > 64) threads = 64;
-  std::vector<std::thread> pool;
-  const int64_t chunk = (n + threads - 1) / threads;
-  for (int t = 0; t < threads; ++t) {
-    const int64_t lo = t * chunk, hi = lo + chunk < n ? lo + chunk : n;
-    if (lo >= hi) break;
-    pool.emplace_back(work, lo, hi);
-  }
-  for (auto& th : pool) th.join();
+  const int64_t chunk = std::max<int64_t>(256, (n + 4 * threads - 1) / (4 * threads));
+  const int64_t nchunks = (n + chunk - 1) / chunk;
+  const std::function<void(int64_t)> fn = [&](int64_t k) {
+    work(k * chunk, std::min(n, (k + 1) * chunk));
+  };
+  pool().run(threads - 1, nchunks, fn);
   return 0;
 }

@@ -449,6 +449,22 @@ int ensure_P(vmi_ctx* c, int64_t P, bool hist) {
   return 0;
 }
 
+// Pinned host staging for P poses: matrices (P x 12 f64), then MI (f64) and
+// status (i32) read back; grow-only.
+int ensure_pinned(vmi_ctx* c, int64_t P) {
+  if (P <= c->h_mats_cap) return 0;
+  if (c->h_mats) cudaFreeHost(c->h_mats);
+  c->h_mats = nullptr;
+  c->h_mats_cap = 0;
+  CK(c, cudaMallocHost(&c->h_mats, (size_t)P * (96 + 12)));
+  c->h_mats_cap = P;
+  return 0;
+}
+double* pinned_mi(const vmi_ctx* c) { return c->h_mats + 12 * c->h_mats_cap; }
+int32_t* pinned_status(const vmi_ctx* c) {
+  return reinterpret_cast<int32_t*>(pinned_mi(c) + c->h_mats_cap);
+}
+
 int check_ready(vmi_ctx* c) {
   if (!c) return VMI_ERR_ARG;
   if (!c->params_set) return fail(c, VMI_ERR_STATE, "vmi_set_params not called");
@@ -1048,30 +1064,33 @@ int vmi_eval_poses(vmi_ctx* c, const double* poses, int64_t P, double* mi_out, i
   if (P < 0 || (P > 0 && (!poses || !mi_out || !status_out))) return fail(c, VMI_ERR_ARG, "bad arguments");
   if (P == 0) return 0;
   cudaSetDevice(c->device);
-  if ((rc = ensure_P(c, P, hist_out != nullptr))) return rc;
-  if (P > c->h_mats_cap) {
-    if (c->h_mats) cudaFreeHost(c->h_mats);
-    c->h_mats = nullptr;
-    c->h_mats_cap = 0;
-    CK(c, cudaMallocHost(&c->h_mats, (size_t)P * 96));
-    c->h_mats_cap = P;
-  }
+  if ((rc = ensure_P(c, P, hist_out != nullptr)) || (rc = ensure_pinned(c, P))) return rc;
   if (!c->copy_stream) CK(c, cudaStreamCreateWithFlags(&c->copy_stream, cudaStreamNonBlocking));
   if (!c->copy_done) CK(c, cudaEventCreateWithFlags(&c->copy_done, cudaEventDisableTiming));
+  static const bool trace = std::getenv("VMI_TRACE") != nullptr;  // phase timings to stderr
+  const auto t0 = std::chrono::steady_clock::now();
+  auto lap = [&](const char* what) {
+    if (trace)
+      std::fprintf(stderr, "[vmi_eval_poses] %-14s %8.3f ms\n", what,
+                   std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count());
+  };
   const int W = c->g.bins + 1;
   long long* dh = hist_out ? c->d_hist : nullptr;
-  // head: long enough for its kernel (~0.5 us/pose at C2) to cover the host
-  // conversion of the rest (~25 ns/pose on one thread, less with threads)
-  const int64_t head = P < 8192 ? P : std::max<int64_t>(2048, P / 16);
+  // head: long enough for its kernel (~0.4 us/pose at C2) to cover the host
+  // conversion of the rest (~8 ns/pose on the box's 16 pooled threads) and
+  // its upload; short, so the GPU starts early
+  const int64_t head = P < 8192 ? P : std::max<int64_t>(2048, P / 32);
   if (vmi_poses_to_mats(poses, head, c->h_mats, 0)) return fail(c, VMI_ERR_ARG, "poses_to_mats");
   CK(c, cudaMemcpyAsync(c->d_mats, c->h_mats, head * 96, cudaMemcpyHostToDevice, c->stream));
   if ((rc = launch_fast_eval(c, c->d_mats, head, c->d_mi, c->d_status, dh, c->d_total, c->stream))) return rc;
+  lap("head launched");
   if (P > head) {
     const int64_t n = P - head;
     if (vmi_poses_to_mats(poses + 6 * head, n, c->h_mats + 12 * head, 0)) {
       cudaStreamSynchronize(c->stream);
       return fail(c, VMI_ERR_ARG, "poses_to_mats");
     }
+    lap("tail converted");
     CK(c, cudaMemcpyAsync(c->d_mats + 12 * head, c->h_mats + 12 * head, n * 96,
                           cudaMemcpyHostToDevice, c->copy_stream));
     CK(c, cudaEventRecord(c->copy_done, c->copy_stream));
@@ -1081,13 +1100,31 @@ int vmi_eval_poses(vmi_ctx* c, const double* poses, int64_t P, double* mi_out, i
                                c->stream)))
       return rc;
   }
-  if ((rc = do_fixups(c, c->d_mats, P, c->d_mi, c->d_status, dh, c->d_total, c->stream, nullptr))) return rc;
-  CK(c, cudaMemcpyAsync(mi_out, c->d_mi, P * 8, cudaMemcpyDeviceToHost, c->stream));
-  CK(c, cudaMemcpyAsync(status_out, c->d_status, P * 4, cudaMemcpyDeviceToHost, c->stream));
+  // MI + status through pinned staging; the statuses read back also tell
+  // do_fixups which poses to re-run (no second status read)
+  double* hmi = pinned_mi(c);
+  int32_t* hst = pinned_status(c);
+  CK(c, cudaMemcpyAsync(hmi, c->d_mi, P * 8, cudaMemcpyDeviceToHost, c->stream));
+  CK(c, cudaMemcpyAsync(hst, c->d_status, P * 4, cudaMemcpyDeviceToHost, c->stream));
+  CK(c, cudaStreamSynchronize(c->stream));
+  lap("kernels done");
+  bool flagged = false;
+  for (int64_t p = 0; p < P && !flagged; ++p) flagged = (hst[p] & VMI_FLAG_RECHECK) != 0;
+  if (flagged) {
+    std::vector<int32_t> hs(hst, hst + P);
+    if ((rc = do_fixups(c, c->d_mats, P, c->d_mi, c->d_status, dh, c->d_total, c->stream, nullptr,
+                        nullptr, hs.data())))
+      return rc;
+    CK(c, cudaMemcpyAsync(hmi, c->d_mi, P * 8, cudaMemcpyDeviceToHost, c->stream));
+    CK(c, cudaMemcpyAsync(hst, c->d_status, P * 4, cudaMemcpyDeviceToHost, c->stream));
+  }
   if (hist_out)
     CK(c, cudaMemcpyAsync(hist_out, dh, (size_t)P * W * W * 8, cudaMemcpyDeviceToHost, c->stream));
   if (total_out) CK(c, cudaMemcpyAsync(total_out, c->d_total, P * 8, cudaMemcpyDeviceToHost, c->stream));
   CK(c, cudaStreamSynchronize(c->stream));
+  std::memcpy(mi_out, hmi, (size_t)P * 8);
+  std::memcpy(status_out, hst, (size_t)P * 4);
+  lap("results copied");
   return 0;
 }
 
@@ -1670,16 +1707,6 @@ int ensure_pp(vmi_ctx* c, int64_t P) {
   CK(c, cudaMalloc(&c->d_pose_pair, 4 * (size_t)P));
   CK(c, cudaMalloc(&c->d_hash, 8 * (size_t)P));
   c->cap_pp = P;
-  return 0;
-}
-
-int ensure_pinned(vmi_ctx* c, int64_t P) {
-  if (P <= c->h_mats_cap) return 0;
-  if (c->h_mats) cudaFreeHost(c->h_mats);
-  c->h_mats = nullptr;
-  c->h_mats_cap = 0;
-  CK(c, cudaMallocHost(&c->h_mats, (size_t)P * 96));
-  c->h_mats_cap = P;
   return 0;
 }
 

@@ -242,7 +242,6 @@ class MIEngine:
         ``exact_value`` the winner's MI is always the host re-score (what a
         sharded search compares across ranks).
         """
-        poses = as_pose_array(poses)
         if mi is None:
             mi, _ = self.evaluate(poses)
         top = float(np.max(mi))
@@ -251,7 +250,7 @@ class MIEngine:
         tied = np.nonzero(mi >= top - abs(top) * rel_tie)[0]
         if tied.size == 1 and not exact_value:
             return int(tied[0]), float(mi[tied[0]])
-        _, _, hist, _ = self.evaluate(poses[tied], histograms=True)
+        _, _, hist, _ = self.evaluate(as_pose_array(poses)[tied], histograms=True)
         exact = np.array([mutual_information_exact(h, self.include_phi)[0] for h in hist])
         k = int(np.argmax(exact))
         return int(tied[k]), float(exact[k])

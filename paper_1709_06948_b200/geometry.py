@@ -111,7 +111,9 @@ def as_pose_array(poses) -> np.ndarray:
         arr = arr[None, :]
     if arr.ndim != 2 or arr.shape[1] != 6:
         raise ValueError(f"poses must be (P, 6), got {arr.shape}")
-    if not np.isfinite(arr).all():
+    # any NaN / inf makes the sum non-finite; a finite sum proves every entry
+    # finite (one pass instead of a full boolean mask on large batches)
+    if not np.isfinite(arr.sum()) and not np.isfinite(arr).all():
         raise ValueError("poses contain non-finite components")
     return arr
 

@@ -18,7 +18,8 @@ from paper_1709_06948_b200 import _lib
 
 
 def header_symbols() -> list[str]:
-    src = open(os.path.join(ROOT, "include", "vmi.h")).read()
+    with open(os.path.join(ROOT, "include", "vmi.h")) as fh:
+        src = fh.read()
     return sorted(set(re.findall(r"^\s*(?:const\s+)?[a-z0-9_]+\*?\s+\*?(vmi_[a-z0-9_]+)\(", src,
                                  re.M)))
 
