@@ -349,13 +349,14 @@ __global__ void __launch_bounds__(THREADS, 1)
                 long long* __restrict__ hist_out, long long* __restrict__ total_out,
                 FeatureDump dump, double2* __restrict__ gsums, int npass,
                 const PairDesc* __restrict__ pairs, const int32_t* __restrict__ pose_pair,
-                unsigned long long* __restrict__ hash_out) {
+                unsigned long long* __restrict__ hash_out, unsigned int* __restrict__ sched) {
   static_assert(NS == 1, "one span per thread");
   static_assert(sizeof(PairDesc) % 4 == 0 && sizeof(PairDesc) / 4 <= THREADS, "descriptor copy");
   __shared__ __align__(16) PairDesc desc_s;
   __shared__ double hull_s[6][THREADS / 32];
   __shared__ unsigned long long hash_s[THREADS / 32];
   __shared__ __align__(16) uint32_t cst_s[6];  // A's extents (single pair), 1/res (lo, hi)
+  __shared__ long long nxt_s;                   // the CTA's next pose
   extern __shared__ __align__(16) unsigned char smem[];
   const int W = g.bins + 1;
   const FastSmem L = fast_layout(KIND, cap, W, THREADS, F32 ? 1 : 0, NS, MULTI ? 1 : 0);
@@ -430,10 +431,20 @@ __global__ void __launch_bounds__(THREADS, 1)
     cst_s[4] = (uint32_t)__double2loint(g.inv_res); cst_s[5] = (uint32_t)__double2hiint(g.inv_res);
   }
 
-  // the next pose's matrix is loaded one pose ahead (its L2 latency hides
-  // behind the current pose instead of stalling the whole CTA at pose start)
+  // Poses after each CTA's first are claimed from a launch-wide ticket
+  // counter (sched, zeroed by the host), one pose ahead: a CTA that drew
+  // cheap poses takes more, so the launch ends within ~one pose time on every
+  // SM instead of waiting for the slowest CTA's fixed share.  Without sched:
+  // the static stride.  The next pose's matrix is loaded one pose ahead (its
+  // L2 latency hides behind the current pose).
+  auto claim = [&](long long cur) -> long long {
+    return sched ? (long long)gridDim.x + (long long)atomicAdd(sched, 1u) : cur + gridDim.x;
+  };
+  if (tid == 0) nxt_s = claim(blockIdx.x);
+  __syncthreads();
   double mat_next = (tid < 12 && blockIdx.x < P) ? mats[(int64_t)blockIdx.x * 12 + tid] : 0.0;
-  for (int64_t p = blockIdx.x; p < P; p += gridDim.x) {
+  for (int64_t p = blockIdx.x, nx = 0; p < P; p = nx) {
+    nx = nxt_s;  // (read by every thread before the barrier below; re-claimed after it)
     if (MP && tid < (int)(sizeof(PairDesc) / 4))
       reinterpret_cast<uint32_t*>(&desc_s)[tid] =
           reinterpret_cast<const uint32_t*>(pairs + pose_pair[p])[tid];
@@ -444,13 +455,14 @@ __global__ void __launch_bounds__(THREADS, 1)
     if (tid < 12) {
 #if VMI_MAT_PREFETCH
       mat_s[tid] = mat_next;
-      if (p + gridDim.x < P) mat_next = mats[(p + gridDim.x) * 12 + tid];
+      if (nx < P) mat_next = mats[nx * 12 + tid];
 #else
       mat_s[tid] = mats[p * 12 + tid];
       (void)mat_next;
 #endif
     }
     __syncthreads();
+    if (tid == 0) nxt_s = claim(nx);
     const RefView& A = MP ? desc_s.A : A0;
     const QueryView& B = MP ? desc_s.B : B0;
     const double m0 = mat_s[0], m1 = mat_s[1], m2 = mat_s[2], m3 = mat_s[3], m4 = mat_s[4],
@@ -1183,9 +1195,13 @@ static cudaError_t launch_fast_t(const FastLaunch& fl, cudaStream_t st) {
   if ((int)smem > optin) return cudaErrorInvalidValue;
   cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, optin);
   if (e != cudaSuccess) return e;
+  if (fl.sched) {
+    cudaError_t z = cudaMemsetAsync(fl.sched, 0, sizeof(unsigned int), st);
+    if (z != cudaSuccess) return z;
+  }
   k<<<fl.grid, THREADS, smem, st>>>(fl.g, fl.A, fl.B, fl.mats, fl.P, fl.cap, fl.mi, fl.status,
                                     fl.hist, fl.total, fl.dump, fl.sums, fl.npass, fl.pairs,
-                                    fl.pose_pair, fl.hash);
+                                    fl.pose_pair, fl.hash, fl.sched);
   return cudaGetLastError();
 }
 

@@ -8,6 +8,7 @@
 #include <cstdio>
 #include <algorithm>
 #include <array>
+#include <atomic>
 #include <cstdlib>
 #include <cstring>
 #include <chrono>
@@ -181,6 +182,8 @@ struct vmi_ctx {
   size_t cap_avox_tmp = 0, cap_akeys = 0, cap_avalues = 0, cap_upload = 0;
   void* d_upload = nullptr;  // staging for host uploads
   int* d_counter = nullptr;  // device scalar scratch
+  unsigned int* d_sched = nullptr;       // fast-kernel pose tickets, kSchedSlots (one per launch in flight)
+  std::atomic<unsigned> sched_next{0};
   void* d_fix = nullptr;     // re-planned re-runs: indices, matrices, outputs
   int64_t cap_fix = 0;
   long long* d_fix_hist = nullptr;
@@ -465,6 +468,21 @@ int32_t* pinned_status(const vmi_ctx* c) {
   return reinterpret_cast<int32_t*>(pinned_mi(c) + c->h_mats_cap);
 }
 
+// A ticket counter for one fast-kernel launch (dynamic pose scheduling): a
+// ring of slots, so launches in flight on other streams (the lockstep
+// optimiser's lanes) never share one; each launch zeroes its slot in stream
+// order.  VMI_SCHED=0: the static stride (A/B).
+constexpr unsigned kSchedSlots = 64;
+unsigned int* next_sched(vmi_ctx* c) {
+  static const bool off = [] { const char* e = std::getenv("VMI_SCHED"); return e && e[0] == '0'; }();
+  if (off) return nullptr;
+  if (!c->d_sched && cudaMalloc(&c->d_sched, kSchedSlots * sizeof(unsigned int)) != cudaSuccess) {
+    c->d_sched = nullptr;
+    return nullptr;
+  }
+  return c->d_sched + (c->sched_next.fetch_add(1) % kSchedSlots);
+}
+
 int check_ready(vmi_ctx* c) {
   if (!c) return VMI_ERR_ARG;
   if (!c->params_set) return fail(c, VMI_ERR_STATE, "vmi_set_params not called");
@@ -497,6 +515,7 @@ int launch_fast_eval(vmi_ctx* c, const double* mats_dev, int64_t P, double* mi, 
   fl.mats = mats_dev;
   fl.P = P;
   fl.grid = (int)(P < c->sm_count ? P : c->sm_count);
+  fl.sched = next_sched(c);
   fl.streams = c->streams;
   plan_table(c, fl.g.kind, c->cur.b_voxels, c->cur.is_f32, &fl.cap, &fl.npass, &fl.multi);
   int rc = ensure_sums(c, fl.g.kind, fl.grid, fl.cap);
@@ -648,7 +667,7 @@ int vmi_destroy(vmi_ctx* c) {
   release_pair(c->cur);
   for (auto& ps : c->set) release_pair(ps);
   release_scratch(c);
-  cudaFree(c->d_counter); cudaFree(c->d_fix); cudaFree(c->d_fix_hist);
+  cudaFree(c->d_counter); cudaFree(c->d_fix); cudaFree(c->d_fix_hist); cudaFree(c->d_sched);
   cudaFree(c->d_pairs); cudaFree(c->d_pose_pair); cudaFree(c->d_hash); cudaFree(c->d_setv);
   for (auto& l : c->lanes) {
     if (l.st) cudaStreamSynchronize(l.st);
@@ -1662,6 +1681,7 @@ int eval_pairs_device(vmi_ctx* c, int64_t P, const int32_t* pair_host, long long
   fl.mats = bf.mats;
   fl.P = P;
   fl.grid = (int)(P < c->sm_count ? P : c->sm_count);
+  fl.sched = next_sched(c);
   fl.streams = c->streams;
   plan_table(c, fl.g.kind, bvox, any_f64 ? 0 : 1, &fl.cap, &fl.npass, &fl.multi);
   fl.mi = bf.mi;

@@ -36,6 +36,7 @@ struct FastLaunch {
   const PairDesc* pairs = nullptr;
   const int32_t* pose_pair = nullptr;
   unsigned long long* hash = nullptr;  // per-pose 64-bit identity of the joint histogram
+  unsigned int* sched = nullptr;  // dynamic pose scheduling: a ticket counter (zeroed per launch)
 };
 size_t fast_smem_bytes(int kind, int cap, int bins, int threads, int f32, int ns, int multi);
 int fast_slot_bytes(int kind, int multi);  // shared-memory bytes per table slot
