@@ -52,6 +52,9 @@ def parse():
     ap.add_argument("--threads", type=int, default=0, help="CTA size (0 = library default)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--e2e-steps", type=int, default=3)
+    ap.add_argument("--rot", action="store_true",
+                    help="pose grids: rotation-major path (vmi_eval_rot_device; measured slower "
+                         "on B200, see DESIGN)")
     ap.add_argument("--config", default="c2", choices=["c1", "c1v", "c2", "c3", "c4", "c5"],
                     help="SURVEY.md 8(d) workload (c2 = the headline; c1v = C1's unordered "
                          "scans with the VARZ feature)")
@@ -470,7 +473,18 @@ def run_ours(args, world, rank, local):
     bytes_per_pose = rec_bytes * b.shape[0] + vb + 8.0
 
     stream = torch.cuda.Stream(device=local)
-    mats = torch.from_numpy(_lib.poses_to_mats(poses)).to(f"cuda:{local}")
+    mats_h = _lib.poses_to_mats(poses)
+    mats = torch.from_numpy(mats_h).to(f"cuda:{local}")
+    # pose grids (C1, C3): rotation-major -- scan B rotated once per distinct
+    # rotation, the point loop reads the rotated copy (vmi_eval_rot_device);
+    # the plan (grouping + permutation) is host preprocessing of the poses,
+    # like poses_to_mats; the rotation kernel itself is inside the timed step
+    rots_h, pm_h, ridx_h, perm_h = _lib.rotation_plan(poses, mats_h)
+    use_rot = args.rot and rots_h.shape[0] * 16 <= P
+    if use_rot:
+        dv = f"cuda:{local}"
+        d_rots, d_pm = torch.from_numpy(rots_h).to(dv), torch.from_numpy(pm_h).to(dv)
+        d_ridx, d_perm = torch.from_numpy(ridx_h).to(dv), torch.from_numpy(perm_h).to(dv)
     mi = torch.empty(P, dtype=torch.float64, device=f"cuda:{local}")
     st = torch.empty(P, dtype=torch.int32, device=f"cuda:{local}")
     flush = torch.empty(256 * 1024 * 1024 // 4, dtype=torch.float32, device=f"cuda:{local}")
@@ -482,10 +496,20 @@ def run_ours(args, world, rank, local):
         s = stream.cuda_stream
         if ev:
             ev[0].record(stream)
-        ctx.eval_device(mats.data_ptr(), P, mi.data_ptr(), st.data_ptr(), stream=s)
-        if ev:
-            ev[1].record(stream)
-        fixups_total += ctx.eval_fixups(mats.data_ptr(), P, mi.data_ptr(), st.data_ptr(), stream=s)
+        if use_rot:  # rotate + point loop + fix-ups + scatter to pose order
+            x0 = ctx.counters()["exact_poses"]
+            ctx.eval_rot_device(d_rots.data_ptr(), rots_h.shape[0], d_pm.data_ptr(),
+                                d_ridx.data_ptr(), d_perm.data_ptr(), P, mi.data_ptr(),
+                                st.data_ptr(), stream=s)
+            if ev:
+                ev[1].record(stream)
+            fixups_total += ctx.counters()["exact_poses"] - x0
+        else:
+            ctx.eval_device(mats.data_ptr(), P, mi.data_ptr(), st.data_ptr(), stream=s)
+            if ev:
+                ev[1].record(stream)
+            fixups_total += ctx.eval_fixups(mats.data_ptr(), P, mi.data_ptr(), st.data_ptr(),
+                                            stream=s)
         best, idx = ctx.argmax_device(mi.data_ptr(), P, stream=s)
         if dist is not None:
             with torch.cuda.stream(stream):
@@ -547,14 +571,18 @@ def run_ours(args, world, rank, local):
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": total_ms / args.steps, "higher_is_better": True,
         "scaling": wl.scaling, "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-        "config": config(args, world, wl, P),
+        "config": dict(config(args, world, wl, P), rotation_major=(
+            f"{rots_h.shape[0]} distinct rotations: scan B rotated once per rotation (k_rotate, "
+            "inside the timed step), the point loop reads the rotated copy" if use_rot else False)),
         "roofline": {
             "bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
             "frac": achieved / peak, "peak_source": peak_src,
             "traffic": prof["dram_bytes_per_launch"] if prof else None,
             "traffic_source": (f"{prof['source']} ({prof['poses_per_launch']} poses per launch)"
                                if prof else "no ncu capture of this config"),
-            "kernel": "k_pose_fast (K1, fused transform/voxelize/aggregate/histogram/MI)",
+            "kernel": ("k_pose_fast (K1, fused transform/voxelize/aggregate/histogram/MI)"
+                       + (" ROT instantiation (pre-rotated double4 records) + k_rotate + fix-up "
+                          "check + scatter to pose order" if use_rot else "")),
             "kernel_ms": kern_s * 1e3,
             "algorithmic_bytes_per_pose": bytes_per_pose,
             "mean_vb_in_aabb_a": vb,
@@ -562,7 +590,9 @@ def run_ours(args, world, rank, local):
             "issue_ceiling": issue_c,
             "fp64_ceiling": fp64_c,
         },
-        "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": int(P * 96),
+        "e2e": {"value": e2e_value, "unit": UNIT,
+                "h2d_bytes_per_step": int(P * 96 + ((P * 12 + rots_h.shape[0] * 96)
+                                                    if use_rot and P >= 4096 else 0)),
                 "d2h_bytes_per_step": int(P * 12),
                 "path": "MIEngine.evaluate(host poses P x 6 f64) -> host MI + status, "
                         "MIEngine.best (np.argmax + near-tie re-score); H2D = the P x 12 f64 "

@@ -140,6 +140,25 @@ int vmi_eval_fixups(vmi_ctx* ctx, const double* mats_dev, int64_t P, double* mi_
                     int64_t* n_fixed);
 #define VMI_FLAG_RECHECK 0x100
 
+/* Pose grids (rotations repeat): rotation-major evaluation.  Scan B is rotated
+   once per distinct rotation (R copies; rots12_dev: R x 12 matrices, rows 0-2
+   used) and the point loop reads the copy of rotation rot_idx_dev[q] for the
+   pose in slot q (mats_dev: P x 12, slots in rotation-major order so CTAs
+   share a copy in L2).  Fix-ups included (synchronous); results are written
+   at perm_dev[q] (the slot's pose in the caller's order), bit-identical to
+   vmi_eval_device + vmi_eval_fixups on the unpermuted batch.  Replaces the
+   per-pose transform of the reference's grid consumers (sweep_axis,
+   align.py:191-197; cli.py:202's grid argmax) for repeated rotations.
+   VMI_ERR_UNSUPPORTED: too many rotations for the memory budget (VMI_ROT_MB,
+   default 4096) or a table that needs the multi-pass layout.  With VMI_ROT=1,
+   vmi_eval_poses takes this path by itself for grid batches (>= 4096 poses,
+   distinct rotations <= P/16, no histograms).  Measured slower than the
+   per-pose path on B200 (the 32-byte rotated records double the point loop's
+   L2 traffic), hence opt-in. */
+int vmi_eval_rot_device(vmi_ctx* ctx, const double* rots12_dev, int64_t R, const double* mats_dev,
+                        const int32_t* rot_idx_dev, const int64_t* perm_dev, int64_t P,
+                        double* mi_dev, int32_t* status_dev, int64_t* total_dev, void* stream);
+
 /* Exact (sort-based, reference-order) evaluation of P poses: the slow
    cross-check path, bit-exact features by construction. */
 int vmi_eval_exact(vmi_ctx* ctx, const double* mats, int64_t P, double* mi_out,

@@ -27,7 +27,8 @@ EXPORTS = (
     "vmi_set_reference_points", "vmi_set_reference_records_f32", "vmi_set_reference_features", "vmi_get_reference_features",
     "vmi_set_query_points", "vmi_set_query_records_f32", "vmi_set_query_hull",
     "vmi_poses_to_mats", "vmi_eval",
-    "vmi_eval_poses", "vmi_eval_device", "vmi_eval_fixups", "vmi_eval_exact", "vmi_query_features",
+    "vmi_eval_poses", "vmi_eval_device", "vmi_eval_fixups", "vmi_eval_rot_device", "vmi_eval_exact",
+    "vmi_query_features",
     "vmi_fast_features",
     "vmi_argmax_device", "vmi_topk_device", "vmi_launch_count", "vmi_set_tuning", "vmi_set_passes",
     "vmi_nm_run", "vmi_set_pairs", "vmi_eval_pairs", "vmi_align_pairs", "vmi_get_counters",
@@ -131,6 +132,8 @@ def load(path: str = LIB_PATH):
     L.vmi_eval_poses.argtypes = [_ctx, _d, ctypes.c_int64, _d, _i32, _i64, _i64]
     L.vmi_eval_device.argtypes = [_ctx, _vp, ctypes.c_int64, _vp, _vp, _vp, _vp, _vp]
     L.vmi_eval_fixups.argtypes = [_ctx, _vp, ctypes.c_int64, _vp, _vp, _vp, _vp, _vp, _i64]
+    L.vmi_eval_rot_device.argtypes = [_ctx, _vp, ctypes.c_int64, _vp, _vp, _vp, ctypes.c_int64, _vp,
+                                      _vp, _vp, _vp]
     L.vmi_eval_exact.argtypes = [_ctx, _d, ctypes.c_int64, _d, _i32, _i64, _i64]
     L.vmi_query_features.argtypes = [_ctx, _d, _i64, _d, ctypes.c_int64, _i64, _i64, _i32]
     L.vmi_fast_features.argtypes = [_ctx, _d, _i64, _d, ctypes.c_int64, _i64, _i32]
@@ -157,6 +160,19 @@ def load(path: str = LIB_PATH):
 
 def ptr(a: np.ndarray, t):
     return a.ctypes.data_as(t)
+
+
+def rotation_plan(poses: np.ndarray, mats: np.ndarray):
+    """Rotation-major plan of a pose grid for vmi_eval_rot_device: (rots (R, 12)
+    one matrix per distinct (rx, ry, rz), mats in rotation-major slot order,
+    rot_idx (P,) i32 per slot, perm (P,) i64 = each slot's pose index)."""
+    poses = np.ascontiguousarray(poses, dtype=np.float64).reshape(-1, 6)
+    keys = np.ascontiguousarray(poses[:, 3:6]).view(np.uint64)
+    _, first, inv = np.unique(keys, axis=0, return_index=True, return_inverse=True)
+    inv = inv.reshape(-1)
+    perm = np.argsort(inv, kind="stable").astype(np.int64)
+    rots = np.ascontiguousarray(mats[first])
+    return rots, np.ascontiguousarray(mats[perm]), inv[perm].astype(np.int32), perm
 
 
 def poses_to_mats(poses: np.ndarray, threads: int = 0) -> np.ndarray:
@@ -373,6 +389,14 @@ class Context:
                     hist_ptr: int = 0, total_ptr: int = 0):
         self.check(self._L.vmi_eval_device(self._h, mats_ptr, P, mi_ptr, st_ptr, hist_ptr or None,
                                            total_ptr or None, stream or None), "vmi_eval_device")
+
+    def eval_rot_device(self, rots_ptr: int, R: int, mats_ptr: int, ridx_ptr: int, perm_ptr: int,
+                        P: int, mi_ptr: int, st_ptr: int, stream: int = 0, total_ptr: int = 0):
+        """vmi_eval_rot_device: a rotation-major plan (rotation_plan) on device
+        pointers; MI / statuses land in the caller's pose order (fix-ups done)."""
+        self.check(self._L.vmi_eval_rot_device(self._h, rots_ptr, R, mats_ptr, ridx_ptr, perm_ptr, P,
+                                               mi_ptr, st_ptr, total_ptr or None, stream or None),
+                   "vmi_eval_rot_device")
 
     def eval_fixups(self, mats_ptr: int, P: int, mi_ptr: int, st_ptr: int, stream: int = 0,
                     hist_ptr: int = 0, total_ptr: int = 0) -> int:

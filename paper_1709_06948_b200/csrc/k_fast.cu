@@ -98,9 +98,15 @@ __device__ __forceinline__ uint32_t slot_of(uint32_t lin, uint32_t cap) {
 #ifndef VMI_STAGES_OCC
 #define VMI_STAGES_OCC 3
 #endif
-template <bool F32, bool MULTI = false, int KIND = 0>
+// pre-rotated double4 records (ROT): a 3-deep ring of 32-byte records takes
+// the shared memory of the float4 path's 6-deep one
+#ifndef VMI_STAGES_ROT
+#define VMI_STAGES_ROT 3
+#endif
+template <bool F32, bool MULTI = false, int KIND = 0, bool ROT = false>
 __host__ __device__ constexpr int kStages() {
-  return MULTI ? VMI_STAGESM : (F32 ? (KIND == 2 ? VMI_STAGES_OCC : VMI_STAGES) : VMI_STAGES64);
+  return ROT ? VMI_STAGES_ROT
+             : MULTI ? VMI_STAGESM : (F32 ? (KIND == 2 ? VMI_STAGES_OCC : VMI_STAGES) : VMI_STAGES64);
 }
 template <typename Rec>
 __device__ __forceinline__ void cp_async_rec(uint32_t dst, const Rec* src) {
@@ -186,13 +192,13 @@ struct VarzTable {
 #ifndef VMI_PG64
 #define VMI_PG64 1
 #endif
-template <bool F32, bool MULTI>
+template <bool F32, bool MULTI, bool ROT = false>
 __host__ __device__ constexpr int kPGt() {  // points per queue push
-  return MULTI ? VMI_PGM : (F32 ? VMI_PG : VMI_PG64);
+  return ROT ? VMI_PG : MULTI ? VMI_PGM : (F32 ? VMI_PG : VMI_PG64);
 }
-template <bool F32, bool MULTI>
+template <bool F32, bool MULTI, bool ROT = false>
 __host__ __device__ constexpr int kQueueT() {  // warp queue entries: > 32*kPG + 31, pow2
-  return kPGt<F32, MULTI>() == 1 ? 64 : 128;
+  return kPGt<F32, MULTI, ROT>() == 1 ? 64 : 128;
 }
 
 // Shared-memory layout helper (bytes), mirrored by fast_smem_bytes() on the host.
@@ -206,15 +212,19 @@ __host__ __device__ inline FastSmem fast_layout(int kind, int cap, int W, int th
   FastSmem L;
   size_t off = 0;
   L.stage = off;
+  // f32: record kind -- 0 double4 input, 1 float4 split, 2 pre-rotated double4
   const int stages = multi ? kStages<true, true>()
+                           : f32 == 2 ? kStages<false, false, 0, true>()
                            : (f32 ? (kind == 2 ? kStages<true, false, 2>() : kStages<true>())
                                   : kStages<false>());
-  off += (size_t)threads * ns * (f32 ? 16 : 32) * stages;
+  off += (size_t)threads * ns * (f32 == 1 ? 16 : 32) * stages;
   L.table = off;
   off += (size_t)cap * slot_bytes(kind, multi);
   off = (off + 15) & ~size_t(15);
   L.queue = off;
-  const int queue = multi ? kQueueT<true, true>() : (f32 ? kQueueT<true, false>() : kQueueT<false, false>());
+  const int queue = multi ? kQueueT<true, true>()
+                  : f32 == 2 ? kQueueT<false, false, true>()
+                  : (f32 ? kQueueT<true, false>() : kQueueT<false, false>());
   // + one warp queue of slack: the kernel aligns the queues to their size
   off += (size_t)(threads / 32 + 1) * queue * rec_bytes(kind);
   off = (off + 15) & ~size_t(15);
@@ -341,7 +351,10 @@ __device__ __forceinline__ double pin_reg(double v) {
 
 // MP (multi-pair): pose p scores pair pose_pair[p] of pairs[] (descriptor
 // copied to shared memory per pose); otherwise the kernel parameters A0/B0.
-template <int THREADS, int NS, int KIND, bool F32, int MODE, bool MULTI, bool MP>
+// ROT (rotation-major grids): scan B's records are already rotated -- pose p
+// reads the double4 (R p)_xyz records of rotation rot_idx[p] (k_rotate), so
+// the per-point FMA chains are skipped; X = RN((R p)_x + t_x) as always.
+template <int THREADS, int NS, int KIND, bool F32, int MODE, bool MULTI, bool MP, bool ROT = false>
 __global__ void __launch_bounds__(THREADS, 1)
     k_pose_fast(GridParams g, const __grid_constant__ RefView A0,
                 const __grid_constant__ QueryView B0, const double* __restrict__ mats, int64_t P,
@@ -349,7 +362,9 @@ __global__ void __launch_bounds__(THREADS, 1)
                 long long* __restrict__ hist_out, long long* __restrict__ total_out,
                 FeatureDump dump, double2* __restrict__ gsums, int npass,
                 const PairDesc* __restrict__ pairs, const int32_t* __restrict__ pose_pair,
-                unsigned long long* __restrict__ hash_out, unsigned int* __restrict__ sched) {
+                unsigned long long* __restrict__ hash_out, unsigned int* __restrict__ sched,
+                const int32_t* __restrict__ rot_idx, int64_t rot_stride) {
+  static_assert(!ROT || (!F32 && !MULTI && !MP), "pre-rotated records: double4, single pass, one pair");
   static_assert(NS == 1, "one span per thread");
   static_assert(sizeof(PairDesc) % 4 == 0 && sizeof(PairDesc) / 4 <= THREADS, "descriptor copy");
   __shared__ __align__(16) PairDesc desc_s;
@@ -359,8 +374,8 @@ __global__ void __launch_bounds__(THREADS, 1)
   __shared__ long long nxt_s;                   // the CTA's next pose
   extern __shared__ __align__(16) unsigned char smem[];
   const int W = g.bins + 1;
-  const FastSmem L = fast_layout(KIND, cap, W, THREADS, F32 ? 1 : 0, NS, MULTI ? 1 : 0);
-  constexpr int kPG = kPGt<F32, MULTI>();
+  const FastSmem L = fast_layout(KIND, cap, W, THREADS, ROT ? 2 : (F32 ? 1 : 0), NS, MULTI ? 1 : 0);
+  constexpr int kPG = kPGt<F32, MULTI, ROT>();
   const uint32_t stage_base = (uint32_t)__cvta_generic_to_shared(smem + L.stage);
   uint32_t* hist = reinterpret_cast<uint32_t*>(smem + L.hist);
   uint32_t* marg = reinterpret_cast<uint32_t*>(smem + L.marg);
@@ -383,7 +398,7 @@ __global__ void __launch_bounds__(THREADS, 1)
   // warp queue: AoS records, VARZ 32 B {lin, n, -, -, S1, S2}, COUNT 8 B {lin, n},
   // occupancy 4 B {lin}
   constexpr uint32_t kRec = (uint32_t)rec_bytes(KIND);
-  constexpr int kQueue = kQueueT<F32, MULTI>();
+  constexpr int kQueue = kQueueT<F32, MULTI, ROT>();
   // Each warp's queue is aligned to its size QB, so a record address is
   // qbase | (byte offset mod QB): one LOP3 per push.
   constexpr uint32_t QB = (uint32_t)kQueue * kRec;
@@ -726,9 +741,9 @@ __global__ void __launch_bounds__(THREADS, 1)
           // an integer can floor differently from the reference, and such a
           // point (about 1 in 10^8) takes the reference's own X = RN(s + t) and
           // IEEE quotient.
-          const double sx = rot_row(x, y, z, m0, m1, m2);
-          const double sy = rot_row(x, y, z, m3, m4, m5);
-          const double sz = rot_row(x, y, z, m6, m7, m8);
+          const double sx = ROT ? x : rot_row(x, y, z, m0, m1, m2);
+          const double sy = ROT ? y : rot_row(x, y, z, m3, m4, m5);
+          const double sz = ROT ? z : rot_row(x, y, z, m6, m7, m8);
           // q' = RN(s * RN(1/res) + RN(u * RN(1/res))) in one FMA: besides the
           // rounding of c = u * RN(1/res) (|u / res| 2^-53 < 2^-32), the same
           // bound as RN(RN(s + u) * RN(1/res)).  VARZ keeps Zp = RN(s + u) for
@@ -764,9 +779,9 @@ __global__ void __launch_bounds__(THREADS, 1)
             lin = kNoVoxel;  // another pass's partition
           return;
         }
-        const double X = xform_row(x, y, z, m0, m1, m2, t0);
-        const double Y = xform_row(x, y, z, m3, m4, m5, t1);
-        const double sz = rot_row(x, y, z, m6, m7, m8);
+        const double X = ROT ? __dadd_rn(x, t0) : xform_row(x, y, z, m0, m1, m2, t0);
+        const double Y = ROT ? __dadd_rn(y, t1) : xform_row(x, y, z, m3, m4, m5, t1);
+        const double sz = ROT ? z : rot_row(x, y, z, m6, m7, m8);
         const double Z = __dadd_rn(sz, t2);  // = xform_row
         const double fx = __dadd_rd(grid_q<MODE>(X, g.origin[0], g.res, g.inv_res), kc0);
         const double fy = __dadd_rd(grid_q<MODE>(Y, g.origin[1], g.res, g.inv_res), kc1);
@@ -788,7 +803,8 @@ __global__ void __launch_bounds__(THREADS, 1)
       };
 
       using Rec = typename std::conditional<F32, float4, double4>::type;
-      const Rec* pts = reinterpret_cast<const Rec*>(B.pts) + tid;
+      const Rec* pts = reinterpret_cast<const Rec*>(B.pts) +
+                       (ROT ? (size_t)rot_idx[p] * (size_t)rot_stride : (size_t)0) + tid;
       const int full = B.span - 1;  // iterations every span owns
       // Scan-B records are staged through shared memory with cp.async: each
       // thread streams its own span S-1 records ahead into a private ring slot
@@ -797,7 +813,7 @@ __global__ void __launch_bounds__(THREADS, 1)
       // commit group from a running pointer; the span layout is padded with
       // kStagePadRows rows, so rows past the span are issued unconditionally
       // (and never read back).
-      constexpr int S = kStages<F32, MULTI, KIND>();
+      constexpr int S = kStages<F32, MULTI, KIND, ROT>();
       // (opaque: otherwise rebuilt from the CTA's shared window base, an
       // S2UR SR_CgaCtaId round trip, before every group)
       const uint32_t my_stage = pin_u32(stage_base + (uint32_t)tid * (uint32_t)sizeof(Rec));
@@ -996,10 +1012,10 @@ __global__ void __launch_bounds__(THREADS, 1)
         constexpr int NW = THREADS / 32;
         constexpr int kWR = MULTI ? VMI_WALK_RING_M : VMI_WALK_RING;  // ring entries; kWU ballots per scan step / entries per lane
         constexpr int kWU = kWR / 64;
-        static_assert(kStages<F32, MULTI, KIND>() * NS * (F32 ? 16 : 32) * 32 >= kWR * 4,
+        static_assert(kStages<F32, MULTI, KIND, ROT>() * NS * (F32 ? 16 : 32) * 32 >= kWR * 4,
                       "walk ring fits the warp's staging slice");
         uint32_t* wl = reinterpret_cast<uint32_t*>(
-            smem + L.stage + (size_t)wid * 32 * NS * (F32 ? 16 : 32) * kStages<F32, MULTI, KIND>());
+            smem + L.stage + (size_t)wid * 32 * NS * (F32 ? 16 : 32) * kStages<F32, MULTI, KIND, ROT>());
         const int per = ((cap + NW - 1) / NW + 31) & ~31;
         const int se = min(cap, wid * per + per);
         int scan = wid * per;
@@ -1176,10 +1192,11 @@ __global__ void __launch_bounds__(THREADS, 1)
   }
 }
 
-template <int THREADS, int NS, int KIND, bool F32, int MODE, bool MULTI, bool MP>
+template <int THREADS, int NS, int KIND, bool F32, int MODE, bool MULTI, bool MP, bool ROT = false>
 static cudaError_t launch_fast_t(const FastLaunch& fl, cudaStream_t st) {
-  auto k = k_pose_fast<THREADS, NS, KIND, F32, MODE, MULTI, MP>;
-  size_t smem = fast_smem_bytes(KIND, fl.cap, fl.g.bins, THREADS, F32 ? 1 : 0, NS, MULTI ? 1 : 0);
+  auto k = k_pose_fast<THREADS, NS, KIND, F32, MODE, MULTI, MP, ROT>;
+  size_t smem = fast_smem_bytes(KIND, fl.cap, fl.g.bins, THREADS, ROT ? 2 : (F32 ? 1 : 0), NS,
+                                MULTI ? 1 : 0);
   // The opt-in is set to the device maximum, never to this launch's size:
   // contexts on other host threads launch the same instantiation with other
   // table sizes, and a smaller per-launch value could land between another
@@ -1201,7 +1218,7 @@ static cudaError_t launch_fast_t(const FastLaunch& fl, cudaStream_t st) {
   }
   k<<<fl.grid, THREADS, smem, st>>>(fl.g, fl.A, fl.B, fl.mats, fl.P, fl.cap, fl.mi, fl.status,
                                     fl.hist, fl.total, fl.dump, fl.sums, fl.npass, fl.pairs,
-                                    fl.pose_pair, fl.hash, fl.sched);
+                                    fl.pose_pair, fl.hash, fl.sched, fl.rot_idx, fl.rot_stride);
   return cudaGetLastError();
 }
 
@@ -1219,8 +1236,19 @@ static cudaError_t launch_grid(const FastLaunch& fl, cudaStream_t st) {
 // table) also runs single-pass when scan B's voxels fit it but not the
 // single-pass table.
 // Multi-pair launches are single-pass only (the host plans them so).
+template <int T, int NS, int KIND>
+static cudaError_t launch_rot(const FastLaunch& fl, cudaStream_t st) {
+  if (fl.multi || fl.pairs || fl.B.is_f32) return cudaErrorInvalidValue;
+  switch (fl.g.mode) {
+    case kGridUnit: return launch_fast_t<T, NS, KIND, false, kGridUnit, false, false, true>(fl, st);
+    case kGridPow2: return launch_fast_t<T, NS, KIND, false, kGridPow2, false, false, true>(fl, st);
+    default: return launch_fast_t<T, NS, KIND, false, kGridGeneral, false, false, true>(fl, st);
+  }
+}
+
 template <int T, int NS, int KIND, bool F32>
 static cudaError_t launch_mode(const FastLaunch& fl, cudaStream_t st) {
+  if (fl.rot_idx) return launch_rot<T, NS, KIND>(fl, st);
   if (fl.pairs) {
     if (fl.multi) return cudaErrorInvalidValue;
     return launch_grid<T, NS, KIND, F32, false, true>(fl, st);
@@ -1237,6 +1265,33 @@ static cudaError_t launch_threads(const FastLaunch& fl, cudaStream_t st) {
   if (fl.g.kind == kKindCount)
     return f32 ? launch_mode<T, NS, 1, true>(fl, st) : launch_mode<T, NS, 1, false>(fl, st);
   return f32 ? launch_mode<T, NS, 2, true>(fl, st) : launch_mode<T, NS, 2, false>(fl, st);
+}
+
+// ---- rotation-major grids: scan B pre-rotated once per distinct rotation ----
+__global__ void k_rotate(const void* __restrict__ pts, int is_f32, int64_t n_rec,
+                         const double* __restrict__ rots12, double4* __restrict__ out) {
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n_rec) return;
+  const double* m = rots12 + 12 * (int64_t)blockIdx.y;
+  double x, y, z;
+  if (is_f32)
+    rec_xyz(reinterpret_cast<const float4*>(pts)[i], x, y, z);
+  else
+    rec_xyz(reinterpret_cast<const double4*>(pts)[i], x, y, z);
+  out[(int64_t)blockIdx.y * n_rec + i] =
+      make_double4(rot_row(x, y, z, m[0], m[1], m[2]), rot_row(x, y, z, m[3], m[4], m[5]),
+                   rot_row(x, y, z, m[6], m[7], m[8]), 0.0);
+}
+
+cudaError_t launch_rotate(const void* pts, int is_f32, int64_t rows, int threads,
+                          const double* rots12, int64_t R, void* out, cudaStream_t st) {
+  if (R <= 0) return cudaSuccess;
+  if (R > 65535) return cudaErrorInvalidValue;
+  const int64_t n = rows * threads;
+  const int T = 256;
+  k_rotate<<<dim3((unsigned)((n + T - 1) / T), (unsigned)R), T, 0, st>>>(
+      pts, is_f32, n, rots12, reinterpret_cast<double4*>(out));
+  return cudaGetLastError();
 }
 
 // NS = 2 (two spans per thread at 256 threads) compiles and is exact, but was

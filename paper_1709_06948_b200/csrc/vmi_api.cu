@@ -183,6 +183,22 @@ struct vmi_ctx {
   void* d_upload = nullptr;  // staging for host uploads
   int* d_counter = nullptr;  // device scalar scratch
   unsigned int* d_sched = nullptr;       // fast-kernel pose tickets, kSchedSlots (one per launch in flight)
+  // rotation-major grids (eval_rot): scan B rotated once per distinct rotation,
+  // the permuted batch's outputs, and (vmi_eval_poses) the plan on the device
+  void* d_rot = nullptr;
+  size_t cap_rot = 0;
+  double* d_rmi = nullptr;
+  int32_t* d_rst = nullptr;
+  long long* d_rtot = nullptr;
+  int64_t cap_rP = 0;
+  double* d_rots = nullptr;
+  size_t cap_rots = 0;
+  int32_t* d_ridx = nullptr;
+  size_t cap_ridx = 0;
+  int64_t* d_perm = nullptr;
+  size_t cap_perm = 0;
+  double* d_pmats = nullptr;
+  size_t cap_pmats = 0;
   std::atomic<unsigned> sched_next{0};
   void* d_fix = nullptr;     // re-planned re-runs: indices, matrices, outputs
   int64_t cap_fix = 0;
@@ -452,21 +468,26 @@ int ensure_P(vmi_ctx* c, int64_t P, bool hist) {
   return 0;
 }
 
-// Pinned host staging for P poses: matrices (P x 12 f64), then MI (f64) and
-// status (i32) read back; grow-only.
+// Pinned host staging for P poses: matrices (P x 12 f64), MI (f64) and status
+// (i32) read back, and a rotation-major plan (i64 permutation, i32 rotation
+// index); grow-only.
 int ensure_pinned(vmi_ctx* c, int64_t P) {
   if (P <= c->h_mats_cap) return 0;
   if (c->h_mats) cudaFreeHost(c->h_mats);
   c->h_mats = nullptr;
   c->h_mats_cap = 0;
-  CK(c, cudaMallocHost(&c->h_mats, (size_t)P * (96 + 12)));
+  CK(c, cudaMallocHost(&c->h_mats, (size_t)P * (96 + 12 + 12)));
   c->h_mats_cap = P;
   return 0;
 }
 double* pinned_mi(const vmi_ctx* c) { return c->h_mats + 12 * c->h_mats_cap; }
-int32_t* pinned_status(const vmi_ctx* c) {
-  return reinterpret_cast<int32_t*>(pinned_mi(c) + c->h_mats_cap);
+int64_t* pinned_perm(const vmi_ctx* c) {
+  return reinterpret_cast<int64_t*>(pinned_mi(c) + c->h_mats_cap);
 }
+int32_t* pinned_status(const vmi_ctx* c) {
+  return reinterpret_cast<int32_t*>(pinned_perm(c) + c->h_mats_cap);
+}
+int32_t* pinned_ridx(const vmi_ctx* c) { return pinned_status(c) + c->h_mats_cap; }
 
 // A ticket counter for one fast-kernel launch (dynamic pose scheduling): a
 // ring of slots, so launches in flight on other streams (the lockstep
@@ -625,6 +646,118 @@ int do_fixups(vmi_ctx* c, const double* mats_dev, int64_t P, double* mi, int32_t
   return 0;
 }
 
+// Rotation-major evaluation of a batch whose rotations repeat (pose grids):
+// scan B is rotated once per distinct rotation (k_rotate, R copies of its
+// span layout as double4 (R p) records), then one fast launch reads, for the
+// pose in slot q, rotation ridx[q]'s copy -- the per-point FMA chains are done
+// R times instead of P times, every other step is the point loop's own, so
+// results are bit-identical to launch_fast_eval.  Slots are in rotation-major
+// order (mats: the permuted matrices) so the CTAs, which take slots in order,
+// share one rotation's copy in L2; perm[q] is slot q's pose in the caller's
+// order, where the MI / statuses / totals are scattered after the fix-ups.
+int64_t rot_stride(const vmi_ctx* c) {
+  return (int64_t)(c->cur.span + kStagePadRows) * c->threads;
+}
+double rot_budget_bytes() {
+  static const double b = [] {
+    const char* e = std::getenv("VMI_ROT_MB");  // device memory for the rotated copies
+    return (e ? std::atof(e) : 4096.0) * 1048576.0;
+  }();
+  return b;
+}
+int eval_rot(vmi_ctx* c, const double* rots12, int64_t R, const double* mats, const int32_t* ridx,
+             const int64_t* perm, int64_t P, double* mi, int32_t* st, long long* total,
+             cudaStream_t stream) {
+  if (P <= 0) return 0;
+  const PairStore& ps = c->cur;
+  const int64_t stride = rot_stride(c);
+  if (R <= 0 || R > 65535 || (double)R * stride * 32.0 > rot_budget_bytes())
+    return fail(c, VMI_ERR_UNSUPPORTED, "rotation-major plan: too many distinct rotations");
+  CK(c, grow(reinterpret_cast<char**>(&c->d_rot), c->cap_rot, (size_t)(R * stride * 32)));
+  if (P > c->cap_rP) {
+    cudaFree(c->d_rmi); cudaFree(c->d_rst); cudaFree(c->d_rtot);
+    c->d_rmi = nullptr; c->d_rst = nullptr; c->d_rtot = nullptr; c->cap_rP = 0;
+    CK(c, cudaMalloc(&c->d_rmi, (size_t)P * 8));
+    CK(c, cudaMalloc(&c->d_rst, (size_t)P * 4));
+    CK(c, cudaMalloc(&c->d_rtot, (size_t)P * 8));
+    c->cap_rP = P;
+  }
+  CK(c, launch_rotate(ps.d_pts, ps.is_f32, ps.span + kStagePadRows, c->threads, rots12, R,
+                      c->d_rot, stream));
+  FastLaunch fl{};
+  fl.g = c->g;
+  fl.g.kind = kernel_kind(c);
+  fl.A = ref_view(ps);
+  fl.B = query_view(c, ps);
+  fl.B.pts = c->d_rot;
+  fl.B.is_f32 = 0;
+  fl.rot_idx = ridx;
+  fl.rot_stride = stride;
+  fl.mats = mats;
+  fl.P = P;
+  fl.grid = (int)(P < c->sm_count ? P : c->sm_count);
+  fl.sched = next_sched(c);
+  fl.streams = c->streams;
+  plan_table(c, fl.g.kind, ps.b_voxels, 2, &fl.cap, &fl.npass, &fl.multi);
+  if (fl.multi)  // (the rotated kernel is single-pass: scan B's voxels fit one table)
+    return fail(c, VMI_ERR_UNSUPPORTED, "rotation-major plan: multi-pass table");
+  int rc = ensure_sums(c, fl.g.kind, fl.grid, fl.cap);
+  if (rc) return rc;
+  fl.sums = c->d_sums;
+  fl.mi = c->d_rmi;
+  fl.status = c->d_rst;
+  fl.total = c->d_rtot;
+  CK(c, launch_fast(fl, stream));
+  c->launches += 2;
+  if ((rc = do_fixups(c, mats, P, c->d_rmi, c->d_rst, nullptr, c->d_rtot, stream, nullptr))) return rc;
+  CK(c, gather_rows<double>(c->d_rmi, perm, P, 1, mi, true, stream));
+  CK(c, gather_rows<int32_t>(c->d_rst, perm, P, 1, st, true, stream));
+  if (total) CK(c, gather_rows<long long>(c->d_rtot, perm, P, 1, total, true, stream));
+  c->launches += total ? 3 : 2;
+  return 0;
+}
+
+// Distinct rotations of P EulerPose rows (by the bits of rx, ry, rz: equal
+// angles give bit-equal matrices): ridx[p] in [0, R), rep[r] = the first pose
+// of rotation r.  Returns R, or -1 as soon as more than max_r are seen.
+int64_t group_rotations(const double* poses, int64_t P, int64_t max_r, int32_t* ridx,
+                        std::vector<int64_t>& rep) {
+  size_t cap = 64;
+  while (cap < 2 * (size_t)max_r + 2) cap <<= 1;
+  struct Slot { uint64_t k[3]; int32_t id; };
+  std::vector<Slot> tab(cap, Slot{{0, 0, 0}, -1});
+  rep.clear();
+  uint64_t last[3] = {~0ull, ~0ull, ~0ull};
+  int32_t last_id = -1;
+  for (int64_t p = 0; p < P; ++p) {
+    uint64_t k[3];
+    std::memcpy(k, poses + 6 * p + 3, 24);
+    if (last_id >= 0 && k[0] == last[0] && k[1] == last[1] && k[2] == last[2]) {
+      ridx[p] = last_id;
+      continue;
+    }
+    uint64_t h = k[0] * 0x9E3779B97F4A7C15ull ^ (k[1] + 0x632BE59BD9B4E019ull) * 0xC2B2AE3D27D4EB4Full ^
+                 (k[2] + 0x165667B19E3779F9ull) * 0x27D4EB2F165667C5ull;
+    h ^= h >> 29;
+    size_t i = (size_t)h & (cap - 1);
+    for (;; i = (i + 1) & (cap - 1)) {
+      Slot& sl = tab[i];
+      if (sl.id < 0) {
+        if ((int64_t)rep.size() >= max_r) return -1;
+        sl.k[0] = k[0]; sl.k[1] = k[1]; sl.k[2] = k[2];
+        sl.id = (int32_t)rep.size();
+        rep.push_back(p);
+        break;
+      }
+      if (sl.k[0] == k[0] && sl.k[1] == k[1] && sl.k[2] == k[2]) break;
+    }
+    ridx[p] = tab[i].id;
+    last[0] = k[0]; last[1] = k[1]; last[2] = k[2];
+    last_id = tab[i].id;
+  }
+  return (int64_t)rep.size();
+}
+
 }  // namespace
 
 extern "C" {
@@ -668,6 +801,8 @@ int vmi_destroy(vmi_ctx* c) {
   for (auto& ps : c->set) release_pair(ps);
   release_scratch(c);
   cudaFree(c->d_counter); cudaFree(c->d_fix); cudaFree(c->d_fix_hist); cudaFree(c->d_sched);
+  cudaFree(c->d_rot); cudaFree(c->d_rmi); cudaFree(c->d_rst); cudaFree(c->d_rtot);
+  cudaFree(c->d_rots); cudaFree(c->d_ridx); cudaFree(c->d_perm); cudaFree(c->d_pmats);
   cudaFree(c->d_pairs); cudaFree(c->d_pose_pair); cudaFree(c->d_hash); cudaFree(c->d_setv);
   for (auto& l : c->lanes) {
     if (l.st) cudaStreamSynchronize(l.st);
@@ -1046,6 +1181,19 @@ int vmi_eval_fixups(vmi_ctx* c, const double* mats_dev, int64_t P, double* mi_de
                    stream ? (cudaStream_t)stream : c->stream, n_fixed);
 }
 
+int vmi_eval_rot_device(vmi_ctx* c, const double* rots12_dev, int64_t R, const double* mats_dev,
+                        const int32_t* rot_idx_dev, const int64_t* perm_dev, int64_t P,
+                        double* mi_dev, int32_t* status_dev, int64_t* total_dev, void* stream) {
+  int rc = check_ready(c);
+  if (rc) return rc;
+  if (P < 0 || (P > 0 && (!rots12_dev || !mats_dev || !rot_idx_dev || !perm_dev || !mi_dev ||
+                          !status_dev)))
+    return fail(c, VMI_ERR_ARG, "bad arguments");
+  cudaSetDevice(c->device);
+  return eval_rot(c, rots12_dev, R, mats_dev, rot_idx_dev, perm_dev, P, mi_dev, status_dev,
+                  (long long*)total_dev, stream ? (cudaStream_t)stream : c->stream);
+}
+
 int vmi_eval(vmi_ctx* c, const double* mats, int64_t P, double* mi_out, int32_t* status_out,
              int64_t* hist_out, int64_t* total_out) {
   int rc = check_ready(c);
@@ -1076,6 +1224,67 @@ extern "C" int vmi_poses_to_mats(const double* poses, int64_t n, double* mats, i
 // memory, uploaded and launched; the host converts the rest while that kernel
 // runs, and their upload runs on a second stream beside it.  Same results as
 // vmi_poses_to_mats + vmi_eval.
+// vmi_eval_poses on a pose grid (rotations repeat): all matrices on the host
+// pool, the rotation plan (group_rotations, a stable counting sort into
+// rotation-major slots), then eval_rot.  Returns 1 when the batch is not a
+// grid (the caller takes the pipelined path), 0 on success, < 0 on error.
+static int eval_poses_rot(vmi_ctx* c, const double* poses, int64_t P, double* mi_out,
+                          int32_t* status_out, int64_t* total_out) {
+  // Opt-in (VMI_ROT=1): measured slower on B200 -- the rotated copies are
+  // 32-byte double4 records (the exact f64 chain results), twice the float4
+  // split records' L2 traffic, and the point loop becomes L2-bound (C3 529 ms
+  // vs 388 ms per 970,299 poses; C1 1.94 vs 1.69 ms).
+  const char* on = std::getenv("VMI_ROT");
+  if (!on || on[0] != '1' || P < 4096 || c->cur.sparse) return 1;
+  int32_t* ridx = pinned_ridx(c);
+  std::vector<int64_t> rep;
+  if (group_rotations(poses, std::min<int64_t>(P, 4096), 512, ridx, rep) < 0) return 1;  // random poses
+  const int64_t R = group_rotations(poses, P, std::min<int64_t>(P / 16, 65535), ridx, rep);
+  if (R <= 0 || (double)R * rot_stride(c) * 32.0 > rot_budget_bytes()) return 1;
+  {  // the rotated kernel is single-pass: skip grids whose table would need passes
+    int cap = 0, np = 0, multi = 0;
+    plan_table(c, kernel_kind(c), c->cur.b_voxels, 2, &cap, &np, &multi);
+    if (multi) return 1;
+  }
+  if (vmi_poses_to_mats(poses, P, c->h_mats, 0)) return fail(c, VMI_ERR_ARG, "poses_to_mats");
+  // stable counting sort by rotation: perm[q] = the pose in slot q
+  int64_t* perm = pinned_perm(c);
+  int32_t* ridx_q = pinned_status(c);  // (scratch until the statuses come back)
+  std::vector<int64_t> start((size_t)R + 1, 0);
+  for (int64_t p = 0; p < P; ++p) ++start[(size_t)ridx[p] + 1];
+  for (int64_t r = 0; r < R; ++r) start[(size_t)r + 1] += start[(size_t)r];
+  for (int64_t p = 0; p < P; ++p) {
+    const int64_t q = start[(size_t)ridx[p]]++;
+    perm[q] = p;
+    ridx_q[q] = ridx[p];
+  }
+  std::vector<double> rots((size_t)R * 12);
+  for (int64_t r = 0; r < R; ++r)
+    std::memcpy(&rots[(size_t)r * 12], c->h_mats + 12 * rep[(size_t)r], 96);
+  CK(c, grow(&c->d_rots, c->cap_rots, (size_t)R * 96));
+  CK(c, grow(&c->d_ridx, c->cap_ridx, (size_t)P * 4));
+  CK(c, grow(&c->d_perm, c->cap_perm, (size_t)P * 8));
+  CK(c, grow(&c->d_pmats, c->cap_pmats, (size_t)P * 96));
+  CK(c, cudaMemcpyAsync(c->d_mats, c->h_mats, (size_t)P * 96, cudaMemcpyHostToDevice, c->stream));
+  CK(c, cudaMemcpyAsync(c->d_perm, perm, (size_t)P * 8, cudaMemcpyHostToDevice, c->stream));
+  CK(c, cudaMemcpyAsync(c->d_ridx, ridx_q, (size_t)P * 4, cudaMemcpyHostToDevice, c->stream));
+  CK(c, cudaMemcpyAsync(c->d_rots, rots.data(), (size_t)R * 96, cudaMemcpyHostToDevice, c->stream));
+  CK(c, gather_rows<double>(c->d_mats, c->d_perm, P, 12, c->d_pmats, false, c->stream));
+  c->launches += 1;
+  int rc = eval_rot(c, c->d_rots, R, c->d_pmats, c->d_ridx, c->d_perm, P, c->d_mi, c->d_status,
+                    total_out ? c->d_total : nullptr, c->stream);
+  if (rc) return rc;
+  double* hmi = pinned_mi(c);
+  int32_t* hst = pinned_status(c);
+  CK(c, cudaMemcpyAsync(hmi, c->d_mi, P * 8, cudaMemcpyDeviceToHost, c->stream));
+  CK(c, cudaMemcpyAsync(hst, c->d_status, P * 4, cudaMemcpyDeviceToHost, c->stream));
+  if (total_out) CK(c, cudaMemcpyAsync(total_out, c->d_total, P * 8, cudaMemcpyDeviceToHost, c->stream));
+  CK(c, cudaStreamSynchronize(c->stream));
+  std::memcpy(mi_out, hmi, (size_t)P * 8);
+  std::memcpy(status_out, hst, (size_t)P * 4);
+  return 0;
+}
+
 int vmi_eval_poses(vmi_ctx* c, const double* poses, int64_t P, double* mi_out, int32_t* status_out,
                    int64_t* hist_out, int64_t* total_out) {
   int rc = check_ready(c);
@@ -1084,6 +1293,10 @@ int vmi_eval_poses(vmi_ctx* c, const double* poses, int64_t P, double* mi_out, i
   if (P == 0) return 0;
   cudaSetDevice(c->device);
   if ((rc = ensure_P(c, P, hist_out != nullptr)) || (rc = ensure_pinned(c, P))) return rc;
+  if (!hist_out) {  // pose grids: rotation-major (one rotated scan B per distinct rotation)
+    rc = eval_poses_rot(c, poses, P, mi_out, status_out, total_out);
+    if (rc <= 0) return rc;
+  }
   if (!c->copy_stream) CK(c, cudaStreamCreateWithFlags(&c->copy_stream, cudaStreamNonBlocking));
   if (!c->copy_done) CK(c, cudaEventCreateWithFlags(&c->copy_done, cudaEventDisableTiming));
   static const bool trace = std::getenv("VMI_TRACE") != nullptr;  // phase timings to stderr

@@ -37,7 +37,17 @@ struct FastLaunch {
   const int32_t* pose_pair = nullptr;
   unsigned long long* hash = nullptr;  // per-pose 64-bit identity of the joint histogram
   unsigned int* sched = nullptr;  // dynamic pose scheduling: a ticket counter (zeroed per launch)
+  // rotation-major grids: B.pts = k_rotate's output, pose p reads rotation
+  // rot_idx[p]'s records (rot_stride records apart); B.is_f32 must be 0
+  const int32_t* rot_idx = nullptr;
+  int64_t rot_stride = 0;
 };
+// Scan B's fast layout (span layout, float4 split or double4 records) rotated
+// by each of R matrices (rows 0-2 of mats12[r*12..]): out[r*stride + i] =
+// double4((R p_i)_x, (R p_i)_y, (R p_i)_z, 0) with the kernel's FMA chains
+// (bit-identical to what the point loop computes); stride = rows * threads.
+cudaError_t launch_rotate(const void* pts, int is_f32, int64_t rows, int threads,
+                          const double* rots12, int64_t R, void* out, cudaStream_t st);
 size_t fast_smem_bytes(int kind, int cap, int bins, int threads, int f32, int ns, int multi);
 int fast_slot_bytes(int kind, int multi);  // shared-memory bytes per table slot
 cudaError_t launch_fast(const FastLaunch& fl, cudaStream_t st);

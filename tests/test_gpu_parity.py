@@ -938,3 +938,89 @@ def test_reference_aabb_over_2_32_voxels_matches_oracle(kind):
         assert_mi_close([mi[i]], [omi])
     assert eng.ctx.counters()["exact_poses"] >= len(poses)
     eng.close()
+
+
+def _grid_batch(n_rot=5, n_trans=1024, seed=11, far=False):
+    """A pose grid: n_rot rotations x n_trans translations, shuffled so slots
+    and poses differ (optionally with out-of-range / far translations)."""
+    rng = np.random.default_rng(seed)
+    rots = rng.uniform(-1, 1, size=(n_rot, 3)) * np.array([0.03, 0.03, 0.4])
+    trans = rng.uniform(-1, 1, size=(n_trans, 3)) * np.array([4.0, 4.0, 0.3])
+    if far:
+        trans[:7] = [[3e6, 0, 0], [1e4, 0, 0], [0, -2e3, 0], [0, 0, 5e2], [2e6, 0, 0], [0, 9e5, 0],
+                     [1.5e3, 1.5e3, 0]]
+    poses = np.concatenate([np.repeat(trans, n_rot, axis=0), np.tile(rots, (n_trans, 1))], axis=1)
+    return poses[rng.permutation(len(poses))]
+
+
+@pytest.mark.parametrize("tag,res,kind", [("c1", 0.5, "count"), ("c1", 0.5, "varz"),
+                                          ("hdl", 1.0, "varz"), ("hdl", 0.3, "varz"),
+                                          ("hdl", 0.2, "varz"), ("hdl", 1.0, "count")])
+def test_rotation_major_grid_equals_plain(monkeypatch, tag, res, kind):
+    """Pose grids go rotation-major (scan B rotated once per distinct rotation,
+    k_rotate + the ROT point loop): MIEngine.evaluate takes that path by itself
+    and vmi_eval_rot_device is its device form.  Both equal the plain
+    per-pose path (vmi_eval) bit for bit, fix-ups (far / out-of-range
+    translations) included, in the caller's pose order."""
+    import torch
+    from paper_1709_06948_b200 import _lib
+    a, b = hdl_pair()
+    if tag == "c1":
+        s = golden("c1_scans.npz")
+        a, b = s["a"], s["b"]
+    monkeypatch.setenv("VMI_ROT", "1")  # (opt-in: measured slower, see DESIGN)
+    poses = _grid_batch(far=True)
+    eng = engine(res, kind=kind)
+    eng.set_reference(np.asarray(a)[:, :3].astype(np.float64), fetch=False)
+    eng.set_query(b)
+    mats = vmi.poses_to_mats(poses)
+    mi0, st0 = eng.evaluate_mats(mats)           # plain path
+    mi1, st1 = eng.evaluate(poses)                # auto: rotation-major
+    np.testing.assert_array_equal(mi1, mi0)
+    np.testing.assert_array_equal(st1, st0)
+    assert (st0 != 0).any() and (st0 == 0).sum() > len(poses) // 2
+    rots, pm, ridx, perm = _lib.rotation_plan(poses, mats)
+    assert rots.shape[0] == 5
+    dev = torch.device("cuda:0")
+    t = lambda x: torch.from_numpy(np.ascontiguousarray(x)).to(dev)
+    d_rots, d_pm, d_ridx, d_perm = t(rots), t(pm), t(ridx), t(perm)
+    mi = torch.empty(len(poses), dtype=torch.float64, device=dev)
+    st = torch.empty(len(poses), dtype=torch.int32, device=dev)
+    try:
+        eng.ctx.eval_rot_device(d_rots.data_ptr(), rots.shape[0], d_pm.data_ptr(),
+                                d_ridx.data_ptr(), d_perm.data_ptr(), len(poses), mi.data_ptr(),
+                                st.data_ptr())
+    except Exception as e:  # a table that needs passes: the plain path serves it (above)
+        assert "multi-pass" in str(e), e
+        eng.close()
+        return
+    torch.cuda.synchronize()
+    np.testing.assert_array_equal(mi.cpu().numpy(), mi0)
+    np.testing.assert_array_equal(st.cpu().numpy(), st0)
+    eng.close()
+
+
+def test_rotation_major_grid_matches_oracle_and_random_batches_stay_plain(monkeypatch):
+    """Spot-check a rotation-major C1 batch against the oracle (MI within 1e-6,
+    statuses equal), and check that a random batch (no repeated rotations) is
+    evaluated identically whichever way it is submitted."""
+    monkeypatch.setenv("VMI_ROT", "1")
+    s = golden("c1_scans.npz")
+    a, b = np.asarray(s["a"])[:, :3], np.asarray(s["b"])[:, :3]
+    eng = engine(0.5, kind="count")
+    eng.set_reference(a)
+    eng.set_query(b)
+    poses = _grid_batch(n_rot=4, n_trans=1200, seed=3)
+    mi, st = eng.evaluate(poses)
+    fa = oracle.feature_map(a, (0, 0, 0), 0.5, "count")
+    idx = np.arange(0, len(poses), 97)
+    omi, ost = oracle.mi_objective_batch(fa, b, oracle.poses_to_mats(poses[idx]), res=0.5)
+    np.testing.assert_array_equal(st[idx], ost)
+    assert_mi_close(mi[idx], omi)
+    from paper_1709_06948_b200.synth import candidate_batch
+    rnd = candidate_batch(EulerPose(1.0, 0.5, 0, 0, 0, 0.1), 5000, seed=9)
+    m1, s1 = eng.evaluate(rnd)
+    m0, s0 = eng.evaluate_mats(vmi.poses_to_mats(rnd))
+    np.testing.assert_array_equal(m1, m0)
+    np.testing.assert_array_equal(s1, s0)
+    eng.close()
