@@ -41,7 +41,8 @@ def main() -> None:
     st = torch.empty(P, dtype=torch.int32, device="cuda")
     eng.evaluate(poses)
     eng.ctx.eval(mats_h)
-    rows = {k: [] for k in ("conv", "evaluate", "eval_mats", "device", "best")}
+    rows = {k: [] for k in ("conv", "evaluate", "eval_mats", "device", "device_split", "best")}
+    head = max(2048, P // 32)
     for _ in range(args.reps):
         t0 = time.perf_counter()
         _lib.poses_to_mats(poses)
@@ -61,6 +62,12 @@ def main() -> None:
         eng.ctx.eval_device(mats.data_ptr(), P, mi.data_ptr(), st.data_ptr())
         torch.cuda.synchronize()
         rows["device"].append(time.perf_counter() - t0)
+        t0 = time.perf_counter()  # the head / tail launches vmi_eval_poses makes
+        eng.ctx.eval_device(mats.data_ptr(), head, mi.data_ptr(), st.data_ptr())
+        eng.ctx.eval_device(mats[head:].data_ptr(), P - head, mi[head:].data_ptr(),
+                            st[head:].data_ptr())
+        torch.cuda.synchronize()
+        rows["device_split"].append(time.perf_counter() - t0)
     for k, v in rows.items():
         print(f"{args.config} {k:10s} {np.median(v) * 1e3:8.3f} ms  (min {np.min(v) * 1e3:.3f})")
 
