@@ -65,6 +65,9 @@ __device__ __forceinline__ uint32_t slot_of(uint32_t lin, uint32_t cap) {
 // per-point pivot arithmetic.  The per-point offset r (|r| <= 2^-53 |Z|) moves
 // a voxel's variance by at most res |r|max + r^2 (var_shift), and the sums'
 // own rounding is bounded through S2 + S1^2/n whatever the pivot.
+#ifndef VMI_OCC_BUCKET  // occupancy kind: 4-slot buckets (see flush_rec)
+#define VMI_OCC_BUCKET 1
+#endif
 #ifndef VMI_PIN_CONST  // general resolutions: AABB extents / 1/res in registers in the point loop
 #define VMI_PIN_CONST 1
 #endif
@@ -619,6 +622,34 @@ __global__ void __launch_bounds__(THREADS, 1)
             else atomicAdd(&hist[ba_occ * W + g.occ_bin], 1u);  // (injected A features)
           }
         };
+        if constexpr (KIND == kKindOcc && VMI_OCC_BUCKET) {
+          // Occupancy keys in 16-byte buckets of four slots: one LDS.128 finds
+          // the key or the bucket's first free slot (a CAS there), so nearly
+          // every lane is done in one round -- linear probing one slot at a
+          // time kept a few lanes (and the warp) in the probe loop on most
+          // drains.  Keys are never removed during a pose, so every lane with
+          // a given key walks the same buckets to the same first free slot.
+          if (!has) return;
+          const uint32_t nb = ucap >> 2;
+          uint32_t b = slot_of(r0.x, nb);
+          for (uint32_t probes = 0;;) {
+            const uint32_t ba = key_sa + 16u * b;
+            const uint4 w = ld_shared_v4(ba);
+            if (w.x == r0.x || w.y == r0.x || w.z == r0.x || w.w == r0.x) break;  // present
+            const uint32_t j = w.x == kEmpty32 ? 0u : w.y == kEmpty32 ? 1u
+                             : w.z == kEmpty32 ? 2u : w.w == kEmpty32 ? 3u : 4u;
+            if (j == 4u) {  // full: the next bucket
+              if (++b == nb) b = 0;
+              if (++probes >= nb) { misc[7] = 1; break; }  // table full -> exact path
+              continue;
+            }
+            const uint32_t old = atom_cas_shared(ba + 4u * j, kEmpty32, r0.x);
+            if (old == kEmpty32) { count_new(); break; }
+            if (old == r0.x) break;
+            // another key took that slot: read the bucket again
+          }
+          return;
+        }
         // first probe = one CAS (hit or insert), no branch before the atomics;
         // shared-window addresses (key_sa / cnt_sa) avoid generic -> shared
         // conversions in this loop
