@@ -18,6 +18,7 @@ from .types import (DEFAULT_BIN_COUNT, DEFAULT_UPPER_CLAMP, KEY_INDEX_MAX, KEY_I
                     NO_OVERLAP_SENTINEL, AlignmentConfig, BinningSpec, FeatureKind, FeatureMap,
                     GridSpec, JointHistogram, MIResult)
 from ._lib import VmiError, poses_to_mats
+from .scan_io import load_kitti_bin, save_kitti_bin
 
 __all__ = [
     "AlignmentReport", "align", "align_batch", "OptimResult", "SimplexConfig", "nelder_mead_maximize_batched",
@@ -30,5 +31,5 @@ __all__ = [
     "as_pose_array", "euler_to_transform", "DEFAULT_BIN_COUNT", "DEFAULT_UPPER_CLAMP",
     "KEY_INDEX_MAX", "KEY_INDEX_MIN", "NO_OVERLAP_SENTINEL", "AlignmentConfig", "BinningSpec",
     "FeatureKind", "FeatureMap", "GridSpec", "JointHistogram", "MIResult", "VmiError",
-    "poses_to_mats",
+    "poses_to_mats", "load_kitti_bin", "save_kitti_bin",
 ]
