@@ -184,6 +184,8 @@ def poses_to_mats(poses: np.ndarray, threads: int = 0) -> np.ndarray:
     poses = np.ascontiguousarray(poses, dtype=np.float64).reshape(-1, 6)
     out = np.empty((poses.shape[0], 12), dtype=np.float64)
     rc = load().vmi_poses_to_mats(ptr(poses, _d), poses.shape[0], ptr(out, _d), int(threads))
+    if rc == -2:
+        raise ValueError("poses contain non-finite components")
     if rc:
         raise VmiError(f"vmi_poses_to_mats failed ({rc})")
     return out
@@ -205,7 +207,7 @@ class Context:
     def check(self, rc: int, what: str):
         if rc:
             msg = self._L.vmi_last_error(self._h).decode()
-            if rc == -1 and "empty cloud" in msg:
+            if rc == -1 and ("empty cloud" in msg or "non-finite components" in msg):
                 raise ValueError(msg)
             if rc == -1:
                 raise ValueError(f"{what}: {msg}")

@@ -92,10 +92,14 @@ Pool& pool() {
 
 extern "C" int vmi_poses_to_mats(const double* poses, int64_t n, double* mats, int threads) {
   if (n < 0 || (n > 0 && (!poses || !mats))) return -1;
+  std::atomic<bool> bad{false};  // a non-finite component: -2 (EulerPose validation, geometry.py:68-102)
   auto work = [&](int64_t lo, int64_t hi) {
+    bool nf = false;
     for (int64_t p = lo; p < hi; ++p) {
       const double* v = poses + 6 * p;
       double* m = mats + 12 * p;
+      nf |= !(std::isfinite(v[0]) && std::isfinite(v[1]) && std::isfinite(v[2]) &&
+              std::isfinite(v[3]) && std::isfinite(v[4]) && std::isfinite(v[5]));
       const double sr = std::sin(v[3]), cr = std::cos(v[3]);
       const double sp = std::sin(v[4]), cp = std::cos(v[4]);
       const double sy = std::sin(v[5]), cy = std::cos(v[5]);
@@ -112,6 +116,7 @@ extern "C" int vmi_poses_to_mats(const double* poses, int64_t n, double* mats, i
       m[10] = v[1];
       m[11] = v[2];
     }
+    if (nf) bad.store(true);
   };
   int hw = (int)std::thread::hardware_concurrency();
   if (threads <= 0) {
@@ -122,7 +127,7 @@ extern "C" int vmi_poses_to_mats(const double* poses, int64_t n, double* mats, i
   }
   if (n < 512 || threads == 1) {
     work(0, n);
-    return 0;
+    return bad.load() ? -2 : 0;
   }
   if (threads > 64) threads = 64;
   const int64_t chunk = std::max<int64_t>(256, (n + 4 * threads - 1) / (4 * threads));
@@ -131,5 +136,5 @@ extern "C" int vmi_poses_to_mats(const double* poses, int64_t n, double* mats, i
     work(k * chunk, std::min(n, (k + 1) * chunk));
   };
   pool().run(threads - 1, nchunks, fn);
-  return 0;
+  return bad.load() ? -2 : 0;
 }

@@ -1246,7 +1246,7 @@ static int eval_poses_rot(vmi_ctx* c, const double* poses, int64_t P, double* mi
     plan_table(c, kernel_kind(c), c->cur.b_voxels, 2, &cap, &np, &multi);
     if (multi) return 1;
   }
-  if (vmi_poses_to_mats(poses, P, c->h_mats, 0)) return fail(c, VMI_ERR_ARG, "poses_to_mats");
+  if (vmi_poses_to_mats(poses, P, c->h_mats, 0)) return fail(c, VMI_ERR_ARG, "poses contain non-finite components");
   // stable counting sort by rotation: perm[q] = the pose in slot q
   int64_t* perm = pinned_perm(c);
   int32_t* ridx_q = pinned_status(c);  // (scratch until the statuses come back)
@@ -1312,7 +1312,7 @@ int vmi_eval_poses(vmi_ctx* c, const double* poses, int64_t P, double* mi_out, i
   // conversion of the rest (~8 ns/pose on the box's 16 pooled threads) and
   // its upload; short, so the GPU starts early
   const int64_t head = P < 8192 ? P : std::max<int64_t>(2048, P / 32);
-  if (vmi_poses_to_mats(poses, head, c->h_mats, 0)) return fail(c, VMI_ERR_ARG, "poses_to_mats");
+  if (vmi_poses_to_mats(poses, head, c->h_mats, 0)) return fail(c, VMI_ERR_ARG, "poses contain non-finite components");
   CK(c, cudaMemcpyAsync(c->d_mats, c->h_mats, head * 96, cudaMemcpyHostToDevice, c->stream));
   if ((rc = launch_fast_eval(c, c->d_mats, head, c->d_mi, c->d_status, dh, c->d_total, c->stream))) return rc;
   lap("head launched");
@@ -1320,7 +1320,7 @@ int vmi_eval_poses(vmi_ctx* c, const double* poses, int64_t P, double* mi_out, i
     const int64_t n = P - head;
     if (vmi_poses_to_mats(poses + 6 * head, n, c->h_mats + 12 * head, 0)) {
       cudaStreamSynchronize(c->stream);
-      return fail(c, VMI_ERR_ARG, "poses_to_mats");
+      return fail(c, VMI_ERR_ARG, "poses contain non-finite components");
     }
     lap("tail converted");
     CK(c, cudaMemcpyAsync(c->d_mats + 12 * head, c->h_mats + 12 * head, n * 96,
@@ -1954,7 +1954,7 @@ int upload_pair_poses(vmi_ctx* c, const double* poses, const int32_t* pair, int6
     if (pair[p] < 0 || pair[p] >= c->n_set) return fail(c, VMI_ERR_ARG, "pair index out of range");
   int rc;
   if ((rc = ensure_P(c, P, hist)) || (rc = ensure_pp(c, P)) || (rc = ensure_pinned(c, P))) return rc;
-  if (vmi_poses_to_mats(poses, P, c->h_mats, 0)) return fail(c, VMI_ERR_ARG, "poses_to_mats");
+  if (vmi_poses_to_mats(poses, P, c->h_mats, 0)) return fail(c, VMI_ERR_ARG, "poses contain non-finite components");
   CK(c, cudaMemcpyAsync(c->d_mats, c->h_mats, (size_t)P * 96, cudaMemcpyHostToDevice, c->stream));
   CK(c, cudaMemcpyAsync(c->d_pose_pair, pair, (size_t)P * 4, cudaMemcpyHostToDevice, c->stream));
   return 0;
@@ -2040,7 +2040,7 @@ int vmi_align_pairs(vmi_ctx* c, int64_t K, const double* x0, const double steps[
     double* h_mats = reinterpret_cast<double*>(hb);
     for (int64_t p = 0; p < n; ++p)
       if (run[p] < 0 || run[p] >= c->n_set) return fail(c, VMI_ERR_ARG, "pair index out of range");
-    if (vmi_poses_to_mats(poses, n, h_mats, 1)) return fail(c, VMI_ERR_ARG, "poses_to_mats");
+    if (vmi_poses_to_mats(poses, n, h_mats, 1)) return fail(c, VMI_ERR_ARG, "poses contain non-finite components");
     CK(c, cudaMemcpyAsync(const_cast<double*>(bf.mats), h_mats, (size_t)n * 96,
                           cudaMemcpyHostToDevice, c->stream));
     CK(c, cudaMemcpyAsync(const_cast<int32_t*>(bf.pose_pair), run, (size_t)n * 4,

@@ -194,7 +194,8 @@ class MIEngine:
             mi, st, hist, total = self.ctx.eval(self.mats(poses), want_hist=histograms,
                                                 bins=self.bins, exact=True)
         else:  # pose -> matrix on the host, overlapped with the GPU (vmi_eval_poses)
-            mi, st, hist, total = self.ctx.eval_poses(as_pose_array(poses), want_hist=histograms,
+            mi, st, hist, total = self.ctx.eval_poses(as_pose_array(poses, check_finite=False),
+                                                      want_hist=histograms,
                                                       bins=self.bins)
         if histograms:
             return mi, st, hist, total

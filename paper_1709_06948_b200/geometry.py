@@ -99,8 +99,10 @@ def euler_to_transform(pose: EulerPose) -> np.ndarray:
     return t
 
 
-def as_pose_array(poses) -> np.ndarray:
-    """Accept EulerPose objects, (6,) or (P, 6) arrays; return (P, 6) f64."""
+def as_pose_array(poses, check_finite: bool = True) -> np.ndarray:
+    """Accept EulerPose objects, (6,) or (P, 6) arrays; return (P, 6) f64.
+    ``check_finite=False``: the caller's native conversion validates instead
+    (vmi_poses_to_mats fails on a non-finite component)."""
     if isinstance(poses, EulerPose) or (hasattr(poses, "as_vector")
                                         and hasattr(poses, "rz")):
         return np.asarray(poses.as_vector(), dtype=np.float64)[None, :]
@@ -113,7 +115,7 @@ def as_pose_array(poses) -> np.ndarray:
         raise ValueError(f"poses must be (P, 6), got {arr.shape}")
     # any NaN / inf makes the sum non-finite; a finite sum proves every entry
     # finite (one pass instead of a full boolean mask on large batches)
-    if not np.isfinite(arr.sum()) and not np.isfinite(arr).all():
+    if check_finite and not np.isfinite(arr.sum()) and not np.isfinite(arr).all():
         raise ValueError("poses contain non-finite components")
     return arr
 

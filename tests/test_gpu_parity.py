@@ -1024,3 +1024,26 @@ def test_rotation_major_grid_matches_oracle_and_random_batches_stay_plain(monkey
     np.testing.assert_array_equal(m1, m0)
     np.testing.assert_array_equal(s1, s0)
     eng.close()
+
+
+@pytest.mark.parametrize("P", [5, 3000, 20000])
+def test_non_finite_pose_raises_and_engine_recovers(P):
+    """A NaN / inf pose component raises ValueError (EulerPose validation,
+    geometry.py:68-102) -- from the host conversion, wherever the pose sits in
+    the batch (head or pipelined tail) -- and the engine keeps working."""
+    s = golden("c1_scans.npz")
+    eng = engine(0.5, kind="count")
+    eng.set_reference(np.asarray(s["a"])[:, :3])
+    eng.set_query(np.asarray(s["b"])[:, :3])
+    poses = np.zeros((P, 6))
+    poses[:, 0] = np.linspace(-1, 1, P)
+    ok_mi, ok_st = eng.evaluate(poses)
+    for bad in (np.nan, np.inf):
+        q = poses.copy()
+        q[P - 1, 4] = bad
+        with pytest.raises(ValueError, match="non-finite"):
+            eng.evaluate(q)
+    mi, st = eng.evaluate(poses)
+    np.testing.assert_array_equal(mi, ok_mi)
+    np.testing.assert_array_equal(st, ok_st)
+    eng.close()
