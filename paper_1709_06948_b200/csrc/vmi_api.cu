@@ -1309,12 +1309,18 @@ int vmi_eval_poses(vmi_ctx* c, const double* poses, int64_t P, double* mi_out, i
   const int W = c->g.bins + 1;
   long long* dh = hist_out ? c->d_hist : nullptr;
   // head: long enough for its kernel (~0.4 us/pose at C2) to cover the host
-  // conversion of the rest (~8 ns/pose on the box's 16 pooled threads) and
-  // its upload; short, so the GPU starts early
-  const int64_t head = P < 8192 ? P : std::max<int64_t>(2048, P / 32);
+  // conversion of the rest (~8 ns/pose on the box's 16 pooled threads, with
+  // wake-up jitter up to ~1 ms) and its upload (VMI_TRACE: P/32 left GPU
+  // gaps of up to 0.2 ms before the tail launch)
+  const int64_t head = P < 8192 ? P : std::max<int64_t>(2048, P / 16);
   if (vmi_poses_to_mats(poses, head, c->h_mats, 0)) return fail(c, VMI_ERR_ARG, "poses contain non-finite components");
   CK(c, cudaMemcpyAsync(c->d_mats, c->h_mats, head * 96, cudaMemcpyHostToDevice, c->stream));
+  cudaEvent_t tev[4] = {nullptr, nullptr, nullptr, nullptr};  // VMI_TRACE: GPU phase times
+  if (trace)
+    for (auto& e : tev) cudaEventCreate(&e);
+  if (trace) cudaEventRecord(tev[0], c->stream);
   if ((rc = launch_fast_eval(c, c->d_mats, head, c->d_mi, c->d_status, dh, c->d_total, c->stream))) return rc;
+  if (trace) cudaEventRecord(tev[1], c->stream);
   lap("head launched");
   if (P > head) {
     const int64_t n = P - head;
@@ -1327,10 +1333,12 @@ int vmi_eval_poses(vmi_ctx* c, const double* poses, int64_t P, double* mi_out, i
                           cudaMemcpyHostToDevice, c->copy_stream));
     CK(c, cudaEventRecord(c->copy_done, c->copy_stream));
     CK(c, cudaStreamWaitEvent(c->stream, c->copy_done, 0));
+    if (trace) cudaEventRecord(tev[2], c->stream);
     if ((rc = launch_fast_eval(c, c->d_mats + 12 * head, n, c->d_mi + head, c->d_status + head,
                                dh ? dh + (size_t)head * W * W : nullptr, c->d_total + head,
                                c->stream)))
       return rc;
+    if (trace) cudaEventRecord(tev[3], c->stream);
   }
   // MI + status through pinned staging; the statuses read back also tell
   // do_fixups which poses to re-run (no second status read)
@@ -1340,6 +1348,15 @@ int vmi_eval_poses(vmi_ctx* c, const double* poses, int64_t P, double* mi_out, i
   CK(c, cudaMemcpyAsync(hst, c->d_status, P * 4, cudaMemcpyDeviceToHost, c->stream));
   CK(c, cudaStreamSynchronize(c->stream));
   lap("kernels done");
+  if (trace && P > head) {
+    float h = 0, g = 0, t = 0;
+    cudaEventElapsedTime(&h, tev[0], tev[1]);
+    cudaEventElapsedTime(&g, tev[1], tev[2]);
+    cudaEventElapsedTime(&t, tev[2], tev[3]);
+    std::fprintf(stderr, "[vmi_eval_poses] gpu: head %.3f ms, gap %.3f ms, tail %.3f ms\n", h, g, t);
+  }
+  if (trace)
+    for (auto& e : tev) if (e) cudaEventDestroy(e);
   bool flagged = false;
   for (int64_t p = 0; p < P && !flagged; ++p) flagged = (hst[p] & VMI_FLAG_RECHECK) != 0;
   if (flagged) {
