@@ -79,13 +79,20 @@ class Pool {
 Pool& pool() {
   // never destroyed: detached workers may still wait on it at exit.  A forked
   // child gets a fresh pool (its copy's workers and lock state are not usable).
-  static Pool* p = nullptr;
-  static pid_t owner = 0;
-  if (!p || owner != getpid()) {
-    p = new Pool;
-    owner = getpid();
+  static std::atomic<Pool*> p{nullptr};
+  static std::atomic<pid_t> owner{0};
+  static std::mutex init_m;  // (held for a moment; first use from several threads)
+  Pool* q = p.load();
+  if (!q || owner.load() != getpid()) {
+    std::lock_guard<std::mutex> g(init_m);
+    q = p.load();
+    if (!q || owner.load() != getpid()) {
+      q = new Pool;
+      p.store(q);
+      owner.store(getpid());
+    }
   }
-  return *p;
+  return *q;
 }
 
 }  // namespace
