@@ -2023,7 +2023,14 @@ int vmi_align_pairs(vmi_ctx* c, int64_t K, const double* x0, const double steps[
   cfg.x_tol = x_tol;
   cfg.restarts = restarts;
   // below ~two poses per SM a launch costs the same for 1 or 4 probes per run
-  cfg.spec_budget = 2 * (int64_t)c->sm_count;
+  // (VMI_SPEC: poses per SM.  A/B at C5: 2 -> 432 lockstep steps, 3,790 /s;
+  // 8 -> 419, 3,855; 64 -> 303 steps but 2x the probes, 2,947 /s -- the step
+  // count is set by the slowest pairs, each step's latency by one pose per SM)
+  static const double spec = [] {
+    const char* e = std::getenv("VMI_SPEC");
+    return e ? std::atof(e) : 2.0;
+  }();
+  cfg.spec_budget = (int64_t)(spec * c->sm_count);
   cudaSetDevice(c->device);
   // Two lanes of runs alternate on the context stream: lane l's batch
   // (matrices built on the host into pinned memory, upload, one multi-pair
