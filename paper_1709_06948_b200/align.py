@@ -17,6 +17,7 @@ from dataclasses import dataclass
 
 import numpy as np
 
+from ._lib import poses_to_mats
 from .engine import MIEngine, mutual_information_exact
 from .errors import NoOverlapError
 from .geometry import (EulerPose, as_pose_array, euler_to_transform, normalized,
@@ -168,12 +169,14 @@ def align_batch(pairs, t0s, cfg: AlignmentConfig | None = None, device: int = 0,
                                 simplex.restarts)
         wall = time.perf_counter() - start
         est = [normalized(EulerPose.from_vector(o["best_x"][k])) for k in range(K)]
-        _, st, _, hist = eng.evaluate_pairs(np.stack([e.as_vector() for e in est]), np.arange(K),
-                                            histograms=True)
+        est_vec = np.stack([e.as_vector() for e in est])
+        _, st, _, hist = eng.evaluate_pairs(est_vec, np.arange(K), histograms=True)
         t_final = time.perf_counter()
     finally:
         if engine is None:
             eng.close()
+    # euler_to_transform of every estimate in one native call (the same bits)
+    est_mats = poses_to_mats(est_vec)
     out = []
     redo = 0
     for k in range(K):
@@ -195,8 +198,11 @@ def align_batch(pairs, t0s, cfg: AlignmentConfig | None = None, device: int = 0,
         final_mi = (mutual_information_exact(hist[k], cfg.phi_enabled)[0] if st[k] == 0
                     else NO_OVERLAP_SENTINEL)
         n = int(o["trace_len"][k])
+        estimated = np.eye(4)
+        estimated[:3, :3] = est_mats[k, :9].reshape(3, 3)
+        estimated[:3, 3] = est_mats[k, 9:]
         out.append(AlignmentReport(
-            estimated=euler_to_transform(est[k]), estimated_pose=est[k], initial_pose=init[k],
+            estimated=estimated, estimated_pose=est[k], initial_pose=init[k],
             final_mi=float(final_mi), mi_trace=[*o["trace"][k, :n].tolist(), float(final_mi)],
             iterations=int(o["iterations"][k]), wall_time=wall,
             termination=NM_TERMINATION[int(o["termination"][k])],
