@@ -65,6 +65,9 @@ __device__ __forceinline__ uint32_t slot_of(uint32_t lin, uint32_t cap) {
 // per-point pivot arithmetic.  The per-point offset r (|r| <= 2^-53 |Z|) moves
 // a voxel's variance by at most res |r|max + r^2 (var_shift), and the sums'
 // own rounding is bounded through S2 + S1^2/n whatever the pivot.
+#ifndef VMI_OCC_BFREE
+#define VMI_OCC_BFREE 1
+#endif
 #ifndef VMI_OCC_BUCKET  // occupancy kind: 4-slot buckets (see flush_rec)
 #define VMI_OCC_BUCKET 1
 #endif
@@ -638,9 +641,17 @@ __global__ void __launch_bounds__(THREADS, 1)
           for (uint32_t probes = 0;;) {
             const uint32_t ba = key_sa + 16u * b;
             const uint4 w = ld_shared_v4(ba);
+#if VMI_OCC_BFREE  // branch-free bucket scan: masks, then the first free slot by FFS
+            const bool present = (w.x == r0.x) | (w.y == r0.x) | (w.z == r0.x) | (w.w == r0.x);
+            if (present) break;
+            const uint32_t em = (uint32_t)(w.x == kEmpty32) | ((uint32_t)(w.y == kEmpty32) << 1) |
+                                ((uint32_t)(w.z == kEmpty32) << 2) | ((uint32_t)(w.w == kEmpty32) << 3);
+            const uint32_t j = em ? (uint32_t)__ffs((int)em) - 1u : 4u;
+#else
             if (w.x == r0.x || w.y == r0.x || w.z == r0.x || w.w == r0.x) break;  // present
             const uint32_t j = w.x == kEmpty32 ? 0u : w.y == kEmpty32 ? 1u
                              : w.z == kEmpty32 ? 2u : w.w == kEmpty32 ? 3u : 4u;
+#endif
             if (j == 4u) {  // full: the next bucket
               if (++b == nb) b = 0;
               if (++probes >= nb) { misc[7] = 1; break; }  // table full -> exact path
