@@ -65,6 +65,9 @@ __device__ __forceinline__ uint32_t slot_of(uint32_t lin, uint32_t cap) {
 // per-point pivot arithmetic.  The per-point offset r (|r| <= 2^-53 |Z|) moves
 // a voxel's variance by at most res |r|max + r^2 (var_shift), and the sums'
 // own rounding is bounded through S2 + S1^2/n whatever the pivot.
+#ifndef VMI_PROBE4  // VARZ / COUNT collisions: linear probing four slots per LDS.128
+#define VMI_PROBE4 1
+#endif
 #ifndef VMI_OCC_BFREE
 #define VMI_OCC_BFREE 1
 #endif
@@ -684,6 +687,41 @@ __global__ void __launch_bounds__(THREADS, 1)
         if (done) {
           add(sl);
         } else if (has) {  // collision: linear probing from the next slot
+#if VMI_PROBE4
+          // the same slot order, four slots per LDS.128: the first slot at or
+          // after pos holding the key or free decides (masks + FFS, no
+          // per-slot branches).  A/B: C1v 2.87 -> 2.69 ms, C1 1.69 -> 1.68;
+          // the unit-resolution instantiation (C2, C3, C5) measured slower
+          // with it (26.57 -> 26.85 ms) and keeps the one-slot loop below.
+          if constexpr (MODE != kGridUnit) {
+          uint32_t pos = sl + 1 == ucap ? 0u : sl + 1;
+          for (uint32_t probes = 1;;) {
+            const uint32_t g4 = pos & ~3u, off = pos & 3u;
+            const uint4 w = ld_shared_v4(key_sa + 4u * g4);
+            uint32_t valid = (0xFu << off) & 0xFu;
+            if (ucap - g4 < 4u) valid &= (1u << (ucap - g4)) - 1u;
+            const uint32_t eq = ((uint32_t)(w.x == r0.x) | ((uint32_t)(w.y == r0.x) << 1) |
+                                 ((uint32_t)(w.z == r0.x) << 2) | ((uint32_t)(w.w == r0.x) << 3)) & valid;
+            const uint32_t em = ((uint32_t)(w.x == kEmpty32) | ((uint32_t)(w.y == kEmpty32) << 1) |
+                                 ((uint32_t)(w.z == kEmpty32) << 2) | ((uint32_t)(w.w == kEmpty32) << 3)) & valid;
+            const uint32_t dec = eq | em;
+            if (dec) {
+              const uint32_t j = (uint32_t)__ffs((int)dec) - 1u;
+              if ((eq >> j) & 1u) { add(g4 + j); break; }
+              const uint32_t old = atom_cas_shared(key_sa + 4u * (g4 + j), kEmpty32, r0.x);
+              if (old == kEmpty32) count_new();
+              if (old == kEmpty32 || old == r0.x) { add(g4 + j); break; }
+              pos = g4 + j + 1u;  // another key took it: probe on past it
+            } else {
+              probes += __popc(valid);
+              pos = g4 + 4u;
+            }
+            if (pos >= ucap) pos = 0;
+            if (probes >= ucap) { misc[7] = 1; break; }  // table full -> exact path
+          }
+          return;
+          }
+#endif
           uint32_t probes = 1;
           while (true) {
             if (++sl == ucap) sl = 0;
