@@ -65,6 +65,10 @@ __device__ __forceinline__ uint32_t slot_of(uint32_t lin, uint32_t cap) {
 // per-point pivot arithmetic.  The per-point offset r (|r| <= 2^-53 |Z|) moves
 // a voxel's variance by at most res |r|max + r^2 (var_shift), and the sums'
 // own rounding is bounded through S2 + S1^2/n whatever the pivot.
+// A/B (r02): C2 26.56 -> 26.04 ms, C4 32.98 -> 32.30, C1 1.68 -> 1.665
+#ifndef VMI_HULL_SPLIT  // the point loop compiled twice: with / without per-point bounds
+#define VMI_HULL_SPLIT 1
+#endif
 #ifndef VMI_PROBE4  // VARZ / COUNT collisions: linear probing four slots per LDS.128
 #define VMI_PROBE4 1
 #endif
@@ -915,7 +919,10 @@ __global__ void __launch_bounds__(THREADS, 1)
         src += kPG * kRowBytes;
         cp_async_commit();
       };
-      auto group_body = [&](int slot0) {  // the group starts in ring slot slot0
+      // hb: the hull supplies the bounds (compile-time in the main loop when
+      // VMI_HULL_SPLIT: two copies of it, no per-group branch)
+      auto group_body = [&](int slot0, auto hb) {  // the group starts in ring slot slot0
+        constexpr bool kHB = decltype(hb)::value;
         cp_async_wait<kGroups - 1>();  // rows r .. r+kPG-1 have landed
         uint32_t l[kPG];
         double D[kPG];
@@ -928,7 +935,7 @@ __global__ void __launch_bounds__(THREADS, 1)
           locate(x, y, z, l[u], D[u], ix[u], iy[u], iz[u]);
         }
         issue_group(slot0);  // refill the slots just consumed with rows r+S ..
-        if (!hull_bounds) {  // bounds: one min/max tree per group (3-input VIMNMX3)
+        if (VMI_HULL_SPLIT ? !kHB : !hull_bounds) {  // bounds: one min/max tree per group
           int n0 = ix[0], n1 = iy[0], n2 = iz[0], x0 = ix[0], x1 = iy[0], x2 = iz[0];
 #pragma unroll
           for (int u = 1; u < kPG; ++u) {
@@ -947,11 +954,17 @@ __global__ void __launch_bounds__(THREADS, 1)
       for (int gi = 0; gi < kGroups; ++gi) issue_group(gi * kPG);  // rows 0 .. S-1 in flight
       int rr = 0;
       // one trip = one lap of the ring (compile-time slots), then the last groups
-      for (; rr + S <= full; rr += S) {
+      auto main_loop = [&](auto hb) {
+        for (; rr + S <= full; rr += S) {
 #pragma unroll
-        for (int gi = 0; gi < kGroups; ++gi) group_body(gi * kPG);
-      }
-      for (; rr + kPG <= full; rr += kPG) group_body(rr % S);
+          for (int gi = 0; gi < kGroups; ++gi) group_body(gi * kPG, hb);
+        }
+        for (; rr + kPG <= full; rr += kPG) group_body(rr % S, hb);
+      };
+      if (VMI_HULL_SPLIT && hull_bounds)
+        main_loop(std::true_type{});
+      else
+        main_loop(std::false_type{});
       cp_async_wait<0>();
       VMI_TR("main loop done", rr)
       for (; rr <= full; ++rr) {  // leftover (< kPG) points and the ragged last row
