@@ -18,11 +18,11 @@ import os
 ROOT = os.path.abspath(os.path.join(os.path.dirname(__file__), ".."))
 # config -> (summary file, poses in the captured launch)
 SOURCES = {
-    "c1": ("profiles/r02_v11_c1_k_pose_fast_full.json", 6069),
-    "c1v": ("profiles/r02_v11_c1v_k_pose_fast_full.json", 6069),
-    "c2": ("profiles/r02_v11_c2_k_pose_fast_full.json", 65536),
-    "c3": ("profiles/r02_v11_c3_k_pose_fast_full.json", 970299),
-    "c4": ("profiles/r02_v11_c4_k_pose_fast_full.json", 65536),
+    "c1": ("profiles/r02_v12_c1_k_pose_fast_full.json", 6069),
+    "c1v": ("profiles/r02_v12_c1v_k_pose_fast_full.json", 6069),
+    "c2": ("profiles/r02_v12_c2_k_pose_fast_full.json", 65536),
+    "c3": ("profiles/r02_v12_c3_k_pose_fast_full.json", 970299),
+    "c4": ("profiles/r02_v12_c4_k_pose_fast_full.json", 65536),
 }
 
 
